@@ -1,0 +1,121 @@
+"""Pins for oracle O3/O4 (RS over the strip layout) against textbook RS and brute force."""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import matrices as mx
+from oracle import rs
+from synth import stripe_data
+
+
+def poly_mul_no_table(a, b):
+    """Independent test-side product: carry-less multiply, then reduce by long division."""
+    prod = 0
+    for i in range(8):
+        if (b >> i) & 1:
+            prod ^= a << i
+    for deg in range(14, 7, -1):
+        if (prod >> deg) & 1:
+            prod ^= 0x11D << (deg - 8)
+    return prod
+
+
+def brute_force_strip_rs(rows, blocks):
+    """Per (offset, bit) scalar loops: gather a byte, multiply without tables, scatter."""
+    n, B = blocks.shape
+    S = B // 8
+    out = np.zeros((len(rows), B), dtype=np.uint8)
+    for o in range(S):
+        for b in range(8):
+            xs = []
+            for j in range(n):
+                xs.append(sum(((int(blocks[j, k * S + o]) >> b) & 1) << k for k in range(8)))
+            for i, row in enumerate(rows):
+                y = 0
+                for j in range(n):
+                    y ^= poly_mul_no_table(row[j], xs[j])
+                for r in range(8):
+                    if (y >> r) & 1:
+                        out[i, r * S + o] |= 1 << b
+    return out
+
+
+@pytest.mark.parametrize("n,p,kind,B", [(4, 2, "cauchy", 16), (4, 2, "cauchy", 8),
+                                        (10, 4, "isal", 24), (3, 3, "sysvand", 16)])
+def test_three_paths_agree_tiny(n, p, kind, B):
+    rng = np.random.default_rng(n * 100 + B)
+    g = mx.coding_matrix(n, p, kind)
+    data = rng.integers(0, 256, size=(n, B), dtype=np.uint8)
+    a = rs.encode(g, n, data)
+    b = rs.bitmatrix_apply(mx.to_bitmatrix(g[n:]), data)
+    c = brute_force_strip_rs(g[n:], data)
+    assert (a == b).all() and (a == c).all()
+
+
+def test_bitplane_reduction_to_bytewise_rs():
+    # If strip (j,k) byte o bit b = bit k of data byte 8o+b, the de-transposed
+    # output equals textbook byte-wise RS y_i[t] = sum_j R_ij d_j[t].
+    n, p, S = 4, 2, 8
+    g = mx.coding_matrix(n, p, "cauchy")
+    rng = np.random.default_rng(5)
+    d = rng.integers(0, 256, size=(n, 8 * S), dtype=np.uint8)      # byte data
+    blocks = np.zeros((n, 8 * S), dtype=np.uint8)
+    for j in range(n):
+        for t in range(8 * S):
+            o, b = divmod(t, 8)
+            for k in range(8):
+                if (d[j, t] >> k) & 1:
+                    blocks[j, k * S + o] |= 1 << b
+    out = rs.encode(g, n, blocks)
+    for i in range(p):
+        for t in range(8 * S):
+            o, b = divmod(t, 8)
+            y = sum(((int(out[i, k * S + o]) >> b) & 1) << k for k in range(8))
+            want = 0
+            for j in range(n):
+                want ^= poly_mul_no_table(g[n + i][j], int(d[j, t]))
+            assert y == want
+
+
+def test_raid5_parity0_and_linearity():
+    g = mx.coding_matrix(10, 4, "isal")
+    d1 = stripe_data(7, 0, 10, 256)
+    d2 = stripe_data(7, 1, 10, 256)
+    p1 = rs.encode(g, 10, d1)
+    assert (p1[0] == np.bitwise_xor.reduce(d1, axis=0)).all()
+    assert (rs.encode(g, 10, d1 ^ d2) == p1 ^ rs.encode(g, 10, d2)).all()
+    assert not rs.encode(g, 10, np.zeros_like(d1)).any()
+
+
+@pytest.mark.parametrize("n,p,kind", [(4, 2, "cauchy"), (10, 4, "isal")])
+def test_roundtrip_all_patterns(n, p, kind):
+    g = mx.coding_matrix(n, p, kind)
+    data = stripe_data(11, 3, n, 64)
+    blocks = np.concatenate([data, rs.encode(g, n, data)])
+    pats = list(itertools.combinations(range(n + p), p))
+    if len(pats) > 120:
+        pats = pats[::9]
+    for erased in pats:
+        surv, rows = mx.decode_rows(g, n, list(erased))
+        rec = rs.decode(rows, blocks[surv])
+        assert (rec == blocks[list(erased)]).all()
+
+
+def test_one_hot_columns():
+    # feeding strip c = 0xFF.., all others 0, makes output strip r = 0xFF.. iff bit (r, c) set
+    g = mx.coding_matrix(4, 2, "cauchy")
+    bits = mx.to_bitmatrix(g[4:])
+    for c in range(32):
+        blocks = np.zeros((4, 16), dtype=np.uint8)
+        j, k = divmod(c, 8)
+        blocks[j, 2 * k:2 * k + 2] = 0xFF
+        out = rs.encode(g, 4, blocks).reshape(16, 2)
+        for r in range(16):
+            assert (out[r] == (0xFF if bits[r, c] else 0)).all()
+
+
+def test_rejects_ragged():
+    with pytest.raises(ValueError):
+        rs.apply_rows([[1]], np.zeros((1, 12), dtype=np.uint8))
+    assert rs.apply_rows([[1]], np.zeros((1, 0), dtype=np.uint8)).shape == (1, 0)
