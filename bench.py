@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""bench.py -- device-timed RS(n,p) XOR-SLP encode/decode throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2|cfg3|cfg4|cfg5]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+    python bench.py --impl reference          # the CPU oracle arm (rank 0 only)
+
+Metric (BASELINE.json): GB/s of data (10^9 bytes of the n data blocks per stripe,
+reading R14), device-timed with CUDA events on the launching stream, max over
+ranks; value = all ranks' data / that time.  A "step" is one pass of the device
+hot path over the workload's stripes: one launch of the
+compiled program over every stripe.  Compilation (H1-H7) is untimed.
+
+Default workload = BASELINE configs[1] (cfg2): RS(10,4) encode of 1024 stripes x
+10 x 1 MiB per GPU (weak scaling: rank r owns global stripes [r*1024, (r+1)*1024)).
+Inputs (10 GiB) exceed the 126 MB L2, so no flush is needed between steps.
+"""
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RS encode/decode GB/s of data (device-timed) at 1/2/4/8 B200; % of roofline"
+MiB = 1 << 20
+
+WORKLOADS = {
+    "cfg2": dict(desc="RS(10,4) encode, 1024 stripes x 10 x 1 MiB per GPU (BASELINE configs[1])",
+                 n=10, p=4, B=MiB, S=1024, op="encode", seed=2),
+    "cfg3": dict(desc="RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures, "
+                      "one interpreter launch with a program per stripe (BASELINE configs[2])",
+                 n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3),
+    "cfg5": dict(desc="RS(20,4) encode, 8192 stripes x 20 x 1 MiB sharded over the GPUs; chunks "
+                      "of <=2048 stripes per launch (BASELINE configs[4])",
+                 n=20, p=4, B=MiB, S=8192, op="encode_sharded", seed=5, chunk=2048),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="xslp", choices=["xslp", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--compress", default="xorrepair", choices=["none", "repair", "xorrepair"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "straight", "interp"])
+    ap.add_argument("--lanes", type=int, default=1)
+    ap.add_argument("--threads", type=int, default=256)
+    ap.add_argument("--block-bytes", type=int, default=0, help="override block size")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def measured_peak():
+    for path in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic(workload):
+    """dram bytes per launch from a committed `ncu --set full` capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    def __init__(self, dev_index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self.stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop.set()
+            self.t.join()
+
+    def summary(self):
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(s), "source": "nvml" if self.ok else "unavailable"}
+
+
+# ------------------------------------------------------------------------------------------
+def oracle_baseline(wl, budget_s=12.0):
+    """The CPU oracle as it stands (oracle/rs.py, numpy, one core) on a bounded sample."""
+    import numpy as np
+    import synth
+    from oracle import matrices as mx
+    from oracle import rs
+    n, p, B = wl["n"], wl["p"], wl["B"]
+    g = mx.coding_matrix(n, p)
+    done, t0, s = 0, time.perf_counter(), 0
+    if wl["op"] == "decode_multi":
+        rows_cache = {}
+    while True:
+        data = synth.stripe_data(wl["seed"], s, n, B)
+        if wl["op"] == "decode_multi":
+            er = tuple(synth.erasure_pattern(wl["seed"], s, n + p, wl["e"]))
+            if er not in rows_cache:
+                rows_cache[er] = mx.decode_rows(g, n, list(er))
+            surv, rows = rows_cache[er]
+            blocks = np.concatenate([data, data[:p]])   # survivor bytes: any n blocks
+            rs.decode(rows, blocks[:n])
+        else:
+            rs.encode(g, n, data)
+        done += 1
+        s += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(done * n * B / dt / 1e9, 6), "unit": "GB/s", "cores": 1,
+            "kind": "oracle",
+            "sample": f"{done} stripe(s) of the workload ({n} x {B} B data each), oracle/rs.py "
+                      f"table-driven RS on the bit-transposed view, numpy single thread, "
+                      f"{dt:.1f} s"}
+
+
+def run_reference(args, wl, rank, world):
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    import synth
+    from oracle import matrices as mx
+    from oracle import rs
+    n, p, B = wl["n"], wl["p"], wl["B"]
+    g = mx.coding_matrix(n, p)
+
+    def step(s):
+        data = synth.stripe_data(wl["seed"], s, n, B)
+        if wl["op"] == "decode_multi":
+            er = synth.erasure_pattern(wl["seed"], s, n + p, wl["e"])
+            surv, rows = mx.decode_rows(g, n, er)
+            rs.decode(rows, np.concatenate([data, data[:p]])[:n])
+        else:
+            rs.encode(g, n, data)
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    dt = time.perf_counter() - t0
+    v = args.steps * n * B / dt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt / max(1, args.steps) * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": config_of(args, wl, None),
+            "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"each step = 1 stripe ({n} x {B} B data) of the workload "
+                                       "through oracle/rs.py on one host core"},
+            "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_of(args, wl, stats):
+    c = {"workload": f"{args.workload}: {wl['desc']}", "n": wl["n"], "p": wl["p"],
+         "block_bytes": wl["B"], "stripes_per_gpu": wl["S"] if wl["op"] != "encode_sharded"
+         else wl["S"] // max(1, args.gpus),
+         "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": f"{args.compress}+fuse+dfs",
+         "kernel": args.kernel, "lane_words": args.lanes, "threads": args.threads,
+         "l2": "inputs larger than the 126 MB L2; no flush between steps",
+         "parallelism": f"stripe-sharded x{args.gpus}, no collective"}
+    if stats:
+        c["slp"] = {k: stats[k] for k in ("xor_count", "mem_count", "n_instr", "nvar", "maxlive",
+                                          "regs", "spill_bytes")}
+    return c
+
+
+# ------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    wl = dict(WORKLOADS[args.workload])
+    if args.block_bytes:
+        scale = wl["B"] // args.block_bytes
+        wl["B"] = args.block_bytes
+        wl["S"] = wl["S"] * max(1, scale)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, wl, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import paper_2108_02692_b200 as X
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    n, p, B = wl["n"], wl["p"], wl["B"]
+    G = X.xslp_coding_matrix(n, p)
+    stream = torch.cuda.current_stream()
+
+    # ---- compile (untimed, H1-H7) ----
+    t0 = time.perf_counter()
+    if wl["op"] == "decode_multi":
+        import synth
+        S = wl["S"]
+        s0 = rank * S
+        pats = [tuple(synth.erasure_pattern(wl["seed"], s0 + s, n + p, wl["e"])) for s in range(S)]
+        uniq = sorted(set(pats))
+        dec = [X.xslp_decode_bitmatrix(G, n, p, er) for er in uniq]
+        progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,
+                               threads=args.threads)
+        prog = progs[0]
+        m_out = wl["e"]
+    else:
+        prog = X.xslp_compile(X.xslp_encode_bitmatrix(G, n, p), compress=args.compress,
+                              kernel=args.kernel, lane_words=args.lanes, threads=args.threads,
+                              block_bytes_hint=B)
+        m_out = p
+    compile_s = time.perf_counter() - t0
+    stats = prog.stats()
+
+    # ---- device buffers and seeded inputs (untimed) ----
+    if wl["op"] == "encode_sharded":
+        S_total = wl["S"]
+        per = S_total // world
+        S = min(per, wl["chunk"])
+        nchunks = (per + S - 1) // S
+        stripe0 = rank * per
+    else:
+        S = wl["S"]
+        nchunks = 1
+        stripe0 = rank * S
+    n_in = n
+    din = torch.empty((S, n_in, B), dtype=torch.uint8, device="cuda")
+    dout = torch.empty((S, m_out, B), dtype=torch.uint8, device="cuda")
+    X.xslp_fill_random(din, S, n_in, B, seed=wl["seed"], stripe0=stripe0)
+    ti = X.block_table(din, S, n_in, B)
+    to = X.block_table(dout, S, m_out, B)
+    if wl["op"] == "decode_multi":
+        idx = torch.tensor([uniq.index(er) for er in pats], dtype=torch.int32, device="cuda")
+
+    def launch():
+        if wl["op"] == "decode_multi":
+            X.xslp_decode_batch_multi(progs, idx, ti, to, S, B, stream=stream)
+        else:
+            X.xslp_encode_batch(prog, ti, to, S, B, stream=stream)
+
+    def step():
+        for _ in range(nchunks):
+            launch()
+
+    # sanity (torch, not the product): RAID-5 row of the [I; 2^ij] encode
+    launch()
+    torch.cuda.synchronize()
+    if wl["op"] != "decode_multi":
+        acc = din[:, 0].clone()
+        for j in range(1, n):
+            acc ^= din[:, j]
+        if not torch.equal(acc, dout[:, 0]):
+            raise SystemExit("sanity check failed: parity block 0 != XOR of data blocks")
+        del acc
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = X.xslp_launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(local) as clk:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            step()
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+    launches = X.xslp_launch_count() - l0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    data_bytes_step = S * nchunks * n * B * world
+    value = data_bytes_step * args.steps / (total_ms / 1e3) / 1e9
+
+    # roofline of the dominant (only) kernel: algorithmic bytes per launch / launch time
+    alg_bytes_launch = S * (n_in + m_out) * B
+    launch_ms = sum(per_step) / len(per_step) / nchunks
+    achieved = alg_bytes_launch / (launch_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload),
+            "peak_source": peak_src, "kernel": "xslp_interp_kernel" if wl["op"] == "decode_multi"
+            else ("xslp_sl_batch" if stats["regs"] and args.kernel != "interp" else "xslp_interp_kernel"),
+            "alg_bytes_per_launch": alg_bytes_launch, "launch_ms": round(launch_ms, 4),
+            "alg_bytes_per_data_byte": round((n_in + m_out) / n, 4)}
+
+    # ---- e2e through the host-buffer C-ABI call ----
+    e2e = None
+    if not args.no_e2e and wl["op"] == "encode":
+        try:
+            h_in = torch.empty((S, n, B), dtype=torch.uint8, pin_memory=True)
+            h_out = torch.empty((S, p, B), dtype=torch.uint8, pin_memory=True)
+            h_in.copy_(din)
+            X.xslp_encode_host(prog, h_in, h_out, S, B, stream=stream)   # warm
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            e0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                X.xslp_encode_host(prog, h_in, h_out, S, B, stream=stream)
+            torch.cuda.synchronize()
+            et = torch.tensor([time.perf_counter() - e0], dtype=torch.float64, device="cuda")
+            if dist:
+                dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            ok = bool((h_out[:, 0].cuda() == dout[:, 0]).all().item())
+            e2e = {"value": round(S * n * B * world * args.e2e_steps / float(et.item()) / 1e9, 3),
+                   "unit": "GB/s", "h2d_bytes_per_step": S * n * B, "d2h_bytes_per_step": S * p * B,
+                   "steps": args.e2e_steps, "api": "xslp_encode_host (pinned host buffers, "
+                   "chunked H2D / kernel / D2H on two streams)", "check_parity0": ok}
+            del h_in, h_out
+        except Exception as ex:  # report, do not hide
+            e2e = {"value": None, "unit": "GB/s", "error": str(ex)[:200]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_baseline(wl)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                "config": config_of(args, wl, stats), "roofline": roof, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+                "compile_s": round(compile_s, 3),
+                "step_ms": {"min": round(min(per_step), 4), "median": round(sorted(per_step)[len(per_step) // 2], 4),
+                            "max": round(max(per_step), 4)}}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

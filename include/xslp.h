@@ -1,0 +1,195 @@
+/*
+ * xslp.h -- C ABI of libxslp: XOR straight-line-program (SLP_xor) erasure coding on B200.
+ *
+ * What it computes (arXiv 2108.02692, Uezato SC'21; "P:n" = line n of the paper
+ * text, section tags as in DESIGN.md):
+ *   RS(n,p) over GF(2^8) (polynomial x^8+x^4+x^3+x^2+1) is lowered to a
+ *   GF(2) bitmatrix V~ ([Intro]) and lifted to an SLP_xor whose
+ *   constants are the 8n input strips and whose goals are the 8p parity (or 8e
+ *   recovered) strips ([Appr]).  The host compiler shrinks it with
+ *   RePair / XorRePair ([SLP]), XOR fusion ([Fus]) and the
+ *   DFS pebble-game schedule ([Peb]); the device executes it over
+ *   byte arrays with hand-written sm_100a kernels.
+ *
+ * Strip layout: a block of B bytes is 8 contiguous strips of B/8
+ * bytes; constant c_{8j+k} is strip k of input block j, goal g_{8i+r} is strip r
+ * of output block i.  Bitmatrix entry (8i+r, 8j+k) = bit r of (G_ij * 2^k)
+ * (LSB-first byte<->bit-vector map, reading R3).
+ *
+ * Conventions for every call
+ *   - Return value: XSLP_OK (0) or a negative XSLP_E* code.  Calls never abort;
+ *     the message of the last failure on the calling thread is xslp_last_error().
+ *   - Host pointers are plain C arrays owned by the caller and only read/written
+ *     during the call.  Device pointers are owned by the caller; the library
+ *     never frees them.  Device calls are asynchronous on the given stream (a
+ *     cudaStream_t passed as void*; NULL = legacy default stream) and use the
+ *     calling thread's current CUDA device.
+ *   - Device buffers: every block pointer 16-byte aligned; outputs must not
+ *     alias inputs; block_bytes must be a multiple of 32 (so a strip is a whole
+ *     number of 32-bit words).  block_bytes == 0 or nstripes == 0 is a no-op.
+ *   - Bitmatrices are row-major, one byte (0 or 1) per bit.
+ *   - There is no CPU fallback: a device call on a machine without a usable CUDA
+ *     device fails with XSLP_ECUDA.
+ */
+#ifndef XSLP_H
+#define XSLP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XSLP_OK 0
+#define XSLP_EINVAL (-1)         /* null / out-of-range / misaligned / non-divisible argument */
+#define XSLP_ESINGULAR (-2)      /* singular GF(2^8) matrix */
+#define XSLP_EUNRECOVERABLE (-3) /* more than p erasures */
+#define XSLP_ECUDA (-4)          /* CUDA runtime error, or no device */
+#define XSLP_ENOMEM (-5)         /* host or device allocation failed */
+#define XSLP_ECOMPILE (-6)       /* PTX -> sm_100a compilation failed */
+
+/* Coding-matrix families (readings R1, R2). */
+#define XSLP_RS_ISAL 0    /* [I_n; R], R[i][j] = (2^i)^j: reproduces the paper's counts */
+#define XSLP_RS_SYSVAND 1 /* [I_n; M V^-1], the text's reduced Vandermonde */
+#define XSLP_CAUCHY 2     /* [I_n; R], R[i][j] = inv((n+i) xor j) (BASELINE cfg1) */
+
+#define XSLP_COMPRESS_NONE 0      /* the lifted SLP of P:599-629 ("Base") */
+#define XSLP_COMPRESS_REPAIR 1    /* RePair */
+#define XSLP_COMPRESS_XORREPAIR 2 /* XorRePair = RePair + Rebuild */
+
+#define XSLP_SCHED_NONE 0 /* keep creation order */
+#define XSLP_SCHED_DFS 1  /* DFS post-order + pebble reuse */
+
+#define XSLP_KERNEL_AUTO 0     /* straight-line kernel when compiled, else interpreter */
+#define XSLP_KERNEL_STRAIGHT 1 /* the JIT-compiled straight-line specialisation */
+#define XSLP_KERNEL_INTERP 2   /* the generic SLP interpreter kernel */
+
+typedef struct xslp_opts {
+  int32_t compress;        /* XSLP_COMPRESS_*; default XORREPAIR */
+  int32_t fuse;            /* 1 = XOR fusion; default 1 */
+  int32_t schedule;        /* XSLP_SCHED_*; default DFS */
+  int32_t specialise;      /* 1 = emit PTX and compile the straight-line kernel now; default 1 */
+  int32_t lane_words;      /* 32-bit words per thread per strip in the straight-line kernel: 1, 2 or 4; default 1 */
+  int32_t threads;         /* CTA size of both kernels (32..1024, multiple of 32); default 256 */
+  int64_t block_bytes_hint;/* if > 0, bake strip = hint/8 into the straight-line kernel's addressing */
+  int32_t kernel;          /* XSLP_KERNEL_* used by xslp_encode/decode(_batch); default AUTO */
+  int32_t goal_order;      /* DFS root order: 0 = by the term order of the goal nodes, 1 = goal index */
+} xslp_opts;
+
+typedef struct xslp_stats {
+  int32_t n_const;    /* constants (input strips) = columns of the bitmatrix */
+  int32_t n_goals;    /* goals (output strips) = rows of the bitmatrix */
+  int64_t xor_count;  /* #xor = sum(arity - 1) over instructions */
+  int64_t mem_count;  /* #M = sum(arity + 1) */
+  int32_t n_instr;    /* instructions */
+  int32_t nvar;       /* NVar of the program as dumped (pebbles after DFS) */
+  int32_t maxlive;    /* max live 32-bit values per lane under eager goal stores (interpreter slots) */
+  int32_t n_copy_goals; /* goals equal to one constant (identity rows) */
+  int32_t n_zero_goals; /* goals equal to the empty set (all-zero rows) */
+  int32_t regs;       /* registers per thread of the straight-line kernel (0 if not compiled) */
+  int32_t spill_bytes;/* local-memory spill stores of the straight-line kernel */
+  double compile_ms;  /* host compile time of xslp_compile (SLP passes + PTX -> cubin) */
+} xslp_stats;
+
+typedef struct xslp_program xslp_program; /* opaque, immutable after compile, thread-safe to share */
+
+/* Fill opts with the defaults listed above. */
+void xslp_default_opts(xslp_opts *opts);
+
+/* ---- host helpers: matrices -------------------------------- */
+
+/* gf_out: (n+p) x n bytes, row-major; 1 <= n, 0 <= p, n+p <= 255. */
+int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out);
+
+/* bits_out: (8p) x (8n), the lowering x~ of the parity rows of gf ((n+p) x n). */
+int xslp_encode_bitmatrix(const uint8_t *gf, int n, int p, uint8_t *bits_out);
+
+/* Decode bitmatrix for the erased block indices erased[0..ne) (0-based, any order,
+ * 1 <= ne <= p).  Survivors are the first n non-erased indices ascending; goals are
+ * the erased blocks in ascending index: a data block e is row e of M^-1, a parity
+ * block e is G[e] M^-1 (reading R4).
+ * bits_out: (8ne) x (8n); survivors_out: n ints.  Errors: XSLP_EUNRECOVERABLE if
+ * ne > p, XSLP_EINVAL for bad/duplicate indices, XSLP_ESINGULAR if M is singular. */
+int xslp_decode_bitmatrix(const uint8_t *gf, int n, int p, const int32_t *erased, int ne,
+                          uint8_t *bits_out, int32_t *survivors_out);
+
+/* ---- compile (host, untimed) ------------------------------------------------------- */
+
+/* bits: out_rows x in_cols (in_cols a multiple of 8, out_rows a multiple of 8, in_cols <= 512).
+ * opts may be NULL (defaults).  *out receives a new program (free with xslp_free). */
+int xslp_compile(const uint8_t *bits, int out_rows, int in_cols, const xslp_opts *opts,
+                 xslp_program **out);
+
+/* Compile an SLP given in the text format (below) instead of a bitmatrix.  With
+ * compress = NONE its instruction structure is kept and only fused/scheduled;
+ * otherwise its goal sets are recomputed and compressed.  n_const = number of
+ * constants c0..c{n_const-1} (any positive count; the device path additionally
+ * needs a multiple of 8). */
+int xslp_compile_text(const char *text, int n_const, const xslp_opts *opts, xslp_program **out);
+
+int xslp_program_stats(const xslp_program *prog, xslp_stats *stats);
+
+/* Text of the program.  form 0: the scheduled MultiSLP with the paper's pebble
+ * names and a final "return" line; form 1: the interpreter's slot program
+ * (initial "s<k> = c<j>" loads, slot instructions, "out <g> = ..." stores);
+ * form 2: the straight-line kernel's PTX.  Format: one statement per line,
+ * "<var> = <term> ^ <term> ...", "out <g> = <term>", "return <term> ...", terms
+ * c<j> (constant), 0 (empty set) or a variable name; statements are sequential.
+ * Writes at most cap bytes including the NUL; returns the full length needed
+ * (excluding the NUL), or a negative error. */
+int64_t xslp_program_dump(const xslp_program *prog, int form, char *buf, size_t cap);
+
+void xslp_free(xslp_program *prog);
+
+/* ---- device application (timed hot path) ---------------------------------------- */
+
+/* One stripe: in_blocks[0..n) and out_blocks[0..m) are HOST arrays of DEVICE
+ * pointers (n = n_const/8 input blocks, m = n_goals/8 output blocks).  For
+ * encode, inputs are the data blocks and outputs the parity blocks; for decode,
+ * inputs are the survivors in survivors_out order and outputs the erased blocks
+ * in ascending index.  xslp_encode and xslp_decode are the same operation. */
+int xslp_encode(const xslp_program *prog, const uint8_t *const *in_blocks,
+                uint8_t *const *out_blocks, size_t block_bytes, void *stream);
+int xslp_decode(const xslp_program *prog, const uint8_t *const *in_blocks,
+                uint8_t *const *out_blocks, size_t block_bytes, void *stream);
+
+/* Many stripes, one program: d_in_tbl / d_out_tbl are DEVICE arrays of device
+ * pointers, [nstripes][n] and [nstripes][m] row-major. */
+int xslp_encode_batch(const xslp_program *prog, const uint8_t *const *d_in_tbl,
+                      uint8_t *const *d_out_tbl, int nstripes, size_t block_bytes, void *stream);
+
+/* Many stripes, a program per stripe (heterogeneous erasure patterns):
+ * progs[0..nprogs) share n_const and n_goals; d_prog_of_stripe is a DEVICE
+ * int32 array [nstripes] of indices into progs.  Runs the interpreter kernel
+ * in one launch (nprogs == 1 behaves like xslp_encode_batch). */
+int xslp_decode_batch_multi(const xslp_program *const *progs, int nprogs,
+                            const int32_t *d_prog_of_stripe, const uint8_t *const *d_in_tbl,
+                            uint8_t *const *d_out_tbl, int nstripes, size_t block_bytes,
+                            void *stream);
+
+/* End-to-end form with HOST buffers: h_in = [nstripes][n][block_bytes] and
+ * h_out = [nstripes][m][block_bytes], contiguous (ideally pinned) host memory.
+ * Stages chunks of stripes through device memory owned by the program's
+ * per-device workspace, overlapping host->device copies, the kernel and
+ * device->host copies; synchronous (returns when h_out is written). */
+int xslp_encode_host(const xslp_program *prog, const uint8_t *h_in, uint8_t *h_out,
+                     int nstripes, size_t block_bytes, void *stream);
+
+/* Seeded synthetic input on the device (same counter-based generator as the
+ * repo's synth module; no coding arithmetic): d_buf = [nstripes][nblocks][block_bytes],
+ * block j of global stripe s word i = splitmix64(seed*0x9E3779B97F4A7C15 +
+ * ((s*64 + j) << 40) + i), s = stripe0 + local index.  block_bytes % 8 == 0. */
+int xslp_fill_random(uint8_t *d_buf, int nstripes, int nblocks, size_t block_bytes,
+                     uint64_t seed, int64_t stripe0, void *stream);
+
+/* Number of kernels this library launched on the calling process so far. */
+int64_t xslp_launch_count(void);
+
+const char *xslp_last_error(void);
+const char *xslp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XSLP_H */

@@ -1,0 +1,272 @@
+"""paper_2108_02692_b200 -- B200-native XOR straight-line-program erasure coding.
+
+Thin Python binding over the C ABI of ``libxslp.so`` (include/xslp.h): argument
+marshalling only.  Every step of the hot path runs in the library (host
+compiler in C++, device kernels in CUDA for sm_100a).  There is no CPU
+fallback: importing this package without the built library raises, and device
+calls on a machine without a CUDA device raise ``XslpError`` (XSLP_ECUDA).
+
+Function names follow the C ABI (``xslp_compile``, ``xslp_encode_batch`` ...).
+Buffers may be given as torch tensors (their ``data_ptr()`` is used), numpy
+arrays (host), or raw integer addresses.  ``stream`` is a ``torch.cuda.Stream``,
+a raw ``cudaStream_t`` integer, or None for torch's current stream.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBPATH = os.path.join(_HERE, "libxslp.so")
+
+if not os.path.exists(_LIBPATH):
+    raise ImportError(
+        f"{_LIBPATH} is missing: build it with `python -m paper_2108_02692_b200.build` "
+        "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(_LIBPATH)
+
+XSLP_OK, XSLP_EINVAL, XSLP_ESINGULAR, XSLP_EUNRECOVERABLE = 0, -1, -2, -3
+XSLP_ECUDA, XSLP_ENOMEM, XSLP_ECOMPILE = -4, -5, -6
+XSLP_RS_ISAL, XSLP_RS_SYSVAND, XSLP_CAUCHY = 0, 1, 2
+XSLP_COMPRESS_NONE, XSLP_COMPRESS_REPAIR, XSLP_COMPRESS_XORREPAIR = 0, 1, 2
+XSLP_SCHED_NONE, XSLP_SCHED_DFS = 0, 1
+XSLP_KERNEL_AUTO, XSLP_KERNEL_STRAIGHT, XSLP_KERNEL_INTERP = 0, 1, 2
+
+KINDS = {"isal": XSLP_RS_ISAL, "sysvand": XSLP_RS_SYSVAND, "cauchy": XSLP_CAUCHY}
+COMPRESS = {"none": 0, "repair": 1, "xorrepair": 2}
+KERNELS = {"auto": 0, "straight": 1, "interp": 2}
+
+
+class xslp_opts(ctypes.Structure):
+    _fields_ = [("compress", ctypes.c_int32), ("fuse", ctypes.c_int32),
+                ("schedule", ctypes.c_int32), ("specialise", ctypes.c_int32),
+                ("lane_words", ctypes.c_int32), ("threads", ctypes.c_int32),
+                ("block_bytes_hint", ctypes.c_int64), ("kernel", ctypes.c_int32),
+                ("goal_order", ctypes.c_int32)]
+
+
+class xslp_stats(ctypes.Structure):
+    _fields_ = [("n_const", ctypes.c_int32), ("n_goals", ctypes.c_int32),
+                ("xor_count", ctypes.c_int64), ("mem_count", ctypes.c_int64),
+                ("n_instr", ctypes.c_int32), ("nvar", ctypes.c_int32),
+                ("maxlive", ctypes.c_int32), ("n_copy_goals", ctypes.c_int32),
+                ("n_zero_goals", ctypes.c_int32), ("regs", ctypes.c_int32),
+                ("spill_bytes", ctypes.c_int32), ("compile_ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_P = ctypes.c_void_p
+_sig = {
+    "xslp_default_opts": (None, [ctypes.POINTER(xslp_opts)]),
+    "xslp_coding_matrix": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]),
+    "xslp_encode_bitmatrix": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P]),
+    "xslp_decode_bitmatrix": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int, _P, _P]),
+    "xslp_compile": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(xslp_opts),
+                                    ctypes.POINTER(_P)]),
+    "xslp_compile_text": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(xslp_opts),
+                                         ctypes.POINTER(_P)]),
+    "xslp_program_stats": (ctypes.c_int, [_P, ctypes.POINTER(xslp_stats)]),
+    "xslp_program_dump": (ctypes.c_int64, [_P, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t]),
+    "xslp_free": (None, [_P]),
+    "xslp_encode": (ctypes.c_int, [_P, _P, _P, ctypes.c_size_t, _P]),
+    "xslp_decode": (ctypes.c_int, [_P, _P, _P, ctypes.c_size_t, _P]),
+    "xslp_encode_batch": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_size_t, _P]),
+    "xslp_decode_batch_multi": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int,
+                                               ctypes.c_size_t, _P]),
+    "xslp_encode_host": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_size_t, _P]),
+    "xslp_fill_random": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_size_t,
+                                        ctypes.c_uint64, ctypes.c_int64, _P]),
+    "xslp_launch_count": (ctypes.c_int64, []),
+    "xslp_last_error": (ctypes.c_char_p, []),
+    "xslp_version": (ctypes.c_char_p, []),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_sig)
+
+
+class XslpError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def _check(rc):
+    if rc < 0:
+        raise XslpError(rc, _lib.xslp_last_error().decode())
+    return rc
+
+
+def _ptr(x):
+    """Address of a torch tensor / numpy array / integer / None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    raise TypeError(f"cannot take the address of {type(x)}")
+
+
+def _stream(s):
+    if s is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else 0
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def default_opts(**kw):
+    o = xslp_opts()
+    _lib.xslp_default_opts(ctypes.byref(o))
+    for k, v in kw.items():
+        if k == "compress" and isinstance(v, str):
+            v = COMPRESS[v]
+        if k == "kernel" and isinstance(v, str):
+            v = KERNELS[v]
+        if not hasattr(o, k):
+            raise TypeError(f"unknown option {k}")
+        setattr(o, k, int(v))
+    return o
+
+
+class Program:
+    """An immutable compiled program (owns an ``xslp_program*``)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stats(self):
+        s = xslp_stats()
+        _check(_lib.xslp_program_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def dump(self, form=0):
+        n = _check(_lib.xslp_program_dump(self._h, form, None, 0))
+        buf = ctypes.create_string_buffer(n + 1)
+        _check(_lib.xslp_program_dump(self._h, form, buf, n + 1))
+        return buf.value.decode()
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _lib.xslp_free(h)
+
+
+# ---- matrices -----------------------------------------------------------------------
+def xslp_coding_matrix(n, p, kind="isal"):
+    out = np.zeros((n + p, n), dtype=np.uint8)
+    _check(_lib.xslp_coding_matrix(n, p, KINDS.get(kind, kind), out.ctypes.data))
+    return out
+
+
+def xslp_encode_bitmatrix(gf, n, p):
+    gf = np.ascontiguousarray(gf, dtype=np.uint8)
+    out = np.zeros((8 * p, 8 * n), dtype=np.uint8)
+    _check(_lib.xslp_encode_bitmatrix(gf.ctypes.data, n, p, out.ctypes.data))
+    return out
+
+
+def xslp_decode_bitmatrix(gf, n, p, erased):
+    gf = np.ascontiguousarray(gf, dtype=np.uint8)
+    er = np.ascontiguousarray(list(erased), dtype=np.int32)
+    out = np.zeros((8 * len(er), 8 * n), dtype=np.uint8)
+    surv = np.zeros(n, dtype=np.int32)
+    _check(_lib.xslp_decode_bitmatrix(gf.ctypes.data, n, p, er.ctypes.data if len(er) else None,
+                                      len(er), out.ctypes.data, surv.ctypes.data))
+    return out, surv
+
+
+# ---- compile ------------------------------------------------------------------------
+def xslp_compile(bits, opts=None, **kw):
+    bits = np.ascontiguousarray(bits, dtype=np.uint8)
+    o = opts if opts is not None else default_opts(**kw)
+    h = _P()
+    _check(_lib.xslp_compile(bits.ctypes.data if bits.size else None, bits.shape[0], bits.shape[1],
+                             ctypes.byref(o), ctypes.byref(h)))
+    return Program(h.value)
+
+
+def xslp_compile_text(text, n_const, opts=None, **kw):
+    o = opts if opts is not None else default_opts(**kw)
+    h = _P()
+    _check(_lib.xslp_compile_text(text.encode(), n_const, ctypes.byref(o), ctypes.byref(h)))
+    return Program(h.value)
+
+
+# ---- device -------------------------------------------------------------------------
+def _ptr_array(ptrs):
+    arr = (ctypes.c_void_p * max(1, len(ptrs)))(*[_ptr(p) for p in ptrs])
+    return arr
+
+
+def xslp_encode(prog, in_blocks, out_blocks, block_bytes, stream=None):
+    a, b = _ptr_array(in_blocks), _ptr_array(out_blocks)
+    _check(_lib.xslp_encode(prog.handle, a, b, block_bytes, _stream(stream)))
+
+
+def xslp_decode(prog, in_blocks, out_blocks, block_bytes, stream=None):
+    a, b = _ptr_array(in_blocks), _ptr_array(out_blocks)
+    _check(_lib.xslp_decode(prog.handle, a, b, block_bytes, _stream(stream)))
+
+
+def xslp_encode_batch(prog, d_in_tbl, d_out_tbl, nstripes, block_bytes, stream=None):
+    _check(_lib.xslp_encode_batch(prog.handle, _ptr(d_in_tbl), _ptr(d_out_tbl), nstripes,
+                                  block_bytes, _stream(stream)))
+
+
+def xslp_decode_batch_multi(progs, d_prog_of_stripe, d_in_tbl, d_out_tbl, nstripes, block_bytes,
+                            stream=None):
+    arr = (ctypes.c_void_p * len(progs))(*[p.handle for p in progs])
+    _check(_lib.xslp_decode_batch_multi(arr, len(progs), _ptr(d_prog_of_stripe), _ptr(d_in_tbl),
+                                        _ptr(d_out_tbl), nstripes, block_bytes, _stream(stream)))
+
+
+def xslp_encode_host(prog, h_in, h_out, nstripes, block_bytes, stream=None):
+    _check(_lib.xslp_encode_host(prog.handle, _ptr(h_in), _ptr(h_out), nstripes, block_bytes,
+                                 _stream(stream)))
+
+
+def xslp_fill_random(d_buf, nstripes, nblocks, block_bytes, seed, stripe0=0, stream=None):
+    _check(_lib.xslp_fill_random(_ptr(d_buf), nstripes, nblocks, block_bytes, seed, stripe0,
+                                 _stream(stream)))
+
+
+def xslp_launch_count():
+    return _lib.xslp_launch_count()
+
+
+def xslp_version():
+    return _lib.xslp_version().decode()
+
+
+def block_table(base, nstripes, nblocks, block_bytes, device=None):
+    """Device pointer table [nstripes][nblocks] for a contiguous
+    [nstripes][nblocks][block_bytes] buffer starting at ``base`` (torch int64 tensor)."""
+    import torch
+    b = _ptr(base)
+    idx = torch.arange(nstripes * nblocks, dtype=torch.int64)
+    tbl = idx * int(block_bytes) + int(b)
+    return tbl.to(device if device is not None else "cuda")
+
+
+def compile_many(bits_list, workers=None, **kw):
+    """Compile several bitmatrices concurrently (the C++ compiler runs outside the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    workers = workers or min(32, os.cpu_count() or 1)
+    o = default_opts(**kw)
+    with ThreadPoolExecutor(workers) as ex:
+        return list(ex.map(lambda b: xslp_compile(b, opts=o), bits_list))

@@ -1,0 +1,259 @@
+// C ABI: host entry points (matrices, compile, stats, dump, errors).
+// Device entry points live in device.cu.
+#include <algorithm>
+#include <chrono>
+#include <set>
+
+#include "xslp_internal.h"
+
+namespace xslp {
+static thread_local std::string g_err;
+void set_last_error(const std::string &m) { g_err = m; }
+}  // namespace xslp
+
+using namespace xslp;
+
+#define API_BEGIN try {
+#define API_END                                        \
+  }                                                    \
+  catch (const Error &e) {                             \
+    set_last_error(e.what());                          \
+    return e.code;                                     \
+  }                                                    \
+  catch (const std::bad_alloc &) {                     \
+    set_last_error("out of host memory");              \
+    return XSLP_ENOMEM;                                \
+  }                                                    \
+  catch (const std::exception &e) {                    \
+    set_last_error(e.what());                          \
+    return XSLP_EINVAL;                                \
+  }                                                    \
+  return XSLP_OK;
+
+extern "C" void xslp_default_opts(xslp_opts *o) {
+  if (!o) return;
+  o->compress = XSLP_COMPRESS_XORREPAIR;
+  o->fuse = 1;
+  o->schedule = XSLP_SCHED_DFS;
+  o->specialise = 1;
+  o->lane_words = 1;
+  o->threads = 256;
+  o->block_bytes_hint = 0;
+  o->kernel = XSLP_KERNEL_AUTO;
+  o->goal_order = 0;
+}
+
+extern "C" int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out) {
+  API_BEGIN
+  if (!gf_out || n < 1 || p < 0 || n + p > 255) throw Error(XSLP_EINVAL, "bad (n, p)");
+  auto g = gf::coding_matrix(n, p, kind);
+  std::copy(g.begin(), g.end(), gf_out);
+  API_END
+}
+
+extern "C" int xslp_encode_bitmatrix(const uint8_t *gf_in, int n, int p, uint8_t *bits_out) {
+  API_BEGIN
+  if (!gf_in || !bits_out || n < 1 || p < 0 || n + p > 255) throw Error(XSLP_EINVAL, "bad (n, p)");
+  std::vector<uint8_t> r(gf_in + (size_t)n * n, gf_in + (size_t)(n + p) * n);
+  auto b = gf::to_bits(r, p, n);
+  std::copy(b.begin(), b.end(), bits_out);
+  API_END
+}
+
+extern "C" int xslp_decode_bitmatrix(const uint8_t *g, int n, int p, const int32_t *erased, int ne,
+                                     uint8_t *bits_out, int32_t *survivors_out) {
+  API_BEGIN
+  if (!g || !bits_out || !survivors_out || n < 1 || p < 0 || n + p > 255 || ne < 0 ||
+      (ne > 0 && !erased))
+    throw Error(XSLP_EINVAL, "bad arguments");
+  if (ne > p) throw Error(XSLP_EUNRECOVERABLE, "more erasures than parity blocks");
+  std::set<int> es;
+  for (int i = 0; i < ne; ++i) {
+    if (erased[i] < 0 || erased[i] >= n + p) throw Error(XSLP_EINVAL, "erasure index out of range");
+    if (!es.insert(erased[i]).second) throw Error(XSLP_EINVAL, "duplicate erasure index");
+  }
+  std::vector<int> surv;
+  for (int i = 0; i < n + p && (int)surv.size() < n; ++i)
+    if (!es.count(i)) surv.push_back(i);
+  std::vector<uint8_t> M((size_t)n * n);
+  for (int r = 0; r < n; ++r)
+    for (int c = 0; c < n; ++c) M[r * n + c] = g[(size_t)surv[r] * n + c];
+  auto Mi = gf::invert(M, n);
+  std::vector<uint8_t> rows;
+  for (int e : es) {
+    if (e < n) {
+      rows.insert(rows.end(), Mi.begin() + (size_t)e * n, Mi.begin() + (size_t)(e + 1) * n);
+    } else {
+      for (int c = 0; c < n; ++c) {
+        uint8_t s = 0;
+        for (int k = 0; k < n; ++k) s ^= gf::mul(g[(size_t)e * n + k], Mi[(size_t)k * n + c]);
+        rows.push_back(s);
+      }
+    }
+  }
+  auto b = gf::to_bits(rows, ne, n);
+  std::copy(b.begin(), b.end(), bits_out);
+  std::copy(surv.begin(), surv.end(), survivors_out);
+  API_END
+}
+
+namespace {
+
+void finish(Program &P, const std::vector<Bits> *want) {
+  auto t0 = std::chrono::steady_clock::now();
+  const xslp_opts &o = P.opts;
+  if (o.fuse) fuse(P.slp);
+  if (o.schedule == XSLP_SCHED_DFS) schedule_dfs(P.slp, o.goal_order);
+  if (want) {  // the compiler checks its own output against the goal sets
+    auto got = evaluate(P.slp);
+    if (got.size() != want->size()) throw Error(XSLP_EINVAL, "internal: goal count changed");
+    for (size_t i = 0; i < got.size(); ++i)
+      if (!(got[i] == (*want)[i])) throw Error(XSLP_EINVAL, "internal: compiled SLP differs from its input");
+  }
+  if (o.schedule == XSLP_SCHED_DFS) {
+    P.nvar = paper_pebbles(P.slp, P.pebble);
+  } else {
+    P.pebble.clear();
+    P.nvar = P.slp.n_vars;
+  }
+  int maxlive = 0;
+  build_bytecode(P.slp, P.code, P.nslots, maxlive);
+  auto &st = P.stats;
+  st.n_const = P.n_const;
+  st.n_goals = P.n_goals;
+  st.xor_count = st.mem_count = 0;
+  for (auto &in : P.slp.ins) {
+    st.xor_count += (int64_t)in.ops.size() - 1;
+    st.mem_count += (int64_t)in.ops.size() + 1;
+  }
+  st.n_instr = (int)P.slp.ins.size();
+  st.nvar = P.nvar;
+  st.maxlive = maxlive;
+  st.n_copy_goals = st.n_zero_goals = 0;
+  for (int g : P.slp.goal) {
+    if (g < 0) st.n_zero_goals++;
+    else if (g < P.n_const) st.n_copy_goals++;
+  }
+  st.regs = st.spill_bytes = 0;
+  const bool device_ok = P.n_const % 8 == 0 && P.n_goals % 8 == 0 && P.n_const > 0 &&
+                         P.n_const / 8 + P.n_goals / 8 <= 128;
+  if (o.specialise && device_ok) {
+    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads);
+    P.cubin_generic = ptx_to_cubin(P.ptx_generic, &st.regs, &st.spill_bytes);
+    if (o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0) {
+      P.baked_strip = o.block_bytes_hint / 8;
+      P.ptx_baked = emit_ptx(P.slp, o.lane_words, P.baked_strip, o.threads);
+      P.cubin_baked = ptx_to_cubin(P.ptx_baked, &st.regs, &st.spill_bytes);
+    }
+  }
+  st.compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void check_opts(const xslp_opts &o) {
+  if (o.compress < 0 || o.compress > 2) throw Error(XSLP_EINVAL, "bad compress option");
+  if (o.schedule < 0 || o.schedule > 1) throw Error(XSLP_EINVAL, "bad schedule option");
+  if (o.lane_words != 1 && o.lane_words != 2 && o.lane_words != 4)
+    throw Error(XSLP_EINVAL, "lane_words must be 1, 2 or 4");
+  if (o.threads < 32 || o.threads > 1024 || o.threads % 32) throw Error(XSLP_EINVAL, "bad threads");
+  if (o.kernel < 0 || o.kernel > 2) throw Error(XSLP_EINVAL, "bad kernel option");
+}
+
+}  // namespace
+
+extern "C" int xslp_compile(const uint8_t *bits, int out_rows, int in_cols, const xslp_opts *opts,
+                            xslp_program **out) {
+  API_BEGIN
+  if (!out) throw Error(XSLP_EINVAL, "null out");
+  *out = nullptr;
+  if (!bits && out_rows * in_cols > 0) throw Error(XSLP_EINVAL, "null bitmatrix");
+  if (out_rows < 0 || in_cols <= 0 || in_cols > 512 || out_rows > 4096)
+    throw Error(XSLP_EINVAL, "bitmatrix shape out of range");
+  auto t0 = std::chrono::steady_clock::now();
+  auto P = std::make_unique<Program>();
+  if (opts) P->opts = *opts; else xslp_default_opts(&P->opts);
+  check_opts(P->opts);
+  P->n_const = in_cols;
+  P->n_goals = out_rows;
+  std::vector<Bits> goals(out_rows, Bits(in_cols));
+  for (int r = 0; r < out_rows; ++r)
+    for (int c = 0; c < in_cols; ++c) {
+      uint8_t b = bits[(size_t)r * in_cols + c];
+      if (b > 1) throw Error(XSLP_EINVAL, "bitmatrix entries must be 0 or 1");
+      if (b) goals[r].set(c);
+    }
+  if (P->opts.compress == XSLP_COMPRESS_NONE)
+    P->slp = lift(goals, in_cols, P->opts.fuse != 0);
+  else
+    P->slp = compress(goals, in_cols, P->opts.compress == XSLP_COMPRESS_XORREPAIR);
+  P->stats.compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  finish(*P, &goals);
+  *out = reinterpret_cast<xslp_program *>(P.release());
+  API_END
+}
+
+extern "C" int xslp_compile_text(const char *text, int n_const, const xslp_opts *opts,
+                                 xslp_program **out) {
+  API_BEGIN
+  if (!out || !text || n_const <= 0 || n_const > 512) throw Error(XSLP_EINVAL, "bad arguments");
+  *out = nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto P = std::make_unique<Program>();
+  if (opts) P->opts = *opts; else xslp_default_opts(&P->opts);
+  check_opts(P->opts);
+  Slp s = parse_text(text, n_const);
+  auto goals = evaluate(s);
+  P->n_const = n_const;
+  P->n_goals = (int)goals.size();
+  if (P->opts.compress == XSLP_COMPRESS_NONE) P->slp = s;
+  else P->slp = compress(goals, n_const, P->opts.compress == XSLP_COMPRESS_XORREPAIR);
+  P->stats.compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  finish(*P, &goals);
+  *out = reinterpret_cast<xslp_program *>(P.release());
+  API_END
+}
+
+extern "C" int xslp_program_stats(const xslp_program *prog, xslp_stats *st) {
+  API_BEGIN
+  if (!prog || !st) throw Error(XSLP_EINVAL, "null argument");
+  *st = reinterpret_cast<const Program *>(prog)->stats;
+  API_END
+}
+
+extern "C" int64_t xslp_program_dump(const xslp_program *prog, int form, char *buf, size_t cap) {
+  try {
+    if (!prog) throw Error(XSLP_EINVAL, "null program");
+    const Program &P = *reinterpret_cast<const Program *>(prog);
+    std::string s;
+    if (form == 0) {
+      s = "# xslp program: n_const=" + std::to_string(P.n_const) + " n_goals=" +
+          std::to_string(P.n_goals) + " xor=" + std::to_string(P.stats.xor_count) + " mem=" +
+          std::to_string(P.stats.mem_count) + " instr=" + std::to_string(P.stats.n_instr) +
+          " nvar=" + std::to_string(P.stats.nvar) + " maxlive=" + std::to_string(P.stats.maxlive) + "\n";
+      s += dump_pebbles(P.slp, P.pebble);
+    } else if (form == 1) {
+      s = dump_slots(P.code, P.n_const);
+    } else if (form == 2) {
+      s = P.ptx_baked.empty() ? P.ptx_generic : P.ptx_baked;
+    } else {
+      throw Error(XSLP_EINVAL, "bad dump form");
+    }
+    if (buf && cap) {
+      size_t k = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), k);
+      buf[k] = 0;
+    }
+    return (int64_t)s.size();
+  } catch (const Error &e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception &e) {
+    set_last_error(e.what());
+    return XSLP_EINVAL;
+  }
+}
+
+extern "C" void xslp_free(xslp_program *prog) { delete reinterpret_cast<Program *>(prog); }
+
+extern "C" const char *xslp_last_error(void) { return g_err.c_str(); }
+
+extern "C" const char *xslp_version(void) { return "xslp 0.1 (sm_100a)"; }

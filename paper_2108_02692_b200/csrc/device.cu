@@ -1,0 +1,542 @@
+// Device side of libxslp: the generic SLP interpreter kernel, the seeded fill kernel,
+// loading of the JIT-compiled straight-line kernels, and the C-ABI launch entry
+// points (xslp_encode / decode / *_batch / decode_batch_multi / encode_host).
+//
+// Hot path: H8 load strips -> H9 execute the scheduled MultiSLP -> H10 store goals
+// -> H11 grid over (stripe x tile); the paper's blocked loop
+// "for i in 0..len/B { v1[i] = xor(...) ... }" ([Peb]) becomes one
+// thread per word position, registers (straight-line) or shared-memory slots
+// (interpreter) standing in for the paper's L1-resident blocks.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+
+#include "xslp_internal.h"
+
+namespace xslp {
+
+static std::atomic<int64_t> g_launches{0};
+
+#define CUDA_OK(x)                                                                      \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      throw Error(XSLP_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+// ---------------------------------------------------------------------------------
+// Interpreter kernel (A29: "run optimized SLPs line-by-line ... in the interpreter
+// style").  One thread = one 32-bit word position of every strip of one
+// stripe.  Slot s of the thread lives at smem[s * blockDim.x + tid] (bank-conflict
+// free); bytecode format in compiler.cpp build_bytecode().  Each CTA reads its own
+// program, so one launch can run a different program per stripe (cfg3).
+struct OnePtrs {
+  const uint8_t *p[128];
+};
+
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+__global__ void __launch_bounds__(1024) xslp_interp_kernel(
+    const uint16_t *__restrict__ code_pool, const int64_t *__restrict__ prog_off,
+    const int32_t *__restrict__ prog_of_stripe, const uint8_t *const *__restrict__ in_tbl,
+    uint8_t *const *__restrict__ out_tbl, int n_in, int n_out, uint64_t strip, uint32_t words,
+    uint32_t stripe_base, OnePtrs one) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t T = blockDim.x;
+  const uint32_t w = blockIdx.x * T + threadIdx.x;
+  if (w >= words) return;
+  const uint32_t s = blockIdx.y + stripe_base;
+  const int prog = prog_of_stripe ? prog_of_stripe[s] : 0;
+  const uint16_t *code = code_pool + prog_off[prog];
+  uint32_t *my = sm + threadIdx.x;
+  const uint8_t *const *in;
+  uint8_t *const *out;
+  if (in_tbl) {
+    in = in_tbl + (size_t)s * n_in;
+    out = out_tbl + (size_t)s * n_out;
+  } else {
+    in = one.p;
+    out = (uint8_t *const *)(one.p + n_in);
+  }
+  const size_t off = (size_t)w * 4;
+  int pc = 0;
+  const int nl = code[pc++];
+  int i = 0;
+  for (; i + 8 <= nl; i += 8) {  // batches of 8 independent loads in flight
+    uint32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = code[pc + 2 * (i + u)];
+      v[u] = ld_stream((const uint32_t *)(in[c >> 3] + (c & 7) * strip + off));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) my[code[pc + 2 * (i + u) + 1] * T] = v[u];
+  }
+  for (; i < nl; ++i) {
+    const int c = code[pc + 2 * i];
+    my[code[pc + 2 * i + 1] * T] = ld_stream((const uint32_t *)(in[c >> 3] + (c & 7) * strip + off));
+  }
+  pc += 2 * nl;
+  const int ni = code[pc++];
+  for (int k = 0; k < ni; ++k) {
+    const int hdr = code[pc++];
+    const int arity = hdr & 0xfff;
+    const int dst = (hdr & 0x8000) ? code[pc++] : -1;
+    const int ng = code[pc++];
+    const int gp = pc;
+    pc += ng;
+    uint32_t acc = 0;
+    int a = 0;
+    for (; a + 2 <= arity; a += 2) acc ^= my[code[pc + a] * T] ^ my[code[pc + a + 1] * T];
+    if (a < arity) acc ^= my[code[pc + a] * T];
+    pc += arity;
+    if (dst >= 0) my[dst * T] = acc;
+    for (int g = 0; g < ng; ++g) {
+      const int gi = code[gp + g];
+      __stcs((uint32_t *)(out[gi >> 3] + (gi & 7) * strip + off), acc);
+    }
+  }
+}
+
+// Seeded synthetic bytes (same counter-based generator as synth/__init__.py).
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void xslp_fill_kernel(uint64_t *buf, uint64_t wpb, int nblocks, uint64_t total,
+                                 uint64_t seed, int64_t stripe0) {
+  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t w = idx % wpb, blk = idx / wpb;
+    const uint64_t s = blk / nblocks + (uint64_t)stripe0, j = blk % nblocks;
+    const uint64_t base = seed * 0x9E3779B97F4A7C15ull + ((s * 64 + j) << 40);
+    buf[idx] = splitmix64(base + w);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Per-program device state.
+struct Program::Dev {
+  uint16_t *d_code = nullptr;
+  int64_t *d_off = nullptr;
+};
+
+struct JitLib {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t batch = nullptr, one = nullptr;
+};
+
+// Libraries are context independent (cudaLibraryLoadData); keyed by program serial.
+static std::mutex g_mu;
+static std::map<const Program *, std::pair<JitLib, JitLib>> g_libs;
+
+static void load_lib(const std::vector<char> &cubin, JitLib &L) {
+  if (cubin.empty() || L.lib) return;
+  CUDA_OK(cudaLibraryLoadData(&L.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+  CUDA_OK(cudaLibraryGetKernel(&L.batch, L.lib, "xslp_sl_batch"));
+  CUDA_OK(cudaLibraryGetKernel(&L.one, L.lib, "xslp_sl_one"));
+}
+
+static std::pair<JitLib, JitLib> libs_of(const Program *p) {
+  std::lock_guard<std::mutex> g(g_mu);
+  auto &e = g_libs[p];
+  load_lib(p->cubin_generic, e.first);
+  load_lib(p->cubin_baked, e.second);
+  return e;
+}
+
+static int current_device() {
+  int d = -1;
+  CUDA_OK(cudaGetDevice(&d));
+  return d;
+}
+
+static std::shared_ptr<Program::Dev> dev_of(const Program *p) {
+  const int d = current_device();
+  std::lock_guard<std::mutex> g(p->mu);
+  auto &e = p->dev[d];
+  if (!e) {
+    auto D = std::make_shared<Program::Dev>();
+    CUDA_OK(cudaMalloc(&D->d_code, p->code.size() * 2));
+    CUDA_OK(cudaMemcpy(D->d_code, p->code.data(), p->code.size() * 2, cudaMemcpyHostToDevice));
+    int64_t z = 0;
+    CUDA_OK(cudaMalloc(&D->d_off, 8));
+    CUDA_OK(cudaMemcpy(D->d_off, &z, 8, cudaMemcpyHostToDevice));
+    e = D;
+  }
+  return e;
+}
+
+Program::~Program() {
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_libs.find(this);
+    if (it != g_libs.end()) {
+      if (it->second.first.lib) cudaLibraryUnload(it->second.first.lib);
+      if (it->second.second.lib) cudaLibraryUnload(it->second.second.lib);
+      g_libs.erase(it);
+    }
+  }
+  int cur = -1;
+  bool have = cudaGetDevice(&cur) == cudaSuccess;
+  for (auto &kv : dev) {
+    if (!kv.second) continue;
+    cudaSetDevice(kv.first);
+    cudaFree(kv.second->d_code);
+    cudaFree(kv.second->d_off);
+  }
+  if (have) cudaSetDevice(cur);
+}
+
+// ---------------------------------------------------------------------------------
+static void check_geometry(const Program *p, size_t block_bytes) {
+  if (block_bytes % 32)
+    throw Error(XSLP_EINVAL, "block_bytes must be a multiple of 32 (strip = whole 32-bit words)");
+  if (p->n_const % 8 || p->n_goals % 8)
+    throw Error(XSLP_EINVAL, "program does not act on whole blocks");
+  if (block_bytes / 8 / 4 > 0xffffffffull) throw Error(XSLP_EINVAL, "block too large");
+}
+
+static int interp_threads(const Program *const *progs, int np, int want) {
+  int nslots = 1;
+  for (int i = 0; i < np; ++i) nslots = std::max(nslots, progs[i]->nslots);
+  const int maxsm = 227 * 1024;
+  int T = std::min(want, (maxsm / (nslots * 4)) / 32 * 32);
+  if (T < 32) throw Error(XSLP_EINVAL, "program needs too many interpreter slots");
+  return T;
+}
+
+static void set_smem_attr() {
+  static std::mutex m;
+  static std::map<int, bool> done;
+  int d = current_device();
+  std::lock_guard<std::mutex> g(m);
+  if (done[d]) return;
+  CUDA_OK(cudaFuncSetAttribute(xslp_interp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               227 * 1024));
+  done[d] = true;
+}
+
+// Launch the interpreter over `nstripes` stripes (tables) or one stripe (one != null).
+static void launch_interp(const uint16_t *code_pool, const int64_t *offs, const int32_t *pos,
+                          int np_threads_T, const Program *p0, int nslots_max,
+                          const uint8_t *const *in_tbl, uint8_t *const *out_tbl, int nstripes,
+                          size_t block_bytes, cudaStream_t st, const OnePtrs *one) {
+  set_smem_attr();
+  const uint64_t strip = block_bytes / 8;
+  const uint32_t words = (uint32_t)(strip / 4);
+  const int T = np_threads_T;
+  const size_t smem = (size_t)nslots_max * T * 4;
+  OnePtrs op{};
+  if (one) op = *one;
+  for (int base = 0; base < nstripes; base += 65535) {
+    dim3 grid((words + T - 1) / T, std::min(65535, nstripes - base));
+    xslp_interp_kernel<<<grid, T, smem, st>>>(code_pool, offs, pos, in_tbl, out_tbl,
+                                              p0->n_const / 8, p0->n_goals / 8, strip, words,
+                                              (uint32_t)base, op);
+    CUDA_OK(cudaGetLastError());
+    g_launches++;
+  }
+}
+
+static bool can_straight(const Program *p, size_t block_bytes, bool &baked) {
+  const int L = p->opts.lane_words;
+  const uint64_t strip = block_bytes / 8;
+  baked = !p->cubin_baked.empty() && (int64_t)strip == p->baked_strip;
+  if (p->cubin_generic.empty() && !baked) return false;
+  return strip % (4 * L) == 0;
+}
+
+static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *const *d_out,
+                        const int32_t *d_ids, int nstripes, size_t block_bytes,
+                        cudaStream_t st) {
+  check_geometry(p, block_bytes);
+  if (nstripes < 0) throw Error(XSLP_EINVAL, "nstripes < 0");
+  if (!d_in || !d_out) throw Error(XSLP_EINVAL, "null pointer table");
+  if (nstripes == 0 || block_bytes == 0) return;
+  bool baked = false;
+  const int kind = p->opts.kernel;
+  bool straight = kind != XSLP_KERNEL_INTERP && can_straight(p, block_bytes, baked);
+  if (kind == XSLP_KERNEL_STRAIGHT && !straight)
+    throw Error(XSLP_EINVAL, "straight-line kernel unavailable for this block size / program");
+  if (straight) {
+    auto libs = libs_of(p);
+    const JitLib &L = baked ? libs.second : libs.first;
+    const int T = p->opts.threads;
+    uint64_t strip = block_bytes / 8;
+    uint32_t words = (uint32_t)(strip / (4 * p->opts.lane_words));
+    for (int base = 0; base < nstripes; base += 65535) {
+      uint32_t b = (uint32_t)base;
+      void *args[] = {(void *)&d_in, (void *)&d_out, (void *)&d_ids, &strip, &words, &b};
+      dim3 grid((words + T - 1) / T, std::min(65535, nstripes - base));
+      CUDA_OK(cudaLaunchKernel((const void *)L.batch, grid, dim3(T), args, 0, st));
+      g_launches++;
+    }
+    return;
+  }
+  if (d_ids) throw Error(XSLP_EINVAL, "stripe id lists need the straight-line kernel");
+  auto D = dev_of(p);
+  const Program *ps[1] = {p};
+  const int T = interp_threads(ps, 1, p->opts.threads);
+  launch_interp(D->d_code, D->d_off, nullptr, T, p, p->nslots, d_in, d_out, nstripes,
+                block_bytes, st, nullptr);
+}
+
+static void apply_one(const Program *p, const uint8_t *const *in, uint8_t *const *out,
+                      size_t block_bytes, cudaStream_t st) {
+  check_geometry(p, block_bytes);
+  if (!in || !out) throw Error(XSLP_EINVAL, "null block pointer array");
+  const int n_in = p->n_const / 8, n_out = p->n_goals / 8;
+  if (n_in + n_out > 128) throw Error(XSLP_EINVAL, "too many blocks");
+  OnePtrs one{};
+  for (int j = 0; j < n_in; ++j) {
+    if (!in[j] || ((uintptr_t)in[j] & 15)) throw Error(XSLP_EINVAL, "input block pointer null or not 16-byte aligned");
+    one.p[j] = in[j];
+  }
+  for (int i = 0; i < n_out; ++i) {
+    if (!out[i] || ((uintptr_t)out[i] & 15)) throw Error(XSLP_EINVAL, "output block pointer null or not 16-byte aligned");
+    one.p[n_in + i] = out[i];
+  }
+  if (block_bytes == 0) return;
+  bool baked = false;
+  const int kind = p->opts.kernel;
+  bool straight = kind != XSLP_KERNEL_INTERP && can_straight(p, block_bytes, baked);
+  if (kind == XSLP_KERNEL_STRAIGHT && !straight)
+    throw Error(XSLP_EINVAL, "straight-line kernel unavailable for this block size / program");
+  if (straight) {
+    auto libs = libs_of(p);
+    const JitLib &L = baked ? libs.second : libs.first;
+    const int T = p->opts.threads;
+    uint64_t strip = block_bytes / 8;
+    uint32_t words = (uint32_t)(strip / (4 * p->opts.lane_words));
+    void *args[] = {&one, &strip, &words};
+    CUDA_OK(cudaLaunchKernel((const void *)L.one, dim3((words + T - 1) / T), dim3(T), args, 0, st));
+    g_launches++;
+    return;
+  }
+  auto D = dev_of(p);
+  const Program *ps[1] = {p};
+  const int T = interp_threads(ps, 1, p->opts.threads);
+  launch_interp(D->d_code, D->d_off, nullptr, T, p, p->nslots, nullptr, nullptr, 1, block_bytes,
+                st, &one);
+}
+
+// Pools of several programs' bytecode for one heterogeneous launch, cached by the
+// programs' identities per device.
+struct Pool {
+  uint16_t *code = nullptr;
+  int64_t *off = nullptr;
+};
+static std::map<std::pair<int, std::vector<const Program *>>, Pool> g_pools;
+
+static Pool pool_of(const Program *const *progs, int np) {
+  const int d = current_device();
+  std::vector<const Program *> key(progs, progs + np);
+  std::lock_guard<std::mutex> g(g_mu);
+  auto it = g_pools.find({d, key});
+  if (it != g_pools.end()) return it->second;
+  std::vector<uint16_t> all;
+  std::vector<int64_t> off;
+  for (int i = 0; i < np; ++i) {
+    off.push_back((int64_t)all.size());
+    all.insert(all.end(), progs[i]->code.begin(), progs[i]->code.end());
+  }
+  Pool P;
+  CUDA_OK(cudaMalloc(&P.code, all.size() * 2));
+  CUDA_OK(cudaMemcpy(P.code, all.data(), all.size() * 2, cudaMemcpyHostToDevice));
+  CUDA_OK(cudaMalloc(&P.off, off.size() * 8));
+  CUDA_OK(cudaMemcpy(P.off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+  g_pools[{d, key}] = P;
+  return P;
+}
+
+// ---------------------------------------------------------------------------------
+// Host-buffer path: chunks of stripes staged through two device buffer sets on two
+// internal streams so the H2D copy of chunk c+1 overlaps the kernel and D2H of chunk c.
+struct HostWs {
+  size_t cap_in = 0, cap_out = 0;
+  uint8_t *din[2] = {nullptr, nullptr}, *dout[2] = {nullptr, nullptr};
+  const uint8_t **tin[2] = {nullptr, nullptr};
+  uint8_t **tout[2] = {nullptr, nullptr};
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t ev = nullptr;
+  int n_in = -1, n_out = -1, chunk = -1;
+  size_t B = 0;
+};
+static std::map<int, HostWs> g_ws;
+
+static void host_apply(const Program *p, const uint8_t *h_in, uint8_t *h_out, int nstripes,
+                       size_t B, cudaStream_t user) {
+  check_geometry(p, B);
+  if (nstripes < 0) throw Error(XSLP_EINVAL, "nstripes < 0");
+  if (!h_in || !h_out) throw Error(XSLP_EINVAL, "null host buffer");
+  if (nstripes == 0 || B == 0) return;
+  const int d = current_device();
+  const int n_in = p->n_const / 8, n_out = p->n_goals / 8;
+  const size_t target = (size_t)256 << 20;
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>(nstripes, target / (n_in * B)));
+  std::lock_guard<std::mutex> g(g_mu);
+  HostWs &w = g_ws[d];
+  if (!w.st[0]) {
+    CUDA_OK(cudaStreamCreateWithFlags(&w.st[0], cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&w.st[1], cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&w.ev, cudaEventDisableTiming));
+  }
+  const size_t need_in = (size_t)chunk * n_in * B, need_out = (size_t)chunk * n_out * B;
+  if (need_in > w.cap_in || need_out > w.cap_out) {
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(w.din[b]);
+      cudaFree(w.dout[b]);
+      CUDA_OK(cudaMalloc(&w.din[b], need_in));
+      CUDA_OK(cudaMalloc(&w.dout[b], need_out));
+    }
+    w.cap_in = need_in;
+    w.cap_out = need_out;
+    w.n_in = -1;
+  }
+  if (w.n_in != n_in || w.n_out != n_out || w.chunk != chunk || w.B != B) {
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(w.tin[b]);
+      cudaFree(w.tout[b]);
+      std::vector<const uint8_t *> ti((size_t)chunk * n_in);
+      std::vector<uint8_t *> to((size_t)chunk * n_out);
+      for (size_t i = 0; i < ti.size(); ++i) ti[i] = w.din[b] + i * B;
+      for (size_t i = 0; i < to.size(); ++i) to[i] = w.dout[b] + i * B;
+      CUDA_OK(cudaMalloc(&w.tin[b], ti.size() * 8));
+      CUDA_OK(cudaMalloc(&w.tout[b], to.size() * 8));
+      CUDA_OK(cudaMemcpy(w.tin[b], ti.data(), ti.size() * 8, cudaMemcpyHostToDevice));
+      CUDA_OK(cudaMemcpy(w.tout[b], to.data(), to.size() * 8, cudaMemcpyHostToDevice));
+    }
+    w.n_in = n_in;
+    w.n_out = n_out;
+    w.chunk = chunk;
+    w.B = B;
+  }
+  CUDA_OK(cudaEventRecord(w.ev, user));
+  CUDA_OK(cudaStreamWaitEvent(w.st[0], w.ev, 0));
+  CUDA_OK(cudaStreamWaitEvent(w.st[1], w.ev, 0));
+  int c = 0;
+  for (int s0 = 0; s0 < nstripes; s0 += chunk, ++c) {
+    const int b = c & 1;
+    const int ns = std::min(chunk, nstripes - s0);
+    CUDA_OK(cudaMemcpyAsync(w.din[b], h_in + (size_t)s0 * n_in * B, (size_t)ns * n_in * B,
+                            cudaMemcpyHostToDevice, w.st[b]));
+    apply_batch(p, w.tin[b], w.tout[b], nullptr, ns, B, w.st[b]);
+    CUDA_OK(cudaMemcpyAsync(h_out + (size_t)s0 * n_out * B, w.dout[b], (size_t)ns * n_out * B,
+                            cudaMemcpyDeviceToHost, w.st[b]));
+  }
+  CUDA_OK(cudaStreamSynchronize(w.st[0]));
+  CUDA_OK(cudaStreamSynchronize(w.st[1]));
+}
+
+}  // namespace xslp
+
+// =====================================================================================
+// C ABI (device entry points)
+using namespace xslp;
+
+#define API_BEGIN try {
+#define API_END                                        \
+  }                                                    \
+  catch (const Error &e) {                             \
+    set_last_error(e.what());                          \
+    return e.code;                                     \
+  }                                                    \
+  catch (const std::bad_alloc &) {                     \
+    set_last_error("out of host memory");              \
+    return XSLP_ENOMEM;                                \
+  }                                                    \
+  catch (const std::exception &e) {                    \
+    set_last_error(e.what());                          \
+    return XSLP_EINVAL;                                \
+  }                                                    \
+  return XSLP_OK;
+
+static const Program *P(const xslp_program *p) {
+  if (!p) throw Error(XSLP_EINVAL, "null program");
+  return reinterpret_cast<const Program *>(p);
+}
+
+extern "C" int xslp_encode(const xslp_program *prog, const uint8_t *const *in_blocks,
+                           uint8_t *const *out_blocks, size_t block_bytes, void *stream) {
+  API_BEGIN
+  apply_one(P(prog), in_blocks, out_blocks, block_bytes, (cudaStream_t)stream);
+  API_END
+}
+
+extern "C" int xslp_decode(const xslp_program *prog, const uint8_t *const *in_blocks,
+                           uint8_t *const *out_blocks, size_t block_bytes, void *stream) {
+  return xslp_encode(prog, in_blocks, out_blocks, block_bytes, stream);
+}
+
+extern "C" int xslp_encode_batch(const xslp_program *prog, const uint8_t *const *d_in_tbl,
+                                 uint8_t *const *d_out_tbl, int nstripes, size_t block_bytes,
+                                 void *stream) {
+  API_BEGIN
+  apply_batch(P(prog), d_in_tbl, d_out_tbl, nullptr, nstripes, block_bytes, (cudaStream_t)stream);
+  API_END
+}
+
+extern "C" int xslp_decode_batch_multi(const xslp_program *const *progs, int nprogs,
+                                       const int32_t *d_prog_of_stripe,
+                                       const uint8_t *const *d_in_tbl, uint8_t *const *d_out_tbl,
+                                       int nstripes, size_t block_bytes, void *stream) {
+  API_BEGIN
+  if (!progs || nprogs <= 0) throw Error(XSLP_EINVAL, "no programs");
+  std::vector<const Program *> ps;
+  for (int i = 0; i < nprogs; ++i) ps.push_back(P(progs[i]));
+  for (auto q : ps)
+    if (q->n_const != ps[0]->n_const || q->n_goals != ps[0]->n_goals)
+      throw Error(XSLP_EINVAL, "programs disagree on constants/goals");
+  if (nprogs == 1) {
+    apply_batch(ps[0], d_in_tbl, d_out_tbl, nullptr, nstripes, block_bytes, (cudaStream_t)stream);
+  } else {
+    check_geometry(ps[0], block_bytes);
+    if (!d_prog_of_stripe || !d_in_tbl || !d_out_tbl) throw Error(XSLP_EINVAL, "null table");
+    if (nstripes < 0) throw Error(XSLP_EINVAL, "nstripes < 0");
+    if (nstripes == 0 || block_bytes == 0) return XSLP_OK;
+    Pool pool = pool_of(ps.data(), nprogs);
+    int nsl = 1;
+    for (auto q : ps) nsl = std::max(nsl, q->nslots);
+    const int T = interp_threads(ps.data(), nprogs, ps[0]->opts.threads);
+    launch_interp(pool.code, pool.off, d_prog_of_stripe, T, ps[0], nsl, d_in_tbl, d_out_tbl,
+                  nstripes, block_bytes, (cudaStream_t)stream, nullptr);
+  }
+  API_END
+}
+
+extern "C" int xslp_encode_host(const xslp_program *prog, const uint8_t *h_in, uint8_t *h_out,
+                                int nstripes, size_t block_bytes, void *stream) {
+  API_BEGIN
+  host_apply(P(prog), h_in, h_out, nstripes, block_bytes, (cudaStream_t)stream);
+  API_END
+}
+
+extern "C" int xslp_fill_random(uint8_t *d_buf, int nstripes, int nblocks, size_t block_bytes,
+                                uint64_t seed, int64_t stripe0, void *stream) {
+  API_BEGIN
+  if (!d_buf || nstripes < 0 || nblocks < 0 || block_bytes % 8 || ((uintptr_t)d_buf & 7))
+    throw Error(XSLP_EINVAL, "bad fill arguments");
+  const uint64_t wpb = block_bytes / 8;
+  const uint64_t total = wpb * (uint64_t)nblocks * (uint64_t)nstripes;
+  if (total == 0) return XSLP_OK;
+  int dev = current_device(), sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t want = (total + 255) / 256;
+  const int grid = (int)std::min<uint64_t>(want, (uint64_t)sms * 16);
+  xslp_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((uint64_t *)d_buf, wpb, nblocks, total,
+                                                          seed, stripe0);
+  CUDA_OK(cudaGetLastError());
+  g_launches++;
+  API_END
+}
+
+extern "C" int64_t xslp_launch_count(void) { return g_launches.load(); }

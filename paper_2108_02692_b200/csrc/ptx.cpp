@@ -1,0 +1,240 @@
+// Straight-line specialisation: the scheduled MultiSLP emitted as PTX for sm_100a and
+// compiled in-process to a cubin (nvPTXCompiler, no GPU needed).
+//
+// Execution model: a thread owns `lanes` consecutive 32-bit
+// words at one offset of every strip of its stripe (coalesced: a warp reads
+// 128*lanes contiguous bytes of each strip).  Constants are loaded from HBM once,
+// every variable of the SLP is a register, each variadic XOR of arity a becomes
+// ceil((a-1)/2) 3-input XORs (lop3.b32 with truth table 0x96), and each goal is stored
+// as soon as it is computed.  This is the paper's blocked interpreter loop
+// ([Peb]) with the block = one thread's words and "cache" = registers.
+//
+// Two entries per module:
+//   xslp_sl_batch(in_tbl, out_tbl, stripe_ids, strip_bytes, words, stripe_base)
+//     stripe = stripe_ids ? stripe_ids[ctaid.y + stripe_base] : ctaid.y + stripe_base;
+//     block pointers from the device tables in_tbl[stripe*n_in + j], out_tbl[stripe*n_out + i]
+//   xslp_sl_one(ptrs[128], strip_bytes, words)
+//     one stripe, pointers passed by value (in[0..n_in), out[n_in..n_in+n_out))
+// With a baked strip size the 8 strips of a block are addressed by immediate offsets.
+#include <sstream>
+
+#include <nvPTXCompiler.h>
+
+#include "xslp_internal.h"
+
+namespace xslp {
+
+namespace {
+
+struct Emitter {
+  const Slp &s;
+  int L;
+  int64_t baked;
+  int threads;
+  int n_in, n_out;
+  std::ostringstream o;
+  Emitter(const Slp &s_, int L_, int64_t baked_, int threads_)
+      : s(s_), L(L_), baked(baked_), threads(threads_), n_in(s_.n_const / 8),
+        n_out((int)(s_.goal.size() / 8)) {}
+
+  std::string creg(int c, int l) { return "%c" + std::to_string(c * L + l); }
+  std::string vreg(int v, int l) { return "%v" + std::to_string(v * L + l); }
+  std::string treg(int t, int l) { return t < s.n_const ? creg(t, l) : vreg(t - s.n_const, l); }
+
+  const char *vsuf() { return L == 1 ? ".u32" : (L == 2 ? ".v2.u32" : ".v4.u32"); }
+  std::string vec(const std::vector<std::string> &r) {
+    if (L == 1) return r[0];
+    std::string x = "{";
+    for (int l = 0; l < L; ++l) x += (l ? ", " : "") + r[l];
+    return x + "}";
+  }
+
+  // address of strip k of block register `base` (already offset by the thread's word)
+  std::string addr(const std::string &base, int k, int &tmpctr) {
+    if (k == 0) return "[" + base + "]";
+    if (baked > 0) return "[" + base + "+" + std::to_string((int64_t)k * baked) + "]";
+    std::string t = "%ta" + std::to_string(tmpctr++);
+    o << "  add.s64 " << t << ", " << base << ", %sk" << k << ";\n";
+    return "[" + t + "]";
+  }
+
+  void body(bool one) {
+    const int nc = s.n_const;
+    std::vector<char> used(nc, 0);
+    std::vector<int> last_c(nc, -1);
+    for (size_t k = 0; k < s.ins.size(); ++k)
+      for (int t : s.ins[k].ops)
+        if (t < nc) { used[t] = 1; last_c[t] = (int)k; }
+    for (int g : s.goal)
+      if (g >= 0 && g < nc) used[g] = 1;
+    std::vector<char> blk_used(n_in, 0);
+    for (int c = 0; c < nc; ++c)
+      if (used[c]) blk_used[c / 8] = 1;
+
+    o << "  mov.u32 %s0, %ctaid.x;\n  mov.u32 %s1, %ntid.x;\n  mov.u32 %s2, %tid.x;\n";
+    o << "  mad.lo.u32 %s3, %s0, %s1, %s2;\n";
+    o << "  ld.param.u32 %s4, [p_words];\n";
+    o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $DONE;\n";
+    o << "  mul.wide.u32 %off, %s3, " << 4 * L << ";\n";
+    if (baked <= 0) {
+      o << "  ld.param.u64 %sk1, [p_strip];\n";
+      for (int k = 2; k < 8; ++k) o << "  mul.lo.u64 %sk" << k << ", %sk1, " << k << ";\n";
+    }
+    if (!one) {
+      o << "  mov.u32 %s5, %ctaid.y;\n  ld.param.u32 %s6, [p_base];\n  add.u32 %s5, %s5, %s6;\n";
+      o << "  ld.param.u64 %rd0, [p_ids];\n  setp.eq.u64 %p1, %rd0, 0;\n  @%p1 bra $NOIDS;\n";
+      o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n";
+      o << "  ld.global.nc.u32 %s5, [%rd1];\n$NOIDS:\n";
+      o << "  ld.param.u64 %rd2, [p_in];\n  ld.param.u64 %rd3, [p_out];\n";
+      o << "  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
+      o << "  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+    }
+    for (int j = 0; j < n_in; ++j) {
+      if (!blk_used[j]) continue;
+      if (one) o << "  ld.param.u64 %ib" << j << ", [p_ptrs+" << 8 * j << "];\n";
+      else o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+      o << "  add.s64 %ib" << j << ", %ib" << j << ", %off;\n";
+    }
+    for (int i = 0; i < n_out; ++i) {
+      if (one) o << "  ld.param.u64 %ob" << i << ", [p_ptrs+" << 8 * (n_in + i) << "];\n";
+      else o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+      o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
+    }
+    int tmp = 0;
+    // loads: every used constant, up front (maximum memory-level parallelism; ptxas
+    // schedules them against register pressure)
+    for (int c = 0; c < nc; ++c) {
+      if (!used[c]) continue;
+      std::vector<std::string> r;
+      for (int l = 0; l < L; ++l) r.push_back(creg(c, l));
+      std::string a = addr("%ib" + std::to_string(c / 8), c % 8, tmp);
+      o << "  ld.global.nc.L1::no_allocate" << vsuf() << " " << vec(r) << ", " << a << ";\n";
+    }
+    // goals that are constants or zero
+    std::vector<std::vector<int>> goals_of_var(s.n_vars);
+    for (size_t g = 0; g < s.goal.size(); ++g) {
+      int t = s.goal[g];
+      if (t >= nc) { goals_of_var[t - nc].push_back((int)g); continue; }
+      std::vector<std::string> r;
+      for (int l = 0; l < L; ++l) r.push_back(t < 0 ? std::string("%zero") : creg(t, l));
+      store((int)g, r, tmp);
+    }
+    // the program
+    for (size_t k = 0; k < s.ins.size(); ++k) {
+      const auto &in = s.ins[k];
+      const auto &ops = in.ops;
+      for (int l = 0; l < L; ++l) {
+        std::string d = vreg(in.var, l);
+        size_t i;
+        if (ops.size() == 2) {
+          o << "  xor.b32 " << d << ", " << treg(ops[0], l) << ", " << treg(ops[1], l) << ";\n";
+          continue;
+        }
+        o << "  lop3.b32 " << d << ", " << treg(ops[0], l) << ", " << treg(ops[1], l) << ", "
+          << treg(ops[2], l) << ", 0x96;\n";
+        for (i = 3; i + 1 < ops.size(); i += 2)
+          o << "  lop3.b32 " << d << ", " << d << ", " << treg(ops[i], l) << ", "
+            << treg(ops[i + 1], l) << ", 0x96;\n";
+        if (i < ops.size()) o << "  xor.b32 " << d << ", " << d << ", " << treg(ops[i], l) << ";\n";
+      }
+      for (int g : goals_of_var[in.var]) {
+        std::vector<std::string> r;
+        for (int l = 0; l < L; ++l) r.push_back(vreg(in.var, l));
+        store(g, r, tmp);
+      }
+    }
+    o << "$DONE:\n  ret;\n";
+  }
+
+  void store(int g, const std::vector<std::string> &r, int &tmp) {
+    std::string a = addr("%ob" + std::to_string(g / 8), g % 8, tmp);
+    o << "  st.global" << vsuf() << " " << a << ", " << vec(r) << ";\n";
+  }
+
+  void decls(int ntmp_guess) {
+    o << "  .reg .pred %p<4>;\n  .reg .b32 %s<8>;\n  .reg .b64 %rd<8>;\n  .reg .b64 %off;\n";
+    o << "  .reg .b32 %zero;\n";
+    o << "  .reg .b64 %sk<8>;\n";
+    o << "  .reg .b64 %ib<" << std::max(1, n_in) << ">;\n  .reg .b64 %ob<" << std::max(1, n_out) << ">;\n";
+    o << "  .reg .b32 %c<" << std::max(1, s.n_const * L) << ">;\n";
+    o << "  .reg .b32 %v<" << std::max(1, s.n_vars * L) << ">;\n";
+    o << "  .reg .b64 %ta<" << std::max(1, ntmp_guess) << ">;\n";
+    o << "  mov.u32 %zero, 0;\n";
+  }
+
+  std::string run() {
+    o << "//\n// xslp straight-line kernel: " << s.n_const << " constants, " << s.goal.size()
+      << " goals, " << s.ins.size() << " instructions, lanes=" << L << ", strip="
+      << (baked > 0 ? std::to_string(baked) : std::string("runtime")) << "\n//\n";
+    o << ".version 8.8\n.target sm_100a\n.address_size 64\n\n";
+    const int ntmp = s.n_const + (int)s.goal.size() + 8;
+    o << ".visible .entry xslp_sl_batch(\n  .param .u64 p_in,\n  .param .u64 p_out,\n"
+         "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
+         "  .param .u32 p_base)\n.maxntid "
+      << threads << ", 1, 1\n{\n";
+    decls(ntmp);
+    body(false);
+    o << "}\n\n";
+    o << ".visible .entry xslp_sl_one(\n  .param .align 8 .b8 p_ptrs[1024],\n"
+         "  .param .u64 p_strip,\n  .param .u32 p_words)\n.maxntid "
+      << threads << ", 1, 1\n{\n";
+    decls(ntmp);
+    body(true);
+    o << "}\n";
+    return o.str();
+  }
+};
+
+}  // namespace
+
+std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads) {
+  if (s.n_const % 8 || s.goal.size() % 8)
+    throw Error(XSLP_EINVAL, "device programs need whole blocks (constants and goals multiples of 8)");
+  if (s.n_const / 8 + s.goal.size() / 8 > 128)
+    throw Error(XSLP_EINVAL, "too many blocks for one kernel (n + m > 128)");
+  Emitter e(s, lanes, baked_strip, threads);
+  return e.run();
+}
+
+std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill) {
+  nvPTXCompilerHandle h = nullptr;
+  if (nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS)
+    throw Error(XSLP_ECOMPILE, "nvPTXCompilerCreate failed");
+  const char *opts[] = {"--gpu-name=sm_100a", "-O3", "--verbose"};
+  nvPTXCompileResult r = nvPTXCompilerCompile(h, 3, opts);
+  if (r != NVPTXCOMPILE_SUCCESS) {
+    size_t n = 0;
+    nvPTXCompilerGetErrorLogSize(h, &n);
+    std::string log(n + 1, '\0');
+    if (n) nvPTXCompilerGetErrorLog(h, &log[0]);
+    nvPTXCompilerDestroy(&h);
+    throw Error(XSLP_ECOMPILE, "ptx compile failed (" + std::to_string((int)r) + "): " + log);
+  }
+  size_t n = 0;
+  nvPTXCompilerGetCompiledProgramSize(h, &n);
+  std::vector<char> bin(n);
+  nvPTXCompilerGetCompiledProgram(h, bin.data());
+  size_t ln = 0;
+  nvPTXCompilerGetInfoLogSize(h, &ln);
+  std::string info(ln + 1, '\0');
+  if (ln) nvPTXCompilerGetInfoLog(h, &info[0]);
+  nvPTXCompilerDestroy(&h);
+  // parse "Used N registers" / "N bytes spill stores" of the batch entry (first listed)
+  if (regs) {
+    *regs = 0;
+    auto p = info.find("Used ");
+    if (p != std::string::npos) *regs = std::atoi(info.c_str() + p + 5);
+  }
+  if (spill) {
+    *spill = 0;
+    auto p = info.find("bytes spill stores");
+    if (p != std::string::npos) {
+      auto q = info.rfind(',', p);
+      size_t st = (q == std::string::npos) ? 0 : q + 1;
+      *spill = std::atoi(info.c_str() + st);
+    }
+  }
+  return bin;
+}
+
+}  // namespace xslp

@@ -1,0 +1,117 @@
+// Internal declarations of libxslp (product side; shares nothing with oracle/).
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/xslp.h"
+
+namespace xslp {
+
+// ---- errors -------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+void set_last_error(const std::string &msg);
+
+// ---- GF(2^8) ---------------------------------------------------------
+namespace gf {
+uint8_t mul(uint8_t a, uint8_t b);
+uint8_t inv(uint8_t a);
+uint8_t pow(uint8_t a, int e);
+// (n+p) x n row-major coding matrix of the given family.
+std::vector<uint8_t> coding_matrix(int n, int p, int kind);
+// Gauss-Jordan inverse of an n x n matrix; throws Error(XSLP_ESINGULAR).
+std::vector<uint8_t> invert(const std::vector<uint8_t> &m, int n);
+// x~ lowering of an a x b matrix into (8a) x (8b) bits.
+std::vector<uint8_t> to_bits(const std::vector<uint8_t> &m, int a, int b);
+}  // namespace gf
+
+// ---- bitset over constants ----------------------------------------------------------
+struct Bits {
+  std::vector<uint64_t> w;
+  Bits() = default;
+  explicit Bits(int nbits) : w((nbits + 63) / 64, 0) {}
+  void set(int i) { w[i >> 6] |= 1ull << (i & 63); }
+  bool get(int i) const { return (w[i >> 6] >> (i & 63)) & 1; }
+  void flip(int i) { w[i >> 6] ^= 1ull << (i & 63); }
+  int count() const {
+    int c = 0;
+    for (auto x : w) c += __builtin_popcountll(x);
+    return c;
+  }
+  Bits &operator^=(const Bits &o) {
+    for (size_t i = 0; i < w.size(); ++i) w[i] ^= o.w[i];
+    return *this;
+  }
+  bool operator==(const Bits &o) const { return w == o.w; }
+  bool any() const {
+    for (auto x : w)
+      if (x) return true;
+    return false;
+  }
+};
+
+// ---- the multi-ary SLP (MultiSLP) -----------------------------------------
+// Terms: t < n_const is constant c_t; t >= n_const is variable (t - n_const), i.e.
+// the value defined by instruction (t - n_const) of `ins` before scheduling.
+struct Ins {
+  int var;               // variable id defined here (SSA)
+  std::vector<int> ops;  // operand terms
+};
+
+struct Slp {
+  int n_const = 0;
+  int n_vars = 0;                // variables ids are 0..n_vars-1
+  std::vector<Ins> ins;          // topologically ordered
+  std::vector<int> goal;         // per goal: term (constant, variable+n_const) or -1 = zero
+  int term_of_var(int v) const { return n_const + v; }
+  bool is_const(int t) const { return t >= 0 && t < n_const; }
+};
+
+// A compiled device program.
+struct Program {
+  xslp_opts opts;
+  int n_const = 0, n_goals = 0;
+  Slp slp;                         // scheduled program (SSA)
+  std::vector<int> pebble;         // paper pebble id per variable
+  int nvar = 0;
+  xslp_stats stats{};
+  // interpreter bytecode (uint16 words) and slot count
+  std::vector<uint16_t> code;
+  int nslots = 0;
+  // straight-line kernel(s): generic addressing + optional baked strip size
+  std::string ptx_generic, ptx_baked;
+  std::vector<char> cubin_generic, cubin_baked;
+  int64_t baked_strip = 0;
+  // device state, per device ordinal
+  struct Dev;
+  mutable std::mutex mu;
+  mutable std::map<int, std::shared_ptr<Dev>> dev;
+  ~Program();
+};
+
+// compiler passes (compiler.cpp)
+Slp lift(const std::vector<Bits> &goals, int n_const, bool multi);
+Slp compress(const std::vector<Bits> &goals, int n_const, bool xor_rebuild);
+void fuse(Slp &s);
+void schedule_dfs(Slp &s, int goal_order);
+int paper_pebbles(const Slp &s, std::vector<int> &pebble);
+void build_bytecode(const Slp &s, std::vector<uint16_t> &code, int &nslots, int &maxlive);
+std::vector<Bits> evaluate(const Slp &s);
+std::string dump_pebbles(const Slp &s, const std::vector<int> &pebble);
+std::string dump_slots(const std::vector<uint16_t> &code, int n_const);
+Slp parse_text(const std::string &text, int n_const);
+
+// PTX (ptx.cpp)
+std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads);
+std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill);
+
+}  // namespace xslp

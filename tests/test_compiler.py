@@ -1,0 +1,256 @@
+"""Host-side product tests (no GPU): the C-ABI library loads and exports the header's
+symbols; the C++ compiler matches the oracle's matrices and the paper's worked
+examples; every compiled program (paper pebble form and interpreter slot form) is
+semantically equal to its bitmatrix under the oracle's set evaluator."""
+import itertools
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2108_02692_b200 as X
+from oracle import matrices as mx
+from oracle import slp as oslp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+G = os.path.join(ROOT, "tests", "golden")
+
+
+def golden(name):
+    with open(os.path.join(G, name + ".slp")) as f:
+        return f.read()
+
+
+def test_library_exports_every_header_symbol():
+    with open(os.path.join(ROOT, "include", "xslp.h")) as f:
+        hdr = f.read()
+    names = set(re.findall(r"\b(xslp_[a-z_]+)\s*\(", hdr))
+    assert len(names) >= 18
+    for n in names:
+        assert hasattr(X._lib, n), n
+    assert set(X.EXPORTED) == names
+    assert "sm_100a" in X.xslp_version()
+
+
+@pytest.mark.parametrize("n,p,kind", [(10, 4, "isal"), (4, 2, "cauchy"), (10, 4, "sysvand"),
+                                      (20, 4, "isal"), (8, 3, "isal")])
+def test_matrices_match_oracle(n, p, kind):
+    g = X.xslp_coding_matrix(n, p, kind)
+    assert g.tolist() == mx.coding_matrix(n, p, kind)
+    assert (X.xslp_encode_bitmatrix(g, n, p) == mx.to_bitmatrix(g[n:].tolist())).all()
+
+
+def test_decode_bitmatrix_matches_oracle():
+    g = X.xslp_coding_matrix(10, 4)
+    og = mx.coding_matrix(10, 4)
+    for er in [(2, 4, 5, 6), (0, 2, 3, 9), (10, 11, 12, 13), (3,), (1, 12), (13, 0, 7)]:
+        bits, surv = X.xslp_decode_bitmatrix(g, 10, 4, er)
+        osurv, rows = mx.decode_rows(og, 10, list(er))
+        assert surv.tolist() == osurv
+        assert (bits == mx.to_bitmatrix(rows)).all()
+
+
+def test_decode_bitmatrix_errors():
+    g = X.xslp_coding_matrix(10, 4)
+    with pytest.raises(X.XslpError) as e:
+        X.xslp_decode_bitmatrix(g, 10, 4, [0, 1, 2, 3, 4])
+    assert e.value.code == X.XSLP_EUNRECOVERABLE
+    with pytest.raises(X.XslpError) as e:
+        X.xslp_decode_bitmatrix(g, 10, 4, [0, 0])
+    assert e.value.code == X.XSLP_EINVAL
+    with pytest.raises(X.XslpError) as e:
+        X.xslp_decode_bitmatrix(g, 10, 4, [14])
+    assert e.value.code == X.XSLP_EINVAL
+
+
+def test_singular_matrix():
+    g = np.array([[1, 0], [0, 1], [1, 1], [2, 2]], dtype=np.uint8)  # rows 2 and 3 dependent
+    with pytest.raises(X.XslpError) as e:
+        X.xslp_decode_bitmatrix(g, 2, 2, [0, 1])
+    assert e.value.code == X.XSLP_ESINGULAR
+
+
+# ---- paper worked examples through the product compiler ---------------------------------
+
+def _sets(bits):
+    return oslp.rows_to_sets(bits)
+
+
+def test_repair_P0_is_P1():
+    p = X.xslp_compile_text(golden("P0"), 4, compress="repair", fuse=0, schedule=0, specialise=0)
+    assert p.stats()["xor_count"] == 5
+    text = p.dump()
+    assert oslp.evaluate(text) == oslp.evaluate(golden("P0"))
+    # exact pair sequence (a,b),(t1,c),(t2,d),(b,c),(t4,d)
+    want = ["c0 ^ c1", "p0 ^ c2", "p1 ^ c3", "c1 ^ c2", "p3 ^ c3"]
+    got = [l.split("=", 1)[1].strip() for l in text.splitlines() if "=" in l and not l.startswith("#")]
+    assert got == want
+
+
+def test_xorrepair_P0_is_P2():
+    p = X.xslp_compile_text(golden("P0"), 4, compress="xorrepair", fuse=0, schedule=0, specialise=0)
+    assert p.stats()["xor_count"] == 4
+    text = p.dump()
+    assert oslp.evaluate(text) == oslp.evaluate(golden("P0"))
+    assert "p2 ^ c0" in text                                      # t4 <- a ^ t3
+
+
+def test_intro_compression():
+    p = X.xslp_compile_text(golden("intro_P"), 7, compress="xorrepair", fuse=1, schedule=1,
+                            specialise=0)
+    s = p.stats()
+    assert s["xor_count"] == 5
+    assert oslp.evaluate(p.dump()) == oslp.evaluate(golden("intro_P"))
+
+
+def test_fusion_examples():
+    p = X.xslp_compile_text(golden("fusion_chain"), 4, compress="none", fuse=1, schedule=0,
+                            specialise=0)
+    assert p.stats()["mem_count"] == 5 and p.stats()["n_instr"] == 1
+    a = X.xslp_compile_text(golden("fusion_A"), 7, compress="none", fuse=1, schedule=0,
+                            specialise=0)
+    assert a.stats()["mem_count"] == 14                           # fuse(A) = C
+    b = X.xslp_compile_text(golden("fusion_B"), 7, compress="none", fuse=1, schedule=0,
+                            specialise=0)
+    assert b.stats()["mem_count"] == 12 and b.stats()["n_instr"] == 3   # v1 used twice: kept
+    unf = X.xslp_compile_text(golden("fusion_B"), 7, compress="none", fuse=0, schedule=0,
+                              specialise=0)
+    assert unf.stats()["mem_count"] == 12
+
+
+def test_dfs_on_Peg():
+    # DFS heuristic on G_eg: NVar 4, CCap 7, IOcost(., 8) = 10
+    p = X.xslp_compile_text(golden("P_eg"), 7, compress="none", fuse=0, schedule=1, specialise=0)
+    text = p.dump()
+    assert p.stats()["nvar"] == 4
+    assert oslp.ccap(text) == 7 and oslp.iocost(text, 8) == 10
+    assert oslp.evaluate(text) == oslp.evaluate(golden("P_eg"))
+    body = [l for l in text.splitlines() if "=" in l and not l.startswith("#")]
+    # post-order C D v2 A B v1 E F v3 G v4 v5
+    assert [l.split("=")[1].strip() for l in body] == [
+        "c2 ^ c3", "c0 ^ c1", "p1 ^ c4 ^ c5", "p2 ^ c0 ^ c6", "p1 ^ p2 ^ p3"]
+    assert body[-1].startswith("p3 =")                            # v5 takes v4's pebble
+
+
+# ---- RS programs: semantics and the paper's tables ---------------------------------------
+
+CFGS = [("enc", 10, 4, None), ("dec", 10, 4, (2, 4, 5, 6)), ("dec", 10, 4, (0, 2, 3, 9)),
+        ("enc", 4, 2, None), ("dec", 4, 2, (0, 1)), ("enc", 10, 2, None), ("dec", 10, 4, (10, 11, 12, 13)),
+        ("dec", 10, 4, (5,)), ("enc", 20, 4, None)]
+
+
+def _bits(kind, n, p, er, family="isal"):
+    fam = "cauchy" if (n, p) == (4, 2) else family
+    g = X.xslp_coding_matrix(n, p, fam)
+    if kind == "enc":
+        return X.xslp_encode_bitmatrix(g, n, p)
+    return X.xslp_decode_bitmatrix(g, n, p, er)[0]
+
+
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: f"{c[0]}{c[1]}_{c[2]}_{c[3]}")
+@pytest.mark.parametrize("comp", ["none", "repair", "xorrepair"])
+def test_semantic_equality(cfg, comp):
+    if cfg[1] == 20 and comp != "xorrepair":
+        pytest.skip("covered by xorrepair")
+    bits = _bits(*cfg)
+    want = _sets(bits)
+    for fuse, sched in ((1, 1), (0, 0)):
+        p = X.xslp_compile(bits, compress=comp, fuse=fuse, schedule=sched, specialise=0)
+        assert oslp.evaluate(p.dump()) == want
+        assert oslp.evaluate(p.dump(1)) == want                   # interpreter slot program
+        s = p.stats()
+        text = oslp.parse(p.dump())
+        assert s["xor_count"] == oslp.xor_count(text)
+        assert s["mem_count"] == oslp.mem_count(text)
+
+
+def test_printed_counts_exact():
+    # unoptimised P_enc / P_dec: #xor 755 / 1368
+    for cfg, want in ((CFGS[0], 755), (CFGS[1], 1368)):
+        p = X.xslp_compile(_bits(*cfg), compress="none", fuse=0, schedule=0, specialise=0)
+        s = p.stats()
+        assert s["xor_count"] == want and s["mem_count"] == 3 * want   # binary chain: #M = 3 #xor
+        # fused-uncompressed P^{+F}: one instruction per goal, NVar 32
+        pf = X.xslp_compile(_bits(*cfg), compress="none", fuse=1, schedule=0, specialise=0).stats()
+        assert pf["nvar"] == 32 and pf["n_instr"] == 32 and pf["xor_count"] == want
+
+
+def _within(got, want, tol):
+    return abs(got - want) <= tol * want
+
+
+def test_stage_tables_within_tolerance():
+    # Co / Fu(Co) columns of P:1652-1654 and P:1681-1683; heuristic tie-breaks differ, +-5%
+    for cfg, (x_co, ninst, mem) in ((CFGS[0], (385, 146, 677)), (CFGS[1], (511, 206, 923))):
+        bits = _bits(*cfg)
+        co = X.xslp_compile(bits, compress="xorrepair", fuse=0, schedule=0, specialise=0).stats()
+        fu = X.xslp_compile(bits, compress="xorrepair", fuse=1, schedule=1, specialise=0).stats()
+        assert _within(co["xor_count"], x_co, 0.05)
+        assert co["mem_count"] == 3 * co["xor_count"]
+        assert fu["xor_count"] == co["xor_count"]                # fusion keeps #xor (reading R7)
+        assert _within(fu["n_instr"], ninst, 0.05)
+        assert _within(fu["mem_count"], mem, 0.05)
+        assert _within(fu["nvar"], {146: 88, 206: 125}[ninst], 0.10)
+
+
+FIG1 = {(8, 4): (121, 170, 543, 747), (9, 4): (132, 182, 611, 829), (10, 4): (146, 206, 677, 923),
+        (8, 3): (75, 129, 364, 561), (9, 3): (87, 144, 417, 641), (10, 3): (96, 145, 471, 661),
+        (8, 2): (26, 65, 180, 286), (9, 2): (29, 73, 202, 322), (10, 2): (30, 77, 222, 352)}
+
+
+@pytest.mark.parametrize("np_", list(FIG1))
+def test_figure1_grid(np_):
+    # Figure 1: instructions and #M of the optimised programs
+    n, p = np_
+    ie, id_, me, md = FIG1[np_]
+    er = [2, 4, 5, 6][:p]
+    se = X.xslp_compile(_bits("enc", n, p, None), specialise=0).stats()
+    sd = X.xslp_compile(_bits("dec", n, p, er), specialise=0).stats()
+    assert _within(se["mem_count"], me, 0.05) and _within(sd["mem_count"], md, 0.05)
+    assert _within(se["n_instr"], ie, 0.10) and _within(sd["n_instr"], id_, 0.10)
+
+
+def test_copy_and_zero_goals():
+    bits = np.zeros((16, 16), dtype=np.uint8)
+    bits[0, 3] = 1                      # copy goal
+    bits[2, [1, 2, 5]] = 1
+    bits[3, [1, 2, 5, 7]] = 1
+    bits[9, :] = 1                      # row 1 (zero) and others
+    p = X.xslp_compile(bits, specialise=1)
+    s = p.stats()
+    assert s["n_copy_goals"] == 1 and s["n_zero_goals"] == 16 - 4
+    assert oslp.evaluate(p.dump()) == _sets(bits)
+    assert oslp.evaluate(p.dump(1)) == _sets(bits)
+    assert "xslp_sl_batch" in p.dump(2)
+
+
+def test_ptx_compiles_for_sm100a_without_gpu():
+    for lanes in (1, 2, 4):
+        p = X.xslp_compile(_bits(*CFGS[0]), lane_words=lanes, block_bytes_hint=1 << 20)
+        s = p.stats()
+        assert s["regs"] > 0 and s["spill_bytes"] == 0 or lanes > 1
+        ptx = p.dump(2)
+        assert ".target sm_100a" in ptx and "lop3.b32" in ptx
+        assert f"+{7 * (1 << 17)}]" in ptx                         # baked strip offsets
+
+
+def test_compile_errors():
+    with pytest.raises(X.XslpError):
+        X.xslp_compile(np.zeros((8, 0), dtype=np.uint8))
+    with pytest.raises(X.XslpError):
+        X.xslp_compile(np.full((8, 8), 2, dtype=np.uint8))
+    with pytest.raises(X.XslpError):
+        X.xslp_compile(np.ones((8, 8), dtype=np.uint8), lane_words=3)
+    with pytest.raises(X.XslpError):
+        X.xslp_compile_text("x = c0 ^ y\nreturn x", 4)
+
+
+def test_device_call_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    p = X.xslp_compile(_bits(*CFGS[3]), specialise=0)
+    with pytest.raises(X.XslpError) as e:
+        X.xslp_encode_batch(p, 1 << 20, 1 << 21, 1, 4096, stream=0)
+    assert e.value.code == X.XSLP_ECUDA

@@ -1,0 +1,327 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle, bit-exact.
+
+Inputs are seeded (synth); expected values come only from oracle/ (or, for the
+full-size roundtrip property, from the seeded generator itself).  Sizes: small
+cases compare every byte and span several CTA tiles plus a ragged tail; the
+BASELINE-size cases run in the bench's launch configuration and compare sampled
+stripes with the oracle, plus properties checked over all stripes.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2108_02692_b200 as X  # noqa: E402
+from oracle import matrices as mx  # noqa: E402
+from oracle import rs  # noqa: E402
+import synth  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.init()
+
+
+def dev_buf(nstripes, nblocks, B):
+    return torch.empty((nstripes, nblocks, B), dtype=torch.uint8, device="cuda")
+
+
+def host_data(seed, stripes, n, B):
+    return np.stack([synth.stripe_data(seed, s, n, B) for s in stripes])
+
+
+def run_batch(prog, din, dout, B, nstripes=None):
+    ns = din.shape[0] if nstripes is None else nstripes
+    ti = X.block_table(din, din.shape[0], din.shape[1], B)
+    to = X.block_table(dout, dout.shape[0], dout.shape[1], B)
+    X.xslp_encode_batch(prog, ti, to, ns, B)
+    torch.cuda.synchronize()
+
+
+def compile_enc(n, p, kind="isal", **kw):
+    g = X.xslp_coding_matrix(n, p, kind)
+    return g, X.xslp_compile(X.xslp_encode_bitmatrix(g, n, p), **kw)
+
+
+# ---- generator ---------------------------------------------------------------------------
+
+def test_fill_matches_synth():
+    n, B = 10, 4096
+    d = dev_buf(3, n, B)
+    X.xslp_fill_random(d, 3, n, B, seed=42, stripe0=5)
+    torch.cuda.synchronize()
+    want = host_data(42, [5, 6, 7], n, B)
+    assert (d.cpu().numpy() == want).all()
+
+
+# ---- cfg1: RS(4,2) Cauchy, one stripe of 4 x 4 KiB ----------------------------------------
+
+@pytest.mark.parametrize("kernel", ["straight", "interp"])
+def test_cfg1_encode_decode(kernel):
+    n, p, B = 4, 2, 4096
+    g, enc = compile_enc(n, p, "cauchy", kernel=kernel)
+    og = mx.coding_matrix(n, p, "cauchy")
+    data = host_data(1, [0], n, B)[0]
+    want_par = rs.encode(og, n, data)
+    d = torch.from_numpy(data).cuda()
+    par = torch.zeros((p, B), dtype=torch.uint8, device="cuda")
+    X.xslp_encode(enc, [d[j] for j in range(n)], [par[i] for i in range(p)], B)
+    torch.cuda.synchronize()
+    assert (par.cpu().numpy() == want_par).all()
+    blocks = np.concatenate([data, want_par])           # oracle blocks as decode input
+    dblocks = torch.from_numpy(blocks).cuda()
+    for e in (1, 2):
+        for erased in itertools.combinations(range(n + p), e):
+            bits, surv = X.xslp_decode_bitmatrix(g, n, p, erased)
+            dec = X.xslp_compile(bits, kernel=kernel)
+            out = torch.zeros((e, B), dtype=torch.uint8, device="cuda")
+            X.xslp_decode(dec, [dblocks[s] for s in surv], [out[i] for i in range(e)], B)
+            torch.cuda.synchronize()
+            assert (out.cpu().numpy() == blocks[list(erased)]).all(), erased
+
+
+# ---- multi-tile, ragged tail, all kernel variants and compressors -------------------------
+
+@pytest.mark.parametrize("comp", ["none", "repair", "xorrepair"])
+@pytest.mark.parametrize("kern,lanes", [("straight", 1), ("straight", 2), ("straight", 4),
+                                        ("interp", 1)])
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_rs10_encode_small_full_compare(comp, kern, lanes, p):
+    n, B, S = 10, 9600, 5          # strip 1200 B = 300 words: two 256-thread tiles, ragged tail
+    og = mx.coding_matrix(n, p)
+    _, prog = compile_enc(n, p, compress=comp, kernel=kern, lane_words=lanes,
+                          fuse=1 if comp != "repair" else 0, schedule=1 if comp != "repair" else 0)
+    data = host_data(4, range(S), n, B)
+    din = torch.from_numpy(data).cuda()
+    dout = torch.full((S, p, B), 0xAB, dtype=torch.uint8, device="cuda")
+    run_batch(prog, din, dout, B)
+    got = dout.cpu().numpy()
+    for s in range(S):
+        assert (got[s] == rs.encode(og, n, data[s])).all(), s
+
+
+def test_baked_and_generic_strip():
+    n, p = 10, 4
+    og = mx.coding_matrix(n, p)
+    _, prog = compile_enc(n, p, block_bytes_hint=8192)
+    for B in (8192, 4096):            # baked kernel, then the generic-address kernel
+        data = host_data(9, range(3), n, B)
+        din = torch.from_numpy(data).cuda()
+        dout = dev_buf(3, p, B)
+        run_batch(prog, din, dout, B)
+        for s in range(3):
+            assert (dout[s].cpu().numpy() == rs.encode(og, n, data[s])).all()
+
+
+# ---- cfg3-style heterogeneous decode (one program per stripe) ----------------------------
+
+def _decode_inputs(seed, S, n, p, B, e):
+    g = mx.coding_matrix(n, p)
+    pats, blocks = [], []
+    for s in range(S):
+        er = synth.erasure_pattern(seed, s, n + p, e)
+        data = synth.stripe_data(seed, s, n, B)
+        blocks.append(np.concatenate([data, rs.encode(g, n, data)]))
+        pats.append(tuple(er))
+    return pats, blocks
+
+
+@pytest.mark.parametrize("kern", ["interp", "straight"])
+def test_heterogeneous_decode(kern):
+    n, p, B, S = 10, 4, 4096, 24
+    pats, blocks = _decode_inputs(3, S, n, p, B, 4)
+    g = X.xslp_coding_matrix(n, p)
+    uniq = sorted(set(pats))
+    progs, survs = [], {}
+    for er in uniq:
+        bits, surv = X.xslp_decode_bitmatrix(g, n, p, er)
+        progs.append(X.xslp_compile(bits, kernel=kern))
+        survs[er] = surv
+    idx = torch.tensor([uniq.index(er) for er in pats], dtype=torch.int32, device="cuda")
+    surv_blocks = np.stack([blocks[s][survs[pats[s]]] for s in range(S)])
+    din = torch.from_numpy(surv_blocks).cuda()
+    dout = dev_buf(S, 4, B)
+    ti = X.block_table(din, S, n, B)
+    to = X.block_table(dout, S, 4, B)
+    if kern == "interp":
+        X.xslp_decode_batch_multi(progs, idx, ti, to, S, B)
+    else:   # grouped: one launch per pattern over its stripes (host groups)
+        for k, pr in enumerate(progs):
+            sel = [s for s in range(S) if pats[s] == uniq[k]]
+            sti = ti.view(S, n)[sel].contiguous()
+            sto = to.view(S, 4)[sel].contiguous()
+            X.xslp_encode_batch(pr, sti, sto, len(sel), B)
+    torch.cuda.synchronize()
+    got = dout.cpu().numpy()
+    for s in range(S):
+        assert (got[s] == blocks[s][list(pats[s])]).all(), (s, pats[s])
+
+
+# ---- edge cases ------------------------------------------------------------------------
+
+def test_edge_cases():
+    n, p = 4, 2
+    _, prog = compile_enc(n, p, "cauchy")
+    d = dev_buf(1, n, 4096)
+    o = dev_buf(1, p, 4096)
+    ti, to = X.block_table(d, 1, n, 4096), X.block_table(o, 1, p, 4096)
+    X.xslp_encode_batch(prog, ti, to, 0, 4096)         # no stripes: no-op
+    X.xslp_encode_batch(prog, ti, to, 1, 0)            # empty blocks: no-op
+    with pytest.raises(X.XslpError) as e:
+        X.xslp_encode_batch(prog, ti, to, 1, 4000)     # strip not whole words
+    assert e.value.code == X.XSLP_EINVAL
+    with pytest.raises(X.XslpError) as e:
+        X.xslp_encode(prog, [d[0, j, 4:] for j in range(n)], [o[0, i] for i in range(p)], 1024)
+    assert e.value.code == X.XSLP_EINVAL               # misaligned pointer
+    torch.cuda.synchronize()
+
+
+def test_copy_and_zero_goals_on_device():
+    rng = np.random.default_rng(0)
+    bits = np.zeros((16, 24), dtype=np.uint8)
+    bits[0, 3] = 1
+    bits[1, 17] = 1
+    bits[2, [1, 2, 5]] = 1
+    bits[5, :] = 1
+    bits[9:, :] = rng.integers(0, 2, size=(7, 24))
+    B = 2048
+    data = host_data(8, [0], 3, B)[0]
+    want = rs.bitmatrix_apply(bits, data)
+    for kern in ("straight", "interp"):
+        prog = X.xslp_compile(bits, kernel=kern)
+        din = torch.from_numpy(data).cuda()
+        out = torch.full((2, B), 0x5A, dtype=torch.uint8, device="cuda")
+        X.xslp_encode(prog, [din[j] for j in range(3)], [out[0], out[1]], B)
+        torch.cuda.synchronize()
+        assert (out.cpu().numpy() == want).all()
+
+
+def test_host_buffer_path():
+    n, p, B, S = 10, 4, 65536, 40
+    og = mx.coding_matrix(n, p)
+    _, prog = compile_enc(n, p)
+    data = host_data(12, range(S), n, B)
+    h_in = torch.from_numpy(data).pin_memory()
+    h_out = torch.zeros((S, p, B), dtype=torch.uint8).pin_memory()
+    X.xslp_encode_host(prog, h_in, h_out, S, B)
+    got = h_out.numpy()
+    for s in (0, 17, S - 1):
+        assert (got[s] == rs.encode(og, n, data[s])).all()
+    # all stripes: RAID-5 parity row
+    assert (got[:, 0] == np.bitwise_xor.reduce(data, axis=1)).all()
+
+
+# ---- BASELINE-size cases in the bench launch configuration ------------------------------
+
+def _xor_reduce(t):
+    acc = t[:, 0].clone()
+    for j in range(1, t.shape[1]):
+        acc ^= t[:, j]
+    return acc
+
+
+def test_cfg2_full_size_sampled():
+    # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); straight-line kernel, baked strip
+    n, p, B, S = 10, 4, 1 << 20, 1024
+    og = mx.coding_matrix(n, p)
+    _, prog = compile_enc(n, p, block_bytes_hint=B)
+    din = dev_buf(S, n, B)
+    X.xslp_fill_random(din, S, n, B, seed=2)
+    dout = dev_buf(S, p, B)
+    run_batch(prog, din, dout, B)
+    assert torch.equal(dout[:, 0], _xor_reduce(din))       # RAID-5 row over every stripe
+    for s in (0, 511, 1023):
+        data = synth.stripe_data(2, s, n, B)
+        assert (din[s].cpu().numpy() == data).all()
+        assert (dout[s].cpu().numpy() == rs.encode(og, n, data)).all(), s
+    del din, dout
+    torch.cuda.empty_cache()
+
+
+def test_cfg3_full_size_roundtrip_sampled():
+    # RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures (configs[2])
+    n, p, B, S = 10, 4, 1 << 20, 1024
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    _, enc = compile_enc(n, p, block_bytes_hint=B)
+    allb = dev_buf(S, n + p, B)
+    X.xslp_fill_random(allb, S, n + p, B, seed=3)            # data part regenerated below
+    data = dev_buf(S, n, B)
+    X.xslp_fill_random(data, S, n, B, seed=3)
+    allb[:, :n] = data
+    ti = X.block_table(allb, S, n + p, B).view(S, n + p)
+    X.xslp_encode_batch(enc, ti[:, :n].contiguous(), ti[:, n:].contiguous(), S, B)
+    pats = [tuple(synth.erasure_pattern(3, s, n + p, 4)) for s in range(S)]
+    uniq = sorted(set(pats))
+    progs, survs = [], {}
+    for er in uniq:
+        bits, surv = X.xslp_decode_bitmatrix(g, n, p, er)
+        progs.append(X.xslp_compile(bits, specialise=0))
+        survs[er] = surv
+    idx = torch.tensor([uniq.index(er) for er in pats], dtype=torch.int32, device="cuda")
+    tin = torch.stack([ti[s, torch.as_tensor(survs[pats[s]], dtype=torch.long)] for s in range(S)])
+    out = dev_buf(S, 4, B)
+    to = X.block_table(out, S, 4, B)
+    X.xslp_decode_batch_multi(progs, idx, tin.contiguous(), to, S, B)
+    torch.cuda.synchronize()
+    # roundtrip property on every stripe: erased data blocks equal the regenerated data
+    for s in range(S):
+        for k, e in enumerate(pats[s]):
+            if e < n:
+                assert torch.equal(out[s, k], data[s, e]), (s, e)
+    # oracle on sampled stripes: parity and the decode of the oracle's blocks
+    for s in (0, 700):
+        d = synth.stripe_data(3, s, n, B)
+        blocks = np.concatenate([d, rs.encode(og, n, d)])
+        assert (allb[s].cpu().numpy() == blocks).all()
+        surv, rows = mx.decode_rows(og, n, list(pats[s]))
+        assert (out[s].cpu().numpy() == rs.decode(rows, blocks[surv])).all()
+    del allb, data, out
+    torch.cuda.empty_cache()
+
+
+def test_cfg5_rs20_reduced():
+    # RS(20,4) encode + one seeded 4-erasure decode; 16 stripes x 20 x 1 MiB (configs[4] shape)
+    n, p, B, S = 20, 4, 1 << 20, 16
+    og = mx.coding_matrix(n, p)
+    g, enc = compile_enc(n, p, block_bytes_hint=B)
+    allb = dev_buf(S, n + p, B)
+    X.xslp_fill_random(allb, S, n + p, B, seed=5)
+    d = dev_buf(S, n, B)
+    X.xslp_fill_random(d, S, n, B, seed=5)
+    allb[:, :n] = d
+    ti = X.block_table(allb, S, n + p, B).view(S, n + p)
+    X.xslp_encode_batch(enc, ti[:, :n].contiguous(), ti[:, n:].contiguous(), S, B)
+    er = synth.erasure_pattern(5, 0, n + p, 4)
+    bits, surv = X.xslp_decode_bitmatrix(g, n, p, er)
+    dec = X.xslp_compile(bits, block_bytes_hint=B)
+    out = dev_buf(S, 4, B)
+    X.xslp_encode_batch(dec, ti[:, torch.as_tensor(surv, dtype=torch.long)].contiguous(),
+                        X.block_table(out, S, 4, B), S, B)
+    torch.cuda.synchronize()
+    assert torch.equal(out, allb[:, er])
+    s = 9
+    h = synth.stripe_data(5, s, n, B)
+    assert (allb[s, n:].cpu().numpy() == rs.encode(og, n, h)).all()
+
+
+def test_shards_equal_single_run():
+    # 8-shard decomposition run serially on one GPU equals the 1-shard run
+    n, p, B, S = 10, 4, 65536, 64
+    _, prog = compile_enc(n, p, block_bytes_hint=B)
+    full_in = dev_buf(S, n, B)
+    X.xslp_fill_random(full_in, S, n, B, seed=21)
+    full_out = dev_buf(S, p, B)
+    run_batch(prog, full_in, full_out, B)
+    per = S // 8
+    for r in range(8):
+        si = dev_buf(per, n, B)
+        X.xslp_fill_random(si, per, n, B, seed=21, stripe0=r * per)
+        so = dev_buf(per, p, B)
+        run_batch(prog, si, so, B)
+        assert torch.equal(so, full_out[r * per:(r + 1) * per])
