@@ -25,6 +25,10 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+def log(*a):
+    print(f"[bench {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
+
+
 METRIC = "RS encode/decode GB/s of data (device-timed) at 1/2/4/8 B200; % of roofline"
 MiB = 1 << 20
 
@@ -270,6 +274,7 @@ def main():
                               block_bytes_hint=B)
         m_out = p
     compile_s = time.perf_counter() - t0
+    log(f'compiled in {compile_s:.2f} s', prog.stats())
     stats = prog.stats()
 
     # ---- device buffers and seeded inputs (untimed) ----
@@ -313,6 +318,7 @@ def main():
             raise SystemExit("sanity check failed: parity block 0 != XOR of data blocks")
         del acc
 
+    log('sanity ok; warmup')
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -328,6 +334,7 @@ def main():
             ev[i + 1].record(stream)
         torch.cuda.synchronize()
     launches = X.xslp_launch_count() - l0
+    log('timed region done')
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -379,6 +386,7 @@ def main():
         except Exception as ex:  # report, do not hide
             e2e = {"value": None, "unit": "GB/s", "error": str(ex)[:200]}
 
+    log('e2e', e2e)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_baseline(wl)

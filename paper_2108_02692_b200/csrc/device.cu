@@ -372,6 +372,7 @@ struct HostWs {
   size_t B = 0;
 };
 static std::map<int, HostWs> g_ws;
+static std::mutex g_ws_mu;  // separate from g_mu: host_apply calls apply_batch (which takes g_mu)
 
 static void host_apply(const Program *p, const uint8_t *h_in, uint8_t *h_out, int nstripes,
                        size_t B, cudaStream_t user) {
@@ -383,7 +384,7 @@ static void host_apply(const Program *p, const uint8_t *h_in, uint8_t *h_out, in
   const int n_in = p->n_const / 8, n_out = p->n_goals / 8;
   const size_t target = (size_t)256 << 20;
   const int chunk = (int)std::max<size_t>(1, std::min<size_t>(nstripes, target / (n_in * B)));
-  std::lock_guard<std::mutex> g(g_mu);
+  std::lock_guard<std::mutex> g(g_ws_mu);
   HostWs &w = g_ws[d];
   if (!w.st[0]) {
     CUDA_OK(cudaStreamCreateWithFlags(&w.st[0], cudaStreamNonBlocking));

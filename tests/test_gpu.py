@@ -173,7 +173,7 @@ def test_edge_cases():
     X.xslp_encode_batch(prog, ti, to, 0, 4096)         # no stripes: no-op
     X.xslp_encode_batch(prog, ti, to, 1, 0)            # empty blocks: no-op
     with pytest.raises(X.XslpError) as e:
-        X.xslp_encode_batch(prog, ti, to, 1, 4000)     # strip not whole words
+        X.xslp_encode_batch(prog, ti, to, 1, 4008)     # strip not whole words
     assert e.value.code == X.XSLP_EINVAL
     with pytest.raises(X.XslpError) as e:
         X.xslp_encode(prog, [d[0, j, 4:] for j in range(n)], [o[0, i] for i in range(p)], 1024)
