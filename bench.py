@@ -52,9 +52,11 @@ def parse():
     ap.add_argument("--impl", default="xslp", choices=["xslp", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--compress", default="xorrepair", choices=["none", "repair", "xorrepair"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "straight", "interp"])
+    ap.add_argument("--kernel", default="auto",
+                    choices=["auto", "straight", "interp", "tma", "grouped", "grouped_tma"])
+    ap.add_argument("--streams", type=int, default=8, help="internal streams for grouped decode")
     ap.add_argument("--lanes", type=int, default=1)
-    ap.add_argument("--threads", type=int, default=256)
+    ap.add_argument("--threads", type=int, default=128)
     ap.add_argument("--block-bytes", type=int, default=0, help="override block size")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -211,6 +213,15 @@ def run_reference(args, wl, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def kernel_name(args, wl, stats):
+    k = args.kernel
+    if k == "interp":
+        return "xslp_interp_kernel"
+    if k in ("tma", "grouped_tma"):
+        return "xslp_sl_tma"
+    return "xslp_sl_batch"
+
+
 def config_of(args, wl, stats):
     c = {"workload": f"{args.workload}: {wl['desc']}", "n": wl["n"], "p": wl["p"],
          "block_bytes": wl["B"], "stripes_per_gpu": wl["S"] if wl["op"] != "encode_sharded"
@@ -221,7 +232,7 @@ def config_of(args, wl, stats):
          "parallelism": f"stripe-sharded x{args.gpus}, no collective"}
     if stats:
         c["slp"] = {k: stats[k] for k in ("xor_count", "mem_count", "n_instr", "nvar", "maxlive",
-                                          "regs", "spill_bytes")}
+                                          "regs", "spill_bytes", "regs_tma", "spill_bytes_tma")}
     return c
 
 
@@ -264,8 +275,15 @@ def main():
         pats = [tuple(synth.erasure_pattern(wl["seed"], s0 + s, n + p, wl["e"])) for s in range(S)]
         uniq = sorted(set(pats))
         dec = [X.xslp_decode_bitmatrix(G, n, p, er) for er in uniq]
-        progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,
-                               threads=args.threads)
+        mode = "grouped" if args.kernel == "auto" else args.kernel
+        if mode == "interp":
+            progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,
+                                   threads=args.threads)
+        else:   # one JIT straight-line (or TMA) kernel per distinct erasure pattern
+            progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=1,
+                                   threads=args.threads, lane_words=args.lanes,
+                                   block_bytes_hint=B,
+                                   kernel="tma" if mode in ("tma", "grouped_tma") else "straight")
         prog = progs[0]
         m_out = wl["e"]
     else:
@@ -295,11 +313,17 @@ def main():
     ti = X.block_table(din, S, n_in, B)
     to = X.block_table(dout, S, m_out, B)
     if wl["op"] == "decode_multi":
-        idx = torch.tensor([uniq.index(er) for er in pats], dtype=torch.int32, device="cuda")
+        pos = [uniq.index(er) for er in pats]
+        idx = torch.tensor(pos, dtype=torch.int32, device="cuda")
+        gids, goff = X.group_stripes(pos, len(progs))
+        gids = torch.from_numpy(gids).cuda()
 
     def launch():
-        if wl["op"] == "decode_multi":
+        if wl["op"] == "decode_multi" and mode == "interp":
             X.xslp_decode_batch_multi(progs, idx, ti, to, S, B, stream=stream)
+        elif wl["op"] == "decode_multi":
+            X.xslp_decode_batch_grouped(progs, gids, goff, ti, to, B, nstreams=args.streams,
+                                        stream=stream)
         else:
             X.xslp_encode_batch(prog, ti, to, S, B, stream=stream)
 
@@ -348,14 +372,13 @@ def main():
     value = data_bytes_step * args.steps / (total_ms / 1e3) / 1e9
 
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / launch time
-    alg_bytes_launch = S * (n_in + m_out) * B
+    alg_bytes_launch = S * (n_in + m_out) * B        # per step (= per launch unless grouped)
     launch_ms = sum(per_step) / len(per_step) / nchunks
     achieved = alg_bytes_launch / (launch_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload),
-            "peak_source": peak_src, "kernel": "xslp_interp_kernel" if wl["op"] == "decode_multi"
-            else ("xslp_sl_batch" if stats["regs"] and args.kernel != "interp" else "xslp_interp_kernel"),
+            "peak_source": peak_src, "kernel": kernel_name(args, wl, stats),
             "alg_bytes_per_launch": alg_bytes_launch, "launch_ms": round(launch_ms, 4),
             "alg_bytes_per_data_byte": round((n_in + m_out) / n, 4)}
 

@@ -64,6 +64,8 @@ extern "C" {
 #define XSLP_KERNEL_AUTO 0     /* straight-line kernel when compiled, else interpreter */
 #define XSLP_KERNEL_STRAIGHT 1 /* the JIT-compiled straight-line specialisation */
 #define XSLP_KERNEL_INTERP 2   /* the generic SLP interpreter kernel */
+#define XSLP_KERNEL_TMA 3      /* straight-line kernel with TMA (cp.async.bulk) staging of the
+                                  constant strips in shared memory; needs block_bytes % 128 == 0 */
 
 typedef struct xslp_opts {
   int32_t compress;        /* XSLP_COMPRESS_*; default XORREPAIR */
@@ -71,10 +73,11 @@ typedef struct xslp_opts {
   int32_t schedule;        /* XSLP_SCHED_*; default DFS */
   int32_t specialise;      /* 1 = emit PTX and compile the straight-line kernel now; default 1 */
   int32_t lane_words;      /* 32-bit words per thread per strip in the straight-line kernel: 1, 2 or 4; default 1 */
-  int32_t threads;         /* CTA size of both kernels (32..1024, multiple of 32); default 256 */
+  int32_t threads;         /* CTA size of the kernels (32..1024, multiple of 32); default 128 */
   int64_t block_bytes_hint;/* if > 0, bake strip = hint/8 into the straight-line kernel's addressing */
   int32_t kernel;          /* XSLP_KERNEL_* used by xslp_encode/decode(_batch); default AUTO */
   int32_t goal_order;      /* DFS root order: 0 = by the term order of the goal nodes, 1 = goal index */
+  int32_t min_blocks;      /* if > 0, ask ptxas for this many resident CTAs per SM (.minnctapersm) */
 } xslp_opts;
 
 typedef struct xslp_stats {
@@ -89,6 +92,8 @@ typedef struct xslp_stats {
   int32_t n_zero_goals; /* goals equal to the empty set (all-zero rows) */
   int32_t regs;       /* registers per thread of the straight-line kernel (0 if not compiled) */
   int32_t spill_bytes;/* local-memory spill stores of the straight-line kernel */
+  int32_t regs_tma;   /* registers per thread of the TMA-staged straight-line kernel */
+  int32_t spill_bytes_tma; /* its spill stores */
   double compile_ms;  /* host compile time of xslp_compile (SLP passes + PTX -> cubin) */
 } xslp_stats;
 
@@ -167,6 +172,17 @@ int xslp_decode_batch_multi(const xslp_program *const *progs, int nprogs,
                             const int32_t *d_prog_of_stripe, const uint8_t *const *d_in_tbl,
                             uint8_t *const *d_out_tbl, int nstripes, size_t block_bytes,
                             void *stream);
+
+/* Many stripes, a program per stripe, grouped: the stripes of program i are
+ * d_stripe_ids[group_offsets[i] .. group_offsets[i+1]) (a DEVICE int32 array of stripe
+ * indices into d_in_tbl / d_out_tbl); group_offsets is a HOST array of nprogs+1
+ * non-decreasing offsets.  Each program's straight-line (or TMA) kernel runs over its
+ * own stripes; launches fan out over `nstreams` internal streams that fork from and
+ * join back into `stream`.  Programs must share n_const and n_goals. */
+int xslp_decode_batch_grouped(const xslp_program *const *progs, int nprogs,
+                              const int32_t *d_stripe_ids, const int32_t *group_offsets,
+                              const uint8_t *const *d_in_tbl, uint8_t *const *d_out_tbl,
+                              size_t block_bytes, int nstreams, void *stream);
 
 /* End-to-end form with HOST buffers: h_in = [nstripes][n][block_bytes] and
  * h_out = [nstripes][m][block_bytes], contiguous (ideally pinned) host memory.

@@ -31,11 +31,11 @@ XSLP_ECUDA, XSLP_ENOMEM, XSLP_ECOMPILE = -4, -5, -6
 XSLP_RS_ISAL, XSLP_RS_SYSVAND, XSLP_CAUCHY = 0, 1, 2
 XSLP_COMPRESS_NONE, XSLP_COMPRESS_REPAIR, XSLP_COMPRESS_XORREPAIR = 0, 1, 2
 XSLP_SCHED_NONE, XSLP_SCHED_DFS = 0, 1
-XSLP_KERNEL_AUTO, XSLP_KERNEL_STRAIGHT, XSLP_KERNEL_INTERP = 0, 1, 2
+XSLP_KERNEL_AUTO, XSLP_KERNEL_STRAIGHT, XSLP_KERNEL_INTERP, XSLP_KERNEL_TMA = 0, 1, 2, 3
 
 KINDS = {"isal": XSLP_RS_ISAL, "sysvand": XSLP_RS_SYSVAND, "cauchy": XSLP_CAUCHY}
 COMPRESS = {"none": 0, "repair": 1, "xorrepair": 2}
-KERNELS = {"auto": 0, "straight": 1, "interp": 2}
+KERNELS = {"auto": 0, "straight": 1, "interp": 2, "tma": 3}
 
 
 class xslp_opts(ctypes.Structure):
@@ -43,7 +43,7 @@ class xslp_opts(ctypes.Structure):
                 ("schedule", ctypes.c_int32), ("specialise", ctypes.c_int32),
                 ("lane_words", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("block_bytes_hint", ctypes.c_int64), ("kernel", ctypes.c_int32),
-                ("goal_order", ctypes.c_int32)]
+                ("goal_order", ctypes.c_int32), ("min_blocks", ctypes.c_int32)]
 
 
 class xslp_stats(ctypes.Structure):
@@ -52,7 +52,8 @@ class xslp_stats(ctypes.Structure):
                 ("n_instr", ctypes.c_int32), ("nvar", ctypes.c_int32),
                 ("maxlive", ctypes.c_int32), ("n_copy_goals", ctypes.c_int32),
                 ("n_zero_goals", ctypes.c_int32), ("regs", ctypes.c_int32),
-                ("spill_bytes", ctypes.c_int32), ("compile_ms", ctypes.c_double)]
+                ("spill_bytes", ctypes.c_int32), ("regs_tma", ctypes.c_int32),
+                ("spill_bytes_tma", ctypes.c_int32), ("compile_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -76,6 +77,8 @@ _sig = {
     "xslp_encode_batch": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_size_t, _P]),
     "xslp_decode_batch_multi": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, ctypes.c_int,
                                                ctypes.c_size_t, _P]),
+    "xslp_decode_batch_grouped": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, _P, ctypes.c_size_t,
+                                                 ctypes.c_int, _P]),
     "xslp_encode_host": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_size_t, _P]),
     "xslp_fill_random": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_size_t,
                                         ctypes.c_uint64, ctypes.c_int64, _P]),
@@ -233,6 +236,27 @@ def xslp_decode_batch_multi(progs, d_prog_of_stripe, d_in_tbl, d_out_tbl, nstrip
     arr = (ctypes.c_void_p * len(progs))(*[p.handle for p in progs])
     _check(_lib.xslp_decode_batch_multi(arr, len(progs), _ptr(d_prog_of_stripe), _ptr(d_in_tbl),
                                         _ptr(d_out_tbl), nstripes, block_bytes, _stream(stream)))
+
+
+def xslp_decode_batch_grouped(progs, d_stripe_ids, group_offsets, d_in_tbl, d_out_tbl, block_bytes,
+                              nstreams=8, stream=None):
+    arr = (ctypes.c_void_p * len(progs))(*[p.handle for p in progs])
+    off = np.ascontiguousarray(group_offsets, dtype=np.int32)
+    if len(off) != len(progs) + 1:
+        raise ValueError("group_offsets needs len(progs) + 1 entries")
+    _check(_lib.xslp_decode_batch_grouped(arr, len(progs), _ptr(d_stripe_ids), off.ctypes.data,
+                                          _ptr(d_in_tbl), _ptr(d_out_tbl), block_bytes, nstreams,
+                                          _stream(stream)))
+
+
+def group_stripes(prog_of_stripe, nprogs):
+    """Host helper: (stripe ids sorted by program, offsets[nprogs+1]) for the grouped call."""
+    pos = np.asarray(prog_of_stripe, dtype=np.int64)
+    order = np.argsort(pos, kind="stable").astype(np.int32)
+    counts = np.bincount(pos, minlength=nprogs)
+    off = np.zeros(nprogs + 1, dtype=np.int32)
+    off[1:] = np.cumsum(counts)
+    return order, off
 
 
 def xslp_encode_host(prog, h_in, h_out, nstripes, block_bytes, stream=None):

@@ -1,6 +1,6 @@
 """Build libxslp.so in-tree with nvcc for sm_100a (no GPU needed).
 
-    python -m paper_2108_02692_b200.build         # or __graft_entry__.build()
+    python paper_2108_02692_b200/build.py [--force]     # or __graft_entry__.build()
 
 The library statically links the CUDA runtime and nvPTXCompiler (the in-process
 PTX -> sm_100a compiler used by the straight-line specialisation), so it loads

@@ -37,10 +37,11 @@ extern "C" void xslp_default_opts(xslp_opts *o) {
   o->schedule = XSLP_SCHED_DFS;
   o->specialise = 1;
   o->lane_words = 1;
-  o->threads = 256;
+  o->threads = 128;
   o->block_bytes_hint = 0;
   o->kernel = XSLP_KERNEL_AUTO;
   o->goal_order = 0;
+  o->min_blocks = 0;
 }
 
 extern "C" int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out) {
@@ -134,16 +135,25 @@ void finish(Program &P, const std::vector<Bits> *want) {
     if (g < 0) st.n_zero_goals++;
     else if (g < P.n_const) st.n_copy_goals++;
   }
-  st.regs = st.spill_bytes = 0;
+  {
+    std::vector<char> u(P.n_const, 0);
+    for (auto &in : P.slp.ins)
+      for (int t : in.ops)
+        if (t < P.n_const) u[t] = 1;
+    for (int g : P.slp.goal)
+      if (g >= 0 && g < P.n_const) u[g] = 1;
+    P.n_used_const = (int)std::count(u.begin(), u.end(), 1);
+  }
+  st.regs = st.spill_bytes = st.regs_tma = st.spill_bytes_tma = 0;
   const bool device_ok = P.n_const % 8 == 0 && P.n_goals % 8 == 0 && P.n_const > 0 &&
                          P.n_const / 8 + P.n_goals / 8 <= 128;
   if (o.specialise && device_ok) {
-    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads);
-    P.cubin_generic = ptx_to_cubin(P.ptx_generic, &st.regs, &st.spill_bytes);
+    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads, o.min_blocks);
+    P.cubin_generic = ptx_to_cubin(P.ptx_generic, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma);
     if (o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0) {
       P.baked_strip = o.block_bytes_hint / 8;
-      P.ptx_baked = emit_ptx(P.slp, o.lane_words, P.baked_strip, o.threads);
-      P.cubin_baked = ptx_to_cubin(P.ptx_baked, &st.regs, &st.spill_bytes);
+      P.ptx_baked = emit_ptx(P.slp, o.lane_words, P.baked_strip, o.threads, o.min_blocks);
+      P.cubin_baked = ptx_to_cubin(P.ptx_baked, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma);
     }
   }
   st.compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -155,7 +165,8 @@ void check_opts(const xslp_opts &o) {
   if (o.lane_words != 1 && o.lane_words != 2 && o.lane_words != 4)
     throw Error(XSLP_EINVAL, "lane_words must be 1, 2 or 4");
   if (o.threads < 32 || o.threads > 1024 || o.threads % 32) throw Error(XSLP_EINVAL, "bad threads");
-  if (o.kernel < 0 || o.kernel > 2) throw Error(XSLP_EINVAL, "bad kernel option");
+  if (o.kernel < 0 || o.kernel > 3) throw Error(XSLP_EINVAL, "bad kernel option");
+  if (o.min_blocks < 0 || o.min_blocks > 32) throw Error(XSLP_EINVAL, "bad min_blocks");
 }
 
 }  // namespace

@@ -131,7 +131,8 @@ struct Program::Dev {
 
 struct JitLib {
   cudaLibrary_t lib = nullptr;
-  cudaKernel_t batch = nullptr, one = nullptr;
+  cudaKernel_t batch = nullptr, one = nullptr, tma = nullptr;
+  std::map<int, int> smem_set;  // device -> max dynamic smem configured for `tma`
 };
 
 // Libraries are context independent (cudaLibraryLoadData); keyed by program serial.
@@ -143,6 +144,7 @@ static void load_lib(const std::vector<char> &cubin, JitLib &L) {
   CUDA_OK(cudaLibraryLoadData(&L.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
   CUDA_OK(cudaLibraryGetKernel(&L.batch, L.lib, "xslp_sl_batch"));
   CUDA_OK(cudaLibraryGetKernel(&L.one, L.lib, "xslp_sl_one"));
+  CUDA_OK(cudaLibraryGetKernel(&L.tma, L.lib, "xslp_sl_tma"));
 }
 
 static std::pair<JitLib, JitLib> libs_of(const Program *p) {
@@ -265,19 +267,37 @@ static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *c
   bool baked = false;
   const int kind = p->opts.kernel;
   bool straight = kind != XSLP_KERNEL_INTERP && can_straight(p, block_bytes, baked);
-  if (kind == XSLP_KERNEL_STRAIGHT && !straight)
+  if ((kind == XSLP_KERNEL_STRAIGHT || kind == XSLP_KERNEL_TMA) && !straight)
     throw Error(XSLP_EINVAL, "straight-line kernel unavailable for this block size / program");
   if (straight) {
-    auto libs = libs_of(p);
-    const JitLib &L = baked ? libs.second : libs.first;
+    const bool tma = kind == XSLP_KERNEL_TMA;
     const int T = p->opts.threads;
     uint64_t strip = block_bytes / 8;
+    if (tma && strip % 16)
+      throw Error(XSLP_EINVAL, "TMA staging needs block_bytes % 128 == 0");
     uint32_t words = (uint32_t)(strip / (4 * p->opts.lane_words));
+    size_t smem = 0;
+    cudaKernel_t k;
+    {
+      libs_of(p);
+      std::lock_guard<std::mutex> g(g_mu);
+      JitLib &L = baked ? g_libs[p].second : g_libs[p].first;
+      k = tma ? L.tma : L.batch;
+      if (tma) {
+        smem = 128 + (size_t)p->n_used_const * 4 * p->opts.lane_words * T;
+        if (smem > 227 * 1024) throw Error(XSLP_EINVAL, "TMA tile does not fit in shared memory; use fewer threads");
+        const int d = current_device();
+        if (L.smem_set[d] < (int)smem) {
+          CUDA_OK(cudaKernelSetAttributeForDevice(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem, d));
+          L.smem_set[d] = (int)smem;
+        }
+      }
+    }
     for (int base = 0; base < nstripes; base += 65535) {
       uint32_t b = (uint32_t)base;
       void *args[] = {(void *)&d_in, (void *)&d_out, (void *)&d_ids, &strip, &words, &b};
       dim3 grid((words + T - 1) / T, std::min(65535, nstripes - base));
-      CUDA_OK(cudaLaunchKernel((const void *)L.batch, grid, dim3(T), args, 0, st));
+      CUDA_OK(cudaLaunchKernel((const void *)k, grid, dim3(T), args, smem, st));
       g_launches++;
     }
     return;
@@ -356,6 +376,56 @@ static Pool pool_of(const Program *const *progs, int np) {
   CUDA_OK(cudaMemcpy(P.off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
   g_pools[{d, key}] = P;
   return P;
+}
+
+// ---------------------------------------------------------------------------------
+// Grouped heterogeneous decode: stripes sorted by program on the host; each program's
+// straight-line kernel runs over its own stripe-id list.  The launches fan out over a
+// per-device pool of internal streams (fork / join with events on the caller's stream)
+// so the small per-pattern kernels overlap on the GPU.
+struct StreamPool {
+  std::vector<cudaStream_t> st;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t fork = nullptr;
+};
+static std::map<int, StreamPool> g_pools_st;
+static std::mutex g_st_mu;
+
+static void grouped(const Program *const *progs, int np, const int32_t *d_ids,
+                    const int32_t *off, const uint8_t *const *d_in, uint8_t *const *d_out,
+                    size_t B, cudaStream_t user, int nstreams) {
+  if (!progs || np <= 0 || !off || !d_ids) throw Error(XSLP_EINVAL, "bad grouped arguments");
+  for (int i = 0; i < np; ++i) {
+    if (!progs[i]) throw Error(XSLP_EINVAL, "null program");
+    if (progs[i]->n_const != progs[0]->n_const || progs[i]->n_goals != progs[0]->n_goals)
+      throw Error(XSLP_EINVAL, "programs disagree on constants/goals");
+    if (off[i + 1] < off[i]) throw Error(XSLP_EINVAL, "group offsets must be non-decreasing");
+  }
+  if (off[0] < 0) throw Error(XSLP_EINVAL, "negative group offset");
+  nstreams = std::max(1, std::min(nstreams, 32));
+  const int d = current_device();
+  std::lock_guard<std::mutex> g(g_st_mu);
+  StreamPool &P = g_pools_st[d];
+  while ((int)P.st.size() < nstreams) {
+    cudaStream_t s;
+    cudaEvent_t e;
+    CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    P.st.push_back(s);
+    P.ev.push_back(e);
+  }
+  if (!P.fork) CUDA_OK(cudaEventCreateWithFlags(&P.fork, cudaEventDisableTiming));
+  CUDA_OK(cudaEventRecord(P.fork, user));
+  for (int k = 0; k < nstreams; ++k) CUDA_OK(cudaStreamWaitEvent(P.st[k], P.fork, 0));
+  for (int i = 0; i < np; ++i) {
+    const int cnt = off[i + 1] - off[i];
+    if (cnt == 0) continue;
+    apply_batch(progs[i], d_in, d_out, d_ids + off[i], cnt, B, P.st[i % nstreams]);
+  }
+  for (int k = 0; k < nstreams; ++k) {
+    CUDA_OK(cudaEventRecord(P.ev[k], P.st[k]));
+    CUDA_OK(cudaStreamWaitEvent(user, P.ev[k], 0));
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -511,6 +581,22 @@ extern "C" int xslp_decode_batch_multi(const xslp_program *const *progs, int npr
     launch_interp(pool.code, pool.off, d_prog_of_stripe, T, ps[0], nsl, d_in_tbl, d_out_tbl,
                   nstripes, block_bytes, (cudaStream_t)stream, nullptr);
   }
+  API_END
+}
+
+extern "C" int xslp_decode_batch_grouped(const xslp_program *const *progs, int nprogs,
+                                         const int32_t *d_stripe_ids, const int32_t *group_offsets,
+                                         const uint8_t *const *d_in_tbl, uint8_t *const *d_out_tbl,
+                                         size_t block_bytes, int nstreams, void *stream) {
+  API_BEGIN
+  if (!progs || nprogs <= 0) throw Error(XSLP_EINVAL, "no programs");
+  std::vector<const Program *> ps;
+  for (int i = 0; i < nprogs; ++i) ps.push_back(P(progs[i]));
+  if (!d_in_tbl || !d_out_tbl) throw Error(XSLP_EINVAL, "null table");
+  check_geometry(ps[0], block_bytes);
+  if (block_bytes == 0) return XSLP_OK;
+  grouped(ps.data(), nprogs, d_stripe_ids, group_offsets, d_in_tbl, d_out_tbl, block_bytes,
+          (cudaStream_t)stream, nstreams);
   API_END
 }
 

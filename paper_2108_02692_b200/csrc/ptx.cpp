@@ -16,6 +16,7 @@
 //   xslp_sl_one(ptrs[128], strip_bytes, words)
 //     one stripe, pointers passed by value (in[0..n_in), out[n_in..n_in+n_out))
 // With a baked strip size the 8 strips of a block are addressed by immediate offsets.
+#include <map>
 #include <sstream>
 
 #include <nvPTXCompiler.h>
@@ -31,10 +32,11 @@ struct Emitter {
   int L;
   int64_t baked;
   int threads;
+  int min_blocks;
   int n_in, n_out;
   std::ostringstream o;
-  Emitter(const Slp &s_, int L_, int64_t baked_, int threads_)
-      : s(s_), L(L_), baked(baked_), threads(threads_), n_in(s_.n_const / 8),
+  Emitter(const Slp &s_, int L_, int64_t baked_, int threads_, int min_blocks_)
+      : s(s_), L(L_), baked(baked_), threads(threads_), min_blocks(min_blocks_), n_in(s_.n_const / 8),
         n_out((int)(s_.goal.size() / 8)) {}
 
   std::string creg(int c, int l) { return "%c" + std::to_string(c * L + l); }
@@ -58,23 +60,30 @@ struct Emitter {
     return "[" + t + "]";
   }
 
-  void body(bool one) {
+  // mode 0: batch, constants loaded from HBM into registers (LDG)
+  // mode 1: one stripe, pointers in the parameter block (LDG)
+  // mode 2: batch, the CTA's tile of every constant strip staged into shared memory by
+  //         TMA bulk copies (cp.async.bulk, one mbarrier), constants read from smem at use
+  void body(int mode) {
+    const bool one = mode == 1, tma = mode == 2;
     const int nc = s.n_const;
     std::vector<char> used(nc, 0);
-    std::vector<int> last_c(nc, -1);
     for (size_t k = 0; k < s.ins.size(); ++k)
       for (int t : s.ins[k].ops)
-        if (t < nc) { used[t] = 1; last_c[t] = (int)k; }
+        if (t < nc) used[t] = 1;
     for (int g : s.goal)
       if (g >= 0 && g < nc) used[g] = 1;
     std::vector<char> blk_used(n_in, 0);
+    std::vector<int> slot(nc, -1);
+    int nused = 0;
     for (int c = 0; c < nc; ++c)
-      if (used[c]) blk_used[c / 8] = 1;
+      if (used[c]) { blk_used[c / 8] = 1; slot[c] = nused++; }
+    const int rowb = 4 * L * threads;  // smem bytes per constant row (TMA mode)
 
     o << "  mov.u32 %s0, %ctaid.x;\n  mov.u32 %s1, %ntid.x;\n  mov.u32 %s2, %tid.x;\n";
     o << "  mad.lo.u32 %s3, %s0, %s1, %s2;\n";
     o << "  ld.param.u32 %s4, [p_words];\n";
-    o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $DONE;\n";
+    if (!tma) o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $DONE;\n";
     o << "  mul.wide.u32 %off, %s3, " << 4 * L << ";\n";
     if (baked <= 0) {
       o << "  ld.param.u64 %sk1, [p_strip];\n";
@@ -89,40 +98,95 @@ struct Emitter {
       o << "  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
       o << "  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
     }
-    for (int j = 0; j < n_in; ++j) {
-      if (!blk_used[j]) continue;
-      if (one) o << "  ld.param.u64 %ib" << j << ", [p_ptrs+" << 8 * j << "];\n";
-      else o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
-      o << "  add.s64 %ib" << j << ", %ib" << j << ", %off;\n";
+    int tmp = 0;
+    if (tma) {
+      // tile = words [ctaid.x*T, +T) of every strip; bytes per strip this tile
+      o << "  mul.lo.u32 %s7, %s0, " << threads << ";\n";          // first group of the tile
+      o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << threads << ";\n";
+      o << "  mul.lo.u32 %nb, %nb, " << 4 * L << ";\n";
+      o << "  mov.u32 %sb, dsm;\n";
+      o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
+      o << "  mbarrier.init.shared::cta.b64 [%sb], 1;\n  fence.mbarrier_init.release.cluster;\n";
+      o << "$INIT:\n  bar.sync 0;\n  @%p2 bra $WAIT;\n";
+      o << "  mul.lo.u32 %s6, %nb, " << nused << ";\n";
+      o << "  mbarrier.arrive.expect_tx.shared::cta.b64 _, [%sb], %s6;\n";
+      o << "  mul.wide.u32 %toff, %s7, " << 4 * L << ";\n";
+      for (int j = 0; j < n_in; ++j) {
+        if (!blk_used[j]) continue;
+        o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+        o << "  add.s64 %ib" << j << ", %ib" << j << ", %toff;\n";
+      }
+      for (int c = 0; c < nc; ++c) {
+        if (!used[c]) continue;
+        std::string a = addr("%ib" + std::to_string(c / 8), c % 8, tmp);
+        o << "  cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%sb+"
+          << 128 + slot[c] * rowb << "], " << a << ", %nb, [%sb];\n";
+      }
+      o << "$WAIT:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%sb], 0;\n  @!%p3 bra $WAIT;\n";
+      o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $DONE;\n";
+      o << "  mul.lo.u32 %sth, %s2, " << 4 * L << ";\n  add.u32 %sth, %sth, %sb;\n";
+    } else {
+      for (int j = 0; j < n_in; ++j) {
+        if (!blk_used[j]) continue;
+        if (one) o << "  ld.param.u64 %ib" << j << ", [p_ptrs+" << 8 * j << "];\n";
+        else o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+        o << "  add.s64 %ib" << j << ", %ib" << j << ", %off;\n";
+      }
     }
     for (int i = 0; i < n_out; ++i) {
       if (one) o << "  ld.param.u64 %ob" << i << ", [p_ptrs+" << 8 * (n_in + i) << "];\n";
       else o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
       o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
     }
-    int tmp = 0;
-    // loads: every used constant, up front (maximum memory-level parallelism; ptxas
-    // schedules them against register pressure)
-    for (int c = 0; c < nc; ++c) {
-      if (!used[c]) continue;
+    std::vector<char> loaded(nc, 0);
+    auto need = [&](int c) {  // make constant c available in registers
+      if (loaded[c]) return;
+      loaded[c] = 1;
       std::vector<std::string> r;
       for (int l = 0; l < L; ++l) r.push_back(creg(c, l));
-      std::string a = addr("%ib" + std::to_string(c / 8), c % 8, tmp);
-      o << "  ld.global.nc.L1::no_allocate" << vsuf() << " " << vec(r) << ", " << a << ";\n";
-    }
+      if (tma)
+        o << "  ld.shared" << vsuf() << " " << vec(r) << ", [%sth+" << 128 + slot[c] * rowb << "];\n";
+      else {
+        std::string a = addr("%ib" + std::to_string(c / 8), c % 8, tmp);  // may emit an add
+        o << "  ld.global.nc.L1::no_allocate" << vsuf() << " " << vec(r) << ", " << a << ";\n";
+      }
+    };
+    // LDG: every used constant up front (maximum memory-level parallelism; ptxas
+    // schedules them against register pressure).  TMA: smem reads at first use.
+    if (!tma)
+      for (int c = 0; c < nc; ++c)
+        if (used[c]) need(c);
     // goals that are constants or zero
     std::vector<std::vector<int>> goals_of_var(s.n_vars);
     for (size_t g = 0; g < s.goal.size(); ++g) {
       int t = s.goal[g];
       if (t >= nc) { goals_of_var[t - nc].push_back((int)g); continue; }
+      if (t >= 0) need(t);
       std::vector<std::string> r;
       for (int l = 0; l < L; ++l) r.push_back(t < 0 ? std::string("%zero") : creg(t, l));
       store((int)g, r, tmp);
     }
     // the program
+    int qn = 0;
     for (size_t k = 0; k < s.ins.size(); ++k) {
       const auto &in = s.ins[k];
       const auto &ops = in.ops;
+      std::map<int, int> q;  // TMA: constant -> fresh register for this instruction
+      for (int t : ops) {
+        if (t >= nc) continue;
+        if (!tma) { need(t); continue; }
+        q[t] = qn;
+        std::vector<std::string> r;
+        for (int l = 0; l < L; ++l) r.push_back("%q" + std::to_string(qn * L + l));
+        ++qn;
+        // volatile: ptxas must not merge repeated reads and keep constants live in
+        // registers (that would recreate the register pressure TMA staging removes)
+        o << "  ld.volatile.shared" << vsuf() << " " << vec(r) << ", [%sth+" << 128 + slot[t] * rowb << "];\n";
+      }
+      auto treg = [&](int t, int l) {
+        if (tma && t < nc) return "%q" + std::to_string(q[t] * L + l);
+        return this->treg(t, l);
+      };
       for (int l = 0; l < L; ++l) {
         std::string d = vreg(in.var, l);
         size_t i;
@@ -159,6 +223,12 @@ struct Emitter {
     o << "  .reg .b32 %c<" << std::max(1, s.n_const * L) << ">;\n";
     o << "  .reg .b32 %v<" << std::max(1, s.n_vars * L) << ">;\n";
     o << "  .reg .b64 %ta<" << std::max(1, ntmp_guess) << ">;\n";
+    o << "  .reg .b32 %sb, %sth, %nb;\n  .reg .b64 %toff;\n";
+    int nq = 0;
+    for (auto &in : s.ins)
+      for (int t : in.ops)
+        if (t < s.n_const) ++nq;
+    o << "  .reg .b32 %q<" << std::max(1, nq * L) << ">;\n";
     o << "  mov.u32 %zero, 0;\n";
   }
 
@@ -167,19 +237,31 @@ struct Emitter {
       << " goals, " << s.ins.size() << " instructions, lanes=" << L << ", strip="
       << (baked > 0 ? std::to_string(baked) : std::string("runtime")) << "\n//\n";
     o << ".version 8.8\n.target sm_100a\n.address_size 64\n\n";
+    o << ".extern .shared .align 128 .b8 dsm[];\n\n";
     const int ntmp = s.n_const + (int)s.goal.size() + 8;
     o << ".visible .entry xslp_sl_batch(\n  .param .u64 p_in,\n  .param .u64 p_out,\n"
          "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
          "  .param .u32 p_base)\n.maxntid "
-      << threads << ", 1, 1\n{\n";
+      << threads << ", 1, 1\n";
+    if (min_blocks > 0) o << ".minnctapersm " << min_blocks << "\n";
+    o << "{\n";
     decls(ntmp);
-    body(false);
+    body(0);
     o << "}\n\n";
     o << ".visible .entry xslp_sl_one(\n  .param .align 8 .b8 p_ptrs[1024],\n"
          "  .param .u64 p_strip,\n  .param .u32 p_words)\n.maxntid "
       << threads << ", 1, 1\n{\n";
     decls(ntmp);
-    body(true);
+    body(1);
+    o << "}\n\n";
+    o << ".visible .entry xslp_sl_tma(\n  .param .u64 p_in,\n  .param .u64 p_out,\n"
+         "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
+         "  .param .u32 p_base)\n.maxntid "
+      << threads << ", 1, 1\n";
+    if (min_blocks > 0) o << ".minnctapersm " << min_blocks << "\n";
+    o << "{\n";
+    decls(ntmp);
+    body(2);
     o << "}\n";
     return o.str();
   }
@@ -187,16 +269,17 @@ struct Emitter {
 
 }  // namespace
 
-std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads) {
+std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks) {
   if (s.n_const % 8 || s.goal.size() % 8)
     throw Error(XSLP_EINVAL, "device programs need whole blocks (constants and goals multiples of 8)");
   if (s.n_const / 8 + s.goal.size() / 8 > 128)
     throw Error(XSLP_EINVAL, "too many blocks for one kernel (n + m > 128)");
-  Emitter e(s, lanes, baked_strip, threads);
+  Emitter e(s, lanes, baked_strip, threads, min_blocks);
   return e.run();
 }
 
-std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill) {
+std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, int *regs_tma,
+                               int *spill_tma) {
   nvPTXCompilerHandle h = nullptr;
   if (nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS)
     throw Error(XSLP_ECOMPILE, "nvPTXCompilerCreate failed");
@@ -219,21 +302,24 @@ std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill) {
   std::string info(ln + 1, '\0');
   if (ln) nvPTXCompilerGetInfoLog(h, &info[0]);
   nvPTXCompilerDestroy(&h);
-  // parse "Used N registers" / "N bytes spill stores" of the batch entry (first listed)
-  if (regs) {
-    *regs = 0;
-    auto p = info.find("Used ");
-    if (p != std::string::npos) *regs = std::atoi(info.c_str() + p + 5);
-  }
-  if (spill) {
-    *spill = 0;
-    auto p = info.find("bytes spill stores");
-    if (p != std::string::npos) {
-      auto q = info.rfind(',', p);
-      size_t st = (q == std::string::npos) ? 0 : q + 1;
-      *spill = std::atoi(info.c_str() + st);
+  // per-entry "Used N registers" / "N bytes spill stores" from the ptxas info log
+  auto entry_info = [&](const std::string &name, int *r, int *sp) {
+    if (r) *r = 0;
+    if (sp) *sp = 0;
+    auto p = info.find("'" + name + "'");
+    if (p == std::string::npos) return;
+    auto nxt = info.find("Compiling entry function", p + 1);
+    std::string blk = info.substr(p, nxt == std::string::npos ? std::string::npos : nxt - p);
+    auto u = blk.find("Used ");
+    if (u != std::string::npos && r) *r = std::atoi(blk.c_str() + u + 5);
+    auto q = blk.find("bytes spill stores");
+    if (q != std::string::npos && sp) {
+      auto c = blk.rfind(',', q);
+      *sp = std::atoi(blk.c_str() + (c == std::string::npos ? 0 : c + 1));
     }
-  }
+  };
+  entry_info("xslp_sl_batch", regs, spill);
+  entry_info("xslp_sl_tma", regs_tma, spill_tma);
   return bin;
 }
 

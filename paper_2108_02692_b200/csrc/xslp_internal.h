@@ -80,6 +80,7 @@ struct Slp {
 struct Program {
   xslp_opts opts;
   int n_const = 0, n_goals = 0;
+  int n_used_const = 0;           // constants read by the program (TMA rows)
   Slp slp;                         // scheduled program (SSA)
   std::vector<int> pebble;         // paper pebble id per variable
   int nvar = 0;
@@ -111,7 +112,8 @@ std::string dump_slots(const std::vector<uint16_t> &code, int n_const);
 Slp parse_text(const std::string &text, int n_const);
 
 // PTX (ptx.cpp)
-std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads);
-std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill);
+std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks);
+std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, int *regs_tma,
+                               int *spill_tma);
 
 }  // namespace xslp

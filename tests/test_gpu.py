@@ -89,7 +89,7 @@ def test_cfg1_encode_decode(kernel):
 
 @pytest.mark.parametrize("comp", ["none", "repair", "xorrepair"])
 @pytest.mark.parametrize("kern,lanes", [("straight", 1), ("straight", 2), ("straight", 4),
-                                        ("interp", 1)])
+                                        ("interp", 1), ("tma", 1), ("tma", 2)])
 @pytest.mark.parametrize("p", [2, 3, 4])
 def test_rs10_encode_small_full_compare(comp, kern, lanes, p):
     n, B, S = 10, 9600, 5          # strip 1200 B = 300 words: two 256-thread tiles, ragged tail
@@ -105,10 +105,11 @@ def test_rs10_encode_small_full_compare(comp, kern, lanes, p):
         assert (got[s] == rs.encode(og, n, data[s])).all(), s
 
 
-def test_baked_and_generic_strip():
+@pytest.mark.parametrize("kern", ["straight", "tma"])
+def test_baked_and_generic_strip(kern):
     n, p = 10, 4
     og = mx.coding_matrix(n, p)
-    _, prog = compile_enc(n, p, block_bytes_hint=8192)
+    _, prog = compile_enc(n, p, block_bytes_hint=8192, kernel=kern)
     for B in (8192, 4096):            # baked kernel, then the generic-address kernel
         data = host_data(9, range(3), n, B)
         din = torch.from_numpy(data).cuda()
@@ -131,7 +132,7 @@ def _decode_inputs(seed, S, n, p, B, e):
     return pats, blocks
 
 
-@pytest.mark.parametrize("kern", ["interp", "straight"])
+@pytest.mark.parametrize("kern", ["interp", "straight", "grouped", "grouped_tma"])
 def test_heterogeneous_decode(kern):
     n, p, B, S = 10, 4, 4096, 24
     pats, blocks = _decode_inputs(3, S, n, p, B, 4)
@@ -140,7 +141,7 @@ def test_heterogeneous_decode(kern):
     progs, survs = [], {}
     for er in uniq:
         bits, surv = X.xslp_decode_bitmatrix(g, n, p, er)
-        progs.append(X.xslp_compile(bits, kernel=kern))
+        progs.append(X.xslp_compile(bits, kernel={"grouped": "straight", "grouped_tma": "tma"}.get(kern, kern)))
         survs[er] = surv
     idx = torch.tensor([uniq.index(er) for er in pats], dtype=torch.int32, device="cuda")
     surv_blocks = np.stack([blocks[s][survs[pats[s]]] for s in range(S)])
@@ -150,6 +151,9 @@ def test_heterogeneous_decode(kern):
     to = X.block_table(dout, S, 4, B)
     if kern == "interp":
         X.xslp_decode_batch_multi(progs, idx, ti, to, S, B)
+    elif kern.startswith("grouped"):
+        ids, off = X.group_stripes(idx.cpu().numpy(), len(progs))
+        X.xslp_decode_batch_grouped(progs, torch.from_numpy(ids).cuda(), off, ti, to, B, nstreams=4)
     else:   # grouped: one launch per pattern over its stripes (host groups)
         for k, pr in enumerate(progs):
             sel = [s for s in range(S) if pats[s] == uniq[k]]
@@ -225,11 +229,12 @@ def _xor_reduce(t):
     return acc
 
 
-def test_cfg2_full_size_sampled():
+@pytest.mark.parametrize("kern", ["straight", "tma"])
+def test_cfg2_full_size_sampled(kern):
     # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); straight-line kernel, baked strip
     n, p, B, S = 10, 4, 1 << 20, 1024
     og = mx.coding_matrix(n, p)
-    _, prog = compile_enc(n, p, block_bytes_hint=B)
+    _, prog = compile_enc(n, p, block_bytes_hint=B, kernel=kern)
     din = dev_buf(S, n, B)
     X.xslp_fill_random(din, S, n, B, seed=2)
     dout = dev_buf(S, p, B)
@@ -285,11 +290,12 @@ def test_cfg3_full_size_roundtrip_sampled():
     torch.cuda.empty_cache()
 
 
-def test_cfg5_rs20_reduced():
+@pytest.mark.parametrize("kern", ["straight", "tma"])
+def test_cfg5_rs20_reduced(kern):
     # RS(20,4) encode + one seeded 4-erasure decode; 16 stripes x 20 x 1 MiB (configs[4] shape)
     n, p, B, S = 20, 4, 1 << 20, 16
     og = mx.coding_matrix(n, p)
-    g, enc = compile_enc(n, p, block_bytes_hint=B)
+    g, enc = compile_enc(n, p, block_bytes_hint=B, kernel=kern, threads=64)
     allb = dev_buf(S, n + p, B)
     X.xslp_fill_random(allb, S, n + p, B, seed=5)
     d = dev_buf(S, n, B)
@@ -299,7 +305,7 @@ def test_cfg5_rs20_reduced():
     X.xslp_encode_batch(enc, ti[:, :n].contiguous(), ti[:, n:].contiguous(), S, B)
     er = synth.erasure_pattern(5, 0, n + p, 4)
     bits, surv = X.xslp_decode_bitmatrix(g, n, p, er)
-    dec = X.xslp_compile(bits, block_bytes_hint=B)
+    dec = X.xslp_compile(bits, block_bytes_hint=B, kernel=kern, threads=64)
     out = dev_buf(S, 4, B)
     X.xslp_encode_batch(dec, ti[:, torch.as_tensor(surv, dtype=torch.long)].contiguous(),
                         X.block_table(out, S, 4, B), S, B)
