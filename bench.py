@@ -38,6 +38,9 @@ WORKLOADS = {
     "cfg3": dict(desc="RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures, "
                       "one interpreter launch with a program per stripe (BASELINE configs[2])",
                  n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3),
+    "pdec": dict(desc="RS(10,4) decode of the paper's P_dec pattern {2,4,5,6} (P:1670) on every "
+                      "stripe, 1024 stripes x 1 MiB",
+                 n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3),
     "cfg5": dict(desc="RS(20,4) encode, 8192 stripes x 20 x 1 MiB sharded over the GPUs; chunks "
                       "of <=2048 stripes per launch (BASELINE configs[4])",
                  n=20, p=4, B=MiB, S=8192, op="encode_sharded", seed=5, chunk=2048),
@@ -286,6 +289,11 @@ def main():
                                    kernel="tma" if mode in ("tma", "grouped_tma") else "straight")
         prog = progs[0]
         m_out = wl["e"]
+    elif wl["op"] == "decode_one":
+        bits, _surv = X.xslp_decode_bitmatrix(G, n, p, wl["erased"])
+        prog = X.xslp_compile(bits, compress=args.compress, kernel=args.kernel,
+                              lane_words=args.lanes, threads=args.threads, block_bytes_hint=B)
+        m_out = len(wl["erased"])
     else:
         prog = X.xslp_compile(X.xslp_encode_bitmatrix(G, n, p), compress=args.compress,
                               kernel=args.kernel, lane_words=args.lanes, threads=args.threads,
@@ -296,16 +304,17 @@ def main():
     stats = prog.stats()
 
     # ---- device buffers and seeded inputs (untimed) ----
-    if wl["op"] == "encode_sharded":
-        S_total = wl["S"]
-        per = S_total // world
+    from paper_2108_02692_b200.shard import max_over_ranks, stripe_range
+    if wl["op"] == "encode_sharded":      # strong split of 8192 stripes over the ranks
+        lo, hi = stripe_range(rank, world, total=wl["S"])
+        per = hi - lo
         S = min(per, wl["chunk"])
         nchunks = (per + S - 1) // S
-        stripe0 = rank * per
-    else:
+        stripe0 = lo
+    else:                                 # weak scaling: S stripes per rank
         S = wl["S"]
         nchunks = 1
-        stripe0 = rank * S
+        stripe0 = stripe_range(rank, world, per_rank=S)[0]
     n_in = n
     din = torch.empty((S, n_in, B), dtype=torch.uint8, device="cuda")
     dout = torch.empty((S, m_out, B), dtype=torch.uint8, device="cuda")
@@ -334,7 +343,7 @@ def main():
     # sanity (torch, not the product): RAID-5 row of the [I; 2^ij] encode
     launch()
     torch.cuda.synchronize()
-    if wl["op"] != "decode_multi":
+    if wl["op"] not in ("decode_multi", "decode_one"):
         acc = din[:, 0].clone()
         for j in range(1, n):
             acc ^= din[:, j]
@@ -364,10 +373,7 @@ def main():
     torch.cuda.synchronize()
     per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = max_over_ranks(total_ms, dist, device="cuda")
     data_bytes_step = S * nchunks * n * B * world
     value = data_bytes_step * args.steps / (total_ms / 1e3) / 1e9
 

@@ -490,18 +490,20 @@ int paper_pebbles(const Slp &s, std::vector<int> &pebble) {
 // (eager stores) and its slot is released after its last operand use (reading R12).
 // Slots are assigned by a linear scan over the straight-line order (exact max-live).
 //
-// Format (uint16 words):
-//   nloads, then nloads x {const, slot}
-//   ninstr, then per instruction: hdr = arity | has_dst << 15, [dst], ngoals, goals[ngoals],
-//   operand slots[arity].  Copy goals are arity-1 instructions without dst; zero goals
-//   arity-0 ones.
+// Format (uint16 words; the whole program is padded to a multiple of 8 words so it
+// can be staged with 16-byte copies):
+//   [0] nloads  [1] ninstr  [2] total words  [3] nslots
+//   nloads x {const, slot}
+//   per instruction: hdr = arity (bits 0-9) | ngoals << 10 (bits 10-13) | has_dst << 15,
+//   [dst], goals[ngoals], pad to an even index, operand slots[arity], pad to even.
+//   Copy goals are arity-1 instructions without dst; zero goals arity-0 ones.
 void build_bytecode(const Slp &s, std::vector<uint16_t> &code, int &nslots, int &maxlive) {
   const int nc = s.n_const, nv = s.n_vars;
   std::vector<int> last_c(nc, -2), last_v(nv, -2);
   for (int k = 0; k < nv; ++k)
     for (int t : s.ins[k].ops) (t < nc ? last_c[t] : last_v[t - nc]) = k;
   std::vector<std::vector<int>> goals_of_var(nv);
-  std::vector<int> copy_goals, zero_goals;
+  std::vector<int> zero_goals;
   std::vector<std::vector<int>> copies_of_const(nc);
   for (size_t g = 0; g < s.goal.size(); ++g) {
     int t = s.goal[g];
@@ -522,7 +524,6 @@ void build_bytecode(const Slp &s, std::vector<uint16_t> &code, int &nslots, int 
   };
   auto release = [&](int sl) { freeslots.insert(sl); --live; };
   std::vector<int> cslot(nc, -1), vslot(nv, -1);
-  code.clear();
   std::vector<uint16_t> loads, body;
   int nloads = 0, nins = 0;
   for (int c = 0; c < nc; ++c) {
@@ -532,18 +533,28 @@ void build_bytecode(const Slp &s, std::vector<uint16_t> &code, int &nslots, int 
     loads.push_back((uint16_t)cslot[c]);
     ++nloads;
   }
-  auto emit = [&](int arity, int dst, const std::vector<int> &gl, const std::vector<int> &ops) {
-    body.push_back((uint16_t)(arity | (dst >= 0 ? 0x8000 : 0)));
+  // body offsets are relative to the header + loads (an even number of words)
+  auto emit1 = [&](int dst, const std::vector<int> &gl, const std::vector<int> &ops) {
+    body.push_back((uint16_t)(ops.size() | (gl.size() << 10) | (dst >= 0 ? 0x8000 : 0)));
     if (dst >= 0) body.push_back((uint16_t)dst);
-    body.push_back((uint16_t)gl.size());
     for (int g : gl) body.push_back((uint16_t)g);
+    if (body.size() & 1) body.push_back(0);
     for (int o : ops) body.push_back((uint16_t)o);
+    if (body.size() & 1) body.push_back(0);
     ++nins;
   };
-  if (!zero_goals.empty()) emit(0, -1, zero_goals, {});
+  auto emit = [&](int dst, const std::vector<int> &gl, const std::vector<int> &ops) {
+    if (ops.size() > 1023) throw Error(XSLP_EINVAL, "instruction arity > 1023");
+    // at most 15 goals per instruction: extra goals recompute the same XOR first
+    size_t i = 15;
+    for (; i < gl.size(); i += 15)
+      emit1(-1, std::vector<int>(gl.begin() + i, gl.begin() + std::min(gl.size(), i + 15)), ops);
+    emit1(dst, std::vector<int>(gl.begin(), gl.begin() + std::min<size_t>(gl.size(), 15)), ops);
+  };
+  if (!zero_goals.empty()) emit(-1, zero_goals, {});
   for (int c = 0; c < nc; ++c) {
     if (copies_of_const[c].empty()) continue;
-    emit(1, -1, copies_of_const[c], {cslot[c]});
+    emit(-1, copies_of_const[c], {cslot[c]});
     if (last_c[c] < -1) { release(cslot[c]); cslot[c] = -1; }
   }
   for (int k = 0; k < nv; ++k) {
@@ -555,15 +566,19 @@ void build_bytecode(const Slp &s, std::vector<uint16_t> &code, int &nslots, int 
     }
     int dst = -1;
     if (last_v[k] > k) dst = vslot[k] = alloc();
-    emit((int)ops.size(), dst, goals_of_var[k], ops);
+    emit(dst, goals_of_var[k], ops);
   }
-  nslots = next;
-  code.push_back((uint16_t)nloads);
+  nslots = std::max(next, 1);
+  code.assign(4, 0);
   code.insert(code.end(), loads.begin(), loads.end());
-  code.push_back((uint16_t)nins);
   code.insert(code.end(), body.begin(), body.end());
-  if (nc > 0xffff || nslots > 0x7fff || nins > 0xffff)
+  while (code.size() % 8) code.push_back(0);
+  code[0] = (uint16_t)nloads;
+  code[1] = (uint16_t)nins;
+  if (code.size() > 0xffff || nc > 0xffff || nslots > 0x7fff || nins > 0xffff)
     throw Error(XSLP_EINVAL, "program too large for the interpreter bytecode");
+  code[2] = (uint16_t)code.size();
+  code[3] = (uint16_t)nslots;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -606,22 +621,20 @@ std::string dump_pebbles(const Slp &s, const std::vector<int> &peb) {
 std::string dump_slots(const std::vector<uint16_t> &code, int n_const) {
   (void)n_const;
   std::ostringstream o;
-  size_t pc = 0;
-  int nl = code[pc++];
+  const int nl = code[0], ni = code[1];
+  size_t pc = 4;
   for (int i = 0; i < nl; ++i, pc += 2) o << "s" << code[pc + 1] << " = c" << code[pc] << "\n";
-  int ni = code[pc++];
   for (int k = 0; k < ni; ++k) {
-    int hdr = code[pc++];
-    int arity = hdr & 0x7fff & 0xfff;
-    int dst = (hdr & 0x8000) ? code[pc++] : -1;
-    int ng = code[pc++];
+    const int hdr = code[pc++];
+    const int arity = hdr & 1023, ng = (hdr >> 10) & 15;
+    const int dst = (hdr & 0x8000) ? code[pc++] : -1;
     std::vector<int> gl(code.begin() + pc, code.begin() + pc + ng);
     pc += ng;
+    pc += pc & 1;
     std::string name = dst >= 0 ? "s" + std::to_string(dst) : "g" + std::to_string(k);
     std::string rhs;
-    if (arity == 0) rhs = "0";
     for (int a = 0; a < arity; ++a) rhs += (a ? " ^ s" : "s") + std::to_string(code[pc + a]);
-    pc += arity;
+    pc += arity + (arity & 1);
     if (arity == 0) {
       for (int g : gl) o << "out " << g << " = 0\n";
       continue;

@@ -41,19 +41,30 @@ __device__ __forceinline__ uint32_t ld_stream(const uint32_t *p) {
   return v;
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Shared memory: [0,128) mbarrier | code (code_cap u16 words) | slot rows [nslots][T] u32.
+// Constants reach their slot rows by TMA bulk copies (one per used constant, issued by
+// thread 0, completion counted on one mbarrier) when `tma` is set (strip % 16 == 0),
+// otherwise by batched per-thread streaming loads.  The bytecode is staged with
+// coalesced 16-byte copies.
 __global__ void __launch_bounds__(1024) xslp_interp_kernel(
     const uint16_t *__restrict__ code_pool, const int64_t *__restrict__ prog_off,
     const int32_t *__restrict__ prog_of_stripe, const uint8_t *const *__restrict__ in_tbl,
     uint8_t *const *__restrict__ out_tbl, int n_in, int n_out, uint64_t strip, uint32_t words,
-    uint32_t stripe_base, OnePtrs one) {
-  extern __shared__ uint32_t sm[];
-  const uint32_t T = blockDim.x;
-  const uint32_t w = blockIdx.x * T + threadIdx.x;
-  if (w >= words) return;
+    uint32_t stripe_base, int code_cap, int tma, OnePtrs one) {
+  extern __shared__ __align__(128) uint8_t smraw[];
+  const uint32_t T = blockDim.x, tid = threadIdx.x;
+  const uint32_t tile0 = blockIdx.x * T;
+  const uint32_t w = tile0 + tid;
   const uint32_t s = blockIdx.y + stripe_base;
   const int prog = prog_of_stripe ? prog_of_stripe[s] : 0;
-  const uint16_t *code = code_pool + prog_off[prog];
-  uint32_t *my = sm + threadIdx.x;
+  const uint16_t *gcode = code_pool + prog_off[prog];
+  uint16_t *code = reinterpret_cast<uint16_t *>(smraw + 128);
+  uint32_t *rows = reinterpret_cast<uint32_t *>(smraw + 128 + (size_t)code_cap * 2);
+  const uint32_t mbar = smem_u32(smraw);
   const uint8_t *const *in;
   uint8_t *const *out;
   if (in_tbl) {
@@ -63,38 +74,75 @@ __global__ void __launch_bounds__(1024) xslp_interp_kernel(
     in = one.p;
     out = (uint8_t *const *)(one.p + n_in);
   }
-  const size_t off = (size_t)w * 4;
-  int pc = 0;
-  const int nl = code[pc++];
-  int i = 0;
-  for (; i + 8 <= nl; i += 8) {  // batches of 8 independent loads in flight
-    uint32_t v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int c = code[pc + 2 * (i + u)];
-      v[u] = ld_stream((const uint32_t *)(in[c >> 3] + (c & 7) * strip + off));
+  // stage the bytecode (total words is a multiple of 8)
+  const int total = __ldg(gcode + 2);
+  for (int i = tid; i < total / 8; i += T)
+    reinterpret_cast<uint4 *>(code)[i] = __ldg(reinterpret_cast<const uint4 *>(gcode) + i);
+  if (tma && tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nl = code[0];
+  const uint32_t ntile = min(T, words - tile0);
+  if (tma) {
+    if (tid == 0) {
+      const uint32_t bytes = ntile * 4;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar),
+                   "r"(bytes * nl) : "memory");
+      for (int i = 0; i < nl; ++i) {
+        const int c = code[4 + 2 * i], slot = code[5 + 2 * i];
+        const uint8_t *src = in[c >> 3] + (c & 7) * strip + (size_t)tile0 * 4;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_u32(rows + (size_t)slot * T)), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+      }
     }
+    asm volatile(
+        "{\n .reg .pred p;\n XSLP_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra XSLP_WAIT_%=;\n}\n" ::"r"(mbar) : "memory");
+    if (w >= words) return;
+  } else {
+    if (w >= words) return;
+    const size_t off = (size_t)w * 4;
+    int i = 0;
+    for (; i + 16 <= nl; i += 16) {  // 16 independent loads in flight per thread
+      uint32_t v[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) my[code[pc + 2 * (i + u) + 1] * T] = v[u];
+      for (int u = 0; u < 16; ++u) {
+        const int c = code[4 + 2 * (i + u)];
+        v[u] = ld_stream((const uint32_t *)(in[c >> 3] + (c & 7) * strip + off));
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) rows[code[5 + 2 * (i + u)] * T + tid] = v[u];
+    }
+    for (; i < nl; ++i) {
+      const int c = code[4 + 2 * i];
+      rows[code[5 + 2 * i] * T + tid] = ld_stream((const uint32_t *)(in[c >> 3] + (c & 7) * strip + off));
+    }
   }
-  for (; i < nl; ++i) {
-    const int c = code[pc + 2 * i];
-    my[code[pc + 2 * i + 1] * T] = ld_stream((const uint32_t *)(in[c >> 3] + (c & 7) * strip + off));
-  }
-  pc += 2 * nl;
-  const int ni = code[pc++];
+  const size_t off = (size_t)w * 4;
+  uint32_t *my = rows + tid;
+  const uint32_t *code32 = reinterpret_cast<const uint32_t *>(code);
+  int pc = 4 + 2 * nl;
+  const int ni = code[1];
   for (int k = 0; k < ni; ++k) {
     const int hdr = code[pc++];
-    const int arity = hdr & 0xfff;
+    const int arity = hdr & 1023, ng = (hdr >> 10) & 15;
     const int dst = (hdr & 0x8000) ? code[pc++] : -1;
-    const int ng = code[pc++];
     const int gp = pc;
     pc += ng;
+    pc += pc & 1;
     uint32_t acc = 0;
-    int a = 0;
-    for (; a + 2 <= arity; a += 2) acc ^= my[code[pc + a] * T] ^ my[code[pc + a + 1] * T];
-    if (a < arity) acc ^= my[code[pc + a] * T];
-    pc += arity;
+    const uint32_t *ops = code32 + (pc >> 1);
+    const int npairs = arity >> 1;
+#pragma unroll 4
+    for (int q = 0; q < npairs; ++q) {
+      const uint32_t w2 = ops[q];
+      acc ^= my[(w2 & 0xffff) * T] ^ my[(w2 >> 16) * T];
+    }
+    if (arity & 1) acc ^= my[code[pc + arity - 1] * T];
+    pc += arity + (arity & 1);
     if (dst >= 0) my[dst * T] = acc;
     for (int g = 0; g < ng; ++g) {
       const int gi = code[gp + g];
@@ -207,12 +255,24 @@ static void check_geometry(const Program *p, size_t block_bytes) {
   if (block_bytes / 8 / 4 > 0xffffffffull) throw Error(XSLP_EINVAL, "block too large");
 }
 
+static size_t interp_smem(int nslots, int code_cap, int T) {
+  return 128 + (size_t)code_cap * 2 + (size_t)nslots * T * 4;
+}
+
+// code words rounded to 64 (128-byte alignment of the slot rows)
+static int code_cap_of(const Program *const *progs, int np) {
+  size_t m = 8;
+  for (int i = 0; i < np; ++i) m = std::max(m, progs[i]->code.size());
+  return (int)((m + 63) / 64 * 64);
+}
+
 static int interp_threads(const Program *const *progs, int np, int want) {
   int nslots = 1;
   for (int i = 0; i < np; ++i) nslots = std::max(nslots, progs[i]->nslots);
-  const int maxsm = 227 * 1024;
-  int T = std::min(want, (maxsm / (nslots * 4)) / 32 * 32);
-  if (T < 32) throw Error(XSLP_EINVAL, "program needs too many interpreter slots");
+  const int cap = code_cap_of(progs, np);
+  int T = want;
+  while (T >= 32 && interp_smem(nslots, cap, T) > 227 * 1024) T -= 32;
+  if (T < 32) throw Error(XSLP_EINVAL, "program too large for the interpreter's shared memory");
   return T;
 }
 
@@ -229,21 +289,22 @@ static void set_smem_attr() {
 
 // Launch the interpreter over `nstripes` stripes (tables) or one stripe (one != null).
 static void launch_interp(const uint16_t *code_pool, const int64_t *offs, const int32_t *pos,
-                          int np_threads_T, const Program *p0, int nslots_max,
+                          int np_threads_T, const Program *p0, int nslots_max, int code_cap,
                           const uint8_t *const *in_tbl, uint8_t *const *out_tbl, int nstripes,
                           size_t block_bytes, cudaStream_t st, const OnePtrs *one) {
   set_smem_attr();
   const uint64_t strip = block_bytes / 8;
   const uint32_t words = (uint32_t)(strip / 4);
   const int T = np_threads_T;
-  const size_t smem = (size_t)nslots_max * T * 4;
+  const size_t smem = interp_smem(nslots_max, code_cap, T);
+  const int tma = (strip % 16 == 0) && in_tbl != nullptr;
   OnePtrs op{};
   if (one) op = *one;
   for (int base = 0; base < nstripes; base += 65535) {
     dim3 grid((words + T - 1) / T, std::min(65535, nstripes - base));
     xslp_interp_kernel<<<grid, T, smem, st>>>(code_pool, offs, pos, in_tbl, out_tbl,
                                               p0->n_const / 8, p0->n_goals / 8, strip, words,
-                                              (uint32_t)base, op);
+                                              (uint32_t)base, code_cap, tma, op);
     CUDA_OK(cudaGetLastError());
     g_launches++;
   }
@@ -306,8 +367,8 @@ static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *c
   auto D = dev_of(p);
   const Program *ps[1] = {p};
   const int T = interp_threads(ps, 1, p->opts.threads);
-  launch_interp(D->d_code, D->d_off, nullptr, T, p, p->nslots, d_in, d_out, nstripes,
-                block_bytes, st, nullptr);
+  launch_interp(D->d_code, D->d_off, nullptr, T, p, p->nslots, code_cap_of(ps, 1), d_in, d_out,
+                nstripes, block_bytes, st, nullptr);
 }
 
 static void apply_one(const Program *p, const uint8_t *const *in, uint8_t *const *out,
@@ -345,8 +406,8 @@ static void apply_one(const Program *p, const uint8_t *const *in, uint8_t *const
   auto D = dev_of(p);
   const Program *ps[1] = {p};
   const int T = interp_threads(ps, 1, p->opts.threads);
-  launch_interp(D->d_code, D->d_off, nullptr, T, p, p->nslots, nullptr, nullptr, 1, block_bytes,
-                st, &one);
+  launch_interp(D->d_code, D->d_off, nullptr, T, p, p->nslots, code_cap_of(ps, 1), nullptr, nullptr,
+                1, block_bytes, st, &one);
 }
 
 // Pools of several programs' bytecode for one heterogeneous launch, cached by the
@@ -578,8 +639,9 @@ extern "C" int xslp_decode_batch_multi(const xslp_program *const *progs, int npr
     int nsl = 1;
     for (auto q : ps) nsl = std::max(nsl, q->nslots);
     const int T = interp_threads(ps.data(), nprogs, ps[0]->opts.threads);
-    launch_interp(pool.code, pool.off, d_prog_of_stripe, T, ps[0], nsl, d_in_tbl, d_out_tbl,
-                  nstripes, block_bytes, (cudaStream_t)stream, nullptr);
+    launch_interp(pool.code, pool.off, d_prog_of_stripe, T, ps[0], nsl,
+                  code_cap_of(ps.data(), nprogs), d_in_tbl, d_out_tbl, nstripes, block_bytes,
+                  (cudaStream_t)stream, nullptr);
   }
   API_END
 }
