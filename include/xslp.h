@@ -145,6 +145,12 @@ int xslp_program_stats(const xslp_program *prog, xslp_stats *stats);
  * (excluding the NUL), or a negative error. */
 int64_t xslp_program_dump(const xslp_program *prog, int form, char *buf, size_t cap);
 
+/* Cache measures of the program as dumped (form 0) on the paper's abstract LRU cache
+ * (P:1007-1091): *ccap = CCap, the least capacity (in blocks) with no reload;
+ * *iocost = IOcost(prog, capacity) = loads + evictions.  Either output may be NULL
+ * (capacity is ignored when iocost is NULL).  Host-side analysis; not on the device path. */
+int xslp_program_cache(const xslp_program *prog, int capacity, int64_t *iocost, int32_t *ccap);
+
 void xslp_free(xslp_program *prog);
 
 /* ---- device application (timed hot path) ---------------------------------------- */

@@ -72,6 +72,8 @@ _sig = {
     "xslp_program_stats": (ctypes.c_int, [_P, ctypes.POINTER(xslp_stats)]),
     "xslp_program_dump": (ctypes.c_int64, [_P, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t]),
     "xslp_free": (None, [_P]),
+    "xslp_program_cache": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
+                                          ctypes.POINTER(ctypes.c_int32)]),
     "xslp_encode": (ctypes.c_int, [_P, _P, _P, ctypes.c_size_t, _P]),
     "xslp_decode": (ctypes.c_int, [_P, _P, _P, ctypes.c_size_t, _P]),
     "xslp_encode_batch": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_size_t, _P]),
@@ -162,6 +164,16 @@ class Program:
         buf = ctypes.create_string_buffer(n + 1)
         _check(_lib.xslp_program_dump(self._h, form, buf, n + 1))
         return buf.value.decode()
+
+    def ccap(self):
+        c = ctypes.c_int32()
+        _check(_lib.xslp_program_cache(self._h, 0, None, ctypes.byref(c)))
+        return c.value
+
+    def iocost(self, capacity):
+        v = ctypes.c_int64()
+        _check(_lib.xslp_program_cache(self._h, capacity, ctypes.byref(v), None))
+        return v.value
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None

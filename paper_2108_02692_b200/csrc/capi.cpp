@@ -100,7 +100,7 @@ extern "C" int xslp_decode_bitmatrix(const uint8_t *g, int n, int p, const int32
 
 namespace {
 
-void finish(Program &P, const std::vector<Bits> *want) {
+void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
   auto t0 = std::chrono::steady_clock::now();
   const xslp_opts &o = P.opts;
   if (o.fuse) fuse(P.slp);
@@ -111,7 +111,9 @@ void finish(Program &P, const std::vector<Bits> *want) {
     for (size_t i = 0; i < got.size(); ++i)
       if (!(got[i] == (*want)[i])) throw Error(XSLP_EINVAL, "internal: compiled SLP differs from its input");
   }
-  if (o.schedule == XSLP_SCHED_DFS) {
+  if (o.schedule == XSLP_SCHED_DFS || (lifted && o.compress == XSLP_COMPRESS_NONE && !o.fuse)) {
+    // DFS pebbles; the unoptimised binary chains ("Base") are in place,
+    // g <- g ^ c, which the same movable-pebble rule reproduces (NVar 32)
     P.nvar = paper_pebbles(P.slp, P.pebble);
   } else {
     P.pebble.clear();
@@ -197,7 +199,7 @@ extern "C" int xslp_compile(const uint8_t *bits, int out_rows, int in_cols, cons
   else
     P->slp = compress(goals, in_cols, P->opts.compress == XSLP_COMPRESS_XORREPAIR);
   P->stats.compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  finish(*P, &goals);
+  finish(*P, &goals, true);
   *out = reinterpret_cast<xslp_program *>(P.release());
   API_END
 }
@@ -218,7 +220,7 @@ extern "C" int xslp_compile_text(const char *text, int n_const, const xslp_opts 
   if (P->opts.compress == XSLP_COMPRESS_NONE) P->slp = s;
   else P->slp = compress(goals, n_const, P->opts.compress == XSLP_COMPRESS_XORREPAIR);
   P->stats.compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  finish(*P, &goals);
+  finish(*P, &goals, P->opts.compress != XSLP_COMPRESS_NONE);
   *out = reinterpret_cast<xslp_program *>(P.release());
   API_END
 }
@@ -261,6 +263,19 @@ extern "C" int64_t xslp_program_dump(const xslp_program *prog, int form, char *b
     set_last_error(e.what());
     return XSLP_EINVAL;
   }
+}
+
+extern "C" int xslp_program_cache(const xslp_program *prog, int capacity, int64_t *iocost,
+                                  int32_t *ccap) {
+  API_BEGIN
+  if (!prog) throw Error(XSLP_EINVAL, "null program");
+  const Program &P = *reinterpret_cast<const Program *>(prog);
+  if (ccap) *ccap = lru_ccap(P.slp, P.pebble);
+  if (iocost) {
+    if (capacity <= 0) throw Error(XSLP_EINVAL, "capacity must be positive");
+    *iocost = lru_iocost(P.slp, P.pebble, capacity);
+  }
+  API_END
 }
 
 extern "C" void xslp_free(xslp_program *prog) { delete reinterpret_cast<Program *>(prog); }

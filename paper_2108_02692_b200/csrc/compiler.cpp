@@ -605,6 +605,73 @@ static std::string tname(const Slp &s, const std::vector<int> &peb, int t) {
   return "p" + std::to_string(peb.empty() ? t - s.n_const : peb[t - s.n_const]);
 }
 
+// ---------------------------------------------------------------------------------------
+// Abstract LRU cache of P:1007-1022 over the program as dumped (pebble names when
+// present): per instruction, touch-or-load the operands in order, then touch-or-allocate
+// the target, evicting the least recently used block when full.  Returns loads,
+// evictions and reloads (a load of a block that was in the cache before).
+struct LruResult { int64_t loads = 0, evictions = 0, reloads = 0; };
+
+static LruResult lru_run(const Slp &s, const std::vector<int> &peb, int cap) {
+  const int nc = s.n_const;
+  auto name = [&](int t) { return t < nc ? t : nc + (peb.empty() ? t - nc : peb[t - nc]); };
+  std::vector<int> cache;  // front = LRU
+  std::vector<char> seen;
+  LruResult r;
+  auto find = [&](int x) { return std::find(cache.begin(), cache.end(), x); };
+  auto room = [&]() {
+    if ((int)cache.size() >= cap) { cache.erase(cache.begin()); r.evictions++; }
+  };
+  for (auto &in : s.ins) {
+    for (int t : in.ops) {
+      int x = name(t);
+      if ((int)seen.size() <= x) seen.resize(x + 1, 0);
+      auto it = find(x);
+      if (it != cache.end()) { cache.erase(it); cache.push_back(x); continue; }
+      room();
+      r.loads++;
+      if (seen[x]) r.reloads++;
+      seen[x] = 1;
+      cache.push_back(x);
+    }
+    int x = name(nc + in.var);
+    if ((int)seen.size() <= x) seen.resize(x + 1, 0);
+    auto it = find(x);
+    if (it != cache.end()) { cache.erase(it); cache.push_back(x); continue; }
+    room();
+    seen[x] = 1;
+    cache.push_back(x);
+  }
+  return r;
+}
+
+int64_t lru_iocost(const Slp &s, const std::vector<int> &peb, int cap) {
+  for (auto &in : s.ins)
+    if ((int)in.ops.size() + 1 > cap) throw Error(XSLP_EINVAL, "capacity smaller than one instruction");
+  auto r = lru_run(s, peb, cap);
+  return r.loads + r.evictions;
+}
+
+// CCap: least capacity without reloads.  LRU has the inclusion property,
+// so reload-freedom is monotone in the capacity and a binary search is exact.
+int lru_ccap(const Slp &s, const std::vector<int> &peb) {
+  int lo = 1, hi = 1;
+  std::set<int> names;
+  const int nc = s.n_const;
+  for (auto &in : s.ins) {
+    lo = std::max(lo, (int)in.ops.size() + 1);
+    for (int t : in.ops) names.insert(t < nc ? t : nc + (peb.empty() ? t - nc : peb[t - nc]));
+    names.insert(nc + (peb.empty() ? in.var : peb[in.var]));
+  }
+  hi = std::max(lo, (int)names.size());
+  if (s.ins.empty()) return 0;
+  while (lo < hi) {
+    int mid = (lo + hi) / 2;
+    if (lru_run(s, peb, mid).reloads == 0) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
 std::string dump_pebbles(const Slp &s, const std::vector<int> &peb) {
   std::ostringstream o;
   for (auto &in : s.ins) {

@@ -108,6 +108,8 @@ int paper_pebbles(const Slp &s, std::vector<int> &pebble);
 void build_bytecode(const Slp &s, std::vector<uint16_t> &code, int &nslots, int &maxlive);
 std::vector<Bits> evaluate(const Slp &s);
 std::string dump_pebbles(const Slp &s, const std::vector<int> &pebble);
+int64_t lru_iocost(const Slp &s, const std::vector<int> &peb, int cap);
+int lru_ccap(const Slp &s, const std::vector<int> &peb);
 std::string dump_slots(const std::vector<uint16_t> &code, int n_const);
 Slp parse_text(const std::string &text, int n_const);
 
