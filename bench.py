@@ -56,7 +56,9 @@ def parse():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--compress", default="xorrepair", choices=["none", "repair", "xorrepair"])
     ap.add_argument("--kernel", default="auto",
-                    choices=["auto", "straight", "interp", "tma", "grouped", "grouped_tma"])
+                    choices=["auto", "straight", "interp", "tma", "pipe", "grouped", "grouped_tma",
+                             "grouped_pipe"])
+    ap.add_argument("--stages", type=int, default=2)
     ap.add_argument("--streams", type=int, default=8, help="internal streams for grouped decode")
     ap.add_argument("--lanes", type=int, default=1)
     ap.add_argument("--threads", type=int, default=128)
@@ -222,6 +224,8 @@ def kernel_name(args, wl, stats):
         return "xslp_interp_kernel"
     if k in ("tma", "grouped_tma"):
         return "xslp_sl_tma"
+    if k in ("pipe", "grouped_pipe"):
+        return "xslp_sl_pipe"
     return "xslp_sl_batch"
 
 
@@ -231,11 +235,13 @@ def config_of(args, wl, stats):
          else wl["S"] // max(1, args.gpus),
          "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": f"{args.compress}+fuse+dfs",
          "kernel": args.kernel, "lane_words": args.lanes, "threads": args.threads,
+         "stages": args.stages,
          "l2": "inputs larger than the 126 MB L2; no flush between steps",
          "parallelism": f"stripe-sharded x{args.gpus}, no collective"}
     if stats:
         c["slp"] = {k: stats[k] for k in ("xor_count", "mem_count", "n_instr", "nvar", "maxlive",
-                                          "regs", "spill_bytes", "regs_tma", "spill_bytes_tma")}
+                                          "regs", "spill_bytes", "regs_tma", "spill_bytes_tma",
+                                          "regs_pipe", "spill_bytes_pipe")}
     return c
 
 
@@ -286,18 +292,21 @@ def main():
             progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=1,
                                    threads=args.threads, lane_words=args.lanes,
                                    block_bytes_hint=B,
-                                   kernel="tma" if mode in ("tma", "grouped_tma") else "straight")
+                                   stages=args.stages,
+                                   kernel={"tma": "tma", "grouped_tma": "tma", "pipe": "pipe",
+                                           "grouped_pipe": "pipe"}.get(mode, "straight"))
         prog = progs[0]
         m_out = wl["e"]
     elif wl["op"] == "decode_one":
         bits, _surv = X.xslp_decode_bitmatrix(G, n, p, wl["erased"])
         prog = X.xslp_compile(bits, compress=args.compress, kernel=args.kernel,
-                              lane_words=args.lanes, threads=args.threads, block_bytes_hint=B)
+                              lane_words=args.lanes, threads=args.threads, block_bytes_hint=B,
+                              stages=args.stages)
         m_out = len(wl["erased"])
     else:
         prog = X.xslp_compile(X.xslp_encode_bitmatrix(G, n, p), compress=args.compress,
                               kernel=args.kernel, lane_words=args.lanes, threads=args.threads,
-                              block_bytes_hint=B)
+                              block_bytes_hint=B, stages=args.stages)
         m_out = p
     compile_s = time.perf_counter() - t0
     log(f'compiled in {compile_s:.2f} s', prog.stats())

@@ -66,6 +66,10 @@ extern "C" {
 #define XSLP_KERNEL_INTERP 2   /* the generic SLP interpreter kernel */
 #define XSLP_KERNEL_TMA 3      /* straight-line kernel with TMA (cp.async.bulk) staging of the
                                   constant strips in shared memory; needs block_bytes % 128 == 0 */
+#define XSLP_KERNEL_PIPE 4     /* persistent warp-specialised variant: a producer warp streams
+                                  tiles by TMA through `stages` shared-memory stages (mbarrier
+                                  full/empty ring) while `threads` consumer threads compute;
+                                  needs block_bytes % 128 == 0 */
 
 typedef struct xslp_opts {
   int32_t compress;        /* XSLP_COMPRESS_*; default XORREPAIR */
@@ -78,6 +82,7 @@ typedef struct xslp_opts {
   int32_t kernel;          /* XSLP_KERNEL_* used by xslp_encode/decode(_batch); default AUTO */
   int32_t goal_order;      /* DFS root order: 0 = by the term order of the goal nodes, 1 = goal index */
   int32_t min_blocks;      /* if > 0, ask ptxas for this many resident CTAs per SM (.minnctapersm) */
+  int32_t stages;          /* shared-memory stages of the PIPE kernel (1..8); default 2 */
 } xslp_opts;
 
 typedef struct xslp_stats {
@@ -94,6 +99,8 @@ typedef struct xslp_stats {
   int32_t spill_bytes;/* local-memory spill stores of the straight-line kernel */
   int32_t regs_tma;   /* registers per thread of the TMA-staged straight-line kernel */
   int32_t spill_bytes_tma; /* its spill stores */
+  int32_t regs_pipe;  /* registers per thread of the persistent TMA pipeline kernel */
+  int32_t spill_bytes_pipe; /* its spill stores */
   double compile_ms;  /* host compile time of xslp_compile (SLP passes + PTX -> cubin) */
 } xslp_stats;
 

@@ -32,10 +32,11 @@ XSLP_RS_ISAL, XSLP_RS_SYSVAND, XSLP_CAUCHY = 0, 1, 2
 XSLP_COMPRESS_NONE, XSLP_COMPRESS_REPAIR, XSLP_COMPRESS_XORREPAIR = 0, 1, 2
 XSLP_SCHED_NONE, XSLP_SCHED_DFS = 0, 1
 XSLP_KERNEL_AUTO, XSLP_KERNEL_STRAIGHT, XSLP_KERNEL_INTERP, XSLP_KERNEL_TMA = 0, 1, 2, 3
+XSLP_KERNEL_PIPE = 4
 
 KINDS = {"isal": XSLP_RS_ISAL, "sysvand": XSLP_RS_SYSVAND, "cauchy": XSLP_CAUCHY}
 COMPRESS = {"none": 0, "repair": 1, "xorrepair": 2}
-KERNELS = {"auto": 0, "straight": 1, "interp": 2, "tma": 3}
+KERNELS = {"auto": 0, "straight": 1, "interp": 2, "tma": 3, "pipe": 4}
 
 
 class xslp_opts(ctypes.Structure):
@@ -43,7 +44,8 @@ class xslp_opts(ctypes.Structure):
                 ("schedule", ctypes.c_int32), ("specialise", ctypes.c_int32),
                 ("lane_words", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("block_bytes_hint", ctypes.c_int64), ("kernel", ctypes.c_int32),
-                ("goal_order", ctypes.c_int32), ("min_blocks", ctypes.c_int32)]
+                ("goal_order", ctypes.c_int32), ("min_blocks", ctypes.c_int32),
+                ("stages", ctypes.c_int32)]
 
 
 class xslp_stats(ctypes.Structure):
@@ -53,7 +55,8 @@ class xslp_stats(ctypes.Structure):
                 ("maxlive", ctypes.c_int32), ("n_copy_goals", ctypes.c_int32),
                 ("n_zero_goals", ctypes.c_int32), ("regs", ctypes.c_int32),
                 ("spill_bytes", ctypes.c_int32), ("regs_tma", ctypes.c_int32),
-                ("spill_bytes_tma", ctypes.c_int32), ("compile_ms", ctypes.c_double)]
+                ("spill_bytes_tma", ctypes.c_int32), ("regs_pipe", ctypes.c_int32),
+                ("spill_bytes_pipe", ctypes.c_int32), ("compile_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -42,6 +42,7 @@ extern "C" void xslp_default_opts(xslp_opts *o) {
   o->kernel = XSLP_KERNEL_AUTO;
   o->goal_order = 0;
   o->min_blocks = 0;
+  o->stages = 2;
 }
 
 extern "C" int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out) {
@@ -146,16 +147,16 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
       if (g >= 0 && g < P.n_const) u[g] = 1;
     P.n_used_const = (int)std::count(u.begin(), u.end(), 1);
   }
-  st.regs = st.spill_bytes = st.regs_tma = st.spill_bytes_tma = 0;
+  st.regs = st.spill_bytes = st.regs_tma = st.spill_bytes_tma = st.regs_pipe = st.spill_bytes_pipe = 0;
   const bool device_ok = P.n_const % 8 == 0 && P.n_goals % 8 == 0 && P.n_const > 0 &&
                          P.n_const / 8 + P.n_goals / 8 <= 128;
   if (o.specialise && device_ok) {
-    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads, o.min_blocks);
-    P.cubin_generic = ptx_to_cubin(P.ptx_generic, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma);
+    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads, o.min_blocks, o.stages);
+    P.cubin_generic = ptx_to_cubin(P.ptx_generic, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma, &st.regs_pipe, &st.spill_bytes_pipe);
     if (o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0) {
       P.baked_strip = o.block_bytes_hint / 8;
-      P.ptx_baked = emit_ptx(P.slp, o.lane_words, P.baked_strip, o.threads, o.min_blocks);
-      P.cubin_baked = ptx_to_cubin(P.ptx_baked, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma);
+      P.ptx_baked = emit_ptx(P.slp, o.lane_words, P.baked_strip, o.threads, o.min_blocks, o.stages);
+      P.cubin_baked = ptx_to_cubin(P.ptx_baked, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma, &st.regs_pipe, &st.spill_bytes_pipe);
     }
   }
   st.compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -167,8 +168,10 @@ void check_opts(const xslp_opts &o) {
   if (o.lane_words != 1 && o.lane_words != 2 && o.lane_words != 4)
     throw Error(XSLP_EINVAL, "lane_words must be 1, 2 or 4");
   if (o.threads < 32 || o.threads > 1024 || o.threads % 32) throw Error(XSLP_EINVAL, "bad threads");
-  if (o.kernel < 0 || o.kernel > 3) throw Error(XSLP_EINVAL, "bad kernel option");
+  if (o.kernel < 0 || o.kernel > 4) throw Error(XSLP_EINVAL, "bad kernel option");
   if (o.min_blocks < 0 || o.min_blocks > 32) throw Error(XSLP_EINVAL, "bad min_blocks");
+  if (o.stages < 1 || o.stages > 8) throw Error(XSLP_EINVAL, "stages must be 1..8");
+  if (o.kernel == XSLP_KERNEL_PIPE && o.threads > 992) throw Error(XSLP_EINVAL, "pipe kernel: threads <= 992");
 }
 
 }  // namespace

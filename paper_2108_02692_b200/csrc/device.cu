@@ -179,8 +179,9 @@ struct Program::Dev {
 
 struct JitLib {
   cudaLibrary_t lib = nullptr;
-  cudaKernel_t batch = nullptr, one = nullptr, tma = nullptr;
-  std::map<int, int> smem_set;  // device -> max dynamic smem configured for `tma`
+  cudaKernel_t batch = nullptr, one = nullptr, tma = nullptr, pipe = nullptr;
+  std::map<int, int> smem_set;       // device -> max dynamic smem configured for `tma`
+  std::map<int, int> smem_set_pipe;  // same for `pipe`
 };
 
 // Libraries are context independent (cudaLibraryLoadData); keyed by program serial.
@@ -193,6 +194,7 @@ static void load_lib(const std::vector<char> &cubin, JitLib &L) {
   CUDA_OK(cudaLibraryGetKernel(&L.batch, L.lib, "xslp_sl_batch"));
   CUDA_OK(cudaLibraryGetKernel(&L.one, L.lib, "xslp_sl_one"));
   CUDA_OK(cudaLibraryGetKernel(&L.tma, L.lib, "xslp_sl_tma"));
+  CUDA_OK(cudaLibraryGetKernel(&L.pipe, L.lib, "xslp_sl_pipe"));
 }
 
 static std::pair<JitLib, JitLib> libs_of(const Program *p) {
@@ -328,8 +330,41 @@ static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *c
   bool baked = false;
   const int kind = p->opts.kernel;
   bool straight = kind != XSLP_KERNEL_INTERP && can_straight(p, block_bytes, baked);
-  if ((kind == XSLP_KERNEL_STRAIGHT || kind == XSLP_KERNEL_TMA) && !straight)
+  if ((kind == XSLP_KERNEL_STRAIGHT || kind == XSLP_KERNEL_TMA || kind == XSLP_KERNEL_PIPE) &&
+      !straight)
     throw Error(XSLP_EINVAL, "straight-line kernel unavailable for this block size / program");
+  if (straight && kind == XSLP_KERNEL_PIPE) {
+    const int T = p->opts.threads, L = p->opts.lane_words;
+    uint64_t strip = block_bytes / 8;
+    if (strip % 16) throw Error(XSLP_EINVAL, "TMA staging needs block_bytes % 128 == 0");
+    uint32_t words = (uint32_t)(strip / (4 * L));
+    uint32_t tps = (words + T - 1) / T;
+    if ((uint64_t)tps * (uint64_t)nstripes > 0xffffffffull) throw Error(XSLP_EINVAL, "too many tiles");
+    uint32_t ntiles = tps * (uint32_t)nstripes;
+    const size_t smem = 128 + (size_t)p->opts.stages * p->n_used_const * 4 * L * T;
+    if (smem > 227 * 1024) throw Error(XSLP_EINVAL, "pipeline stages do not fit in shared memory");
+    cudaKernel_t k;
+    int grid;
+    {
+      libs_of(p);
+      std::lock_guard<std::mutex> g(g_mu);
+      JitLib &J = baked ? g_libs[p].second : g_libs[p].first;
+      k = J.pipe;
+      const int d = current_device();
+      if (J.smem_set_pipe[d] < (int)smem) {
+        CUDA_OK(cudaKernelSetAttributeForDevice(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem, d));
+        J.smem_set_pipe[d] = (int)smem;
+      }
+      int sms = 148, per = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)k, T + 32, smem));
+      grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms * std::max(1, per));
+    }
+    void *args[] = {(void *)&d_in, (void *)&d_out, (void *)&d_ids, &strip, &words, &tps, &ntiles};
+    CUDA_OK(cudaLaunchKernel((const void *)k, dim3(grid), dim3(T + 32), args, smem, st));
+    g_launches++;
+    return;
+  }
   if (straight) {
     const bool tma = kind == XSLP_KERNEL_TMA;
     const int T = p->opts.threads;

@@ -33,10 +33,12 @@ struct Emitter {
   int64_t baked;
   int threads;
   int min_blocks;
+  int stages;
   int n_in, n_out;
   std::ostringstream o;
-  Emitter(const Slp &s_, int L_, int64_t baked_, int threads_, int min_blocks_)
-      : s(s_), L(L_), baked(baked_), threads(threads_), min_blocks(min_blocks_), n_in(s_.n_const / 8),
+  Emitter(const Slp &s_, int L_, int64_t baked_, int threads_, int min_blocks_, int stages_)
+      : s(s_), L(L_), baked(baked_), threads(threads_), min_blocks(min_blocks_), stages(stages_),
+        n_in(s_.n_const / 8),
         n_out((int)(s_.goal.size() / 8)) {}
 
   std::string creg(int c, int l) { return "%c" + std::to_string(c * L + l); }
@@ -138,6 +140,118 @@ struct Emitter {
       else o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
       o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
     }
+    compute(tma, 128, slot, used, tmp);
+    o << "$DONE:\n  ret;\n";
+  }
+
+  // Persistent, warp-specialised TMA pipeline (entry xslp_sl_pipe).  threads = consumer
+  // threads TC (NCW warps) plus one producer warp.  Each CTA walks tiles
+  // tile = ctaid.x + i*nctaid.x (tile -> stripe = tile / tps, tw = tile % tps; a tile is
+  // TC lane-groups of every strip); S shared-memory stages of nused rows x 4*L*TC bytes.
+  // Producer (lane 0 of the last warp): wait empty[st] -> expect_tx on full[st] ->
+  // cp.async.bulk every used strip segment into the stage.  Consumers: wait full[st] ->
+  // run the program reading the stage -> stores -> one arrive per warp on empty[st].
+  void body_pipe(int S) {
+    const int nc = s.n_const;
+    const int TC = threads, NCW = threads / 32;
+    std::vector<char> used(nc, 0);
+    for (size_t k = 0; k < s.ins.size(); ++k)
+      for (int t : s.ins[k].ops)
+        if (t < nc) used[t] = 1;
+    for (int g : s.goal)
+      if (g >= 0 && g < nc) used[g] = 1;
+    std::vector<char> blk_used(n_in, 0);
+    std::vector<int> slot(nc, -1);
+    int nused = 0;
+    for (int c = 0; c < nc; ++c)
+      if (used[c]) { blk_used[c / 8] = 1; slot[c] = nused++; }
+    const int rowb = 4 * L * TC;
+    const int64_t STAGE = (int64_t)nused * rowb;
+    const int EB = 8 * S;  // empty barriers follow the full barriers
+    o << "  mov.u32 %s2, %tid.x;\n  mov.u32 %sb, dsm;\n";
+    o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
+    for (int k = 0; k < S; ++k) {
+      o << "  mbarrier.init.shared::cta.b64 [%sb+" << 8 * k << "], 1;\n";
+      o << "  mbarrier.init.shared::cta.b64 [%sb+" << EB + 8 * k << "], " << NCW << ";\n";
+    }
+    o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
+    o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
+    o << "  ld.param.u64 %rd0, [p_ids];\n  setp.ne.u64 %pids, %rd0, 0;\n";
+    o << "  mov.u32 %nct, %nctaid.x;\n";
+    if (baked <= 0) {
+      o << "  ld.param.u64 %sk1, [p_strip];\n";
+      for (int k = 2; k < 8; ++k) o << "  mul.lo.u64 %sk" << k << ", %sk1, " << k << ";\n";
+    }
+    o << "  shr.u32 %wid, %s2, 5;\n  setp.eq.u32 %pprod, %wid, " << NCW << ";\n  @%pprod bra $PROD;\n";
+    // helper: stripe of %tile -> %s5, tile-in-strip -> %tw
+    auto stripe_of = [&](const char *lab) {
+      o << "  div.u32 %s5, %tile, %tps;\n  rem.u32 %tw, %tile, %tps;\n";
+      o << "  @!%pids bra " << lab << ";\n";
+      o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
+      o << lab << ":\n";
+    };
+    // ---------------- consumers
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n  mov.u32 %lane, %laneid;\n";
+    o << "$CLOOP:\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
+    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n  and.b32 %ph, %ph, 1;\n";
+    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
+    o << "$CW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW;\n";
+    stripe_of("$CID");
+    o << "  mad.lo.u32 %s3, %tw, " << TC << ", %s2;\n";
+    o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $CSKIP;\n";
+    o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
+    o << "  mad.lo.u32 %sth, %s2, " << 4 * L << ", %sth;\n  add.u32 %sth, %sth, 128;\n";
+    o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+    o << "  mul.wide.u32 %off, %s3, " << 4 * L << ";\n";
+    for (int i = 0; i < n_out; ++i) {
+      o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+      o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
+    }
+    int tmp = 0;
+    compute(true, 0, slot, used, tmp);
+    o << "$CSKIP:\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT;\n";
+    o << "  add.u32 %eb, %fb, " << EB << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
+    o << "$CNEXT:\n  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, %nct;\n  bra.uni $CLOOP;\n";
+    // ---------------- producer
+    o << "$PROD:\n  mov.u32 %lane, %laneid;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $DONE;\n";
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n";
+    o << "$PLOOP:\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
+    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n";
+    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
+    o << "  setp.lt.u32 %p5, %it, " << S << ";\n  @%p5 bra $PNW;\n";
+    o << "  sub.u32 %ph, %ph, 1;\n  and.b32 %ph, %ph, 1;\n  add.u32 %eb, %fb, " << EB << ";\n";
+    o << "$PW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%eb], %ph;\n  @!%p3 bra $PW;\n";
+    o << "$PNW:\n";
+    stripe_of("$PID");
+    o << "  mul.lo.u32 %s7, %tw, " << TC << ";\n";
+    o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << TC << ";\n  mul.lo.u32 %nb, %nb, " << 4 * L << ";\n";
+    o << "  mul.lo.u32 %s6, %nb, " << nused << ";\n";
+    o << "  mbarrier.arrive.expect_tx.shared::cta.b64 _, [%fb], %s6;\n";
+    o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
+    o << "  mul.wide.u32 %toff, %s7, " << 4 * L << ";\n";
+    for (int j = 0; j < n_in; ++j) {
+      if (!blk_used[j]) continue;
+      o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+      o << "  add.s64 %ib" << j << ", %ib" << j << ", %toff;\n";
+    }
+    o << "  mul.lo.u32 %dst, %st, " << STAGE << ";\n  add.u32 %dst, %dst, %sb;\n";
+    for (int c = 0; c < nc; ++c) {
+      if (!used[c]) continue;
+      std::string a = addr("%ib" + std::to_string(c / 8), c % 8, tmp);
+      o << "  cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%dst+"
+        << 128 + (int64_t)slot[c] * rowb << "], " << a << ", %nb, [%fb];\n";
+    }
+    o << "  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, %nct;\n  bra.uni $PLOOP;\n";
+    o << "$DONE:\n  ret;\n";
+  }
+
+  // The straight-line program over this thread's words: constants come from HBM (LDG,
+  // all issued up front) or, when `smem`, from shared-memory rows at [%sth + off0 +
+  // slot*rowb] with a fresh volatile read per use; goals are stored when computed.
+  void compute(bool tma, int off0, const std::vector<int> &slot, const std::vector<char> &used,
+               int &tmp) {
+    const int nc = s.n_const;
+    const int rowb = 4 * L * threads;
     std::vector<char> loaded(nc, 0);
     auto need = [&](int c) {  // make constant c available in registers
       if (loaded[c]) return;
@@ -145,7 +259,7 @@ struct Emitter {
       std::vector<std::string> r;
       for (int l = 0; l < L; ++l) r.push_back(creg(c, l));
       if (tma)
-        o << "  ld.shared" << vsuf() << " " << vec(r) << ", [%sth+" << 128 + slot[c] * rowb << "];\n";
+        o << "  ld.shared" << vsuf() << " " << vec(r) << ", [%sth+" << off0 + slot[c] * rowb << "];\n";
       else {
         std::string a = addr("%ib" + std::to_string(c / 8), c % 8, tmp);  // may emit an add
         o << "  ld.global.nc.L1::no_allocate" << vsuf() << " " << vec(r) << ", " << a << ";\n";
@@ -181,7 +295,7 @@ struct Emitter {
         ++qn;
         // volatile: ptxas must not merge repeated reads and keep constants live in
         // registers (that would recreate the register pressure TMA staging removes)
-        o << "  ld.volatile.shared" << vsuf() << " " << vec(r) << ", [%sth+" << 128 + slot[t] * rowb << "];\n";
+        o << "  ld.volatile.shared" << vsuf() << " " << vec(r) << ", [%sth+" << off0 + slot[t] * rowb << "];\n";
       }
       auto treg = [&](int t, int l) {
         if (tma && t < nc) return "%q" + std::to_string(q[t] * L + l);
@@ -207,7 +321,6 @@ struct Emitter {
         store(g, r, tmp);
       }
     }
-    o << "$DONE:\n  ret;\n";
   }
 
   void store(int g, const std::vector<std::string> &r, int &tmp) {
@@ -216,7 +329,7 @@ struct Emitter {
   }
 
   void decls(int ntmp_guess) {
-    o << "  .reg .pred %p<4>;\n  .reg .b32 %s<8>;\n  .reg .b64 %rd<8>;\n  .reg .b64 %off;\n";
+    o << "  .reg .pred %p<5>;\n  .reg .b32 %s<8>;\n  .reg .b64 %rd<8>;\n  .reg .b64 %off;\n";
     o << "  .reg .b32 %zero;\n";
     o << "  .reg .b64 %sk<8>;\n";
     o << "  .reg .b64 %ib<" << std::max(1, n_in) << ">;\n  .reg .b64 %ob<" << std::max(1, n_out) << ">;\n";
@@ -224,6 +337,8 @@ struct Emitter {
     o << "  .reg .b32 %v<" << std::max(1, s.n_vars * L) << ">;\n";
     o << "  .reg .b64 %ta<" << std::max(1, ntmp_guess) << ">;\n";
     o << "  .reg .b32 %sb, %sth, %nb;\n  .reg .b64 %toff;\n";
+    o << "  .reg .b32 %tps, %nt, %nct, %wid, %it, %tile, %lane, %st, %ph, %fb, %eb, %tw, %dst;\n";
+    o << "  .reg .pred %pids, %pprod, %p5;\n";
     int nq = 0;
     for (auto &in : s.ins)
       for (int t : in.ops)
@@ -262,6 +377,14 @@ struct Emitter {
     o << "{\n";
     decls(ntmp);
     body(2);
+    o << "}\n\n";
+    o << ".visible .entry xslp_sl_pipe(\n  .param .u64 p_in,\n  .param .u64 p_out,\n"
+         "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
+         "  .param .u32 p_tps,\n  .param .u32 p_ntiles)\n.maxntid "
+      << threads + 32 << ", 1, 1\n";
+    o << "{\n";
+    decls(ntmp);
+    body_pipe(stages);
     o << "}\n";
     return o.str();
   }
@@ -269,17 +392,18 @@ struct Emitter {
 
 }  // namespace
 
-std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks) {
+std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks,
+                     int stages) {
   if (s.n_const % 8 || s.goal.size() % 8)
     throw Error(XSLP_EINVAL, "device programs need whole blocks (constants and goals multiples of 8)");
   if (s.n_const / 8 + s.goal.size() / 8 > 128)
     throw Error(XSLP_EINVAL, "too many blocks for one kernel (n + m > 128)");
-  Emitter e(s, lanes, baked_strip, threads, min_blocks);
+  Emitter e(s, lanes, baked_strip, threads, min_blocks, stages);
   return e.run();
 }
 
 std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, int *regs_tma,
-                               int *spill_tma) {
+                               int *spill_tma, int *regs_pipe, int *spill_pipe) {
   nvPTXCompilerHandle h = nullptr;
   if (nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS)
     throw Error(XSLP_ECOMPILE, "nvPTXCompilerCreate failed");
@@ -320,6 +444,7 @@ std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, in
   };
   entry_info("xslp_sl_batch", regs, spill);
   entry_info("xslp_sl_tma", regs_tma, spill_tma);
+  entry_info("xslp_sl_pipe", regs_pipe, spill_pipe);
   return bin;
 }
 

@@ -89,7 +89,8 @@ def test_cfg1_encode_decode(kernel):
 
 @pytest.mark.parametrize("comp", ["none", "repair", "xorrepair"])
 @pytest.mark.parametrize("kern,lanes", [("straight", 1), ("straight", 2), ("straight", 4),
-                                        ("interp", 1), ("tma", 1), ("tma", 2)])
+                                        ("interp", 1), ("tma", 1), ("tma", 2), ("pipe", 1),
+                                        ("pipe", 2)])
 @pytest.mark.parametrize("p", [2, 3, 4])
 def test_rs10_encode_small_full_compare(comp, kern, lanes, p):
     n, B, S = 10, 9600, 5          # strip 1200 B = 300 words: two 256-thread tiles, ragged tail
@@ -105,7 +106,7 @@ def test_rs10_encode_small_full_compare(comp, kern, lanes, p):
         assert (got[s] == rs.encode(og, n, data[s])).all(), s
 
 
-@pytest.mark.parametrize("kern", ["straight", "tma"])
+@pytest.mark.parametrize("kern", ["straight", "tma", "pipe"])
 def test_baked_and_generic_strip(kern):
     n, p = 10, 4
     og = mx.coding_matrix(n, p)
@@ -132,7 +133,7 @@ def _decode_inputs(seed, S, n, p, B, e):
     return pats, blocks
 
 
-@pytest.mark.parametrize("kern", ["interp", "straight", "grouped", "grouped_tma"])
+@pytest.mark.parametrize("kern", ["interp", "straight", "grouped", "grouped_tma", "grouped_pipe"])
 def test_heterogeneous_decode(kern):
     n, p, B, S = 10, 4, 4096, 24
     pats, blocks = _decode_inputs(3, S, n, p, B, 4)
@@ -141,7 +142,8 @@ def test_heterogeneous_decode(kern):
     progs, survs = [], {}
     for er in uniq:
         bits, surv = X.xslp_decode_bitmatrix(g, n, p, er)
-        progs.append(X.xslp_compile(bits, kernel={"grouped": "straight", "grouped_tma": "tma"}.get(kern, kern)))
+        progs.append(X.xslp_compile(bits, kernel={"grouped": "straight", "grouped_tma": "tma",
+                                                  "grouped_pipe": "pipe"}.get(kern, kern)))
         survs[er] = surv
     idx = torch.tensor([uniq.index(er) for er in pats], dtype=torch.int32, device="cuda")
     surv_blocks = np.stack([blocks[s][survs[pats[s]]] for s in range(S)])
@@ -229,7 +231,7 @@ def _xor_reduce(t):
     return acc
 
 
-@pytest.mark.parametrize("kern", ["straight", "tma"])
+@pytest.mark.parametrize("kern", ["straight", "tma", "pipe"])
 def test_cfg2_full_size_sampled(kern):
     # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); straight-line kernel, baked strip
     n, p, B, S = 10, 4, 1 << 20, 1024
@@ -290,7 +292,7 @@ def test_cfg3_full_size_roundtrip_sampled():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("kern", ["straight", "tma"])
+@pytest.mark.parametrize("kern", ["straight", "tma", "pipe"])
 def test_cfg5_rs20_reduced(kern):
     # RS(20,4) encode + one seeded 4-erasure decode; 16 stripes x 20 x 1 MiB (configs[4] shape)
     n, p, B, S = 20, 4, 1 << 20, 16
