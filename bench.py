@@ -34,16 +34,20 @@ MiB = 1 << 20
 
 WORKLOADS = {
     "cfg2": dict(desc="RS(10,4) encode, 1024 stripes x 10 x 1 MiB per GPU (BASELINE configs[1])",
-                 n=10, p=4, B=MiB, S=1024, op="encode", seed=2),
+                 n=10, p=4, B=MiB, S=1024, op="encode", seed=2,
+                 tuned=dict(kernel="pipe", threads=256, stages=2)),
     "cfg3": dict(desc="RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures, "
                       "one interpreter launch with a program per stripe (BASELINE configs[2])",
-                 n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3),
+                 n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3,
+                 tuned=dict(kernel="grouped", threads=64, stages=2)),
     "pdec": dict(desc="RS(10,4) decode of the paper's P_dec pattern {2,4,5,6} (P:1670) on every "
                       "stripe, 1024 stripes x 1 MiB",
-                 n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3),
+                 n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3,
+                 tuned=dict(kernel="pipe", threads=256, stages=2)),
     "cfg5": dict(desc="RS(20,4) encode, 8192 stripes x 20 x 1 MiB sharded over the GPUs; chunks "
                       "of <=2048 stripes per launch (BASELINE configs[4])",
-                 n=20, p=4, B=MiB, S=8192, op="encode_sharded", seed=5, chunk=2048),
+                 n=20, p=4, B=MiB, S=8192, op="encode_sharded", seed=5, chunk=2048,
+                 tuned=dict(kernel="pipe", threads=128, stages=2)),
 }
 
 
@@ -55,13 +59,13 @@ def parse():
     ap.add_argument("--impl", default="xslp", choices=["xslp", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--compress", default="xorrepair", choices=["none", "repair", "xorrepair"])
-    ap.add_argument("--kernel", default="auto",
+    ap.add_argument("--kernel", default=None,
                     choices=["auto", "straight", "interp", "tma", "pipe", "grouped", "grouped_tma",
                              "grouped_pipe"])
-    ap.add_argument("--stages", type=int, default=2)
+    ap.add_argument("--stages", type=int, default=None)
     ap.add_argument("--streams", type=int, default=8, help="internal streams for grouped decode")
     ap.add_argument("--lanes", type=int, default=1)
-    ap.add_argument("--threads", type=int, default=128)
+    ap.add_argument("--threads", type=int, default=None)
     ap.add_argument("--block-bytes", type=int, default=0, help="override block size")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -249,6 +253,13 @@ def config_of(args, wl, stats):
 def main():
     args = parse()
     wl = dict(WORKLOADS[args.workload])
+    # per-workload tuned launch defaults (profiles/r01_sweep*.md); flags override
+    for k, v in wl.get("tuned", {}).items():
+        if getattr(args, k) is None:
+            setattr(args, k, v)
+    args.kernel = args.kernel or "auto"
+    args.threads = args.threads or 128
+    args.stages = args.stages or 2
     if args.block_bytes:
         scale = wl["B"] // args.block_bytes
         wl["B"] = args.block_bytes

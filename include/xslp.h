@@ -61,7 +61,8 @@ extern "C" {
 #define XSLP_SCHED_NONE 0 /* keep creation order */
 #define XSLP_SCHED_DFS 1  /* DFS post-order + pebble reuse */
 
-#define XSLP_KERNEL_AUTO 0     /* straight-line kernel when compiled, else interpreter */
+#define XSLP_KERNEL_AUTO 0     /* batched calls: PIPE when its stages fit and there are >= 4 tiles per
+                                  SM, else STRAIGHT; interpreter when nothing was compiled */
 #define XSLP_KERNEL_STRAIGHT 1 /* the JIT-compiled straight-line specialisation */
 #define XSLP_KERNEL_INTERP 2   /* the generic SLP interpreter kernel */
 #define XSLP_KERNEL_TMA 3      /* straight-line kernel with TMA (cp.async.bulk) staging of the

@@ -180,8 +180,9 @@ class Program:
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
-        if h:
-            _lib.xslp_free(h)
+        lib = globals().get("_lib")
+        if h and lib is not None:     # at interpreter shutdown the module may be gone
+            lib.xslp_free(h)
 
 
 # ---- matrices -----------------------------------------------------------------------

@@ -320,6 +320,19 @@ static bool can_straight(const Program *p, size_t block_bytes, bool &baked) {
   return strip % (4 * L) == 0;
 }
 
+// AUTO: the persistent TMA pipeline when its stages fit in shared memory and there are
+// enough tiles to keep every SM busy (measured fastest: profiles/r01_*), otherwise the
+// register-resident LDG kernel.
+static int auto_kernel(const Program *p, size_t block_bytes, int nstripes) {
+  const uint64_t strip = block_bytes / 8;
+  const int T = p->opts.threads, L = p->opts.lane_words;
+  if (strip % 16 || p->opts.threads > 992) return XSLP_KERNEL_STRAIGHT;
+  const size_t smem = 128 + (size_t)p->opts.stages * p->n_used_const * 4 * L * T;
+  const uint64_t tiles = (strip / (4 * L) + T - 1) / T * (uint64_t)nstripes;
+  if (smem > 227 * 1024 || p->opts.stages < 2 || tiles < 4 * 148) return XSLP_KERNEL_STRAIGHT;
+  return XSLP_KERNEL_PIPE;
+}
+
 static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *const *d_out,
                         const int32_t *d_ids, int nstripes, size_t block_bytes,
                         cudaStream_t st) {
@@ -328,8 +341,9 @@ static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *c
   if (!d_in || !d_out) throw Error(XSLP_EINVAL, "null pointer table");
   if (nstripes == 0 || block_bytes == 0) return;
   bool baked = false;
-  const int kind = p->opts.kernel;
+  int kind = p->opts.kernel;
   bool straight = kind != XSLP_KERNEL_INTERP && can_straight(p, block_bytes, baked);
+  if (kind == XSLP_KERNEL_AUTO && straight) kind = auto_kernel(p, block_bytes, nstripes);
   if ((kind == XSLP_KERNEL_STRAIGHT || kind == XSLP_KERNEL_TMA || kind == XSLP_KERNEL_PIPE) &&
       !straight)
     throw Error(XSLP_EINVAL, "straight-line kernel unavailable for this block size / program");
