@@ -44,6 +44,10 @@ WORKLOADS = {
                       "stripe, 1024 stripes x 1 MiB",
                  n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3,
                  tuned=dict(kernel="pipe", threads=256, stages=2)),
+    "cfg4": dict(desc="RS(10,p) encode sweep point (BASELINE configs[3]): total data fixed at "
+                      "10 GiB, stripes = 10 GiB / (n x block)",
+                 n=10, p=4, B=MiB, S=1024, op="encode", seed=4,
+                 tuned=dict(kernel="pipe", threads=256, stages=2)),
     "cfg5": dict(desc="RS(20,4) encode, 8192 stripes x 20 x 1 MiB sharded over the GPUs; chunks "
                       "of <=2048 stripes per launch (BASELINE configs[4])",
                  n=20, p=4, B=MiB, S=8192, op="encode_sharded", seed=5, chunk=2048,
@@ -67,6 +71,9 @@ def parse():
     ap.add_argument("--lanes", type=int, default=1)
     ap.add_argument("--threads", type=int, default=None)
     ap.add_argument("--block-bytes", type=int, default=0, help="override block size")
+    ap.add_argument("--p", type=int, default=0, help="override parity count (cfg4 sweep)")
+    ap.add_argument("--fuse", type=int, default=1)
+    ap.add_argument("--schedule", type=int, default=1, help="1 = DFS, 0 = creation order")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -237,7 +244,7 @@ def config_of(args, wl, stats):
     c = {"workload": f"{args.workload}: {wl['desc']}", "n": wl["n"], "p": wl["p"],
          "block_bytes": wl["B"], "stripes_per_gpu": wl["S"] if wl["op"] != "encode_sharded"
          else wl["S"] // max(1, args.gpus),
-         "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": f"{args.compress}+fuse+dfs",
+         "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": args.compress + ("+fuse" if args.fuse else "") + ("+dfs" if args.schedule else ""),
          "kernel": args.kernel, "lane_words": args.lanes, "threads": args.threads,
          "stages": args.stages,
          "l2": "inputs larger than the 126 MB L2; no flush between steps",
@@ -260,10 +267,12 @@ def main():
     args.kernel = args.kernel or "auto"
     args.threads = args.threads or 128
     args.stages = args.stages or 2
+    if args.p:
+        wl["p"] = args.p
     if args.block_bytes:
-        scale = wl["B"] // args.block_bytes
+        total = wl["S"] * wl["B"]          # keep the data per GPU fixed
         wl["B"] = args.block_bytes
-        wl["S"] = wl["S"] * max(1, scale)
+        wl["S"] = max(1, total // args.block_bytes)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -317,7 +326,8 @@ def main():
     else:
         prog = X.xslp_compile(X.xslp_encode_bitmatrix(G, n, p), compress=args.compress,
                               kernel=args.kernel, lane_words=args.lanes, threads=args.threads,
-                              block_bytes_hint=B, stages=args.stages)
+                              block_bytes_hint=B, stages=args.stages, fuse=args.fuse,
+                              schedule=args.schedule)
         m_out = p
     compile_s = time.perf_counter() - t0
     log(f'compiled in {compile_s:.2f} s', prog.stats())
