@@ -231,12 +231,13 @@ def _xor_reduce(t):
     return acc
 
 
-@pytest.mark.parametrize("kern", ["straight", "tma", "pipe"])
-def test_cfg2_full_size_sampled(kern):
-    # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); straight-line kernel, baked strip
+@pytest.mark.parametrize("kern,threads", [("straight", 128), ("tma", 128), ("pipe", 256)])
+def test_cfg2_full_size_sampled(kern, threads):
+    # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); ("pipe", 256) with 2 stages is the
+    # exact launch configuration bench.py times by default
     n, p, B, S = 10, 4, 1 << 20, 1024
     og = mx.coding_matrix(n, p)
-    _, prog = compile_enc(n, p, block_bytes_hint=B, kernel=kern)
+    _, prog = compile_enc(n, p, block_bytes_hint=B, kernel=kern, threads=threads, stages=2)
     din = dev_buf(S, n, B)
     X.xslp_fill_random(din, S, n, B, seed=2)
     dout = dev_buf(S, p, B)
@@ -250,8 +251,10 @@ def test_cfg2_full_size_sampled(kern):
     torch.cuda.empty_cache()
 
 
-def test_cfg3_full_size_roundtrip_sampled():
-    # RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures (configs[2])
+@pytest.mark.parametrize("mode", ["grouped", "interp"])
+def test_cfg3_full_size_roundtrip_sampled(mode):
+    # RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures (configs[2]);
+    # "grouped" (per-pattern LDG kernels, T=64, 8 streams) is the bench's launch configuration
     n, p, B, S = 10, 4, 1 << 20, 1024
     og = mx.coding_matrix(n, p)
     g = X.xslp_coding_matrix(n, p)
@@ -265,16 +268,27 @@ def test_cfg3_full_size_roundtrip_sampled():
     X.xslp_encode_batch(enc, ti[:, :n].contiguous(), ti[:, n:].contiguous(), S, B)
     pats = [tuple(synth.erasure_pattern(3, s, n + p, 4)) for s in range(S)]
     uniq = sorted(set(pats))
-    progs, survs = [], {}
+    survs = {}
+    bitsl = []
     for er in uniq:
         bits, surv = X.xslp_decode_bitmatrix(g, n, p, er)
-        progs.append(X.xslp_compile(bits, specialise=0))
+        bitsl.append(bits)
         survs[er] = surv
-    idx = torch.tensor([uniq.index(er) for er in pats], dtype=torch.int32, device="cuda")
+    if mode == "grouped":
+        progs = X.compile_many(bitsl, kernel="straight", threads=64, block_bytes_hint=B)
+    else:
+        progs = X.compile_many(bitsl, specialise=0)
+    pos = [uniq.index(er) for er in pats]
+    idx = torch.tensor(pos, dtype=torch.int32, device="cuda")
     tin = torch.stack([ti[s, torch.as_tensor(survs[pats[s]], dtype=torch.long)] for s in range(S)])
     out = dev_buf(S, 4, B)
     to = X.block_table(out, S, 4, B)
-    X.xslp_decode_batch_multi(progs, idx, tin.contiguous(), to, S, B)
+    if mode == "grouped":
+        ids, off = X.group_stripes(pos, len(progs))
+        X.xslp_decode_batch_grouped(progs, torch.from_numpy(ids).cuda(), off, tin.contiguous(), to, B,
+                                    nstreams=8)
+    else:
+        X.xslp_decode_batch_multi(progs, idx, tin.contiguous(), to, S, B)
     torch.cuda.synchronize()
     # roundtrip property on every stripe: erased data blocks equal the regenerated data
     for s in range(S):
@@ -289,6 +303,25 @@ def test_cfg3_full_size_roundtrip_sampled():
         surv, rows = mx.decode_rows(og, n, list(pats[s]))
         assert (out[s].cpu().numpy() == rs.decode(rows, blocks[surv])).all()
     del allb, data, out
+    torch.cuda.empty_cache()
+
+
+def test_pdec_full_size_sampled():
+    # the paper's P_dec (erase {2,4,5,6}) on 1024 stripes x 1 MiB in bench's launch configuration
+    n, p, B, S = 10, 4, 1 << 20, 1024
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    bits, surv = X.xslp_decode_bitmatrix(g, n, p, [2, 4, 5, 6])
+    dec = X.xslp_compile(bits, kernel="pipe", threads=256, stages=2, block_bytes_hint=B)
+    din = dev_buf(S, n, B)
+    X.xslp_fill_random(din, S, n, B, seed=3)          # survivors: arbitrary bytes
+    out = dev_buf(S, 4, B)
+    run_batch(dec, din, out, B)
+    osurv, rows = mx.decode_rows(og, n, [2, 4, 5, 6])
+    assert list(surv) == osurv
+    for s in (0, 777, 1023):
+        assert (out[s].cpu().numpy() == rs.decode(rows, din[s].cpu().numpy())).all(), s
+    del din, out
     torch.cuda.empty_cache()
 
 
