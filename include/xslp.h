@@ -60,6 +60,7 @@ extern "C" {
 
 #define XSLP_SCHED_NONE 0 /* keep creation order */
 #define XSLP_SCHED_DFS 1  /* DFS post-order + pebble reuse */
+#define XSLP_SCHED_GREEDY 2 /* bottom-up greedy with cache capacity greedy_capacity */
 
 #define XSLP_KERNEL_AUTO 0     /* batched calls: PIPE when its stages fit and there are >= 4 tiles per
                                   SM, else STRAIGHT; interpreter when nothing was compiled */
@@ -84,6 +85,7 @@ typedef struct xslp_opts {
   int32_t goal_order;      /* DFS root order: 0 = by the term order of the goal nodes, 1 = goal index */
   int32_t min_blocks;      /* if > 0, ask ptxas for this many resident CTAs per SM (.minnctapersm) */
   int32_t stages;          /* shared-memory stages of the PIPE kernel (1..8); default 2 */
+  int32_t greedy_capacity; /* cache capacity c (blocks) of XSLP_SCHED_GREEDY */
 } xslp_opts;
 
 typedef struct xslp_stats {
@@ -212,6 +214,41 @@ int xslp_encode_host(const xslp_program *prog, const uint8_t *h_in, uint8_t *h_o
  * ((s*64 + j) << 40) + i), s = stripe0 + local index.  block_bytes % 8 == 0. */
 int xslp_fill_random(uint8_t *d_buf, int nstripes, int nblocks, size_t block_bytes,
                      uint64_t seed, int64_t stripe0, void *stream);
+
+/* ---- codec front end ------------------------------------------ */
+
+/* RS(n,p) over arbitrary-length device data.  Data of len bytes is zero-padded to n*B,
+ * B = xslp_codec_block_bytes(len) (a multiple of 128, >= 128); shard j < n is bytes
+ * [jB, (j+1)B) of the padded data, shard n+i is parity block i.  Device shard buffers are
+ * one contiguous (n+p) x B array, 16-byte aligned, owned by the caller.  The codec owns
+ * the encode program and an LRU memo (cache_entries, default 1024 when <= 0) of decode
+ * programs per erasure pattern; it is safe to use from several threads.  kind / opts as
+ * in xslp_coding_matrix / xslp_compile (block_bytes_hint is ignored).  n + p <= 64. */
+typedef struct xslp_codec xslp_codec;
+int xslp_codec_create(int n, int p, int kind, const xslp_opts *opts, int cache_entries,
+                      xslp_codec **out);
+void xslp_codec_free(xslp_codec *codec);
+int64_t xslp_codec_block_bytes(const xslp_codec *codec, int64_t len);
+/* d_data: len device bytes -> d_shards: (n+p) x B (data copied + padded, parity computed). */
+int xslp_codec_encode(const xslp_codec *codec, const uint8_t *d_data, int64_t len, uint8_t *d_shards,
+                      void *stream);
+/* Rebuild the erased shards (any order, <= p) in place from the survivors. */
+int xslp_codec_reconstruct(const xslp_codec *codec, uint8_t *d_shards, const int32_t *erased, int ne,
+                           int64_t len, void *stream);
+/* Rebuild what is needed and write the original len bytes to d_data_out. */
+int xslp_codec_decode(const xslp_codec *codec, uint8_t *d_shards, const int32_t *erased, int ne,
+                      int64_t len, uint8_t *d_data_out, void *stream);
+/* The memoised program for an erasure pattern (ne == 0: the encode program); owned by the codec. */
+int xslp_codec_program(const xslp_codec *codec, const int32_t *erased, int ne,
+                       const xslp_program **out);
+int xslp_codec_cached(const xslp_codec *codec);   /* decode programs currently memoised */
+
+/* 32-byte shard header (SPEC wire format): "XSLP", version 1, n, p, shard index,
+ * original length (u64 LE), block size (u32 LE), 12 reserved zero bytes. */
+int xslp_shard_header(uint8_t *out32, int n, int p, int shard, uint64_t original_length,
+                      uint32_t block_bytes);
+int xslp_shard_header_parse(const uint8_t *in32, int32_t *n, int32_t *p, int32_t *shard,
+                            uint64_t *original_length, uint32_t *block_bytes);
 
 /* Number of kernels this library launched on the calling process so far. */
 int64_t xslp_launch_count(void);

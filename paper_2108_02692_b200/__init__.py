@@ -30,7 +30,7 @@ XSLP_OK, XSLP_EINVAL, XSLP_ESINGULAR, XSLP_EUNRECOVERABLE = 0, -1, -2, -3
 XSLP_ECUDA, XSLP_ENOMEM, XSLP_ECOMPILE = -4, -5, -6
 XSLP_RS_ISAL, XSLP_RS_SYSVAND, XSLP_CAUCHY = 0, 1, 2
 XSLP_COMPRESS_NONE, XSLP_COMPRESS_REPAIR, XSLP_COMPRESS_XORREPAIR = 0, 1, 2
-XSLP_SCHED_NONE, XSLP_SCHED_DFS = 0, 1
+XSLP_SCHED_NONE, XSLP_SCHED_DFS, XSLP_SCHED_GREEDY = 0, 1, 2
 XSLP_KERNEL_AUTO, XSLP_KERNEL_STRAIGHT, XSLP_KERNEL_INTERP, XSLP_KERNEL_TMA = 0, 1, 2, 3
 XSLP_KERNEL_PIPE = 4
 
@@ -45,7 +45,7 @@ class xslp_opts(ctypes.Structure):
                 ("lane_words", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("block_bytes_hint", ctypes.c_int64), ("kernel", ctypes.c_int32),
                 ("goal_order", ctypes.c_int32), ("min_blocks", ctypes.c_int32),
-                ("stages", ctypes.c_int32)]
+                ("stages", ctypes.c_int32), ("greedy_capacity", ctypes.c_int32)]
 
 
 class xslp_stats(ctypes.Structure):
@@ -88,6 +88,22 @@ _sig = {
     "xslp_fill_random": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_size_t,
                                         ctypes.c_uint64, ctypes.c_int64, _P]),
     "xslp_launch_count": (ctypes.c_int64, []),
+    "xslp_codec_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.POINTER(xslp_opts), ctypes.c_int, ctypes.POINTER(_P)]),
+    "xslp_codec_free": (None, [_P]),
+    "xslp_codec_block_bytes": (ctypes.c_int64, [_P, ctypes.c_int64]),
+    "xslp_codec_encode": (ctypes.c_int, [_P, _P, ctypes.c_int64, _P, _P]),
+    "xslp_codec_reconstruct": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int64, _P]),
+    "xslp_codec_decode": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int64, _P, _P]),
+    "xslp_codec_program": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.POINTER(_P)]),
+    "xslp_codec_cached": (ctypes.c_int, [_P]),
+    "xslp_shard_header": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_uint64, ctypes.c_uint32]),
+    "xslp_shard_header_parse": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32),
+                                               ctypes.POINTER(ctypes.c_int32),
+                                               ctypes.POINTER(ctypes.c_int32),
+                                               ctypes.POINTER(ctypes.c_uint64),
+                                               ctypes.POINTER(ctypes.c_uint32)]),
     "xslp_last_error": (ctypes.c_char_p, []),
     "xslp_version": (ctypes.c_char_p, []),
 }
@@ -310,3 +326,63 @@ def compile_many(bits_list, workers=None, **kw):
     o = default_opts(**kw)
     with ThreadPoolExecutor(workers) as ex:
         return list(ex.map(lambda b: xslp_compile(b, opts=o), bits_list))
+
+
+# ---- codec front end ----------------------------------------------------------------
+class Codec:
+    """RS(n,p) over arbitrary-length device data (xslp_codec_*)."""
+
+    def __init__(self, n, p, kind="isal", cache_entries=1024, **opts):
+        o = default_opts(**opts)
+        h = _P()
+        _check(_lib.xslp_codec_create(n, p, KINDS.get(kind, kind), ctypes.byref(o), cache_entries,
+                                      ctypes.byref(h)))
+        self._h, self.n, self.p = h.value, n, p
+
+    def block_bytes(self, length):
+        return _check(_lib.xslp_codec_block_bytes(self._h, length))
+
+    def encode(self, d_data, length, d_shards, stream=None):
+        _check(_lib.xslp_codec_encode(self._h, _ptr(d_data), length, _ptr(d_shards), _stream(stream)))
+
+    def reconstruct(self, d_shards, erased, length, stream=None):
+        er = (ctypes.c_int32 * max(1, len(erased)))(*erased)
+        _check(_lib.xslp_codec_reconstruct(self._h, _ptr(d_shards), er, len(erased), length,
+                                           _stream(stream)))
+
+    def decode(self, d_shards, erased, length, d_out, stream=None):
+        er = (ctypes.c_int32 * max(1, len(erased)))(*erased)
+        _check(_lib.xslp_codec_decode(self._h, _ptr(d_shards), er, len(erased), length, _ptr(d_out),
+                                      _stream(stream)))
+
+    def program_stats(self, erased=()):
+        er = (ctypes.c_int32 * max(1, len(erased)))(*erased)
+        h = _P()
+        _check(_lib.xslp_codec_program(self._h, er, len(erased), ctypes.byref(h)))
+        s = xslp_stats()
+        _check(_lib.xslp_program_stats(h, ctypes.byref(s)))
+        return s.as_dict(), h.value
+
+    def cached(self):
+        return _lib.xslp_codec_cached(self._h)
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        lib = globals().get("_lib")
+        if h and lib is not None:
+            lib.xslp_codec_free(h)
+
+
+def xslp_shard_header(n, p, shard, original_length, block_bytes):
+    out = (ctypes.c_uint8 * 32)()
+    _check(_lib.xslp_shard_header(out, n, p, shard, original_length, block_bytes))
+    return bytes(out)
+
+
+def xslp_shard_header_parse(header):
+    buf = (ctypes.c_uint8 * 32).from_buffer_copy(bytes(header[:32]))
+    n, p, sh = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    ln, bb = ctypes.c_uint64(), ctypes.c_uint32()
+    _check(_lib.xslp_shard_header_parse(buf, ctypes.byref(n), ctypes.byref(p), ctypes.byref(sh),
+                                        ctypes.byref(ln), ctypes.byref(bb)))
+    return dict(n=n.value, p=p.value, shard=sh.value, original_length=ln.value, block_bytes=bb.value)

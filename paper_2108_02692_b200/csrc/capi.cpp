@@ -43,6 +43,7 @@ extern "C" void xslp_default_opts(xslp_opts *o) {
   o->goal_order = 0;
   o->min_blocks = 0;
   o->stages = 2;
+  o->greedy_capacity = 0;
 }
 
 extern "C" int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out) {
@@ -106,13 +107,19 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
   const xslp_opts &o = P.opts;
   if (o.fuse) fuse(P.slp);
   if (o.schedule == XSLP_SCHED_DFS) schedule_dfs(P.slp, o.goal_order);
+  std::vector<int> greedy_peb;
+  int greedy_nvar = 0;
+  if (o.schedule == XSLP_SCHED_GREEDY) greedy_nvar = schedule_greedy(P.slp, o.greedy_capacity, greedy_peb);
   if (want) {  // the compiler checks its own output against the goal sets
     auto got = evaluate(P.slp);
     if (got.size() != want->size()) throw Error(XSLP_EINVAL, "internal: goal count changed");
     for (size_t i = 0; i < got.size(); ++i)
       if (!(got[i] == (*want)[i])) throw Error(XSLP_EINVAL, "internal: compiled SLP differs from its input");
   }
-  if (o.schedule == XSLP_SCHED_DFS || (lifted && o.compress == XSLP_COMPRESS_NONE && !o.fuse)) {
+  if (o.schedule == XSLP_SCHED_GREEDY) {
+    P.pebble = greedy_peb;
+    P.nvar = greedy_nvar;
+  } else if (o.schedule == XSLP_SCHED_DFS || (lifted && o.compress == XSLP_COMPRESS_NONE && !o.fuse)) {
     // DFS pebbles; the unoptimised binary chains ("Base") are in place,
     // g <- g ^ c, which the same movable-pebble rule reproduces (NVar 32)
     P.nvar = paper_pebbles(P.slp, P.pebble);
@@ -164,7 +171,9 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
 
 void check_opts(const xslp_opts &o) {
   if (o.compress < 0 || o.compress > 2) throw Error(XSLP_EINVAL, "bad compress option");
-  if (o.schedule < 0 || o.schedule > 1) throw Error(XSLP_EINVAL, "bad schedule option");
+  if (o.schedule < 0 || o.schedule > 2) throw Error(XSLP_EINVAL, "bad schedule option");
+  if (o.schedule == XSLP_SCHED_GREEDY && o.greedy_capacity < 1)
+    throw Error(XSLP_EINVAL, "greedy scheduling needs greedy_capacity >= 1");
   if (o.lane_words != 1 && o.lane_words != 2 && o.lane_words != 4)
     throw Error(XSLP_EINVAL, "lane_words must be 1, 2 or 4");
   if (o.threads < 32 || o.threads > 1024 || o.threads % 32) throw Error(XSLP_EINVAL, "bad threads");
@@ -175,6 +184,37 @@ void check_opts(const xslp_opts &o) {
 }
 
 }  // namespace
+
+namespace xslp {
+// bitmatrix -> compiled program (shared by xslp_compile and the codec's memo cache)
+std::shared_ptr<Program> compile_bits(const std::vector<uint8_t> &bitv, int out_rows, int in_cols,
+                                      const xslp_opts &o) {
+  const uint8_t *bits = bitv.data();
+  if (out_rows < 0 || in_cols <= 0 || in_cols > 512 || out_rows > 4096)
+    throw Error(XSLP_EINVAL, "bitmatrix shape out of range");
+  if (bitv.size() < (size_t)out_rows * in_cols) throw Error(XSLP_EINVAL, "bitmatrix too short");
+  auto t0 = std::chrono::steady_clock::now();
+  auto P = std::make_shared<Program>();
+  P->opts = o;
+  check_opts(P->opts);
+  P->n_const = in_cols;
+  P->n_goals = out_rows;
+  std::vector<Bits> goals(out_rows, Bits(in_cols));
+  for (int r = 0; r < out_rows; ++r)
+    for (int c = 0; c < in_cols; ++c) {
+      uint8_t b = bits[(size_t)r * in_cols + c];
+      if (b > 1) throw Error(XSLP_EINVAL, "bitmatrix entries must be 0 or 1");
+      if (b) goals[r].set(c);
+    }
+  if (P->opts.compress == XSLP_COMPRESS_NONE)
+    P->slp = lift(goals, in_cols, P->opts.fuse != 0);
+  else
+    P->slp = compress(goals, in_cols, P->opts.compress == XSLP_COMPRESS_XORREPAIR);
+  P->stats.compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  finish(*P, &goals, true);
+  return P;
+}
+}  // namespace xslp
 
 extern "C" int xslp_compile(const uint8_t *bits, int out_rows, int in_cols, const xslp_opts *opts,
                             xslp_program **out) {

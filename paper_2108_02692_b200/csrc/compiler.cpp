@@ -443,6 +443,100 @@ void schedule_dfs(Slp &s, int goal_order) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Bottom-up greedy scheduling with cache capacity c ([Peb]):
+//  (i)   choose a computable node maximising |H|/|C|, C = its children, H = the children
+//        whose block is in the (LRU) cache; ties by the node order (creation order);
+//  (ii)  access H, then the rest of C (operands emitted in that order, each part in the
+//        term order);
+//  (iii) move a movable cached pebble to the node if there is one, else a movable pebble,
+//        else a fresh one; the smallest pebble first.
+// A pebble is movable when its node is not a goal and all its parents are computed (R12).
+// The cache model is the abstract LRU of P:1007-1022 over constants and pebbles.
+// Reorders s.ins in place and returns NVar; pebble[v] receives the pebble of variable v
+// (indices after the reordering).
+int schedule_greedy(Slp &s, int cap, std::vector<int> &pebble) {
+  compact(s);
+  const int nc = s.n_const, nv = s.n_vars;
+  if (cap < 1) throw Error(XSLP_EINVAL, "greedy capacity must be positive");
+  auto ord_less = [&](int x, int y) {  // variables (temporals) before constants
+    bool vx = x >= nc, vy = y >= nc;
+    if (vx != vy) return vx;
+    return x < y;
+  };
+  std::vector<int> nparents(nv, 0), waiting(nv, 0), remaining(nv, 0);
+  std::vector<std::vector<int>> users(nv);
+  std::vector<char> goal(nv, 0), done(nv, 0);
+  for (int k = 0; k < nv; ++k)
+    for (int t : s.ins[k].ops)
+      if (t >= nc) { users[t - nc].push_back(k); nparents[t - nc]++; waiting[k]++; }
+  for (int g : s.goal)
+    if (g >= nc) goal[g - nc] = 1;
+  remaining = nparents;
+  std::set<int> ready;
+  for (int k = 0; k < nv; ++k)
+    if (!waiting[k]) ready.insert(k);
+  std::vector<int> peb(nv, -1);
+  std::set<int> movable;  // pebbles of movable nodes
+  std::vector<int> node_of_peb;
+  std::vector<int> cache;  // LRU names: constant c -> c, pebble q -> nc + q; front = LRU
+  auto in_cache = [&](int name) { return std::find(cache.begin(), cache.end(), name) != cache.end(); };
+  auto touch = [&](int name) {
+    auto it = std::find(cache.begin(), cache.end(), name);
+    if (it != cache.end()) cache.erase(it);
+    else if ((int)cache.size() >= cap) cache.erase(cache.begin());
+    cache.push_back(name);
+  };
+  auto name_of = [&](int t) { return t < nc ? t : nc + peb[t - nc]; };
+  std::vector<Ins> out;
+  std::vector<int> order;
+  while (!ready.empty()) {
+    int best = -1;
+    int64_t bh = -1, bc = 1;
+    for (int k : ready) {
+      int h = 0;
+      for (int t : s.ins[k].ops)
+        if (in_cache(name_of(t))) ++h;
+      const int64_t c = (int64_t)s.ins[k].ops.size();
+      if (best < 0 || h * bc > bh * c) { best = k; bh = h; bc = c; }  // ties keep the smaller node
+    }
+    ready.erase(best);
+    auto ops = s.ins[best].ops;
+    std::vector<int> H, R;
+    for (int t : ops) (in_cache(name_of(t)) ? H : R).push_back(t);
+    std::sort(H.begin(), H.end(), ord_less);
+    std::sort(R.begin(), R.end(), ord_less);
+    ops = H;
+    ops.insert(ops.end(), R.begin(), R.end());
+    for (int t : ops) touch(name_of(t));
+    // children whose last parent is this node become movable (non-goals)
+    for (int t : s.ins[best].ops)
+      if (t >= nc && --remaining[t - nc] == 0 && !goal[t - nc]) movable.insert(peb[t - nc]);
+    int q = -1;
+    for (int m : movable)
+      if (in_cache(nc + m)) { q = m; break; }
+    if (q < 0 && !movable.empty()) q = *movable.begin();
+    if (q >= 0) movable.erase(q);
+    else { q = (int)node_of_peb.size(); node_of_peb.push_back(-1); }
+    peb[best] = q;
+    node_of_peb[q] = best;
+    touch(nc + q);
+    out.push_back({best, ops});
+    order.push_back(best);
+    done[best] = 1;
+    for (int u : users[best])
+      if (--waiting[u] == 0) ready.insert(u);
+  }
+  if ((int)out.size() != nv) throw Error(XSLP_EINVAL, "internal: greedy schedule incomplete");
+  s.ins.swap(out);
+  // compact() renumbers variables in the new order; carry the pebbles along
+  std::vector<int> new_peb(nv);
+  for (int i = 0; i < nv; ++i) new_peb[i] = peb[order[i]];
+  compact(s);
+  pebble = new_peb;
+  return (int)node_of_peb.size();
+}
+
+// ---------------------------------------------------------------------------------------
 // Pebble assignment of the DFS heuristic: "If we have a pebble on G
 // that can move, we reuse it; otherwise, we put a fresh pebble."  A pebble can move
 // when its node is not a goal and all its parents are pebbled (reading R12); among

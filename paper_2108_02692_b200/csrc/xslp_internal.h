@@ -105,6 +105,7 @@ Slp compress(const std::vector<Bits> &goals, int n_const, bool xor_rebuild);
 void fuse(Slp &s);
 void schedule_dfs(Slp &s, int goal_order);
 int paper_pebbles(const Slp &s, std::vector<int> &pebble);
+int schedule_greedy(Slp &s, int cap, std::vector<int> &pebble);
 void build_bytecode(const Slp &s, std::vector<uint16_t> &code, int &nslots, int &maxlive);
 std::vector<Bits> evaluate(const Slp &s);
 std::string dump_pebbles(const Slp &s, const std::vector<int> &pebble);

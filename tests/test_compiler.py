@@ -291,3 +291,27 @@ def test_dataset_averages_within_tolerance():
             assert 0.75 <= mine / paper <= 1.35, (k, mine, paper)  # RePair temporal order differs
         else:
             assert 0.85 <= mine / paper <= 1.15, (k, mine, paper)
+
+
+def test_greedy_on_Peg():
+    # bottom-up greedy with capacity 8 on G_eg: exactly Q_greedy,
+    # NVar 3, CCap 7, IOcost(., 8) = 9
+    p = X.xslp_compile_text(golden("P_eg"), 7, compress="none", fuse=0, schedule=2,
+                            greedy_capacity=8, specialise=0)
+    text = p.dump()
+    assert (p.stats()["nvar"], p.ccap(), p.iocost(8)) == (3, 7, 9)
+    assert oslp.ccap(text) == 7 and oslp.iocost(text, 8) == 9
+    body = [l.strip() for l in text.splitlines() if "=" in l and not l.startswith("#")]
+    assert body == ["p0 = c0 ^ c1", "p1 = p0 ^ c4 ^ c5", "p2 = p1 ^ c0 ^ c6",
+                    "p0 = p0 ^ p1 ^ p2", "p2 = c2 ^ c3"]
+    assert oslp.evaluate(text) == oslp.evaluate(golden("Q_greedy"))
+
+
+@pytest.mark.parametrize("cfg", CFGS[:4], ids=lambda c: f"{c[0]}{c[1]}_{c[2]}")
+@pytest.mark.parametrize("cap", [16, 64, 512])
+def test_greedy_semantics_rs(cfg, cap):
+    bits = _bits(*cfg)
+    p = X.xslp_compile(bits, schedule=2, greedy_capacity=cap, specialise=0)
+    assert oslp.evaluate(p.dump()) == _sets(bits)
+    assert oslp.evaluate(p.dump(1)) == _sets(bits)
+    assert p.ccap() == oslp.ccap(p.dump())
