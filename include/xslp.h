@@ -62,6 +62,11 @@ extern "C" {
 #define XSLP_SCHED_DFS 1  /* DFS post-order + pebble reuse */
 #define XSLP_SCHED_GREEDY 2 /* bottom-up greedy with cache capacity greedy_capacity */
 
+#define XSLP_LAYOUT_STRIP 0 /* a block is 8 contiguous strips; the paper's layout */
+#define XSLP_LAYOUT_BYTE 1  /* a block is plain bytes; outputs equal textbook byte-wise RS
+                                via in-register bit-plane transposes; block_bytes % 32
+                               == 0, block pointers 32-byte aligned; straight-line kernel only */
+
 #define XSLP_KERNEL_AUTO 0     /* batched calls: PIPE when its stages fit and there are >= 4 tiles per
                                   SM, else STRAIGHT; interpreter when nothing was compiled */
 #define XSLP_KERNEL_STRAIGHT 1 /* the JIT-compiled straight-line specialisation */
@@ -86,6 +91,7 @@ typedef struct xslp_opts {
   int32_t min_blocks;      /* if > 0, ask ptxas for this many resident CTAs per SM (.minnctapersm) */
   int32_t stages;          /* shared-memory stages of the PIPE kernel (1..8); default 2 */
   int32_t greedy_capacity; /* cache capacity c (blocks) of XSLP_SCHED_GREEDY */
+  int32_t layout;          /* XSLP_LAYOUT_*; default STRIP */
 } xslp_opts;
 
 typedef struct xslp_stats {

@@ -67,6 +67,24 @@ def decode(goal_rows, survivor_blocks):
     return apply_rows(goal_rows, survivor_blocks)
 
 
+def bytewise_apply(rows, blocks):
+    """Textbook byte-wise RS: out_i[t] = sum_j R_ij d_j[t] over GF(2^8).
+
+    The result the byte-compatible layout must reproduce: the SLP
+    runs on the bit-planes of the bytes, and P:549-558 (x*y = B^-1(x~ B(y))) makes the
+    bit-plane XOR program equal to this per-byte product.  Table-driven, one byte
+    position at a time over whole arrays.
+    """
+    blocks = np.ascontiguousarray(blocks, dtype=np.uint8)
+    n = blocks.shape[0]
+    assert all(len(r) == n for r in rows)
+    out = np.zeros((len(rows), blocks.shape[1]), dtype=np.uint8)
+    for i, row in enumerate(rows):
+        for j in range(n):
+            out[i] ^= MUL[row[j]][blocks[j]]
+    return out
+
+
 def bitmatrix_apply(bits, blocks):
     """(8m x 8n) 0/1 matrix times the 8n strips, as array XORs."""
     blocks = _check(blocks)

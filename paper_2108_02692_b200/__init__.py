@@ -33,6 +33,8 @@ XSLP_COMPRESS_NONE, XSLP_COMPRESS_REPAIR, XSLP_COMPRESS_XORREPAIR = 0, 1, 2
 XSLP_SCHED_NONE, XSLP_SCHED_DFS, XSLP_SCHED_GREEDY = 0, 1, 2
 XSLP_KERNEL_AUTO, XSLP_KERNEL_STRAIGHT, XSLP_KERNEL_INTERP, XSLP_KERNEL_TMA = 0, 1, 2, 3
 XSLP_KERNEL_PIPE = 4
+XSLP_LAYOUT_STRIP, XSLP_LAYOUT_BYTE = 0, 1
+LAYOUTS = {"strip": 0, "byte": 1}
 
 KINDS = {"isal": XSLP_RS_ISAL, "sysvand": XSLP_RS_SYSVAND, "cauchy": XSLP_CAUCHY}
 COMPRESS = {"none": 0, "repair": 1, "xorrepair": 2}
@@ -45,7 +47,8 @@ class xslp_opts(ctypes.Structure):
                 ("lane_words", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("block_bytes_hint", ctypes.c_int64), ("kernel", ctypes.c_int32),
                 ("goal_order", ctypes.c_int32), ("min_blocks", ctypes.c_int32),
-                ("stages", ctypes.c_int32), ("greedy_capacity", ctypes.c_int32)]
+                ("stages", ctypes.c_int32), ("greedy_capacity", ctypes.c_int32),
+                ("layout", ctypes.c_int32)]
 
 
 class xslp_stats(ctypes.Structure):
@@ -157,6 +160,8 @@ def default_opts(**kw):
             v = COMPRESS[v]
         if k == "kernel" and isinstance(v, str):
             v = KERNELS[v]
+        if k == "layout" and isinstance(v, str):
+            v = LAYOUTS[v]
         if not hasattr(o, k):
             raise TypeError(f"unknown option {k}")
         setattr(o, k, int(v))

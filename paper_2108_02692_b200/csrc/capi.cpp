@@ -44,6 +44,7 @@ extern "C" void xslp_default_opts(xslp_opts *o) {
   o->min_blocks = 0;
   o->stages = 2;
   o->greedy_capacity = 0;
+  o->layout = XSLP_LAYOUT_STRIP;
 }
 
 extern "C" int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out) {
@@ -158,18 +159,20 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
   const bool device_ok = P.n_const % 8 == 0 && P.n_goals % 8 == 0 && P.n_const > 0 &&
                          P.n_const / 8 + P.n_goals / 8 <= 128;
   if (o.specialise && device_ok) {
-    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads, o.min_blocks, o.stages);
+    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads, o.min_blocks, o.stages, o.layout);
     P.cubin_generic = ptx_to_cubin(P.ptx_generic, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma, &st.regs_pipe, &st.spill_bytes_pipe);
     if (o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0) {
       P.baked_strip = o.block_bytes_hint / 8;
-      P.ptx_baked = emit_ptx(P.slp, o.lane_words, P.baked_strip, o.threads, o.min_blocks, o.stages);
+      P.ptx_baked = emit_ptx(P.slp, o.lane_words, P.baked_strip, o.threads, o.min_blocks, o.stages,
+                           o.layout);
       P.cubin_baked = ptx_to_cubin(P.ptx_baked, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma, &st.regs_pipe, &st.spill_bytes_pipe);
     }
   }
   st.compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
-void check_opts(const xslp_opts &o) {
+void check_opts(xslp_opts &o) {
+  if (o.layout == XSLP_LAYOUT_BYTE) o.lane_words = 1;  // one 32-byte chunk per thread
   if (o.compress < 0 || o.compress > 2) throw Error(XSLP_EINVAL, "bad compress option");
   if (o.schedule < 0 || o.schedule > 2) throw Error(XSLP_EINVAL, "bad schedule option");
   if (o.schedule == XSLP_SCHED_GREEDY && o.greedy_capacity < 1)
@@ -180,6 +183,12 @@ void check_opts(const xslp_opts &o) {
   if (o.kernel < 0 || o.kernel > 4) throw Error(XSLP_EINVAL, "bad kernel option");
   if (o.min_blocks < 0 || o.min_blocks > 32) throw Error(XSLP_EINVAL, "bad min_blocks");
   if (o.stages < 1 || o.stages > 8) throw Error(XSLP_EINVAL, "stages must be 1..8");
+  if (o.layout != XSLP_LAYOUT_STRIP && o.layout != XSLP_LAYOUT_BYTE) throw Error(XSLP_EINVAL, "bad layout");
+  if (o.layout == XSLP_LAYOUT_BYTE && (o.kernel == XSLP_KERNEL_INTERP || o.kernel == XSLP_KERNEL_TMA ||
+                                       o.kernel == XSLP_KERNEL_PIPE))
+    throw Error(XSLP_EINVAL, "the byte layout runs on the straight-line (LDG) kernel only");
+  if (o.layout == XSLP_LAYOUT_BYTE && !o.specialise)
+    throw Error(XSLP_EINVAL, "the byte layout needs specialise = 1");
   if (o.kernel == XSLP_KERNEL_PIPE && o.threads > 992) throw Error(XSLP_EINVAL, "pipe kernel: threads <= 992");
 }
 

@@ -193,8 +193,10 @@ static void load_lib(const std::vector<char> &cubin, JitLib &L) {
   CUDA_OK(cudaLibraryLoadData(&L.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
   CUDA_OK(cudaLibraryGetKernel(&L.batch, L.lib, "xslp_sl_batch"));
   CUDA_OK(cudaLibraryGetKernel(&L.one, L.lib, "xslp_sl_one"));
-  CUDA_OK(cudaLibraryGetKernel(&L.tma, L.lib, "xslp_sl_tma"));
-  CUDA_OK(cudaLibraryGetKernel(&L.pipe, L.lib, "xslp_sl_pipe"));
+  // the byte layout has no TMA variants
+  if (cudaLibraryGetKernel(&L.tma, L.lib, "xslp_sl_tma") != cudaSuccess) L.tma = nullptr;
+  if (cudaLibraryGetKernel(&L.pipe, L.lib, "xslp_sl_pipe") != cudaSuccess) L.pipe = nullptr;
+  cudaGetLastError();
 }
 
 static std::pair<JitLib, JitLib> libs_of(const Program *p) {
@@ -324,6 +326,7 @@ static bool can_straight(const Program *p, size_t block_bytes, bool &baked) {
 // enough tiles to keep every SM busy (measured fastest: profiles/r01_*), otherwise the
 // register-resident LDG kernel.
 static int auto_kernel(const Program *p, size_t block_bytes, int nstripes) {
+  if (p->opts.layout == XSLP_LAYOUT_BYTE) return XSLP_KERNEL_STRAIGHT;
   const uint64_t strip = block_bytes / 8;
   const int T = p->opts.threads, L = p->opts.lane_words;
   if (strip % 16 || p->opts.threads > 992) return XSLP_KERNEL_STRAIGHT;
@@ -427,12 +430,13 @@ static void apply_one(const Program *p, const uint8_t *const *in, uint8_t *const
   const int n_in = p->n_const / 8, n_out = p->n_goals / 8;
   if (n_in + n_out > 128) throw Error(XSLP_EINVAL, "too many blocks");
   OnePtrs one{};
+  const uintptr_t am = p->opts.layout == XSLP_LAYOUT_BYTE ? 31 : 15;
   for (int j = 0; j < n_in; ++j) {
-    if (!in[j] || ((uintptr_t)in[j] & 15)) throw Error(XSLP_EINVAL, "input block pointer null or not 16-byte aligned");
+    if (!in[j] || ((uintptr_t)in[j] & am)) throw Error(XSLP_EINVAL, "input block pointer null or misaligned");
     one.p[j] = in[j];
   }
   for (int i = 0; i < n_out; ++i) {
-    if (!out[i] || ((uintptr_t)out[i] & 15)) throw Error(XSLP_EINVAL, "output block pointer null or not 16-byte aligned");
+    if (!out[i] || ((uintptr_t)out[i] & am)) throw Error(XSLP_EINVAL, "output block pointer null or misaligned");
     one.p[n_in + i] = out[i];
   }
   if (block_bytes == 0) return;

@@ -34,10 +34,13 @@ struct Emitter {
   int threads;
   int min_blocks;
   int stages;
+  int layout;
   int n_in, n_out;
   std::ostringstream o;
-  Emitter(const Slp &s_, int L_, int64_t baked_, int threads_, int min_blocks_, int stages_)
+  Emitter(const Slp &s_, int L_, int64_t baked_, int threads_, int min_blocks_, int stages_,
+          int layout_)
       : s(s_), L(L_), baked(baked_), threads(threads_), min_blocks(min_blocks_), stages(stages_),
+        layout(layout_),
         n_in(s_.n_const / 8),
         n_out((int)(s_.goal.size() / 8)) {}
 
@@ -245,6 +248,115 @@ struct Emitter {
     o << "$DONE:\n  ret;\n";
   }
 
+  // Byte-compatible layout: blocks are plain byte arrays and the
+  // output equals textbook byte-wise RS.  The SLP runs on bit-planes: a
+  // thread owns a 32-byte chunk of every block (one 256-bit load), and an in-register 8x8
+  // bit transpose per byte lane turns the 8 words W_i into 8 plane words P_k with
+  // P_k bit (8m+i) = bit k of byte 4i+m (so constant c_{8j+k} is plane k of block j).
+  // Goals are transposed back per output block (the network is an involution) and
+  // stored with one 256-bit store when the block's 8 planes are complete.
+  void transpose8(const std::vector<std::string> &w) {
+    static const int S[3] = {4, 2, 1};
+    static const char *MASK[3] = {"0x0F0F0F0F", "0x33333333", "0x55555555"};
+    static const int PAIRS[3][4][2] = {{{0, 4}, {1, 5}, {2, 6}, {3, 7}},
+                                       {{0, 2}, {1, 3}, {4, 6}, {5, 7}},
+                                       {{0, 1}, {2, 3}, {4, 5}, {6, 7}}};
+    for (int st = 0; st < 3; ++st)
+      for (int q = 0; q < 4; ++q) {
+        const std::string &a = w[PAIRS[st][q][0]], &b = w[PAIRS[st][q][1]];
+        o << "  shr.b32 %tx0, " << a << ", " << S[st] << ";\n";
+        o << "  xor.b32 %tx0, %tx0, " << b << ";\n  and.b32 %tx0, %tx0, " << MASK[st] << ";\n";
+        o << "  xor.b32 " << b << ", " << b << ", %tx0;\n";
+        o << "  shl.b32 %tx0, %tx0, " << S[st] << ";\n  xor.b32 " << a << ", " << a << ", %tx0;\n";
+      }
+  }
+
+  void body_byte(bool one) {
+    const int nc = s.n_const;
+    std::vector<char> used(nc, 0);
+    for (auto &in : s.ins)
+      for (int t : in.ops)
+        if (t < nc) used[t] = 1;
+    for (int g : s.goal)
+      if (g >= 0 && g < nc) used[g] = 1;
+    o << "  mov.u32 %s0, %ctaid.x;\n  mov.u32 %s1, %ntid.x;\n  mov.u32 %s2, %tid.x;\n";
+    o << "  mad.lo.u32 %s3, %s0, %s1, %s2;\n  ld.param.u32 %s4, [p_words];\n";
+    o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $DONE;\n  mul.wide.u32 %off, %s3, 32;\n";
+    if (!one) {
+      o << "  mov.u32 %s5, %ctaid.y;\n  ld.param.u32 %s6, [p_base];\n  add.u32 %s5, %s5, %s6;\n";
+      o << "  ld.param.u64 %rd0, [p_ids];\n  setp.eq.u64 %p1, %rd0, 0;\n  @%p1 bra $NOIDS;\n";
+      o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n";
+      o << "  ld.global.nc.u32 %s5, [%rd1];\n$NOIDS:\n";
+      o << "  ld.param.u64 %rd2, [p_in];\n  ld.param.u64 %rd3, [p_out];\n";
+      o << "  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
+      o << "  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+    }
+    for (int j = 0; j < n_in; ++j) {
+      bool any = false;
+      for (int k = 0; k < 8; ++k) any |= used[8 * j + k] != 0;
+      if (!any) continue;
+      if (one) o << "  ld.param.u64 %ib" << j << ", [p_ptrs+" << 8 * j << "];\n";
+      else o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+      o << "  add.s64 %ib" << j << ", %ib" << j << ", %off;\n";
+      std::vector<std::string> w;
+      for (int k = 0; k < 8; ++k) w.push_back(creg(8 * j + k, 0));
+      o << "  ld.global.nc.L1::no_allocate.v8.u32 {";
+      for (int k = 0; k < 8; ++k) o << (k ? ", " : "") << w[k];
+      o << "}, [%ib" << j << "];\n";
+      transpose8(w);
+    }
+    for (int i = 0; i < n_out; ++i) {
+      if (one) o << "  ld.param.u64 %ob" << i << ", [p_ptrs+" << 8 * (n_in + i) << "];\n";
+      else o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+      o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
+    }
+    // when is each output block complete?
+    std::vector<int> ready_at(n_out, -1);  // instruction index after which all 8 goals exist
+    for (int g = 0; g < (int)s.goal.size(); ++g) {
+      int t = s.goal[g], at = -1;
+      if (t >= nc) at = t - nc;  // var ids equal instruction positions (compacted)
+      ready_at[g / 8] = std::max(ready_at[g / 8], at);
+    }
+    auto gval = [&](int g) {
+      int t = s.goal[g];
+      if (t < 0) return std::string("%zero");
+      return treg(t, 0);
+    };
+    auto store_block = [&](int i) {
+      std::vector<std::string> y;
+      for (int r = 0; r < 8; ++r) {
+        std::string reg = "%y" + std::to_string(r);
+        o << "  mov.b32 " << reg << ", " << gval(8 * i + r) << ";\n";
+        y.push_back(reg);
+      }
+      transpose8(y);
+      o << "  st.global.v8.u32 [%ob" << i << "], {";
+      for (int r = 0; r < 8; ++r) o << (r ? ", " : "") << y[r];
+      o << "};\n";
+    };
+    for (int i = 0; i < n_out; ++i)
+      if (ready_at[i] < 0) store_block(i);
+    for (size_t k = 0; k < s.ins.size(); ++k) {
+      const auto &in = s.ins[k];
+      const auto &ops = in.ops;
+      std::string d = vreg(in.var, 0);
+      size_t i;
+      if (ops.size() == 2) {
+        o << "  xor.b32 " << d << ", " << treg(ops[0], 0) << ", " << treg(ops[1], 0) << ";\n";
+      } else {
+        o << "  lop3.b32 " << d << ", " << treg(ops[0], 0) << ", " << treg(ops[1], 0) << ", "
+          << treg(ops[2], 0) << ", 0x96;\n";
+        for (i = 3; i + 1 < ops.size(); i += 2)
+          o << "  lop3.b32 " << d << ", " << d << ", " << treg(ops[i], 0) << ", " << treg(ops[i + 1], 0)
+            << ", 0x96;\n";
+        if (i < ops.size()) o << "  xor.b32 " << d << ", " << d << ", " << treg(ops[i], 0) << ";\n";
+      }
+      for (int b = 0; b < n_out; ++b)
+        if (ready_at[b] == (int)k) store_block(b);
+    }
+    o << "$DONE:\n  ret;\n";
+  }
+
   // The straight-line program over this thread's words: constants come from HBM (LDG,
   // all issued up front) or, when `smem`, from shared-memory rows at [%sth + off0 +
   // slot*rowb] with a fresh volatile read per use; goals are stored when computed.
@@ -339,6 +451,7 @@ struct Emitter {
     o << "  .reg .b32 %sb, %sth, %nb;\n  .reg .b64 %toff;\n";
     o << "  .reg .b32 %tps, %nt, %nct, %wid, %it, %tile, %lane, %st, %ph, %fb, %eb, %tw, %dst;\n";
     o << "  .reg .pred %pids, %pprod, %p5;\n";
+    o << "  .reg .b32 %tx0;\n  .reg .b32 %y<8>;\n";
     int nq = 0;
     for (auto &in : s.ins)
       for (int t : in.ops)
@@ -361,14 +474,15 @@ struct Emitter {
     if (min_blocks > 0) o << ".minnctapersm " << min_blocks << "\n";
     o << "{\n";
     decls(ntmp);
-    body(0);
+    if (layout == XSLP_LAYOUT_BYTE) body_byte(false); else body(0);
     o << "}\n\n";
     o << ".visible .entry xslp_sl_one(\n  .param .align 8 .b8 p_ptrs[1024],\n"
          "  .param .u64 p_strip,\n  .param .u32 p_words)\n.maxntid "
       << threads << ", 1, 1\n{\n";
     decls(ntmp);
-    body(1);
+    if (layout == XSLP_LAYOUT_BYTE) body_byte(true); else body(1);
     o << "}\n\n";
+    if (layout == XSLP_LAYOUT_BYTE) return o.str();  // no TMA variants for the byte layout
     o << ".visible .entry xslp_sl_tma(\n  .param .u64 p_in,\n  .param .u64 p_out,\n"
          "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
          "  .param .u32 p_base)\n.maxntid "
@@ -393,12 +507,13 @@ struct Emitter {
 }  // namespace
 
 std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks,
-                     int stages) {
+                     int stages, int layout) {
   if (s.n_const % 8 || s.goal.size() % 8)
     throw Error(XSLP_EINVAL, "device programs need whole blocks (constants and goals multiples of 8)");
   if (s.n_const / 8 + s.goal.size() / 8 > 128)
     throw Error(XSLP_EINVAL, "too many blocks for one kernel (n + m > 128)");
-  Emitter e(s, lanes, baked_strip, threads, min_blocks, stages);
+  if (layout == XSLP_LAYOUT_BYTE) lanes = 1;
+  Emitter e(s, lanes, baked_strip, threads, min_blocks, stages, layout);
   return e.run();
 }
 

@@ -116,7 +116,7 @@ Slp parse_text(const std::string &text, int n_const);
 
 // PTX (ptx.cpp)
 std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks,
-                     int stages);
+                     int stages, int layout);
 std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, int *regs_tma,
                                int *spill_tma, int *regs_pipe, int *spill_pipe);
 

@@ -78,6 +78,33 @@ def test_bitplane_reduction_to_bytewise_rs():
             assert y == want
 
 
+def test_bytewise_rs_brute_force_and_bitplanes():
+    # bytewise_apply vs per-byte polynomial multiply without tables, and vs the strip-layout
+    # oracle applied to the bit-planes of the bytes
+    rng = np.random.default_rng(17)
+    g = mx.coding_matrix(5, 3, "isal")
+    d = rng.integers(0, 256, size=(5, 40), dtype=np.uint8)
+    out = rs.bytewise_apply(g[5:], d)
+    for i in range(3):
+        for t in range(40):
+            want = 0
+            for j in range(5):
+                want ^= poly_mul_no_table(g[5 + i][j], int(d[j, t]))
+            assert out[i, t] == want
+    assert (rs.bytewise_apply([[1] * 5], d)[0] == np.bitwise_xor.reduce(d, axis=0)).all()
+    # bit-plane view: strip k of block j carries bit k of every byte (B/8 = 40/8 bytes each)
+    planes = np.zeros((5, 8 * 5), dtype=np.uint8)  # 40 bits per plane = 5 bytes per strip
+    for j in range(5):
+        for k in range(8):
+            bits = (d[j] >> k) & 1
+            planes[j, 5 * k:5 * k + 5] = np.packbits(bits, bitorder="little")
+    strip_out = rs.encode(g, 5, planes)
+    for i in range(3):
+        for k in range(8):
+            bits = np.unpackbits(strip_out[i, 5 * k:5 * k + 5], bitorder="little")
+            assert (bits == ((out[i] >> k) & 1)).all()
+
+
 def test_raid5_parity0_and_linearity():
     g = mx.coding_matrix(10, 4, "isal")
     d1 = stripe_data(7, 0, 10, 256)
