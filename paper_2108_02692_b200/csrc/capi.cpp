@@ -154,6 +154,10 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
     for (int g : P.slp.goal)
       if (g >= 0 && g < P.n_const) u[g] = 1;
     P.n_used_const = (int)std::count(u.begin(), u.end(), 1);
+    P.const_reads = 0;
+    for (auto &in : P.slp.ins)
+      for (int t : in.ops)
+        if (t < P.n_const) P.const_reads++;
   }
   st.regs = st.spill_bytes = st.regs_tma = st.spill_bytes_tma = st.regs_pipe = st.spill_bytes_pipe = 0;
   const bool device_ok = P.n_const % 8 == 0 && P.n_goals % 8 == 0 && P.n_const > 0 &&

@@ -81,6 +81,7 @@ struct Program {
   xslp_opts opts;
   int n_const = 0, n_goals = 0;
   int n_used_const = 0;           // constants read by the program (TMA rows)
+  int64_t const_reads = 0;        // constant operand occurrences (smem reads per word, TMA kernels)
   Slp slp;                         // scheduled program (SSA)
   std::vector<int> pebble;         // paper pebble id per variable
   int nvar = 0;
