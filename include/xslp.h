@@ -171,6 +171,13 @@ void xslp_free(xslp_program *prog);
 
 /* ---- device application (timed hot path) ---------------------------------------- */
 
+/* Load the program's device state on the current device (JIT kernels, shared-memory
+ * attributes, occupancy, interpreter bytecode) for block size block_bytes (0 = skip the
+ * size-dependent part).  After it, launches of this program on this device allocate and
+ * synchronise nothing, so they can be captured into CUDA graphs (the host-buffer form
+ * xslp_encode_host is synchronous and cannot be captured). */
+int xslp_prepare(const xslp_program *prog, size_t block_bytes);
+
 /* One stripe: in_blocks[0..n) and out_blocks[0..m) are HOST arrays of DEVICE
  * pointers (n = n_const/8 input blocks, m = n_goals/8 output blocks).  For
  * encode, inputs are the data blocks and outputs the parity blocks; for decode,

@@ -80,6 +80,7 @@ _sig = {
     "xslp_free": (None, [_P]),
     "xslp_program_cache": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
                                           ctypes.POINTER(ctypes.c_int32)]),
+    "xslp_prepare": (ctypes.c_int, [_P, ctypes.c_size_t]),
     "xslp_encode": (ctypes.c_int, [_P, _P, _P, ctypes.c_size_t, _P]),
     "xslp_decode": (ctypes.c_int, [_P, _P, _P, ctypes.c_size_t, _P]),
     "xslp_encode_batch": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_size_t, _P]),
@@ -251,6 +252,10 @@ def xslp_compile_text(text, n_const, opts=None, **kw):
 def _ptr_array(ptrs):
     arr = (ctypes.c_void_p * max(1, len(ptrs)))(*[_ptr(p) for p in ptrs])
     return arr
+
+
+def xslp_prepare(prog, block_bytes=0):
+    _check(_lib.xslp_prepare(prog.handle, block_bytes))
 
 
 def xslp_encode(prog, in_blocks, out_blocks, block_bytes, stream=None):

@@ -182,6 +182,7 @@ struct JitLib {
   cudaKernel_t batch = nullptr, one = nullptr, tma = nullptr, pipe = nullptr;
   std::map<int, int> smem_set;       // device -> max dynamic smem configured for `tma`
   std::map<int, int> smem_set_pipe;  // same for `pipe`
+  std::map<int, int> pipe_occ;       // device -> resident pipe CTAs per SM (at smem_set_pipe)
 };
 
 // Libraries are context independent (cudaLibraryLoadData); keyed by program serial.
@@ -378,7 +379,13 @@ static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *c
       }
       int sms = 148, per = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
-      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)k, T + 32, smem));
+      auto it = J.pipe_occ.find(d);
+      if (it != J.pipe_occ.end()) {
+        per = it->second;
+      } else {
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)k, T + 32, smem));
+        J.pipe_occ[d] = per;
+      }
       grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms * std::max(1, per));
     }
     void *args[] = {(void *)&d_in, (void *)&d_out, (void *)&d_ids, &strip, &words, &tps, &ntiles};
@@ -652,6 +659,40 @@ using namespace xslp;
 static const Program *P(const xslp_program *p) {
   if (!p) throw Error(XSLP_EINVAL, "null program");
   return reinterpret_cast<const Program *>(p);
+}
+
+// Load everything a launch of `prog` may need on the current device (JIT libraries,
+// shared-memory attributes, pipeline occupancy, interpreter bytecode) so later launches do
+// no allocation or synchronous copy and can be captured into a CUDA graph.
+extern "C" int xslp_prepare(const xslp_program *prog, size_t block_bytes) {
+  API_BEGIN
+  const Program *p = P(prog);
+  dev_of(p);  // interpreter bytecode
+  set_smem_attr();
+  libs_of(p);
+  if (block_bytes && block_bytes % 32 == 0 && p->opts.layout != XSLP_LAYOUT_BYTE) {
+    const int T = p->opts.threads, L = p->opts.lane_words;
+    const size_t smem_pipe = 128 + (size_t)p->opts.stages * p->n_used_const * 4 * L * T;
+    const size_t smem_tma = 128 + (size_t)p->n_used_const * 4 * L * T;
+    const int d = current_device();
+    std::lock_guard<std::mutex> g(g_mu);
+    for (JitLib *J : {&g_libs[p].first, &g_libs[p].second}) {
+      if (J->pipe && smem_pipe <= 227 * 1024 && J->smem_set_pipe[d] < (int)smem_pipe) {
+        CUDA_OK(cudaKernelSetAttributeForDevice(J->pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem_pipe, d));
+        J->smem_set_pipe[d] = (int)smem_pipe;
+        int per = 0;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)J->pipe, T + 32, smem_pipe));
+        J->pipe_occ[d] = per;
+      }
+      if (J->tma && smem_tma <= 227 * 1024 && J->smem_set[d] < (int)smem_tma) {
+        CUDA_OK(cudaKernelSetAttributeForDevice(J->tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem_tma, d));
+        J->smem_set[d] = (int)smem_tma;
+      }
+    }
+  }
+  API_END
 }
 
 extern "C" int xslp_encode(const xslp_program *prog, const uint8_t *const *in_blocks,

@@ -410,3 +410,31 @@ def test_byte_layout_full_size_sampled():
         assert (dout[s].cpu().numpy() == rs.bytewise_apply(og[n:], d)).all()
     del din, dout
     torch.cuda.empty_cache()
+
+
+# ---- CUDA graphs: launches are capturable after xslp_prepare -----------------------------
+
+@pytest.mark.parametrize("kern", ["pipe", "straight", "interp"])
+def test_cuda_graph_capture(kern):
+    n, p, B, S = 10, 4, 65536, 64
+    og = mx.coding_matrix(n, p)
+    _, prog = compile_enc(n, p, kernel=kern, threads=256 if kern == "pipe" else 128,
+                          block_bytes_hint=B)
+    X.xslp_prepare(prog, B)
+    din = dev_buf(S, n, B)
+    X.xslp_fill_random(din, S, n, B, seed=44)
+    dout = torch.zeros((S, p, B), dtype=torch.uint8, device="cuda")
+    ti, to = X.block_table(din, S, n, B), X.block_table(dout, S, p, B)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        X.xslp_encode_batch(prog, ti, to, S, B)
+    assert not dout.any()                       # capture does not execute
+    g.replay()
+    torch.cuda.synchronize()
+    for s in (0, S - 1):
+        assert (dout[s].cpu().numpy() == rs.encode(og, n, synth.stripe_data(44, s, n, B))).all()
+    X.xslp_fill_random(din, S, n, B, seed=45)   # replay on new inputs
+    g.replay()
+    torch.cuda.synchronize()
+    assert (dout[3].cpu().numpy() == rs.encode(og, n, synth.stripe_data(45, 3, n, B))).all()
