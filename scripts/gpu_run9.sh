@@ -3,6 +3,6 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu9.log 2>&1
 echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu9.log
-timeout 300 python scripts/sanitize_smoke.py > gpurun_out/sanitize_plain.log 2>&1 && \
-timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 python scripts/sanitize_smoke.py > gpurun_out/memcheck.log 2>&1
-echo "memcheck rc=$?"; tail -15 gpurun_out/memcheck.log
+
+
+

@@ -438,3 +438,55 @@ def test_cuda_graph_capture(kern):
     g.replay()
     torch.cuda.synchronize()
     assert (dout[3].cpu().numpy() == rs.encode(og, n, synth.stripe_data(45, 3, n, B))).all()
+
+
+# ---- size edges: the 65535 grid-row limit and the widest supported code ------------------
+
+@pytest.mark.parametrize("kern", ["straight", "tma", "pipe", "interp"])
+def test_many_stripes_beyond_grid_limit(kern):
+    n, p, B, S = 4, 2, 128, 70000           # > 65535 stripes: launches are chunked
+    og = mx.coding_matrix(n, p, "cauchy")
+    _, prog = compile_enc(n, p, "cauchy", kernel=kern, threads=64)
+    din = dev_buf(S, n, B)
+    X.xslp_fill_random(din, S, n, B, seed=8)
+    dout = torch.zeros((S, p, B), dtype=torch.uint8, device="cuda")
+    run_batch(prog, din, dout, B)
+    for s in (0, 65534, 65535, 65536, S - 1):
+        assert (dout[s].cpu().numpy() == rs.encode(og, n, synth.stripe_data(8, s, n, B))).all(), s
+
+
+def test_widest_code_rs60_4():
+    n, p, B, S = 60, 4, 4096, 2             # 480 constants, 64 blocks per stripe
+    og = mx.coding_matrix(n, p)
+    _, prog = compile_enc(n, p, threads=64)
+    data = host_data(6, range(S), n, B)
+    din = torch.from_numpy(data).cuda()
+    dout = dev_buf(S, p, B)
+    run_batch(prog, din, dout, B)
+    for s in range(S):
+        assert (dout[s].cpu().numpy() == rs.encode(og, n, data[s])).all()
+
+
+def test_concurrent_host_threads():
+    # programs and the library are shared by host threads launching on their own streams
+    from concurrent.futures import ThreadPoolExecutor
+    n, p, B, S = 10, 4, 65536, 16
+    og = mx.coding_matrix(n, p)
+    progs = {k: compile_enc(n, p, kernel=k, threads=64)[1] for k in ("pipe", "straight", "interp")}
+
+    def work(i):
+        kern = ("pipe", "straight", "interp")[i % 3]
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            din = dev_buf(S, n, B)
+            X.xslp_fill_random(din, S, n, B, seed=100 + i, stream=st)
+            dout = dev_buf(S, p, B)
+            X.xslp_encode_batch(progs[kern], X.block_table(din, S, n, B), X.block_table(dout, S, p, B),
+                                S, B, stream=st)
+            st.synchronize()
+            s = i % S
+            return bool((dout[s].cpu().numpy() ==
+                         rs.encode(og, n, synth.stripe_data(100 + i, s, n, B))).all())
+
+    with ThreadPoolExecutor(6) as ex:
+        assert all(ex.map(work, range(12)))
