@@ -41,9 +41,11 @@ WORKLOADS = {
                   n=10, p=4, B=MiB, S=1024, op="encode", seed=2, layout="byte",
                   tuned=dict(kernel="straight", threads=128, stages=2)),
     "cfg3": dict(desc="RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures, "
-                      "one interpreter launch with a program per stripe (BASELINE configs[2])",
+                      "one JIT straight-line kernel per distinct pattern over its stripes, fanned out over "
+                      "internal streams and replayed from a CUDA graph (--kernel interp: one "
+                      "interpreter launch with a program per stripe) (BASELINE configs[2])",
                  n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3,
-                 tuned=dict(kernel="grouped", threads=64, stages=2)),
+                 tuned=dict(kernel="grouped", threads=64, stages=2, graph=1)),
     "pdec": dict(desc="RS(10,4) decode of the paper's P_dec pattern {2,4,5,6} (P:1670) on every "
                       "stripe, 1024 stripes x 1 MiB",
                  n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3,
@@ -56,7 +58,23 @@ WORKLOADS = {
                       "of <=2048 stripes per launch (BASELINE configs[4])",
                  n=20, p=4, B=MiB, S=8192, op="encode_sharded", seed=5, chunk=2048,
                  tuned=dict(kernel="pipe", threads=128, stages=2)),
+    "cfg5d": dict(desc="RS(20,4) decode of one seeded random 4-erasure pattern (synth.erasure_pattern"
+                       "(5, 0, 24, 4)) applied to every stripe, 8192 stripes x 1 MiB sharded over the "
+                       "GPUs; chunks of <=2048 stripes per launch (BASELINE configs[4], decode half)",
+                  n=20, p=4, B=MiB, S=8192, op="decode_sharded", e=4, seed=5, chunk=2048,
+                  tuned=dict(kernel="pipe", threads=128, stages=2)),
 }
+
+SHARDED = ("encode_sharded", "decode_sharded")     # strong scaling: fixed total over the ranks
+DECODE = ("decode_one", "decode_sharded", "decode_multi")
+
+
+def erased_of(wl):
+    """The single erasure pattern of a decode_one / decode_sharded workload."""
+    if "erased" in wl:
+        return tuple(wl["erased"])
+    import synth
+    return tuple(synth.erasure_pattern(wl["seed"], 0, wl["n"] + wl["p"], wl["e"]))
 
 
 def parse():
@@ -78,6 +96,8 @@ def parse():
     ap.add_argument("--p", type=int, default=0, help="override parity count (cfg4 sweep)")
     ap.add_argument("--fuse", type=int, default=1)
     ap.add_argument("--schedule", type=int, default=1, help="1 = DFS, 0 = creation order")
+    ap.add_argument("--graph", type=int, default=None,
+                    help="1 = capture one step's launches into a CUDA graph and replay it per step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -160,6 +180,23 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------
+def oracle_stripe(wl, g, s, rows_cache, synth, mx, rs):
+    """One stripe of the workload through the oracle: encode, or decode of that stripe's
+    erasure pattern (the survivor bytes are the stripe's seeded data blocks: the oracle's
+    cost does not depend on their values)."""
+    n, p, B = wl["n"], wl["p"], wl["B"]
+    data = synth.stripe_data(wl["seed"], s, n, B)
+    if wl["op"] not in DECODE:
+        return rs.encode(g, n, data)
+    if wl["op"] == "decode_multi":
+        er = tuple(synth.erasure_pattern(wl["seed"], s, n + p, wl["e"]))
+    else:
+        er = erased_of(wl)
+    if er not in rows_cache:
+        rows_cache[er] = mx.decode_rows(g, n, list(er))
+    return rs.decode(rows_cache[er][1], data)
+
+
 def oracle_baseline(wl, budget_s=12.0):
     """The CPU oracle as it stands (oracle/rs.py, numpy, one core) on a bounded sample."""
     import numpy as np
@@ -169,19 +206,9 @@ def oracle_baseline(wl, budget_s=12.0):
     n, p, B = wl["n"], wl["p"], wl["B"]
     g = mx.coding_matrix(n, p)
     done, t0, s = 0, time.perf_counter(), 0
-    if wl["op"] == "decode_multi":
-        rows_cache = {}
+    rows_cache = {}
     while True:
-        data = synth.stripe_data(wl["seed"], s, n, B)
-        if wl["op"] == "decode_multi":
-            er = tuple(synth.erasure_pattern(wl["seed"], s, n + p, wl["e"]))
-            if er not in rows_cache:
-                rows_cache[er] = mx.decode_rows(g, n, list(er))
-            surv, rows = rows_cache[er]
-            blocks = np.concatenate([data, data[:p]])   # survivor bytes: any n blocks
-            rs.decode(rows, blocks[:n])
-        else:
-            rs.encode(g, n, data)
+        oracle_stripe(wl, g, s, rows_cache, synth, mx, rs)
         done += 1
         s += 1
         if time.perf_counter() - t0 > budget_s:
@@ -204,14 +231,10 @@ def run_reference(args, wl, rank, world):
     n, p, B = wl["n"], wl["p"], wl["B"]
     g = mx.coding_matrix(n, p)
 
+    rows_cache = {}
+
     def step(s):
-        data = synth.stripe_data(wl["seed"], s, n, B)
-        if wl["op"] == "decode_multi":
-            er = synth.erasure_pattern(wl["seed"], s, n + p, wl["e"])
-            surv, rows = mx.decode_rows(g, n, er)
-            rs.decode(rows, np.concatenate([data, data[:p]])[:n])
-        else:
-            rs.encode(g, n, data)
+        oracle_stripe(wl, g, s, rows_cache, synth, mx, rs)
 
     for i in range(args.warmup):
         step(i)
@@ -223,7 +246,8 @@ def run_reference(args, wl, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt / max(1, args.steps) * 1e3, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "scaling": "strong" if wl["op"] in SHARDED else "weak", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic",
             "config": config_of(args, wl, None),
             "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "sample": f"each step = 1 stripe ({n} x {B} B data) of the workload "
@@ -246,11 +270,11 @@ def kernel_name(args, wl, stats):
 
 def config_of(args, wl, stats):
     c = {"workload": f"{args.workload}: {wl['desc']}", "n": wl["n"], "p": wl["p"],
-         "block_bytes": wl["B"], "stripes_per_gpu": wl["S"] if wl["op"] != "encode_sharded"
+         "block_bytes": wl["B"], "stripes_per_gpu": wl["S"] if wl["op"] not in SHARDED
          else wl["S"] // max(1, args.gpus),
          "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": args.compress + ("+fuse" if args.fuse else "") + ("+dfs" if args.schedule else ""),
          "kernel": args.kernel, "lane_words": args.lanes, "threads": args.threads,
-         "stages": args.stages,
+         "stages": args.stages, "cuda_graph": bool(args.graph),
          "l2": "inputs larger than the 126 MB L2; no flush between steps",
          "parallelism": f"stripe-sharded x{args.gpus}, no collective"}
     if stats:
@@ -271,6 +295,7 @@ def main():
     args.kernel = args.kernel or "auto"
     args.threads = args.threads or 128
     args.stages = args.stages or 2
+    args.graph = int(args.graph or 0)
     if args.p:
         wl["p"] = args.p
     if args.block_bytes:
@@ -321,12 +346,13 @@ def main():
                                            "grouped_pipe": "pipe"}.get(mode, "straight"))
         prog = progs[0]
         m_out = wl["e"]
-    elif wl["op"] == "decode_one":
-        bits, _surv = X.xslp_decode_bitmatrix(G, n, p, wl["erased"])
+    elif wl["op"] in ("decode_one", "decode_sharded"):
+        erased = erased_of(wl)
+        bits, _surv = X.xslp_decode_bitmatrix(G, n, p, erased)
         prog = X.xslp_compile(bits, compress=args.compress, kernel=args.kernel,
                               lane_words=args.lanes, threads=args.threads, block_bytes_hint=B,
                               stages=args.stages)
-        m_out = len(wl["erased"])
+        m_out = len(erased)
     else:
         prog = X.xslp_compile(X.xslp_encode_bitmatrix(G, n, p), compress=args.compress,
                               kernel=args.kernel, lane_words=args.lanes, threads=args.threads,
@@ -339,7 +365,7 @@ def main():
 
     # ---- device buffers and seeded inputs (untimed) ----
     from paper_2108_02692_b200.shard import max_over_ranks, stripe_range
-    if wl["op"] == "encode_sharded":      # strong split of 8192 stripes over the ranks
+    if wl["op"] in SHARDED:               # strong split of 8192 stripes over the ranks
         lo, hi = stripe_range(rank, world, total=wl["S"])
         per = hi - lo
         S = min(per, wl["chunk"])
@@ -350,25 +376,37 @@ def main():
         nchunks = 1
         stripe0 = stripe_range(rank, world, per_rank=S)[0]
     n_in = n
-    din = torch.empty((S, n_in, B), dtype=torch.uint8, device="cuda")
     dout = torch.empty((S, m_out, B), dtype=torch.uint8, device="cuda")
-    X.xslp_fill_random(din, S, n_in, B, seed=wl["seed"], stripe0=stripe0)
-    ti = X.block_table(din, S, n_in, B)
     to = X.block_table(dout, S, m_out, B)
+    if wl["op"] in ("decode_one", "decode_sharded"):
+        # whole codewords (data from the generator, parity by the encode program, untimed);
+        # the decode program reads the n survivors of each stripe through the pointer table
+        din = torch.empty((S, n + p, B), dtype=torch.uint8, device="cuda")
+        X.xslp_fill_random(din, S, n + p, B, seed=wl["seed"], stripe0=stripe0)
+        tall = X.block_table(din, S, n + p, B).view(S, n + p)
+        enc = X.xslp_compile(X.xslp_encode_bitmatrix(G, n, p), block_bytes_hint=B)
+        X.xslp_encode_batch(enc, tall[:, :n].contiguous(), tall[:, n:].contiguous(), S, B,
+                            stream=stream)
+        ti = tall[:, torch.as_tensor(_surv, dtype=torch.long)].contiguous().view(-1)
+        erased_idx = torch.as_tensor(erased, dtype=torch.long)
+    else:
+        din = torch.empty((S, n_in, B), dtype=torch.uint8, device="cuda")
+        X.xslp_fill_random(din, S, n_in, B, seed=wl["seed"], stripe0=stripe0)
+        ti = X.block_table(din, S, n_in, B)
     if wl["op"] == "decode_multi":
         pos = [uniq.index(er) for er in pats]
         idx = torch.tensor(pos, dtype=torch.int32, device="cuda")
         gids, goff = X.group_stripes(pos, len(progs))
         gids = torch.from_numpy(gids).cuda()
 
-    def launch():
+    def launch(st=stream):
         if wl["op"] == "decode_multi" and mode == "interp":
-            X.xslp_decode_batch_multi(progs, idx, ti, to, S, B, stream=stream)
+            X.xslp_decode_batch_multi(progs, idx, ti, to, S, B, stream=st)
         elif wl["op"] == "decode_multi":
             X.xslp_decode_batch_grouped(progs, gids, goff, ti, to, B, nstreams=args.streams,
-                                        stream=stream)
+                                        stream=st)
         else:
-            X.xslp_encode_batch(prog, ti, to, S, B, stream=stream)
+            X.xslp_encode_batch(prog, ti, to, S, B, stream=st)
 
     def step():
         for _ in range(nchunks):
@@ -377,14 +415,35 @@ def main():
     # sanity (torch, not the product): RAID-5 row of the [I; 2^ij] encode
     launch()
     torch.cuda.synchronize()
-    if wl["op"] not in ("decode_multi", "decode_one"):
+    if wl["op"] not in DECODE:
         acc = din[:, 0].clone()
         for j in range(1, n):
             acc ^= din[:, j]
         if not torch.equal(acc, dout[:, 0]):
             raise SystemExit("sanity check failed: parity block 0 != XOR of data blocks")
         del acc
+    elif wl["op"] in ("decode_one", "decode_sharded"):
+        if not torch.equal(dout, din[:, erased_idx]):
+            raise SystemExit("sanity check failed: decoded blocks != the erased blocks")
 
+    graph = None
+    if args.graph:
+        # one step's launches (all per-pattern kernels, their fork/join over the internal
+        # streams) captured once and replayed: removes the host launch cost, not device work
+        for pr in (progs if wl["op"] == "decode_multi" else [prog]):
+            X.xslp_prepare(pr, B)
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        l_before = X.xslp_launch_count()
+        with torch.cuda.graph(graph, stream=cap):
+            launch(cap)
+        graph_launches = X.xslp_launch_count() - l_before
+        stream.wait_stream(cap)
+
+        def step():                         # noqa: F811
+            for _ in range(nchunks):
+                graph.replay()
     log('sanity ok; warmup')
     for _ in range(args.warmup):
         step()
@@ -401,6 +460,8 @@ def main():
             ev[i + 1].record(stream)
         torch.cuda.synchronize()
     launches = X.xslp_launch_count() - l0
+    if graph is not None:                   # kernels replayed from the graph
+        launches += graph_launches * nchunks * args.steps
     log('timed region done')
     if dist:
         dist.barrier()
@@ -424,13 +485,18 @@ def main():
 
     # ---- e2e through the host-buffer C-ABI call ----
     e2e = None
-    if not args.no_e2e and wl["op"] == "encode":
+    if not args.no_e2e and wl["op"] != "decode_multi":
         try:
             # pinned host buffers: the full workload at N=1; at most 16 GiB over all ranks
             Se = min(S, max(1, (16 << 30) // max(1, world) // ((n + p) * B)))
             h_in = torch.empty((Se, n, B), dtype=torch.uint8, pin_memory=True)
-            h_out = torch.empty((Se, p, B), dtype=torch.uint8, pin_memory=True)
-            h_in.copy_(din[:Se])
+            h_out = torch.empty((Se, m_out, B), dtype=torch.uint8, pin_memory=True)
+            if wl["op"] in ("decode_one", "decode_sharded"):   # the survivors of each stripe
+                h_in.copy_(din[:Se, torch.as_tensor(_surv, dtype=torch.long)])
+                want = din[:Se, erased_idx]
+            else:
+                h_in.copy_(din[:Se])
+                want = dout[:Se]
             X.xslp_encode_host(prog, h_in, h_out, Se, B, stream=stream)   # warm
             torch.cuda.synchronize()
             if dist:
@@ -440,13 +506,15 @@ def main():
                 X.xslp_encode_host(prog, h_in, h_out, Se, B, stream=stream)
             torch.cuda.synchronize()
             et = max_over_ranks(time.perf_counter() - e0, dist, device="cuda")
-            ok = bool((h_out[:, 0].cuda() == dout[:Se, 0]).all().item())
+            ok = bool(torch.equal(h_out.cuda(), want))
+            del want
             e2e = {"value": round(Se * n * B * world * args.e2e_steps / et / 1e9, 3),
-                   "unit": "GB/s", "h2d_bytes_per_step": Se * n * B, "d2h_bytes_per_step": Se * p * B,
+                   "unit": "GB/s", "h2d_bytes_per_step": Se * n * B,
+                   "d2h_bytes_per_step": Se * m_out * B,
                    "steps": args.e2e_steps, "stripes_per_gpu": Se,
                    "api": "xslp_encode_host (pinned host buffers, chunked H2D / kernel / D2H on "
                    "two streams), host wall clock around synchronous calls, max over ranks",
-                   "check_parity0": ok}
+                   "check_outputs": ok}
             del h_in, h_out
         except Exception as ex:  # report, do not hide
             e2e = {"value": None, "unit": "GB/s", "error": str(ex)[:200]}
@@ -460,7 +528,8 @@ def main():
         line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                "scaling": "strong" if wl["op"] in SHARDED else "weak", "vs_baseline": None,
+                "dtype": "u32", "data": "synthetic",
                 "config": config_of(args, wl, stats), "roofline": roof, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
                 "compile_s": round(compile_s, 3),

@@ -351,6 +351,36 @@ def test_cfg5_rs20_reduced(kern):
     assert (allb[s, n:].cpu().numpy() == rs.encode(og, n, h)).all()
 
 
+def test_cfg5_full_chunk_sampled():
+    # RS(20,4) encode and the seeded 4-erasure decode (configs[4]) over one bench launch: a chunk
+    # of 2048 stripes x 24 x 1 MiB, PIPE T=128 S=2 (bench.py cfg5 / cfg5d launch configuration)
+    n, p, B, S = 20, 4, 1 << 20, 2048
+    og = mx.coding_matrix(n, p)
+    g, enc = compile_enc(n, p, block_bytes_hint=B, kernel="pipe", threads=128, stages=2)
+    allb = dev_buf(S, n + p, B)
+    X.xslp_fill_random(allb, S, n + p, B, seed=5)   # data words do not depend on nblocks
+    ti = X.block_table(allb, S, n + p, B).view(S, n + p)
+    X.xslp_encode_batch(enc, ti[:, :n].contiguous(), ti[:, n:].contiguous(), S, B)
+    er = synth.erasure_pattern(5, 0, n + p, 4)
+    bits, surv = X.xslp_decode_bitmatrix(g, n, p, er)
+    dec = X.xslp_compile(bits, block_bytes_hint=B, kernel="pipe", threads=128, stages=2)
+    out = dev_buf(S, 4, B)
+    X.xslp_encode_batch(dec, ti[:, torch.as_tensor(surv, dtype=torch.long)].contiguous(),
+                        X.block_table(out, S, 4, B), S, B)
+    torch.cuda.synchronize()
+    assert torch.equal(allb[:, n], _xor_reduce(allb[:, :n]))     # RAID-5 row, every stripe
+    assert torch.equal(out, allb[:, torch.as_tensor(er, dtype=torch.long)])  # roundtrip
+    osurv, rows = mx.decode_rows(og, n, list(er))
+    assert list(surv) == osurv
+    for s in (0, 1337, 2047):
+        d = synth.stripe_data(5, s, n, B)
+        blocks = np.concatenate([d, rs.encode(og, n, d)])
+        assert (allb[s].cpu().numpy() == blocks).all(), s
+        assert (out[s].cpu().numpy() == rs.decode(rows, blocks[osurv])).all(), s
+    del allb, out
+    torch.cuda.empty_cache()
+
+
 def test_shards_equal_single_run():
     # 8-shard decomposition run serially on one GPU equals the 1-shard run
     n, p, B, S = 10, 4, 65536, 64
@@ -438,6 +468,41 @@ def test_cuda_graph_capture(kern):
     g.replay()
     torch.cuda.synchronize()
     assert (dout[3].cpu().numpy() == rs.encode(og, n, synth.stripe_data(45, 3, n, B))).all()
+
+
+def test_cuda_graph_grouped_decode():
+    # heterogeneous decode (per-pattern kernels forked over internal streams) captured into one
+    # graph (bench.py cfg3 --graph 1); replays equal the oracle's decode, also on new inputs
+    n, p, B, S = 10, 4, 8192, 40
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    pats = [tuple(synth.erasure_pattern(46, s, n + p, 4)) for s in range(S)]
+    uniq = sorted(set(pats))
+    dec = [X.xslp_decode_bitmatrix(g, n, p, er) for er in uniq]
+    progs = X.compile_many([d[0] for d in dec], kernel="straight", threads=64, block_bytes_hint=B)
+    for pr in progs:
+        X.xslp_prepare(pr, B)
+    din = dev_buf(S, n, B)                       # survivors: arbitrary bytes
+    out = torch.zeros((S, 4, B), dtype=torch.uint8, device="cuda")
+    ti, to = X.block_table(din, S, n, B), X.block_table(out, S, 4, B)
+    ids, off = X.group_stripes([uniq.index(er) for er in pats], len(progs))
+    ids = torch.from_numpy(ids).cuda()
+    X.xslp_decode_batch_grouped(progs, ids, off, ti, to, B, nstreams=4)   # streams created
+    torch.cuda.synchronize()
+    out.zero_()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        X.xslp_decode_batch_grouped(progs, ids, off, ti, to, B, nstreams=4,
+                                    stream=torch.cuda.current_stream())
+    assert not out.any()
+    for seed in (47, 48):
+        X.xslp_fill_random(din, S, n, B, seed=seed)
+        gr.replay()
+        torch.cuda.synchronize()
+        for s in (0, 17, S - 1):
+            rows = mx.decode_rows(og, n, list(pats[s]))[1]
+            want = rs.decode(rows, synth.stripe_data(seed, s, n, B))
+            assert (out[s].cpu().numpy() == want).all(), (seed, s)
 
 
 # ---- size edges: the 65535 grid-row limit and the widest supported code ------------------
