@@ -63,10 +63,23 @@ WORKLOADS = {
                        "GPUs; chunks of <=2048 stripes per launch (BASELINE configs[4], decode half)",
                   n=20, p=4, B=MiB, S=8192, op="decode_sharded", e=4, seed=5, chunk=2048,
                   tuned=dict(kernel="pipe", threads=128, stages=2)),
+    "xdec": dict(desc="RS(10,4) cross-GPU decode (SURVEY NEXT #4): the 14 blocks of each stripe "
+                      "spread over the GPUs (block j of stripe s on rank (s+j) mod N), rank s mod N "
+                      "decodes stripe s reading its survivors in place from local and NVLink-peer "
+                      "memory; per-stripe seeded 4-of-14 erasures (cfg3's), 1024 stripes x 1 MiB "
+                      "per GPU",
+                 n=10, p=4, B=MiB, S=1024, op="decode_peer", e=4, seed=3,
+                 tuned=dict(kernel="grouped", threads=64, stages=2)),
+    "xdec1": dict(desc="RS(10,4) cross-GPU decode of P_dec {2,4,5,6} on every stripe (one launch "
+                       "whose pointer table mixes local and NVLink-peer survivor blocks), 1024 "
+                       "stripes x 1 MiB per GPU, blocks spread as in xdec",
+                  n=10, p=4, B=MiB, S=1024, op="decode_peer", erased=(2, 4, 5, 6), seed=3,
+                  tuned=dict(kernel="straight", threads=128, stages=2)),
 }
 
 SHARDED = ("encode_sharded", "decode_sharded")     # strong scaling: fixed total over the ranks
-DECODE = ("decode_one", "decode_sharded", "decode_multi")
+DECODE = ("decode_one", "decode_sharded", "decode_multi", "decode_peer")
+NVLINK_GBS = 770.0   # B200_PROFILING.md: measured peer copy bandwidth per direction
 
 
 def erased_of(wl):
@@ -188,7 +201,7 @@ def oracle_stripe(wl, g, s, rows_cache, synth, mx, rs):
     data = synth.stripe_data(wl["seed"], s, n, B)
     if wl["op"] not in DECODE:
         return rs.encode(g, n, data)
-    if wl["op"] == "decode_multi":
+    if "erased" not in wl and "e" in wl:
         er = tuple(synth.erasure_pattern(wl["seed"], s, n + p, wl["e"]))
     else:
         er = erased_of(wl)
@@ -276,7 +289,9 @@ def config_of(args, wl, stats):
          "kernel": args.kernel, "lane_words": args.lanes, "threads": args.threads,
          "stages": args.stages, "cuda_graph": bool(args.graph),
          "l2": "inputs larger than the 126 MB L2; no flush between steps",
-         "parallelism": f"stripe-sharded x{args.gpus}, no collective"}
+         "parallelism": (f"blocks spread over {args.gpus} GPU(s); survivors read in place over "
+                         "NVLink P2P by the decode kernel (no collective)")
+         if wl["op"] == "decode_peer" else f"stripe-sharded x{args.gpus}, no collective"}
     if stats:
         c["slp"] = {k: stats[k] for k in ("xor_count", "mem_count", "n_instr", "nvar", "maxlive",
                                           "regs", "spill_bytes", "regs_tma", "spill_bytes_tma",
@@ -346,6 +361,21 @@ def main():
                                            "grouped_pipe": "pipe"}.get(mode, "straight"))
         prog = progs[0]
         m_out = wl["e"]
+    elif wl["op"] == "decode_peer":
+        import synth
+        from paper_2108_02692_b200 import peer
+        pl = peer.Placement(n, p, world, wl["S"] * world)
+        if "erased" in wl:
+            erasures = lambda s: wl["erased"]                                   # noqa: E731
+        else:
+            erasures = lambda s: synth.erasure_pattern(wl["seed"], s, n + p, wl["e"])  # noqa: E731
+        plan = peer.Plan(pl, rank, erasures)
+        mode = "grouped" if len(plan.keys) > 1 else "straight"
+        progs = peer.compile_plan(X, G, plan, compress=args.compress, threads=args.threads,
+                                  lane_words=args.lanes, block_bytes_hint=B, stages=args.stages,
+                                  kernel="straight")
+        prog = progs[0]
+        m_out = plan.e
     elif wl["op"] in ("decode_one", "decode_sharded"):
         erased = erased_of(wl)
         bits, _surv = X.xslp_decode_bitmatrix(G, n, p, erased)
@@ -378,7 +408,18 @@ def main():
     n_in = n
     dout = torch.empty((S, m_out, B), dtype=torch.uint8, device="cuda")
     to = X.block_table(dout, S, m_out, B)
-    if wl["op"] in ("decode_one", "decode_sharded"):
+    if wl["op"] == "decode_peer":
+        S = len(plan.stripes)
+        dout = torch.empty((S, m_out, B), dtype=torch.uint8, device="cuda")
+        enc = X.xslp_compile(X.xslp_encode_bitmatrix(G, n, p), block_bytes_hint=B)
+        din = torch.empty(pl.storage_shape(B), dtype=torch.uint8, device="cuda")
+        peer.fill_storage(X, pl, rank, din, wl["seed"], enc, chunk=32, stream=stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()                # every rank's storage written before any peer read
+        pdec = peer.PeerDecoder(X, pl, din, dout, plan, progs, dist=dist)
+        remote_blocks, all_blocks = plan.remote_reads()
+    elif wl["op"] in ("decode_one", "decode_sharded"):
         # whole codewords (data from the generator, parity by the encode program, untimed);
         # the decode program reads the n survivors of each stripe through the pointer table
         din = torch.empty((S, n + p, B), dtype=torch.uint8, device="cuda")
@@ -400,7 +441,9 @@ def main():
         gids = torch.from_numpy(gids).cuda()
 
     def launch(st=stream):
-        if wl["op"] == "decode_multi" and mode == "interp":
+        if wl["op"] == "decode_peer":
+            pdec.launch(stream=st, nstreams=args.streams)
+        elif wl["op"] == "decode_multi" and mode == "interp":
             X.xslp_decode_batch_multi(progs, idx, ti, to, S, B, stream=st)
         elif wl["op"] == "decode_multi":
             X.xslp_decode_batch_grouped(progs, gids, goff, ti, to, B, nstreams=args.streams,
@@ -425,12 +468,24 @@ def main():
     elif wl["op"] in ("decode_one", "decode_sharded"):
         if not torch.equal(dout, din[:, erased_idx]):
             raise SystemExit("sanity check failed: decoded blocks != the erased blocks")
+    elif wl["op"] == "decode_peer":       # regenerate a few home codewords locally and compare
+        chk = plan.stripes[:2] + plan.stripes[-2:]
+        full = torch.empty((1, n + p, B), dtype=torch.uint8, device="cuda")
+        for s_ in chk:
+            X.xslp_fill_random(full, 1, n + p, B, seed=wl["seed"], stripe0=s_)
+            tf = X.block_table(full, 1, n + p, B).view(1, n + p)
+            X.xslp_encode_batch(enc, tf[:, :n].contiguous(), tf[:, n:].contiguous(), 1, B)
+            i = plan.stripes.index(s_)
+            want = full[0, list(plan.keys[plan.key_of[i]][0])]
+            if not torch.equal(dout[i], want):
+                raise SystemExit(f"sanity check failed: cross-GPU decode of stripe {s_}")
+        del full
 
     graph = None
     if args.graph:
         # one step's launches (all per-pattern kernels, their fork/join over the internal
         # streams) captured once and replayed: removes the host launch cost, not device work
-        for pr in (progs if wl["op"] == "decode_multi" else [prog]):
+        for pr in (progs if wl["op"] in ("decode_multi", "decode_peer") else [prog]):
             X.xslp_prepare(pr, B)
         cap = torch.cuda.Stream()
         cap.wait_stream(stream)
@@ -482,10 +537,22 @@ def main():
             "peak_source": peak_src, "kernel": kernel_name(args, wl, stats),
             "alg_bytes_per_launch": alg_bytes_launch, "launch_ms": round(launch_ms, 4),
             "alg_bytes_per_data_byte": round((n_in + m_out) / n, 4)}
+    if wl["op"] == "decode_peer":
+        # survivors read over NVLink from peer HBM: the second roof of the fused gather+decode
+        rem_bytes = remote_blocks * B
+        nv = rem_bytes / (launch_ms / 1e3) / 1e9
+        roof["nvlink"] = {"remote_bytes_per_launch": rem_bytes,
+                          "remote_fraction": round(remote_blocks / max(1, all_blocks), 4),
+                          "achieved": round(nv, 1), "peak": NVLINK_GBS, "unit": "GB/s",
+                          "frac": round(nv / NVLINK_GBS, 4),
+                          "peak_source": "B200_PROFILING.md measured peer copy, per direction"}
+        if world > 1 and nv / NVLINK_GBS > roof["frac"]:
+            roof.update(bound="nvlink", achieved=round(nv, 1), peak=NVLINK_GBS,
+                        frac=round(nv / NVLINK_GBS, 4), peak_source=roof["nvlink"]["peak_source"])
 
     # ---- e2e through the host-buffer C-ABI call ----
     e2e = None
-    if not args.no_e2e and wl["op"] != "decode_multi":
+    if not args.no_e2e and wl["op"] not in ("decode_multi", "decode_peer"):
         try:
             # pinned host buffers: the full workload at N=1; at most 16 GiB over all ranks
             Se = min(S, max(1, (16 << 30) // max(1, world) // ((n + p) * B)))

@@ -135,6 +135,16 @@ int xslp_encode_bitmatrix(const uint8_t *gf, int n, int p, uint8_t *bits_out);
 int xslp_decode_bitmatrix(const uint8_t *gf, int n, int p, const int32_t *erased, int ne,
                           uint8_t *bits_out, int32_t *survivors_out);
 
+/* Decode bitmatrix over an explicit survivor set: survivors[0..n) are n distinct non-erased
+ * block indices in the order the decode program will read them (its input block j is block
+ * survivors[j]).  Same goal rows as xslp_decode_bitmatrix (reading R4) with M =
+ * the survivors' rows; any n survivors of an MDS code work.  Used by the
+ * cross-GPU decode to read as many survivors as possible from local memory.  bits_out:
+ * (8ne) x (8n).  Errors: XSLP_EUNRECOVERABLE if ne > p; XSLP_EINVAL for bad, duplicate or
+ * erased survivor indices; XSLP_ESINGULAR if M is singular. */
+int xslp_decode_bitmatrix_from(const uint8_t *gf, int n, int p, const int32_t *erased, int ne,
+                               const int32_t *survivors, uint8_t *bits_out);
+
 /* ---- compile (host, untimed) ------------------------------------------------------- */
 
 /* bits: out_rows x in_cols (in_cols a multiple of 8, out_rows a multiple of 8, in_cols <= 512).
@@ -227,6 +237,38 @@ int xslp_encode_host(const xslp_program *prog, const uint8_t *h_in, uint8_t *h_o
  * ((s*64 + j) << 40) + i), s = stripe0 + local index.  block_bytes % 8 == 0. */
 int xslp_fill_random(uint8_t *d_buf, int nstripes, int nblocks, size_t block_bytes,
                      uint64_t seed, int64_t stripe0, void *stream);
+
+/* ---- peer memory: cross-GPU decode over NVLink ---------------- */
+
+/* A decode whose survivor blocks live on other GPUs of the box reads them in place: the
+ * owning process exports its block storage, the decoding process maps it, and the pointer
+ * tables of xslp_encode_batch / xslp_decode_batch_grouped name the mapped (peer) addresses,
+ * so the kernel's strip loads travel over NVLink 5 / NVSwitch and feed the XORs directly
+ * (no staging copy).  The library never synchronises with other processes: the caller
+ * orders the owner's writes before the reads (e.g. a host barrier after a device sync) and
+ * keeps the exported memory alive until every mapping is closed. */
+#define XSLP_PEER_HANDLE_BYTES 128
+
+/* handle_out (XSLP_PEER_HANDLE_BYTES host bytes): a process-portable handle of the device
+ * allocation containing d_ptr (cudaIpcGetMemHandle of its base) plus d_ptr's offset in it.
+ * d_ptr must come from cudaMalloc (not VMM / expandable segments).  Errors: XSLP_EINVAL for a
+ * non-device pointer, XSLP_ECUDA from the runtime. */
+int xslp_peer_export(const void *d_ptr, uint8_t *handle_out);
+
+/* Map a handle from xslp_peer_export on the current device; *d_ptr_out = the exported
+ * pointer as seen from here.  Another process's allocation is opened once (IPC, peer access
+ * enabled lazily) and reference-counted; a handle exported by this same process returns the
+ * original pointer (peer access from the current device to the exporter's device enabled).
+ * Errors: XSLP_EINVAL for a malformed handle, XSLP_ECUDA when the runtime refuses. */
+int xslp_peer_open(const uint8_t *handle, void **d_ptr_out);
+
+/* Release one xslp_peer_open of d_ptr (the IPC mapping is closed with its last release).
+ * XSLP_EINVAL if d_ptr was not returned by xslp_peer_open. */
+int xslp_peer_close(void *d_ptr);
+
+/* Enable direct access from the current device to peer_device (idempotent); for one process
+ * driving several GPUs.  XSLP_ECUDA if the pair has no P2P path. */
+int xslp_peer_enable(int peer_device);
 
 /* ---- codec front end ------------------------------------------ */
 

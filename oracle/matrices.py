@@ -114,6 +114,32 @@ def decode_rows(g, n, erased):
     return survivors, rows
 
 
+def decode_rows_from(g, n, erased, survivors):
+    """P:526-530 with an explicit survivor set (any n non-erased blocks of an MDS code).
+
+    Input block j of the decode is block survivors[j]; M = those rows of g, and the goal
+    rows are as in decode_rows: erased data block e -> row e of M^-1, erased parity block
+    e -> g[e] . M^-1, erased indices ascending.
+    """
+    total = len(g)
+    erased = sorted(set(erased))
+    survivors = list(survivors)
+    if len(survivors) != n or len(set(survivors)) != n:
+        raise ValueError("need n distinct survivors")
+    if any(s < 0 or s >= total or s in erased for s in survivors):
+        raise ValueError("bad survivor index")
+    if any(e < 0 or e >= total for e in erased):
+        raise ValueError("erasure index out of range")
+    minv = gf_invert([g[i] for i in survivors])
+    rows = []
+    for e in erased:
+        if e < n:
+            rows.append(list(minv[e]))
+        else:
+            rows.append(gf_matmul([g[e]], minv)[0])
+    return rows
+
+
 def tilde(x):
     """8x8 GF(2) matrix of multiply-by-x: entry (r, k) = bit r of x * 2^k."""
     t = np.zeros((8, 8), dtype=np.uint8)

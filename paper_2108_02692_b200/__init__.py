@@ -71,6 +71,12 @@ _sig = {
     "xslp_coding_matrix": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]),
     "xslp_encode_bitmatrix": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P]),
     "xslp_decode_bitmatrix": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int, _P, _P]),
+    "xslp_decode_bitmatrix_from": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int,
+                                                  _P, _P]),
+    "xslp_peer_export": (ctypes.c_int, [_P, _P]),
+    "xslp_peer_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "xslp_peer_close": (ctypes.c_int, [_P]),
+    "xslp_peer_enable": (ctypes.c_int, [ctypes.c_int]),
     "xslp_compile": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(xslp_opts),
                                     ctypes.POINTER(_P)]),
     "xslp_compile_text": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(xslp_opts),
@@ -229,6 +235,48 @@ def xslp_decode_bitmatrix(gf, n, p, erased):
     _check(_lib.xslp_decode_bitmatrix(gf.ctypes.data, n, p, er.ctypes.data if len(er) else None,
                                       len(er), out.ctypes.data, surv.ctypes.data))
     return out, surv
+
+
+def xslp_decode_bitmatrix_from(gf, n, p, erased, survivors):
+    """Decode bitmatrix reading the given n survivors (input block j = block survivors[j])."""
+    gf = np.ascontiguousarray(gf, dtype=np.uint8)
+    er = np.ascontiguousarray(list(erased), dtype=np.int32)
+    sv = np.ascontiguousarray(list(survivors), dtype=np.int32)
+    if len(sv) != n:
+        raise XslpError(-1, "need exactly n survivors")
+    out = np.zeros((8 * len(er), 8 * n), dtype=np.uint8)
+    _check(_lib.xslp_decode_bitmatrix_from(gf.ctypes.data, n, p, er.ctypes.data if len(er) else None,
+                                           len(er), sv.ctypes.data, out.ctypes.data))
+    return out
+
+
+# ---- peer memory (cross-GPU decode) ---------------------------------------------------
+PEER_HANDLE_BYTES = 128
+
+
+def xslp_peer_export(d_ptr):
+    """bytes handle of the device allocation holding d_ptr (tensor or address)."""
+    h = ctypes.create_string_buffer(PEER_HANDLE_BYTES)
+    _check(_lib.xslp_peer_export(_ptr(d_ptr), h))
+    return h.raw
+
+
+def xslp_peer_open(handle):
+    """Address (int) of an exported pointer, mapped on the current device."""
+    if len(handle) != PEER_HANDLE_BYTES:
+        raise XslpError(-1, "bad handle length")
+    out = _P()
+    buf = ctypes.create_string_buffer(bytes(handle), PEER_HANDLE_BYTES)
+    _check(_lib.xslp_peer_open(buf, ctypes.byref(out)))
+    return out.value
+
+
+def xslp_peer_close(d_ptr):
+    _check(_lib.xslp_peer_close(_ptr(d_ptr)))
+
+
+def xslp_peer_enable(peer_device):
+    _check(_lib.xslp_peer_enable(peer_device))
 
 
 # ---- compile ------------------------------------------------------------------------

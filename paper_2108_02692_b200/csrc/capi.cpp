@@ -64,21 +64,11 @@ extern "C" int xslp_encode_bitmatrix(const uint8_t *gf_in, int n, int p, uint8_t
   API_END
 }
 
-extern "C" int xslp_decode_bitmatrix(const uint8_t *g, int n, int p, const int32_t *erased, int ne,
-                                     uint8_t *bits_out, int32_t *survivors_out) {
-  API_BEGIN
-  if (!g || !bits_out || !survivors_out || n < 1 || p < 0 || n + p > 255 || ne < 0 ||
-      (ne > 0 && !erased))
-    throw Error(XSLP_EINVAL, "bad arguments");
-  if (ne > p) throw Error(XSLP_EUNRECOVERABLE, "more erasures than parity blocks");
-  std::set<int> es;
-  for (int i = 0; i < ne; ++i) {
-    if (erased[i] < 0 || erased[i] >= n + p) throw Error(XSLP_EINVAL, "erasure index out of range");
-    if (!es.insert(erased[i]).second) throw Error(XSLP_EINVAL, "duplicate erasure index");
-  }
-  std::vector<int> surv;
-  for (int i = 0; i < n + p && (int)surv.size() < n; ++i)
-    if (!es.count(i)) surv.push_back(i);
+// Goal rows of the erased blocks (ascending index) over the survivors surv (n distinct
+// non-erased indices, in the column order the caller wants): M = the survivors'
+// rows of g; data block e is row e of M^-1, parity block e is g[e] M^-1 (reading R4).
+static std::vector<uint8_t> decode_bits(const uint8_t *g, int n, int p, const std::set<int> &es,
+                                        const std::vector<int> &surv) {
   std::vector<uint8_t> M((size_t)n * n);
   for (int r = 0; r < n; ++r)
     for (int c = 0; c < n; ++c) M[r * n + c] = g[(size_t)surv[r] * n + c];
@@ -95,9 +85,52 @@ extern "C" int xslp_decode_bitmatrix(const uint8_t *g, int n, int p, const int32
       }
     }
   }
-  auto b = gf::to_bits(rows, ne, n);
+  (void)p;
+  return gf::to_bits(rows, (int)es.size(), n);
+}
+
+static std::set<int> erased_set(int n, int p, const int32_t *erased, int ne) {
+  if (ne > p) throw Error(XSLP_EUNRECOVERABLE, "more erasures than parity blocks");
+  std::set<int> es;
+  for (int i = 0; i < ne; ++i) {
+    if (erased[i] < 0 || erased[i] >= n + p) throw Error(XSLP_EINVAL, "erasure index out of range");
+    if (!es.insert(erased[i]).second) throw Error(XSLP_EINVAL, "duplicate erasure index");
+  }
+  return es;
+}
+
+extern "C" int xslp_decode_bitmatrix(const uint8_t *g, int n, int p, const int32_t *erased, int ne,
+                                     uint8_t *bits_out, int32_t *survivors_out) {
+  API_BEGIN
+  if (!g || !bits_out || !survivors_out || n < 1 || p < 0 || n + p > 255 || ne < 0 ||
+      (ne > 0 && !erased))
+    throw Error(XSLP_EINVAL, "bad arguments");
+  auto es = erased_set(n, p, erased, ne);
+  std::vector<int> surv;
+  for (int i = 0; i < n + p && (int)surv.size() < n; ++i)
+    if (!es.count(i)) surv.push_back(i);
+  auto b = decode_bits(g, n, p, es, surv);
   std::copy(b.begin(), b.end(), bits_out);
   std::copy(surv.begin(), surv.end(), survivors_out);
+  API_END
+}
+
+extern "C" int xslp_decode_bitmatrix_from(const uint8_t *g, int n, int p, const int32_t *erased,
+                                          int ne, const int32_t *survivors, uint8_t *bits_out) {
+  API_BEGIN
+  if (!g || !bits_out || !survivors || n < 1 || p < 0 || n + p > 255 || ne < 0 ||
+      (ne > 0 && !erased))
+    throw Error(XSLP_EINVAL, "bad arguments");
+  auto es = erased_set(n, p, erased, ne);
+  std::set<int> seen;
+  std::vector<int> surv(survivors, survivors + n);
+  for (int s : surv) {
+    if (s < 0 || s >= n + p) throw Error(XSLP_EINVAL, "survivor index out of range");
+    if (es.count(s)) throw Error(XSLP_EINVAL, "survivor is erased");
+    if (!seen.insert(s).second) throw Error(XSLP_EINVAL, "duplicate survivor index");
+  }
+  auto b = decode_bits(g, n, p, es, surv);
+  std::copy(b.begin(), b.end(), bits_out);
   API_END
 }
 

@@ -315,3 +315,25 @@ def test_greedy_semantics_rs(cfg, cap):
     assert oslp.evaluate(p.dump()) == _sets(bits)
     assert oslp.evaluate(p.dump(1)) == _sets(bits)
     assert p.ccap() == oslp.ccap(p.dump())
+
+
+def test_decode_bitmatrix_from_matches_oracle():
+    import itertools
+    rng = np.random.default_rng(3)
+    for n, p, kind in [(4, 2, "cauchy"), (10, 4, "isal")]:
+        g = X.xslp_coding_matrix(n, p, kind)
+        og = mx.coding_matrix(n, p, kind)
+        for _ in range(12):
+            e = int(rng.integers(0, p + 1))
+            er = sorted(rng.choice(n + p, e, replace=False).tolist())
+            alive = [i for i in range(n + p) if i not in er]
+            sv = rng.permutation(rng.choice(alive, n, replace=False)).tolist()
+            bits = X.xslp_decode_bitmatrix_from(g, n, p, er, sv)
+            want = mx.to_bitmatrix(mx.decode_rows_from(og, n, er, sv)) if e else np.zeros((0, 8 * n))
+            assert bits.shape == (8 * e, 8 * n) and (bits == want).all()
+        er = [0]
+        with pytest.raises(X.XslpError):
+            X.xslp_decode_bitmatrix_from(g, n, p, er, [0] + list(range(1, n)))   # erased survivor
+        with pytest.raises(X.XslpError) as ei:                                   # > p erasures
+            X.xslp_decode_bitmatrix_from(g, n, p, list(range(p + 1)), list(range(n)))
+        assert ei.value.code == -3

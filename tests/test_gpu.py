@@ -555,3 +555,111 @@ def test_concurrent_host_threads():
 
     with ThreadPoolExecutor(6) as ex:
         assert all(ex.map(work, range(12)))
+
+
+# ---- cross-GPU decode over peer memory ------------------------------
+# One GPU here: the ranks are emulated in one process (their storages on cuda:0, the decode
+# tables built by the same code with the exporter's addresses), and the IPC path is exercised
+# by two processes sharing cuda:0 (no kernel waits on another; host barriers order the work).
+
+def _peer_setup(world, S, B, seed, e):
+    from paper_2108_02692_b200 import peer
+    n, p = 10, 4
+    g = X.xslp_coding_matrix(n, p)
+    enc = X.xslp_compile(X.xslp_encode_bitmatrix(g, n, p), block_bytes_hint=B)
+    pl = peer.Placement(n, p, world, S)
+    stores = []
+    for r in range(world):
+        st = torch.zeros(pl.storage_shape(B), dtype=torch.uint8, device="cuda")
+        peer.fill_storage(X, pl, r, st, seed, enc, chunk=8)
+        stores.append(st)
+    er = lambda s: synth.erasure_pattern(seed, s, n + p, e)   # noqa: E731
+    return peer, g, pl, stores, er
+
+
+@pytest.mark.parametrize("world,e", [(2, 4), (3, 3), (8, 2)])
+def test_peer_decode_emulated_ranks(world, e):
+    n, p, B, S = 10, 4, 65536, 24
+    og = mx.coding_matrix(n, p)
+    peer, g, pl, stores, er = _peer_setup(world, S, B, 51, e)
+    bases = []
+    for st in stores:                                   # same-process export/open round trip
+        a = X.xslp_peer_open(X.xslp_peer_export(st[1]))
+        assert a == st[1].data_ptr()
+        X.xslp_peer_close(a)
+        bases.append(st.data_ptr())
+    for r in range(world):
+        plan = peer.Plan(pl, r, er)
+        progs = peer.compile_plan(X, g, plan, kernel="straight", threads=64, block_bytes_hint=B)
+        out = torch.zeros((len(plan.stripes), plan.e, B), dtype=torch.uint8, device="cuda")
+        tin = torch.from_numpy(plan.in_table(bases, B).reshape(-1)).cuda()
+        tout = torch.from_numpy(plan.out_table(out.data_ptr(), B).reshape(-1)).cuda()
+        ids, off = plan.groups()
+        X.xslp_decode_batch_grouped(progs, torch.from_numpy(ids).cuda(), off, tin, tout, B, nstreams=4)
+        torch.cuda.synchronize()
+        for i, s in enumerate(plan.stripes):
+            erased, surv = plan.keys[plan.key_of[i]]
+            d = synth.stripe_data(51, s, n, B)
+            blocks = np.concatenate([d, rs.encode(og, n, d)])
+            if i < 3:                                   # oracle decode of the survivors read
+                rows = mx.decode_rows_from(og, n, list(erased), list(surv))
+                assert (out[i].cpu().numpy() == rs.decode(rows, blocks[list(surv)])).all()
+            assert (out[i].cpu().numpy() == blocks[list(erased)]).all(), (r, s)
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ok = False
+    try:
+        torch.cuda.set_device(0)
+        from paper_2108_02692_b200 import peer
+        n, p, B, S, seed = 10, 4, 65536, 16, 52
+        g = X.xslp_coding_matrix(n, p)
+        enc = X.xslp_compile(X.xslp_encode_bitmatrix(g, n, p), block_bytes_hint=B)
+        pl = peer.Placement(n, p, world, S)
+        st = torch.zeros(pl.storage_shape(B), dtype=torch.uint8, device="cuda")
+        peer.fill_storage(X, pl, rank, st, seed, enc, chunk=8)
+        er = lambda s: synth.erasure_pattern(seed, s, n + p, 3)   # noqa: E731
+        plan = peer.Plan(pl, rank, er)
+        progs = peer.compile_plan(X, g, plan, kernel="straight", threads=64, block_bytes_hint=B)
+        out = torch.zeros((len(plan.stripes), plan.e, B), dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+        dist.barrier()                                  # every storage written
+        dec = peer.PeerDecoder(X, pl, st, out, plan, progs, dist=dist)
+        assert len(dec.mapped) == world - 1
+        dec.launch()
+        torch.cuda.synchronize()
+        # expected bytes: this rank regenerates every codeword of its home stripes locally
+        full = torch.zeros((S, n + p, B), dtype=torch.uint8, device="cuda")
+        X.xslp_fill_random(full, S, n + p, B, seed=seed)
+        t = X.block_table(full, S, n + p, B).view(S, n + p)
+        X.xslp_encode_batch(enc, t[:, :n].contiguous(), t[:, n:].contiguous(), S, B)
+        torch.cuda.synchronize()
+        ok = all(torch.equal(out[i], full[s, list(plan.keys[plan.key_of[i]][0])])
+                 for i, s in enumerate(plan.stripes))
+        rem, tot = plan.remote_reads()
+        ok = ok and rem > 0
+        dist.barrier()                                  # all reads done before unmapping
+        dec.close()
+        dist.barrier()
+    finally:
+        q.put((rank, ok))
+        dist.destroy_process_group()
+
+
+def test_peer_decode_ipc_two_processes():
+    import os
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29900 + os.getpid() % 97
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+    assert res == [(0, True), (1, True)]

@@ -146,3 +146,52 @@ def test_rejects_ragged():
     with pytest.raises(ValueError):
         rs.apply_rows([[1]], np.zeros((1, 12), dtype=np.uint8))
     assert rs.apply_rows([[1]], np.zeros((1, 0), dtype=np.uint8)).shape == (1, 0)
+
+
+# ---- decode over an explicit survivor set (cross-GPU decode reads local survivors first) ----
+
+def test_decode_from_any_survivor_set_rs42_exhaustive():
+    # MDS: ANY n of the n+p blocks recover the rest; every erasure pattern of
+    # size <= p and every n-subset of the non-erased blocks, in a scrambled column order
+    n, p = 4, 2
+    g = mx.coding_matrix(n, p, "cauchy")
+    data = stripe_data(12, 0, n, 32)
+    blocks = np.concatenate([data, rs.encode(g, n, data)])
+    rng = np.random.default_rng(5)
+    cases = 0
+    for ne in range(0, p + 1):
+        for erased in itertools.combinations(range(n + p), ne):
+            alive = [i for i in range(n + p) if i not in erased]
+            for surv in itertools.combinations(alive, n):
+                surv = list(rng.permutation(surv))
+                rows = mx.decode_rows_from(g, n, list(erased), surv)
+                assert (rs.decode(rows, blocks[surv]) == blocks[list(erased)]).all()
+                cases += 1
+    assert cases == 15 + 6 * 5 + 15 * 1   # 0, 1 and 2 erasures: C(6,4), 6 C(5,4), C(6,2)
+
+
+def test_decode_from_first_n_equals_decode_rows():
+    g = mx.coding_matrix(10, 4, "isal")
+    for erased in ([2, 4, 5, 6], [0, 13], [11], [0, 1, 2, 3]):
+        surv, rows = mx.decode_rows(g, 10, erased)
+        assert mx.decode_rows_from(g, 10, erased, surv) == rows
+
+
+def test_decode_from_raid5_closed_form():
+    # [I; 2^ij]: erase data block j, read the other data blocks and parity 0 -> D_j is their
+    # plain XOR, i.e. every coefficient is 1 whatever the column order
+    n, p = 10, 4
+    g = mx.coding_matrix(n, p, "isal")
+    for j in (0, 6, 9):
+        surv = [n] + [i for i in range(n) if i != j][::-1]
+        assert mx.decode_rows_from(g, n, [j], surv) == [[1] * n]
+
+
+def test_decode_from_rejects_bad_survivors():
+    g = mx.coding_matrix(4, 2, "cauchy")
+    with pytest.raises(ValueError):
+        mx.decode_rows_from(g, 4, [0], [0, 1, 2, 3])      # an erased survivor
+    with pytest.raises(ValueError):
+        mx.decode_rows_from(g, 4, [0], [1, 1, 2, 3])      # duplicate
+    with pytest.raises(ValueError):
+        mx.decode_rows_from(g, 4, [0], [1, 2, 3])         # too few
