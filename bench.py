@@ -104,6 +104,7 @@ def parse():
     ap.add_argument("--stages", type=int, default=None)
     ap.add_argument("--streams", type=int, default=8, help="internal streams for grouped decode")
     ap.add_argument("--lanes", type=int, default=1)
+    ap.add_argument("--groups", type=int, default=None, help="PIPE consumer groups (goal split)")
     ap.add_argument("--threads", type=int, default=None)
     ap.add_argument("--block-bytes", type=int, default=0, help="override block size")
     ap.add_argument("--p", type=int, default=0, help="override parity count (cfg4 sweep)")
@@ -287,7 +288,7 @@ def config_of(args, wl, stats):
          else wl["S"] // max(1, args.gpus),
          "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": args.compress + ("+fuse" if args.fuse else "") + ("+dfs" if args.schedule else ""),
          "kernel": args.kernel, "lane_words": args.lanes, "threads": args.threads,
-         "stages": args.stages, "cuda_graph": bool(args.graph),
+         "stages": args.stages, "groups": args.groups, "cuda_graph": bool(args.graph),
          "l2": "inputs larger than the 126 MB L2; no flush between steps",
          "parallelism": (f"blocks spread over {args.gpus} GPU(s); survivors read in place over "
                          "NVLink P2P by the decode kernel (no collective)")
@@ -295,7 +296,7 @@ def config_of(args, wl, stats):
     if stats:
         c["slp"] = {k: stats[k] for k in ("xor_count", "mem_count", "n_instr", "nvar", "maxlive",
                                           "regs", "spill_bytes", "regs_tma", "spill_bytes_tma",
-                                          "regs_pipe", "spill_bytes_pipe")}
+                                          "regs_pipe", "spill_bytes_pipe", "group_xor")}
     return c
 
 
@@ -310,6 +311,7 @@ def main():
     args.kernel = args.kernel or "auto"
     args.threads = args.threads or 128
     args.stages = args.stages or 2
+    args.groups = args.groups or 1
     args.graph = int(args.graph or 0)
     if args.p:
         wl["p"] = args.p
@@ -381,13 +383,14 @@ def main():
         bits, _surv = X.xslp_decode_bitmatrix(G, n, p, erased)
         prog = X.xslp_compile(bits, compress=args.compress, kernel=args.kernel,
                               lane_words=args.lanes, threads=args.threads, block_bytes_hint=B,
-                              stages=args.stages)
+                              stages=args.stages, groups=args.groups)
         m_out = len(erased)
     else:
         prog = X.xslp_compile(X.xslp_encode_bitmatrix(G, n, p), compress=args.compress,
                               kernel=args.kernel, lane_words=args.lanes, threads=args.threads,
                               block_bytes_hint=B, stages=args.stages, fuse=args.fuse,
-                              schedule=args.schedule, layout=wl.get("layout", "strip"))
+                              schedule=args.schedule, layout=wl.get("layout", "strip"),
+                              groups=args.groups)
         m_out = p
     compile_s = time.perf_counter() - t0
     log(f'compiled in {compile_s:.2f} s', prog.stats())

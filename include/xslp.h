@@ -92,6 +92,11 @@ typedef struct xslp_opts {
   int32_t stages;          /* shared-memory stages of the PIPE kernel (1..8); default 2 */
   int32_t greedy_capacity; /* cache capacity c (blocks) of XSLP_SCHED_GREEDY */
   int32_t layout;          /* XSLP_LAYOUT_*; default STRIP */
+  int32_t groups;          /* PIPE kernel consumer groups (1..4; default 1): the goals are split
+                              into `groups` sets (contiguous, balanced by instruction count) and
+                              each set's sub-program (the instructions its goals reach) runs on
+                              its own `threads` consumer threads over the same shared-memory
+                              stage, so a wide program keeps more warps issuing per SM */
 } xslp_opts;
 
 typedef struct xslp_stats {
@@ -111,6 +116,8 @@ typedef struct xslp_stats {
   int32_t regs_pipe;  /* registers per thread of the persistent TMA pipeline kernel */
   int32_t spill_bytes_pipe; /* its spill stores */
   double compile_ms;  /* host compile time of xslp_compile (SLP passes + PTX -> cubin) */
+  int64_t group_xor;  /* PIPE consumer groups: XORs executed per word position summed over the
+                         groups (>= xor_count: shared temporaries are recomputed); 0 if groups == 1 */
 } xslp_stats;
 
 typedef struct xslp_program xslp_program; /* opaque, immutable after compile, thread-safe to share */

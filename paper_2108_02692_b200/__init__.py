@@ -48,7 +48,7 @@ class xslp_opts(ctypes.Structure):
                 ("block_bytes_hint", ctypes.c_int64), ("kernel", ctypes.c_int32),
                 ("goal_order", ctypes.c_int32), ("min_blocks", ctypes.c_int32),
                 ("stages", ctypes.c_int32), ("greedy_capacity", ctypes.c_int32),
-                ("layout", ctypes.c_int32)]
+                ("layout", ctypes.c_int32), ("groups", ctypes.c_int32)]
 
 
 class xslp_stats(ctypes.Structure):
@@ -59,7 +59,8 @@ class xslp_stats(ctypes.Structure):
                 ("n_zero_goals", ctypes.c_int32), ("regs", ctypes.c_int32),
                 ("spill_bytes", ctypes.c_int32), ("regs_tma", ctypes.c_int32),
                 ("spill_bytes_tma", ctypes.c_int32), ("regs_pipe", ctypes.c_int32),
-                ("spill_bytes_pipe", ctypes.c_int32), ("compile_ms", ctypes.c_double)]
+                ("spill_bytes_pipe", ctypes.c_int32), ("compile_ms", ctypes.c_double),
+                ("group_xor", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -45,6 +45,7 @@ extern "C" void xslp_default_opts(xslp_opts *o) {
   o->stages = 2;
   o->greedy_capacity = 0;
   o->layout = XSLP_LAYOUT_STRIP;
+  o->groups = 1;
 }
 
 extern "C" int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out) {
@@ -193,15 +194,22 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
         if (t < P.n_const) P.const_reads++;
   }
   st.regs = st.spill_bytes = st.regs_tma = st.spill_bytes_tma = st.regs_pipe = st.spill_bytes_pipe = 0;
+  st.group_xor = 0;
   const bool device_ok = P.n_const % 8 == 0 && P.n_goals % 8 == 0 && P.n_const > 0 &&
                          P.n_const / 8 + P.n_goals / 8 <= 128;
   if (o.specialise && device_ok) {
-    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads, o.min_blocks, o.stages, o.layout);
+    if (o.groups > 1 && o.layout == XSLP_LAYOUT_STRIP) {
+      P.groups = split_goals(P.slp, o.groups);
+      for (auto &g : P.groups)
+        for (auto &in : g.ins) st.group_xor += (int64_t)in.ops.size() - 1;
+    }
+    const std::vector<Slp> *gp = P.groups.empty() ? nullptr : &P.groups;
+    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads, o.min_blocks, o.stages, o.layout, gp);
     P.cubin_generic = ptx_to_cubin(P.ptx_generic, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma, &st.regs_pipe, &st.spill_bytes_pipe);
     if (o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0) {
       P.baked_strip = o.block_bytes_hint / 8;
       P.ptx_baked = emit_ptx(P.slp, o.lane_words, P.baked_strip, o.threads, o.min_blocks, o.stages,
-                           o.layout);
+                           o.layout, gp);
       P.cubin_baked = ptx_to_cubin(P.ptx_baked, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma, &st.regs_pipe, &st.spill_bytes_pipe);
     }
   }
@@ -226,7 +234,8 @@ void check_opts(xslp_opts &o) {
     throw Error(XSLP_EINVAL, "the byte layout runs on the straight-line (LDG) kernel only");
   if (o.layout == XSLP_LAYOUT_BYTE && !o.specialise)
     throw Error(XSLP_EINVAL, "the byte layout needs specialise = 1");
-  if (o.kernel == XSLP_KERNEL_PIPE && o.threads > 992) throw Error(XSLP_EINVAL, "pipe kernel: threads <= 992");
+  if (o.groups < 1 || o.groups > 4) throw Error(XSLP_EINVAL, "groups must be 1..4");
+  if (o.threads * o.groups > 992) throw Error(XSLP_EINVAL, "pipe kernel: threads * groups <= 992");
 }
 
 }  // namespace

@@ -891,3 +891,95 @@ Slp parse_text(const std::string &text, int n_const) {
 }
 
 }  // namespace xslp
+
+namespace xslp {
+
+// ---------------------------------------------------------------------------------
+// Goal split for the PIPE kernel's consumer groups.  The goals [0, m) are cut into k
+// contiguous ranges; a range's cost is the issue count of the instructions its goals reach
+// (ceil((arity-1)/2) LOP3s + one shared-memory read per constant operand) plus its stores.
+// Cut points (every goal for m <= 64, else evenly spaced block boundaries) are chosen by a
+// DP minimising the largest range cost; shared temporaries are recomputed per group.
+std::vector<Slp> split_goals(const Slp &s, int k) {
+  const int m = (int)s.goal.size(), nc = s.n_const;
+  if (k < 1) throw Error(XSLP_EINVAL, "split_goals: k < 1");
+  std::vector<int> def(s.n_vars, -1);
+  for (size_t i = 0; i < s.ins.size(); ++i) def[s.ins[i].var] = (int)i;
+  auto reach = [&](int lo, int hi) {
+    std::vector<char> keep(s.ins.size(), 0);
+    std::vector<int> st;
+    for (int g = lo; g < hi; ++g)
+      if (s.goal[g] >= nc) st.push_back(def[s.goal[g] - nc]);
+    while (!st.empty()) {
+      int i = st.back();
+      st.pop_back();
+      if (i < 0 || keep[i]) continue;
+      keep[i] = 1;
+      for (int t : s.ins[i].ops)
+        if (t >= nc) st.push_back(def[t - nc]);
+    }
+    return keep;
+  };
+  auto cost = [&](int lo, int hi) {
+    auto keep = reach(lo, hi);
+    int64_t c = hi - lo;
+    for (size_t i = 0; i < s.ins.size(); ++i) {
+      if (!keep[i]) continue;
+      const auto &ops = s.ins[i].ops;
+      c += ((int64_t)ops.size() - 1 + 1) / 2;
+      for (int t : ops) c += t < nc;
+    }
+    return c;
+  };
+  std::vector<int> pos;  // candidate cut positions, including 0 and m
+  if (m <= 64) {
+    for (int g = 0; g <= m; ++g) pos.push_back(g);
+  } else {
+    const int step = std::max(8, (m / 64 + 7) / 8 * 8);
+    for (int g = 0; g < m; g += step) pos.push_back(g);
+    pos.push_back(m);
+  }
+  const int P = (int)pos.size() - 1;  // segments between consecutive positions
+  k = std::min(k, std::max(1, P));
+  std::map<std::pair<int, int>, int64_t> memo;
+  auto C = [&](int a, int b) {  // cost of goals [pos[a], pos[b])
+    auto key = std::make_pair(a, b);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    int64_t v = cost(pos[a], pos[b]);
+    memo[key] = v;
+    return v;
+  };
+  const int64_t INF = INT64_MAX / 4;
+  // best[j][b]: min over splits of [0, pos[b]) into j non-empty ranges of the max range cost
+  std::vector<std::vector<int64_t>> best(k + 1, std::vector<int64_t>(P + 1, INF));
+  std::vector<std::vector<int>> arg(k + 1, std::vector<int>(P + 1, -1));
+  best[0][0] = 0;
+  for (int j = 1; j <= k; ++j)
+    for (int b = j; b <= P; ++b)
+      for (int a = j - 1; a < b; ++a) {
+        if (best[j - 1][a] >= INF) continue;
+        int64_t v = std::max(best[j - 1][a], C(a, b));
+        if (v < best[j][b]) { best[j][b] = v; arg[j][b] = a; }
+      }
+  std::vector<int> cuts(k + 1);
+  cuts[k] = P;
+  for (int j = k; j >= 1; --j) cuts[j - 1] = arg[j][cuts[j]];
+  std::vector<Slp> out;
+  for (int j = 0; j < k; ++j) {
+    const int lo = pos[cuts[j]], hi = pos[cuts[j + 1]];
+    auto keep = reach(lo, hi);
+    Slp r;
+    r.n_const = s.n_const;
+    r.n_vars = s.n_vars;
+    for (size_t i = 0; i < s.ins.size(); ++i)
+      if (keep[i]) r.ins.push_back(s.ins[i]);
+    r.goal = s.goal;
+    for (int g = 0; g < m; ++g)
+      if (g < lo || g >= hi) r.goal[g] = -2;
+    out.push_back(std::move(r));
+  }
+  return out;
+}
+
+}  // namespace xslp

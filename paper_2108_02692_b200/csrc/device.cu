@@ -330,7 +330,7 @@ static int auto_kernel(const Program *p, size_t block_bytes, int nstripes) {
   if (p->opts.layout == XSLP_LAYOUT_BYTE) return XSLP_KERNEL_STRAIGHT;
   const uint64_t strip = block_bytes / 8;
   const int T = p->opts.threads, L = p->opts.lane_words;
-  if (strip % 16 || p->opts.threads > 992) return XSLP_KERNEL_STRAIGHT;
+  if (strip % 16 || p->opts.threads * std::max<int>(1, (int)p->groups.size()) > 992) return XSLP_KERNEL_STRAIGHT;
   const size_t smem = 128 + (size_t)p->opts.stages * p->n_used_const * 4 * L * T;
   const uint64_t tiles = (strip / (4 * L) + T - 1) / T * (uint64_t)nstripes;
   if (smem > 227 * 1024 || p->opts.stages < 2 || tiles < 4 * 148) return XSLP_KERNEL_STRAIGHT;
@@ -339,6 +339,11 @@ static int auto_kernel(const Program *p, size_t block_bytes, int nstripes) {
   // programs, profiles/r01_cfg4_sweep.md) and the register-resident kernel wins
   if (p->const_reads * 4.0 / (4.0 * p->n_const) > 6.0) return XSLP_KERNEL_STRAIGHT;
   return XSLP_KERNEL_PIPE;
+}
+
+// PIPE CTA size: `groups` consumer groups of `threads` threads plus one producer warp
+static int pipe_block(const Program *p) {
+  return p->opts.threads * (p->groups.empty() ? 1 : (int)p->groups.size()) + 32;
 }
 
 static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *const *d_out,
@@ -383,13 +388,13 @@ static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *c
       if (it != J.pipe_occ.end()) {
         per = it->second;
       } else {
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)k, T + 32, smem));
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)k, pipe_block(p), smem));
         J.pipe_occ[d] = per;
       }
       grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms * std::max(1, per));
     }
     void *args[] = {(void *)&d_in, (void *)&d_out, (void *)&d_ids, &strip, &words, &tps, &ntiles};
-    CUDA_OK(cudaLaunchKernel((const void *)k, dim3(grid), dim3(T + 32), args, smem, st));
+    CUDA_OK(cudaLaunchKernel((const void *)k, dim3(grid), dim3(pipe_block(p)), args, smem, st));
     g_launches++;
     return;
   }
@@ -682,7 +687,7 @@ extern "C" int xslp_prepare(const xslp_program *prog, size_t block_bytes) {
                                                 (int)smem_pipe, d));
         J->smem_set_pipe[d] = (int)smem_pipe;
         int per = 0;
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)J->pipe, T + 32, smem_pipe));
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)J->pipe, pipe_block(p), smem_pipe));
         J->pipe_occ[d] = per;
       }
       if (J->tma && smem_tma <= 227 * 1024 && J->smem_set[d] < (int)smem_tma) {

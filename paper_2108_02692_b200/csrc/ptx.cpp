@@ -28,7 +28,9 @@ namespace xslp {
 namespace {
 
 struct Emitter {
-  const Slp &s;
+  const Slp *sp;                  // the program being emitted (a group's sub-program in PIPE)
+  const Slp &full;                // the whole program (declarations, other entries)
+  const std::vector<Slp> *groups; // PIPE consumer groups, or nullptr
   int L;
   int64_t baked;
   int threads;
@@ -38,15 +40,16 @@ struct Emitter {
   int n_in, n_out;
   std::ostringstream o;
   Emitter(const Slp &s_, int L_, int64_t baked_, int threads_, int min_blocks_, int stages_,
-          int layout_)
-      : s(s_), L(L_), baked(baked_), threads(threads_), min_blocks(min_blocks_), stages(stages_),
+          int layout_, const std::vector<Slp> *groups_)
+      : sp(&s_), full(s_), groups(groups_), L(L_), baked(baked_), threads(threads_), min_blocks(min_blocks_), stages(stages_),
         layout(layout_),
         n_in(s_.n_const / 8),
         n_out((int)(s_.goal.size() / 8)) {}
+  const Slp &cur() const { return *sp; }
 
   std::string creg(int c, int l) { return "%c" + std::to_string(c * L + l); }
   std::string vreg(int v, int l) { return "%v" + std::to_string(v * L + l); }
-  std::string treg(int t, int l) { return t < s.n_const ? creg(t, l) : vreg(t - s.n_const, l); }
+  std::string treg(int t, int l) { return t < cur().n_const ? creg(t, l) : vreg(t - cur().n_const, l); }
 
   const char *vsuf() { return L == 1 ? ".u32" : (L == 2 ? ".v2.u32" : ".v4.u32"); }
   std::string vec(const std::vector<std::string> &r) {
@@ -71,12 +74,12 @@ struct Emitter {
   //         TMA bulk copies (cp.async.bulk, one mbarrier), constants read from smem at use
   void body(int mode) {
     const bool one = mode == 1, tma = mode == 2;
-    const int nc = s.n_const;
+    const int nc = cur().n_const;
     std::vector<char> used(nc, 0);
-    for (size_t k = 0; k < s.ins.size(); ++k)
-      for (int t : s.ins[k].ops)
+    for (size_t k = 0; k < cur().ins.size(); ++k)
+      for (int t : cur().ins[k].ops)
         if (t < nc) used[t] = 1;
-    for (int g : s.goal)
+    for (int g : cur().goal)
       if (g >= 0 && g < nc) used[g] = 1;
     std::vector<char> blk_used(n_in, 0);
     std::vector<int> slot(nc, -1);
@@ -155,13 +158,14 @@ struct Emitter {
   // cp.async.bulk every used strip segment into the stage.  Consumers: wait full[st] ->
   // run the program reading the stage -> stores -> one arrive per warp on empty[st].
   void body_pipe(int S) {
-    const int nc = s.n_const;
+    const int nc = cur().n_const;
     const int TC = threads, NCW = threads / 32;
+    const int G = groups ? (int)groups->size() : 1;  // consumer groups, NCW warps each
     std::vector<char> used(nc, 0);
-    for (size_t k = 0; k < s.ins.size(); ++k)
-      for (int t : s.ins[k].ops)
+    for (size_t k = 0; k < cur().ins.size(); ++k)
+      for (int t : cur().ins[k].ops)
         if (t < nc) used[t] = 1;
-    for (int g : s.goal)
+    for (int g : cur().goal)
       if (g >= 0 && g < nc) used[g] = 1;
     std::vector<char> blk_used(n_in, 0);
     std::vector<int> slot(nc, -1);
@@ -175,7 +179,7 @@ struct Emitter {
     o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
     for (int k = 0; k < S; ++k) {
       o << "  mbarrier.init.shared::cta.b64 [%sb+" << 8 * k << "], 1;\n";
-      o << "  mbarrier.init.shared::cta.b64 [%sb+" << EB + 8 * k << "], " << NCW << ";\n";
+      o << "  mbarrier.init.shared::cta.b64 [%sb+" << EB + 8 * k << "], " << G * NCW << ";\n";
     }
     o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
     o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
@@ -185,7 +189,12 @@ struct Emitter {
       o << "  ld.param.u64 %sk1, [p_strip];\n";
       for (int k = 2; k < 8; ++k) o << "  mul.lo.u64 %sk" << k << ", %sk1, " << k << ";\n";
     }
-    o << "  shr.u32 %wid, %s2, 5;\n  setp.eq.u32 %pprod, %wid, " << NCW << ";\n  @%pprod bra $PROD;\n";
+    o << "  shr.u32 %wid, %s2, 5;\n  setp.eq.u32 %pprod, %wid, " << G * NCW << ";\n  @%pprod bra $PROD;\n";
+    // consumer group of this warp and the thread's column within the group
+    o << "  div.u32 %grp, %wid, " << NCW << ";\n  mul.lo.u32 %ltid, %grp, " << TC << ";\n";
+    o << "  sub.u32 %ltid, %s2, %ltid;\n";
+    for (int g = 1; g < G; ++g)
+      o << "  setp.eq.u32 %p5, %grp, " << g << ";\n  @%p5 bra $C" << g << "START;\n";
     // helper: stripe of %tile -> %s5, tile-in-strip -> %tw
     auto stripe_of = [&](const char *lab) {
       o << "  div.u32 %s5, %tile, %tps;\n  rem.u32 %tw, %tile, %tps;\n";
@@ -193,28 +202,39 @@ struct Emitter {
       o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
       o << lab << ":\n";
     };
-    // ---------------- consumers
-    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n  mov.u32 %lane, %laneid;\n";
-    o << "$CLOOP:\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
-    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n  and.b32 %ph, %ph, 1;\n";
-    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
-    o << "$CW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW;\n";
-    stripe_of("$CID");
-    o << "  mad.lo.u32 %s3, %tw, " << TC << ", %s2;\n";
-    o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $CSKIP;\n";
-    o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
-    o << "  mad.lo.u32 %sth, %s2, " << 4 * L << ", %sth;\n  add.u32 %sth, %sth, 128;\n";
-    o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
-    o << "  mul.wide.u32 %off, %s3, " << 4 * L << ";\n";
-    for (int i = 0; i < n_out; ++i) {
-      o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
-      o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
+    // ---------------- consumers (one loop per group; group g runs its sub-program)
+    for (int g = 0; g < G; ++g) {
+      const std::string x = std::to_string(g);
+      if (groups) sp = &(*groups)[g];
+      o << "$C" << x << "START:\n";
+      o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n  mov.u32 %lane, %laneid;\n";
+      o << "$CLOOP" << x << ":\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
+      o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n  and.b32 %ph, %ph, 1;\n";
+      o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
+      o << "$CW" << x << ":\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW" << x << ";\n";
+      stripe_of(("$CID" + x).c_str());
+      o << "  mad.lo.u32 %s3, %tw, " << TC << ", %ltid;\n";
+      o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $CSKIP" << x << ";\n";
+      o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
+      o << "  mad.lo.u32 %sth, %ltid, " << 4 * L << ", %sth;\n  add.u32 %sth, %sth, 128;\n";
+      o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+      o << "  mul.wide.u32 %off, %s3, " << 4 * L << ";\n";
+      std::vector<char> oused(n_out, 0);
+      for (int q = 0; q < (int)cur().goal.size(); ++q)
+        if (cur().goal[q] != -2) oused[q / 8] = 1;
+      for (int i = 0; i < n_out; ++i) {
+        if (!oused[i]) continue;
+        o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+        o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
+      }
+      int tmp = 0;
+      compute(true, 0, slot, used, tmp);
+      o << "$CSKIP" << x << ":\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT" << x << ";\n";
+      o << "  add.u32 %eb, %fb, " << EB << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
+      o << "$CNEXT" << x << ":\n  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, %nct;\n  bra.uni $CLOOP" << x << ";\n";
     }
+    sp = &full;
     int tmp = 0;
-    compute(true, 0, slot, used, tmp);
-    o << "$CSKIP:\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT;\n";
-    o << "  add.u32 %eb, %fb, " << EB << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
-    o << "$CNEXT:\n  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, %nct;\n  bra.uni $CLOOP;\n";
     // ---------------- producer
     o << "$PROD:\n  mov.u32 %lane, %laneid;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $DONE;\n";
     o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n";
@@ -272,12 +292,12 @@ struct Emitter {
   }
 
   void body_byte(bool one) {
-    const int nc = s.n_const;
+    const int nc = cur().n_const;
     std::vector<char> used(nc, 0);
-    for (auto &in : s.ins)
+    for (auto &in : cur().ins)
       for (int t : in.ops)
         if (t < nc) used[t] = 1;
-    for (int g : s.goal)
+    for (int g : cur().goal)
       if (g >= 0 && g < nc) used[g] = 1;
     o << "  mov.u32 %s0, %ctaid.x;\n  mov.u32 %s1, %ntid.x;\n  mov.u32 %s2, %tid.x;\n";
     o << "  mad.lo.u32 %s3, %s0, %s1, %s2;\n  ld.param.u32 %s4, [p_words];\n";
@@ -312,13 +332,13 @@ struct Emitter {
     }
     // when is each output block complete?
     std::vector<int> ready_at(n_out, -1);  // instruction index after which all 8 goals exist
-    for (int g = 0; g < (int)s.goal.size(); ++g) {
-      int t = s.goal[g], at = -1;
+    for (int g = 0; g < (int)cur().goal.size(); ++g) {
+      int t = cur().goal[g], at = -1;
       if (t >= nc) at = t - nc;  // var ids equal instruction positions (compacted)
       ready_at[g / 8] = std::max(ready_at[g / 8], at);
     }
     auto gval = [&](int g) {
-      int t = s.goal[g];
+      int t = cur().goal[g];
       if (t < 0) return std::string("%zero");
       return treg(t, 0);
     };
@@ -336,8 +356,8 @@ struct Emitter {
     };
     for (int i = 0; i < n_out; ++i)
       if (ready_at[i] < 0) store_block(i);
-    for (size_t k = 0; k < s.ins.size(); ++k) {
-      const auto &in = s.ins[k];
+    for (size_t k = 0; k < cur().ins.size(); ++k) {
+      const auto &in = cur().ins[k];
       const auto &ops = in.ops;
       std::string d = vreg(in.var, 0);
       size_t i;
@@ -362,7 +382,7 @@ struct Emitter {
   // slot*rowb] with a fresh volatile read per use; goals are stored when computed.
   void compute(bool tma, int off0, const std::vector<int> &slot, const std::vector<char> &used,
                int &tmp) {
-    const int nc = s.n_const;
+    const int nc = cur().n_const;
     const int rowb = 4 * L * threads;
     std::vector<char> loaded(nc, 0);
     auto need = [&](int c) {  // make constant c available in registers
@@ -383,9 +403,10 @@ struct Emitter {
       for (int c = 0; c < nc; ++c)
         if (used[c]) need(c);
     // goals that are constants or zero
-    std::vector<std::vector<int>> goals_of_var(s.n_vars);
-    for (size_t g = 0; g < s.goal.size(); ++g) {
-      int t = s.goal[g];
+    std::vector<std::vector<int>> goals_of_var(cur().n_vars);
+    for (size_t g = 0; g < cur().goal.size(); ++g) {
+      int t = cur().goal[g];
+      if (t == -2) continue;  // another consumer group's goal (PIPE split)
       if (t >= nc) { goals_of_var[t - nc].push_back((int)g); continue; }
       if (t >= 0) need(t);
       std::vector<std::string> r;
@@ -394,8 +415,8 @@ struct Emitter {
     }
     // the program
     int qn = 0;
-    for (size_t k = 0; k < s.ins.size(); ++k) {
-      const auto &in = s.ins[k];
+    for (size_t k = 0; k < cur().ins.size(); ++k) {
+      const auto &in = cur().ins[k];
       const auto &ops = in.ops;
       std::map<int, int> q;  // TMA: constant -> fresh register for this instruction
       for (int t : ops) {
@@ -445,28 +466,28 @@ struct Emitter {
     o << "  .reg .b32 %zero;\n";
     o << "  .reg .b64 %sk<8>;\n";
     o << "  .reg .b64 %ib<" << std::max(1, n_in) << ">;\n  .reg .b64 %ob<" << std::max(1, n_out) << ">;\n";
-    o << "  .reg .b32 %c<" << std::max(1, s.n_const * L) << ">;\n";
-    o << "  .reg .b32 %v<" << std::max(1, s.n_vars * L) << ">;\n";
+    o << "  .reg .b32 %c<" << std::max(1, cur().n_const * L) << ">;\n";
+    o << "  .reg .b32 %v<" << std::max(1, cur().n_vars * L) << ">;\n";
     o << "  .reg .b64 %ta<" << std::max(1, ntmp_guess) << ">;\n";
     o << "  .reg .b32 %sb, %sth, %nb;\n  .reg .b64 %toff;\n";
     o << "  .reg .b32 %tps, %nt, %nct, %wid, %it, %tile, %lane, %st, %ph, %fb, %eb, %tw, %dst;\n";
-    o << "  .reg .pred %pids, %pprod, %p5;\n";
+    o << "  .reg .pred %pids, %pprod, %p5;\n  .reg .b32 %grp, %ltid;\n";
     o << "  .reg .b32 %tx0;\n  .reg .b32 %y<8>;\n";
     int nq = 0;
-    for (auto &in : s.ins)
+    for (auto &in : cur().ins)
       for (int t : in.ops)
-        if (t < s.n_const) ++nq;
+        if (t < cur().n_const) ++nq;
     o << "  .reg .b32 %q<" << std::max(1, nq * L) << ">;\n";
     o << "  mov.u32 %zero, 0;\n";
   }
 
   std::string run() {
-    o << "//\n// xslp straight-line kernel: " << s.n_const << " constants, " << s.goal.size()
-      << " goals, " << s.ins.size() << " instructions, lanes=" << L << ", strip="
+    o << "//\n// xslp straight-line kernel: " << cur().n_const << " constants, " << cur().goal.size()
+      << " goals, " << cur().ins.size() << " instructions, lanes=" << L << ", strip="
       << (baked > 0 ? std::to_string(baked) : std::string("runtime")) << "\n//\n";
     o << ".version 8.8\n.target sm_100a\n.address_size 64\n\n";
     o << ".extern .shared .align 128 .b8 dsm[];\n\n";
-    const int ntmp = s.n_const + (int)s.goal.size() + 8;
+    const int ntmp = cur().n_const + (int)cur().goal.size() + 8;
     o << ".visible .entry xslp_sl_batch(\n  .param .u64 p_in,\n  .param .u64 p_out,\n"
          "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
          "  .param .u32 p_base)\n.maxntid "
@@ -495,7 +516,7 @@ struct Emitter {
     o << ".visible .entry xslp_sl_pipe(\n  .param .u64 p_in,\n  .param .u64 p_out,\n"
          "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
          "  .param .u32 p_tps,\n  .param .u32 p_ntiles)\n.maxntid "
-      << threads + 32 << ", 1, 1\n";
+      << threads * (groups ? (int)groups->size() : 1) + 32 << ", 1, 1\n";
     o << "{\n";
     decls(ntmp);
     body_pipe(stages);
@@ -507,13 +528,13 @@ struct Emitter {
 }  // namespace
 
 std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks,
-                     int stages, int layout) {
+                     int stages, int layout, const std::vector<Slp> *groups) {
   if (s.n_const % 8 || s.goal.size() % 8)
     throw Error(XSLP_EINVAL, "device programs need whole blocks (constants and goals multiples of 8)");
   if (s.n_const / 8 + s.goal.size() / 8 > 128)
     throw Error(XSLP_EINVAL, "too many blocks for one kernel (n + m > 128)");
   if (layout == XSLP_LAYOUT_BYTE) lanes = 1;
-  Emitter e(s, lanes, baked_strip, threads, min_blocks, stages, layout);
+  Emitter e(s, lanes, baked_strip, threads, min_blocks, stages, layout, groups);
   return e.run();
 }
 

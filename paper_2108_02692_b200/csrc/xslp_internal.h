@@ -87,6 +87,7 @@ struct Program {
   int nvar = 0;
   xslp_stats stats{};
   // interpreter bytecode (uint16 words) and slot count
+  std::vector<Slp> groups;         // PIPE consumer groups: goal-restricted sub-programs (opts.groups > 1)
   std::vector<uint16_t> code;
   int nslots = 0;
   // straight-line kernel(s): generic addressing + optional baked strip size
@@ -117,7 +118,10 @@ Slp parse_text(const std::string &text, int n_const);
 
 // PTX (ptx.cpp)
 std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks,
-                     int stages, int layout);
+                     int stages, int layout, const std::vector<Slp> *groups = nullptr);
+// Split the goals into k contiguous sets balanced by issue cost; each result keeps the
+// instructions its goals reach (original order and variable ids) and marks the other goals -2.
+std::vector<Slp> split_goals(const Slp &s, int k);
 std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, int *regs_tma,
                                int *spill_tma, int *regs_pipe, int *spill_pipe);
 

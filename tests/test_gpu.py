@@ -325,6 +325,39 @@ def test_pdec_full_size_sampled():
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("groups", [2, 3, 4])
+@pytest.mark.parametrize("case", ["rs10enc", "rs20dec", "cauchy42"])
+def test_pipe_consumer_groups(groups, case):
+    # PIPE kernel with the goals split over consumer groups: every output byte equals the
+    # oracle; ragged last tile (words not a multiple of the group width), baked and generic
+    if case == "rs10enc":
+        n, p, kind, er = 10, 4, "isal", None
+    elif case == "rs20dec":
+        n, p, kind, er = 20, 4, "isal", [0, 5, 21, 23]
+    else:
+        n, p, kind, er = 4, 2, "cauchy", None
+    og = mx.coding_matrix(n, p, kind)
+    g = X.xslp_coding_matrix(n, p, kind)
+    B, S = 8192 + 1152, 5                     # 292 words per strip: 2 tiles of 128 + a ragged 36
+    if er is None:
+        bits, rows, m = X.xslp_encode_bitmatrix(g, n, p), og[n:], p
+    else:
+        bits, _ = X.xslp_decode_bitmatrix(g, n, p, er)
+        rows, m = mx.decode_rows(og, n, er)[1], len(er)
+    for hint in (0, B):
+        prog = X.xslp_compile(bits, kernel="pipe", threads=128, stages=2, groups=groups,
+                              block_bytes_hint=hint)
+        st = prog.stats()
+        assert st["group_xor"] >= st["xor_count"]
+        din = dev_buf(S, n, B)
+        X.xslp_fill_random(din, S, n, B, seed=61 + groups)
+        dout = torch.full((S, m, B), 0xA5, dtype=torch.uint8, device="cuda")
+        run_batch(prog, din, dout, B)
+        for s in range(S):
+            want = rs.apply_rows(rows, synth.stripe_data(61 + groups, s, n, B))
+            assert (dout[s].cpu().numpy() == want).all(), (case, groups, hint, s)
+
+
 @pytest.mark.parametrize("kern", ["straight", "tma", "pipe"])
 def test_cfg5_rs20_reduced(kern):
     # RS(20,4) encode + one seeded 4-erasure decode; 16 stripes x 20 x 1 MiB (configs[4] shape)
