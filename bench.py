@@ -100,11 +100,13 @@ def parse():
     ap.add_argument("--compress", default="xorrepair", choices=["none", "repair", "xorrepair"])
     ap.add_argument("--kernel", default=None,
                     choices=["auto", "straight", "interp", "tma", "pipe", "grouped", "grouped_tma",
-                             "grouped_pipe"])
+                             "grouped_pipe", "multi"])
     ap.add_argument("--stages", type=int, default=None)
     ap.add_argument("--streams", type=int, default=8, help="internal streams for grouped decode")
     ap.add_argument("--lanes", type=int, default=1)
     ap.add_argument("--groups", type=int, default=None, help="PIPE consumer groups (goal split)")
+    ap.add_argument("--per-module", type=int, default=64,
+                    help="programs per fused multi-program kernel (--kernel multi)")
     ap.add_argument("--threads", type=int, default=None)
     ap.add_argument("--block-bytes", type=int, default=0, help="override block size")
     ap.add_argument("--p", type=int, default=0, help="override parity count (cfg4 sweep)")
@@ -279,6 +281,8 @@ def kernel_name(args, wl, stats):
         return "xslp_sl_tma"
     if k in ("pipe", "grouped_pipe"):
         return "xslp_sl_pipe"
+    if k == "multi":
+        return "xslp_sl_multi"
     return "xslp_sl_batch"
 
 
@@ -351,7 +355,13 @@ def main():
         uniq = sorted(set(pats))
         dec = [X.xslp_decode_bitmatrix(G, n, p, er) for er in uniq]
         mode = "grouped" if args.kernel == "auto" else args.kernel
-        if mode == "interp":
+        if mode == "multi":     # fused multi-program pipeline kernels (branch table per stripe)
+            progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,
+                                   threads=args.threads)
+            multi = X.Multi(progs, per_module=args.per_module, threads=args.threads,
+                            stages=args.stages, lane_words=args.lanes, block_bytes_hint=B)
+            log("multi", multi.info())
+        elif mode == "interp":
             progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,
                                    threads=args.threads)
         else:   # one JIT straight-line (or TMA) kernel per distinct erasure pattern
@@ -446,6 +456,8 @@ def main():
     def launch(st=stream):
         if wl["op"] == "decode_peer":
             pdec.launch(stream=st, nstreams=args.streams)
+        elif wl["op"] == "decode_multi" and mode == "multi":
+            X.xslp_multi_decode(multi, idx, gids, goff, ti, to, B, stream=st)
         elif wl["op"] == "decode_multi" and mode == "interp":
             X.xslp_decode_batch_multi(progs, idx, ti, to, S, B, stream=st)
         elif wl["op"] == "decode_multi":

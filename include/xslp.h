@@ -230,6 +230,33 @@ int xslp_decode_batch_grouped(const xslp_program *const *progs, int nprogs,
                               const uint8_t *const *d_in_tbl, uint8_t *const *d_out_tbl,
                               size_t block_bytes, int nstreams, void *stream);
 
+/* Heterogeneous decode in few launches: the programs (same n_const and n_goals; typically one
+ * per erasure pattern) are fused into persistent multi-program pipeline kernels.  A kernel's
+ * producer warp streams the union of its programs' constant strips through `opts->stages`
+ * shared-memory stages by TMA; each consumer warp reads its stripe's program index and jumps
+ * to that program's straight-line code (a branch table), so a kernel serves many erasure
+ * patterns.  Programs are packed per_module (<= 0: 64) to a module; modules compile in
+ * parallel host threads.  opts: threads (consumer threads, <= 992), stages (2..8),
+ * lane_words, block_bytes_hint (> 0: bake that block size in; launches must then use it).
+ * The programs must stay alive while the multi is used.  Free with xslp_multi_free. */
+typedef struct xslp_multi xslp_multi;
+int xslp_multi_create(const xslp_program *const *progs, int nprogs, int per_module,
+                      const xslp_opts *opts, xslp_multi **out);
+/* d_prog_of_stripe: DEVICE int32 [stripes] program index (into the create-time progs) of each
+ * stripe; d_stripe_ids / group_offsets: the stripes of program i are d_stripe_ids[
+ * group_offsets[i] .. group_offsets[i+1]) (DEVICE ids, HOST offsets, as in
+ * xslp_decode_batch_grouped, which must agree with d_prog_of_stripe).  One launch per module
+ * that has stripes, in order on `stream`.  block_bytes % 128 == 0.  Tables as in
+ * xslp_encode_batch. */
+int xslp_multi_decode(const xslp_multi *multi, const int32_t *d_prog_of_stripe,
+                      const int32_t *d_stripe_ids, const int32_t *group_offsets,
+                      const uint8_t *const *d_in_tbl, uint8_t *const *d_out_tbl,
+                      size_t block_bytes, void *stream);
+/* modules, max registers / spill bytes per thread over the modules, host compile time. */
+int xslp_multi_info(const xslp_multi *multi, int32_t *modules, int32_t *regs, int32_t *spill_bytes,
+                    double *compile_ms);
+void xslp_multi_free(xslp_multi *multi);
+
 /* End-to-end form with HOST buffers: h_in = [nstripes][n][block_bytes] and
  * h_out = [nstripes][m][block_bytes], contiguous (ideally pinned) host memory.
  * Stages chunks of stripes through device memory owned by the program's

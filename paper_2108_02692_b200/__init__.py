@@ -96,6 +96,12 @@ _sig = {
     "xslp_decode_batch_grouped": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, _P, ctypes.c_size_t,
                                                  ctypes.c_int, _P]),
     "xslp_encode_host": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_size_t, _P]),
+    "xslp_multi_create": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(xslp_opts),
+                                         ctypes.POINTER(_P)]),
+    "xslp_multi_decode": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "xslp_multi_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                       ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)]),
+    "xslp_multi_free": (None, [_P]),
     "xslp_fill_random": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_size_t,
                                         ctypes.c_uint64, ctypes.c_int64, _P]),
     "xslp_launch_count": (ctypes.c_int64, []),
@@ -338,6 +344,44 @@ def xslp_decode_batch_grouped(progs, d_stripe_ids, group_offsets, d_in_tbl, d_ou
     _check(_lib.xslp_decode_batch_grouped(arr, len(progs), _ptr(d_stripe_ids), off.ctypes.data,
                                           _ptr(d_in_tbl), _ptr(d_out_tbl), block_bytes, nstreams,
                                           _stream(stream)))
+
+
+class Multi:
+    """Programs fused into persistent multi-program pipeline kernels (xslp_multi_*)."""
+
+    def __init__(self, progs, per_module=64, opts=None, **kw):
+        self._progs = list(progs)          # keep the programs alive
+        o = opts if opts is not None else default_opts(**kw)
+        arr = (ctypes.c_void_p * len(self._progs))(*[p.handle for p in self._progs])
+        h = _P()
+        _check(_lib.xslp_multi_create(arr, len(self._progs), per_module, ctypes.byref(o),
+                                      ctypes.byref(h)))
+        self._h = h.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        m, r, s, t = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
+        _check(_lib.xslp_multi_info(self._h, ctypes.byref(m), ctypes.byref(r), ctypes.byref(s),
+                                    ctypes.byref(t)))
+        return {"modules": m.value, "regs": r.value, "spill_bytes": s.value, "compile_ms": t.value}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        lib = globals().get("_lib")
+        if h and lib is not None:
+            lib.xslp_multi_free(h)
+            self._h = None
+
+
+def xslp_multi_decode(multi, d_prog_of_stripe, d_stripe_ids, group_offsets, d_in_tbl, d_out_tbl,
+                      block_bytes, stream=None):
+    off = np.ascontiguousarray(group_offsets, dtype=np.int32)
+    _check(_lib.xslp_multi_decode(multi.handle, _ptr(d_prog_of_stripe), _ptr(d_stripe_ids),
+                                  off.ctypes.data, _ptr(d_in_tbl), _ptr(d_out_tbl), block_bytes,
+                                  _stream(stream)))
 
 
 def group_stripes(prog_of_stripe, nprogs):

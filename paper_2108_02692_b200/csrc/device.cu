@@ -17,6 +17,7 @@
 namespace xslp {
 
 static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches++; }
 
 #define CUDA_OK(x)                                                                      \
   do {                                                                                  \

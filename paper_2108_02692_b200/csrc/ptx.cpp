@@ -46,6 +46,7 @@ struct Emitter {
         n_in(s_.n_const / 8),
         n_out((int)(s_.goal.size() / 8)) {}
   const Slp &cur() const { return *sp; }
+  int decl_vars = -1, decl_nq = -1;  // register declaration sizes when several programs share a body
 
   std::string creg(int c, int l) { return "%c" + std::to_string(c * L + l); }
   std::string vreg(int v, int l) { return "%v" + std::to_string(v * L + l); }
@@ -467,18 +468,163 @@ struct Emitter {
     o << "  .reg .b64 %sk<8>;\n";
     o << "  .reg .b64 %ib<" << std::max(1, n_in) << ">;\n  .reg .b64 %ob<" << std::max(1, n_out) << ">;\n";
     o << "  .reg .b32 %c<" << std::max(1, cur().n_const * L) << ">;\n";
-    o << "  .reg .b32 %v<" << std::max(1, cur().n_vars * L) << ">;\n";
+    o << "  .reg .b32 %v<" << std::max(1, (decl_vars >= 0 ? decl_vars : cur().n_vars) * L) << ">;\n";
     o << "  .reg .b64 %ta<" << std::max(1, ntmp_guess) << ">;\n";
     o << "  .reg .b32 %sb, %sth, %nb;\n  .reg .b64 %toff;\n";
     o << "  .reg .b32 %tps, %nt, %nct, %wid, %it, %tile, %lane, %st, %ph, %fb, %eb, %tw, %dst;\n";
-    o << "  .reg .pred %pids, %pprod, %p5;\n  .reg .b32 %grp, %ltid;\n";
+    o << "  .reg .pred %pids, %pprod, %p5;\n  .reg .b32 %grp, %ltid, %pk, %pfirst, %t1, %chunk;\n";
+    o << "  .reg .b64 %rpm;\n";
     o << "  .reg .b32 %tx0;\n  .reg .b32 %y<8>;\n";
     int nq = 0;
     for (auto &in : cur().ins)
       for (int t : in.ops)
         if (t < cur().n_const) ++nq;
+    if (decl_nq >= 0) nq = decl_nq;
     o << "  .reg .b32 %q<" << std::max(1, nq * L) << ">;\n";
     o << "  mov.u32 %zero, 0;\n";
+  }
+
+  // Multi-program persistent pipeline (entry xslp_sl_multi): like body_pipe, but every stripe
+  // names its own program (p_pos[stripe] - p_first indexes `progs`) and the consumers jump to
+  // that program's code through a branch table (brx.idx).  The producer streams the union of
+  // the programs' constants.  Each CTA owns a contiguous run of tiles (stripes are grouped by
+  // program by the caller), so a CTA changes program rarely and its code stays in cache.
+  void body_multi(int S, const std::vector<const Slp *> &progs) {
+    const int nc = full.n_const;
+    const int TC = threads, NCW = threads / 32;
+    std::vector<char> used(nc, 0);
+    for (const Slp *q : progs) {
+      for (auto &in : q->ins)
+        for (int t : in.ops)
+          if (t < nc) used[t] = 1;
+      for (int g : q->goal)
+        if (g >= 0 && g < nc) used[g] = 1;
+    }
+    std::vector<char> blk_used(n_in, 0);
+    std::vector<int> slot(nc, -1);
+    int nused = 0;
+    for (int c = 0; c < nc; ++c)
+      if (used[c]) { blk_used[c / 8] = 1; slot[c] = nused++; }
+    const int rowb = 4 * L * TC;
+    const int64_t STAGE = (int64_t)nused * rowb;
+    const int EB = 8 * S;
+    o << "  mov.u32 %s2, %tid.x;\n  mov.u32 %sb, dsm;\n";
+    o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
+    for (int k = 0; k < S; ++k) {
+      o << "  mbarrier.init.shared::cta.b64 [%sb+" << 8 * k << "], 1;\n";
+      o << "  mbarrier.init.shared::cta.b64 [%sb+" << EB + 8 * k << "], " << NCW << ";\n";
+    }
+    o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
+    o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
+    o << "  ld.param.u64 %rd0, [p_ids];\n  setp.ne.u64 %pids, %rd0, 0;\n";
+    o << "  ld.param.u64 %rpm, [p_pos];\n  ld.param.u32 %pfirst, [p_first];\n";
+    // contiguous tile range of this CTA: [ctaid*chunk, min(nt, (ctaid+1)*chunk))
+    o << "  mov.u32 %nct, %nctaid.x;\n  add.u32 %chunk, %nt, %nct;\n  sub.u32 %chunk, %chunk, 1;\n";
+    o << "  div.u32 %chunk, %chunk, %nct;\n  mov.u32 %s0, %ctaid.x;\n";
+    o << "  mul.lo.u32 %s1, %s0, %chunk;\n  add.u32 %t1, %s1, %chunk;\n  min.u32 %t1, %t1, %nt;\n";
+    if (baked <= 0) {
+      o << "  ld.param.u64 %sk1, [p_strip];\n";
+      for (int k = 2; k < 8; ++k) o << "  mul.lo.u64 %sk" << k << ", %sk1, " << k << ";\n";
+    }
+    o << "  shr.u32 %wid, %s2, 5;\n  setp.eq.u32 %pprod, %wid, " << NCW << ";\n  @%pprod bra $PROD;\n";
+    auto stripe_of = [&](const char *lab) {
+      o << "  div.u32 %s5, %tile, %tps;\n  rem.u32 %tw, %tile, %tps;\n";
+      o << "  @!%pids bra " << lab << ";\n";
+      o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
+      o << lab << ":\n";
+    };
+    // ---------------- consumers
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %s1;\n  mov.u32 %lane, %laneid;\n";
+    o << "$CLOOP:\n  setp.ge.u32 %p0, %tile, %t1;\n  @%p0 bra $DONE;\n";
+    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n  and.b32 %ph, %ph, 1;\n";
+    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
+    o << "$CW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW;\n";
+    stripe_of("$CID");
+    o << "  mad.lo.u32 %s3, %tw, " << TC << ", %s2;\n";
+    o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $CSKIP;\n";
+    o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
+    o << "  mad.lo.u32 %sth, %s2, " << 4 * L << ", %sth;\n  add.u32 %sth, %sth, 128;\n";
+    o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+    o << "  mul.wide.u32 %off, %s3, " << 4 * L << ";\n";
+    for (int i = 0; i < n_out; ++i) {
+      o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+      o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
+    }
+    o << "  mul.wide.u32 %rd6, %s5, 4;\n  add.s64 %rd6, %rpm, %rd6;\n  ld.global.nc.u32 %pk, [%rd6];\n";
+    o << "  sub.u32 %pk, %pk, %pfirst;\n";
+    o << "  $TBL: .branchtargets ";
+    for (size_t k = 0; k < progs.size(); ++k) o << (k ? ", " : "") << "$K" << k;
+    o << ";\n  brx.idx %pk, $TBL;\n";
+    for (size_t k = 0; k < progs.size(); ++k) {
+      sp = progs[k];
+      o << "$K" << k << ":\n";
+      int tmp = 0;
+      compute(true, 0, slot, used, tmp);
+      o << "  bra.uni $CSKIP;\n";
+    }
+    sp = &full;
+    o << "$CSKIP:\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT;\n";
+    o << "  add.u32 %eb, %fb, " << EB << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
+    o << "$CNEXT:\n  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, 1;\n  bra.uni $CLOOP;\n";
+    // ---------------- producer
+    int tmp = 0;
+    o << "$PROD:\n  mov.u32 %lane, %laneid;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $DONE;\n";
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %s1;\n";
+    o << "$PLOOP:\n  setp.ge.u32 %p0, %tile, %t1;\n  @%p0 bra $DONE;\n";
+    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n";
+    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
+    o << "  setp.lt.u32 %p5, %it, " << S << ";\n  @%p5 bra $PNW;\n";
+    o << "  sub.u32 %ph, %ph, 1;\n  and.b32 %ph, %ph, 1;\n  add.u32 %eb, %fb, " << EB << ";\n";
+    o << "$PW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%eb], %ph;\n  @!%p3 bra $PW;\n";
+    o << "$PNW:\n";
+    stripe_of("$PID");
+    o << "  mul.lo.u32 %s7, %tw, " << TC << ";\n";
+    o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << TC << ";\n  mul.lo.u32 %nb, %nb, " << 4 * L << ";\n";
+    o << "  mul.lo.u32 %s6, %nb, " << nused << ";\n";
+    o << "  mbarrier.arrive.expect_tx.shared::cta.b64 _, [%fb], %s6;\n";
+    o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
+    o << "  mul.wide.u32 %toff, %s7, " << 4 * L << ";\n";
+    for (int j = 0; j < n_in; ++j) {
+      if (!blk_used[j]) continue;
+      o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+      o << "  add.s64 %ib" << j << ", %ib" << j << ", %toff;\n";
+    }
+    o << "  mul.lo.u32 %dst, %st, " << STAGE << ";\n  add.u32 %dst, %dst, %sb;\n";
+    for (int c = 0; c < nc; ++c) {
+      if (!used[c]) continue;
+      std::string a = addr("%ib" + std::to_string(c / 8), c % 8, tmp);
+      o << "  cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%dst+"
+        << 128 + (int64_t)slot[c] * rowb << "], " << a << ", %nb, [%fb];\n";
+    }
+    o << "  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, 1;\n  bra.uni $PLOOP;\n";
+    o << "$DONE:\n  ret;\n";
+  }
+
+  std::string run_multi(const std::vector<const Slp *> &progs) {
+    int mv = 0, mq = 0;
+    for (const Slp *q : progs) {
+      mv = std::max(mv, q->n_vars);
+      int nq = 0;
+      for (auto &in : q->ins)
+        for (int t : in.ops)
+          if (t < q->n_const) ++nq;
+      mq = std::max(mq, nq);
+    }
+    decl_vars = mv;
+    decl_nq = mq;
+    o << "//\n// xslp multi-program pipeline kernel: " << progs.size() << " programs, "
+      << full.n_const << " constants, " << full.goal.size() << " goals, lanes=" << L << "\n//\n";
+    o << ".version 8.8\n.target sm_100a\n.address_size 64\n\n";
+    o << ".extern .shared .align 128 .b8 dsm[];\n\n";
+    o << ".visible .entry xslp_sl_multi(\n  .param .u64 p_in,\n  .param .u64 p_out,\n"
+         "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
+         "  .param .u32 p_tps,\n  .param .u32 p_ntiles,\n  .param .u64 p_pos,\n"
+         "  .param .u32 p_first)\n.maxntid "
+      << threads + 32 << ", 1, 1\n{\n";
+    decls(full.n_const + (int)full.goal.size() + 8);
+    body_multi(stages, progs);
+    o << "}\n";
+    return o.str();
   }
 
   std::string run() {
@@ -538,6 +684,19 @@ std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, 
   return e.run();
 }
 
+std::string emit_ptx_multi(const std::vector<const Slp *> &progs, int lanes, int64_t baked_strip,
+                           int threads, int stages) {
+  if (progs.empty()) throw Error(XSLP_EINVAL, "no programs");
+  const Slp &f = *progs[0];
+  for (const Slp *q : progs)
+    if (q->n_const != f.n_const || q->goal.size() != f.goal.size())
+      throw Error(XSLP_EINVAL, "programs disagree on constants/goals");
+  if (f.n_const % 8 || f.goal.size() % 8 || f.n_const / 8 + f.goal.size() / 8 > 128)
+    throw Error(XSLP_EINVAL, "device programs need whole blocks (n + m <= 128)");
+  Emitter e(f, lanes, baked_strip, threads, 0, stages, XSLP_LAYOUT_STRIP, nullptr);
+  return e.run_multi(progs);
+}
+
 std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, int *regs_tma,
                                int *spill_tma, int *regs_pipe, int *spill_pipe) {
   nvPTXCompilerHandle h = nullptr;
@@ -581,6 +740,7 @@ std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, in
   entry_info("xslp_sl_batch", regs, spill);
   entry_info("xslp_sl_tma", regs_tma, spill_tma);
   entry_info("xslp_sl_pipe", regs_pipe, spill_pipe);
+  if (info.find("'xslp_sl_multi'") != std::string::npos) entry_info("xslp_sl_multi", regs_pipe, spill_pipe);
   return bin;
 }
 

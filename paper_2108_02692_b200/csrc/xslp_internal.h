@@ -122,6 +122,10 @@ std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, 
 // Split the goals into k contiguous sets balanced by issue cost; each result keeps the
 // instructions its goals reach (original order and variable ids) and marks the other goals -2.
 std::vector<Slp> split_goals(const Slp &s, int k);
+// One persistent pipeline kernel (entry xslp_sl_multi) over several programs with the same
+// constants/goals, dispatching per stripe through a branch table.
+std::string emit_ptx_multi(const std::vector<const Slp *> &progs, int lanes, int64_t baked_strip,
+                           int threads, int stages);
 std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, int *regs_tma,
                                int *spill_tma, int *regs_pipe, int *spill_pipe);
 

@@ -170,6 +170,40 @@ def test_heterogeneous_decode(kern):
 
 # ---- edge cases ------------------------------------------------------------------------
 
+@pytest.mark.parametrize("per_module,hint,threads", [(3, 0, 128), (64, 1, 256), (1, 1, 64)])
+def test_multi_program_decode(per_module, hint, threads):
+    # heterogeneous decode through fused multi-program pipeline kernels (branch table per
+    # stripe), several modules, ragged last tile; every byte against the oracle
+    n, p, B, S = 10, 4, 8192 + 1152, 23
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    pats = [tuple(synth.erasure_pattern(71, s, n + p, 4)) for s in range(S)]
+    uniq = sorted(set(pats))
+    progs = X.compile_many([X.xslp_decode_bitmatrix(g, n, p, er)[0] for er in uniq], specialise=0)
+    multi = X.Multi(progs, per_module=per_module, threads=threads, stages=2,
+                    block_bytes_hint=B if hint else 0)
+    info = multi.info()
+    assert info["modules"] == -(-len(uniq) // per_module) and info["spill_bytes"] == 0
+    pos = [uniq.index(er) for er in pats]
+    ids, off = X.group_stripes(pos, len(progs))
+    din = dev_buf(S, n, B)                        # survivors: arbitrary bytes
+    X.xslp_fill_random(din, S, n, B, seed=72)
+    out = torch.full((S, 4, B), 0x5A, dtype=torch.uint8, device="cuda")
+    X.xslp_multi_decode(multi, torch.tensor(pos, dtype=torch.int32, device="cuda"),
+                        torch.from_numpy(ids).cuda(), off, X.block_table(din, S, n, B),
+                        X.block_table(out, S, 4, B), B)
+    torch.cuda.synchronize()
+    for s in range(S):
+        rows = mx.decode_rows(og, n, list(pats[s]))[1]
+        want = rs.decode(rows, synth.stripe_data(72, s, n, B))
+        assert (out[s].cpu().numpy() == want).all(), s
+    if hint:
+        with pytest.raises(X.XslpError):          # kernels were built for B
+            X.xslp_multi_decode(multi, torch.tensor(pos, dtype=torch.int32, device="cuda"),
+                                torch.from_numpy(ids).cuda(), off, X.block_table(din, S, n, B),
+                                X.block_table(out, S, 4, B), B - 128)
+
+
 def test_edge_cases():
     n, p = 4, 2
     _, prog = compile_enc(n, p, "cauchy")
