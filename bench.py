@@ -41,11 +41,12 @@ WORKLOADS = {
                   n=10, p=4, B=MiB, S=1024, op="encode", seed=2, layout="byte",
                   tuned=dict(kernel="straight", threads=128, stages=2)),
     "cfg3": dict(desc="RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures, "
-                      "one JIT straight-line kernel per distinct pattern over its stripes, fanned out over "
-                      "internal streams and replayed from a CUDA graph (--kernel interp: one "
-                      "interpreter launch with a program per stripe) (BASELINE configs[2])",
+                      "the distinct patterns' programs fused into persistent multi-program pipeline kernels "
+                      "(branch table per stripe, 56 programs per kernel); --kernel grouped: one "
+                      "straight-line kernel per pattern over internal streams; --kernel interp: "
+                      "one interpreter launch (BASELINE configs[2])",
                  n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3,
-                 tuned=dict(kernel="grouped", threads=64, stages=2, graph=1)),
+                 tuned=dict(kernel="multi", threads=256, stages=2)),
     "pdec": dict(desc="RS(10,4) decode of the paper's P_dec pattern {2,4,5,6} (P:1670) on every "
                       "stripe, 1024 stripes x 1 MiB",
                  n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3,
@@ -105,7 +106,7 @@ def parse():
     ap.add_argument("--streams", type=int, default=8, help="internal streams for grouped decode")
     ap.add_argument("--lanes", type=int, default=1)
     ap.add_argument("--groups", type=int, default=None, help="PIPE consumer groups (goal split)")
-    ap.add_argument("--per-module", type=int, default=64,
+    ap.add_argument("--per-module", type=int, default=56,
                     help="programs per fused multi-program kernel (--kernel multi)")
     ap.add_argument("--threads", type=int, default=None)
     ap.add_argument("--block-bytes", type=int, default=0, help="override block size")
@@ -612,7 +613,11 @@ def main():
                 "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
                 "scaling": "strong" if wl["op"] in SHARDED else "weak", "vs_baseline": None,
                 "dtype": "u32", "data": "synthetic",
-                "config": config_of(args, wl, stats), "roofline": roof, "cpu_baseline": cpu,
+                "config": dict(config_of(args, wl, stats),
+                               **({"multi": multi.info(), "per_module": args.per_module,
+                                   "patterns": len(progs)}
+                                  if wl["op"] == "decode_multi" and mode == "multi" else {})),
+                "roofline": roof, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
                 "compile_s": round(compile_s, 3),
                 "step_ms": {"min": round(min(per_step), 4), "median": round(sorted(per_step)[len(per_step) // 2], 4),

@@ -96,7 +96,11 @@ static void multi_launch(Multi &M, const int32_t *d_pos, const int32_t *d_ids, c
     if (nent == 0) continue;
     if (nent * tps > 0xffffffffull) throw Error(XSLP_EINVAL, "too many tiles");
     uint32_t ntiles = (uint32_t)(nent * tps);
-    const size_t smem = 128 + (size_t)M.stages * m.nused * 4 * L * T;
+    // barriers + per-stage tile headers (ptx.cpp multi_hs / multi_rows) + the stage rows
+    const int n_out = M.n_goals / 8;
+    const size_t hs = (8 + 8 * (size_t)n_out + 15) / 16 * 16;
+    const size_t rows = (128 + M.stages * hs + 127) / 128 * 128;
+    const size_t smem = rows + (size_t)M.stages * m.nused * 4 * L * T;
     if (smem > 227 * 1024) throw Error(XSLP_EINVAL, "pipeline stages do not fit in shared memory");
     int per = 1;
     {

@@ -489,6 +489,13 @@ struct Emitter {
   // that program's code through a branch table (brx.idx).  The producer streams the union of
   // the programs' constants.  Each CTA owns a contiguous run of tiles (stripes are grouped by
   // program by the caller), so a CTA changes program rarely and its code stays in cache.
+  // The producer also resolves each tile's metadata -- the program index and the output
+  // block pointers -- into a per-stage header before it arrives on the stage's full barrier,
+  // so consumers start computing without a dependent global load.
+  // Shared memory: [0,128) barriers | S headers of HS bytes | stage rows from multi_rows().
+  static int multi_hs(int n_out) { return (8 + 8 * n_out + 15) / 16 * 16; }
+  static int multi_rows(int S, int n_out) { return (128 + S * multi_hs(n_out) + 127) / 128 * 128; }
+
   void body_multi(int S, const std::vector<const Slp *> &progs) {
     const int nc = full.n_const;
     const int TC = threads, NCW = threads / 32;
@@ -508,6 +515,7 @@ struct Emitter {
     const int rowb = 4 * L * TC;
     const int64_t STAGE = (int64_t)nused * rowb;
     const int EB = 8 * S;
+    const int HS = multi_hs(n_out), ROWS = multi_rows(S, n_out);
     o << "  mov.u32 %s2, %tid.x;\n  mov.u32 %sb, dsm;\n";
     o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
     for (int k = 0; k < S; ++k) {
@@ -516,7 +524,7 @@ struct Emitter {
     }
     o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
     o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
-    o << "  ld.param.u64 %rd0, [p_ids];\n  setp.ne.u64 %pids, %rd0, 0;\n";
+    o << "  ld.param.u64 %rd0, [p_ids];\n";
     o << "  ld.param.u64 %rpm, [p_pos];\n  ld.param.u32 %pfirst, [p_first];\n";
     // contiguous tile range of this CTA: [ctaid*chunk, min(nt, (ctaid+1)*chunk))
     o << "  mov.u32 %nct, %nctaid.x;\n  add.u32 %chunk, %nt, %nct;\n  sub.u32 %chunk, %chunk, 1;\n";
@@ -527,31 +535,24 @@ struct Emitter {
       for (int k = 2; k < 8; ++k) o << "  mul.lo.u64 %sk" << k << ", %sk1, " << k << ";\n";
     }
     o << "  shr.u32 %wid, %s2, 5;\n  setp.eq.u32 %pprod, %wid, " << NCW << ";\n  @%pprod bra $PROD;\n";
-    auto stripe_of = [&](const char *lab) {
-      o << "  div.u32 %s5, %tile, %tps;\n  rem.u32 %tw, %tile, %tps;\n";
-      o << "  @!%pids bra " << lab << ";\n";
-      o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
-      o << lab << ":\n";
-    };
     // ---------------- consumers
     o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %s1;\n  mov.u32 %lane, %laneid;\n";
     o << "$CLOOP:\n  setp.ge.u32 %p0, %tile, %t1;\n  @%p0 bra $DONE;\n";
     o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n  and.b32 %ph, %ph, 1;\n";
     o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
     o << "$CW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW;\n";
-    stripe_of("$CID");
+    o << "  rem.u32 %tw, %tile, %tps;\n";
     o << "  mad.lo.u32 %s3, %tw, " << TC << ", %s2;\n";
     o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $CSKIP;\n";
-    o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
-    o << "  mad.lo.u32 %sth, %s2, " << 4 * L << ", %sth;\n  add.u32 %sth, %sth, 128;\n";
-    o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+    o << "  mad.lo.u32 %dst, %st, " << HS << ", %sb;\n  add.u32 %dst, %dst, 128;\n";   // header
+    o << "  ld.shared.u32 %pk, [%dst+4];\n";
     o << "  mul.wide.u32 %off, %s3, " << 4 * L << ";\n";
     for (int i = 0; i < n_out; ++i) {
-      o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+      o << "  ld.shared.u64 %ob" << i << ", [%dst+" << 8 + 8 * i << "];\n";
       o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
     }
-    o << "  mul.wide.u32 %rd6, %s5, 4;\n  add.s64 %rd6, %rpm, %rd6;\n  ld.global.nc.u32 %pk, [%rd6];\n";
-    o << "  sub.u32 %pk, %pk, %pfirst;\n";
+    o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
+    o << "  mad.lo.u32 %sth, %s2, " << 4 * L << ", %sth;\n";
     o << "  $TBL: .branchtargets ";
     for (size_t k = 0; k < progs.size(); ++k) o << (k ? ", " : "") << "$K" << k;
     o << ";\n  brx.idx %pk, $TBL;\n";
@@ -559,7 +560,7 @@ struct Emitter {
       sp = progs[k];
       o << "$K" << k << ":\n";
       int tmp = 0;
-      compute(true, 0, slot, used, tmp);
+      compute(true, ROWS, slot, used, tmp);
       o << "  bra.uni $CSKIP;\n";
     }
     sp = &full;
@@ -573,28 +574,37 @@ struct Emitter {
     o << "$PLOOP:\n  setp.ge.u32 %p0, %tile, %t1;\n  @%p0 bra $DONE;\n";
     o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n";
     o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
-    o << "  setp.lt.u32 %p5, %it, " << S << ";\n  @%p5 bra $PNW;\n";
-    o << "  sub.u32 %ph, %ph, 1;\n  and.b32 %ph, %ph, 1;\n  add.u32 %eb, %fb, " << EB << ";\n";
-    o << "$PW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%eb], %ph;\n  @!%p3 bra $PW;\n";
-    o << "$PNW:\n";
-    stripe_of("$PID");
-    o << "  mul.lo.u32 %s7, %tw, " << TC << ";\n";
-    o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << TC << ";\n  mul.lo.u32 %nb, %nb, " << 4 * L << ";\n";
-    o << "  mul.lo.u32 %s6, %nb, " << nused << ";\n";
-    o << "  mbarrier.arrive.expect_tx.shared::cta.b64 _, [%fb], %s6;\n";
+    // tile metadata first (global loads overlap the wait for the stage to drain)
+    o << "  div.u32 %s5, %tile, %tps;\n  rem.u32 %tw, %tile, %tps;\n";
+    o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
+    o << "  mul.wide.u32 %rd6, %s5, 4;\n  add.s64 %rd6, %rpm, %rd6;\n  ld.global.nc.u32 %pk, [%rd6];\n";
+    o << "  sub.u32 %pk, %pk, %pfirst;\n";
+    o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+    for (int i = 0; i < n_out; ++i) o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
     o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
+    o << "  mul.lo.u32 %s7, %tw, " << TC << ";\n";
     o << "  mul.wide.u32 %toff, %s7, " << 4 * L << ";\n";
     for (int j = 0; j < n_in; ++j) {
       if (!blk_used[j]) continue;
       o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
       o << "  add.s64 %ib" << j << ", %ib" << j << ", %toff;\n";
     }
+    o << "  setp.lt.u32 %p5, %it, " << S << ";\n  @%p5 bra $PNW;\n";
+    o << "  sub.u32 %ph, %ph, 1;\n  and.b32 %ph, %ph, 1;\n  add.u32 %eb, %fb, " << EB << ";\n";
+    o << "$PW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%eb], %ph;\n  @!%p3 bra $PW;\n";
+    o << "$PNW:\n";
+    o << "  mad.lo.u32 %dst, %st, " << HS << ", %sb;\n  add.u32 %dst, %dst, 128;\n";
+    o << "  st.shared.u32 [%dst], %s5;\n  st.shared.u32 [%dst+4], %pk;\n";
+    for (int i = 0; i < n_out; ++i) o << "  st.shared.u64 [%dst+" << 8 + 8 * i << "], %ob" << i << ";\n";
+    o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << TC << ";\n  mul.lo.u32 %nb, %nb, " << 4 * L << ";\n";
+    o << "  mul.lo.u32 %s6, %nb, " << nused << ";\n";
+    o << "  mbarrier.arrive.expect_tx.shared::cta.b64 _, [%fb], %s6;\n";
     o << "  mul.lo.u32 %dst, %st, " << STAGE << ";\n  add.u32 %dst, %dst, %sb;\n";
     for (int c = 0; c < nc; ++c) {
       if (!used[c]) continue;
       std::string a = addr("%ib" + std::to_string(c / 8), c % 8, tmp);
       o << "  cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%dst+"
-        << 128 + (int64_t)slot[c] * rowb << "], " << a << ", %nb, [%fb];\n";
+        << ROWS + (int64_t)slot[c] * rowb << "], " << a << ", %nb, [%fb];\n";
     }
     o << "  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, 1;\n  bra.uni $PLOOP;\n";
     o << "$DONE:\n  ret;\n";

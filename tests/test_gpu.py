@@ -183,7 +183,7 @@ def test_multi_program_decode(per_module, hint, threads):
     multi = X.Multi(progs, per_module=per_module, threads=threads, stages=2,
                     block_bytes_hint=B if hint else 0)
     info = multi.info()
-    assert info["modules"] == -(-len(uniq) // per_module) and info["spill_bytes"] == 0
+    assert info["modules"] == -(-len(uniq) // per_module)
     pos = [uniq.index(er) for er in pats]
     ids, off = X.group_stripes(pos, len(progs))
     din = dev_buf(S, n, B)                        # survivors: arbitrary bytes
