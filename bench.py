@@ -40,6 +40,11 @@ WORKLOADS = {
                        "RS, SURVEY NEXT #3), 1024 stripes x 10 x 1 MiB",
                   n=10, p=4, B=MiB, S=1024, op="encode", seed=2, layout="byte",
                   tuned=dict(kernel="straight", threads=128, stages=2)),
+    "cfg2t": dict(desc="RS(10,4) encode in the byte layout with the paper's approach (1) on the GPU: "
+                       "byte-wise GF(2^8) MM with nibble-table multiplication (PRMT), the comparison "
+                       "point for cfg2b's XOR program, 1024 stripes x 10 x 1 MiB",
+                  n=10, p=4, B=MiB, S=1024, op="encode_gft", seed=2,
+                  tuned=dict(kernel="gftable", threads=256, stages=2)),
     "cfg3": dict(desc="RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures, "
                       "the distinct patterns' programs fused into persistent multi-program pipeline kernels "
                       "(branch table per stripe, 56 programs per kernel); --kernel grouped: one "
@@ -101,7 +106,7 @@ def parse():
     ap.add_argument("--compress", default="xorrepair", choices=["none", "repair", "xorrepair"])
     ap.add_argument("--kernel", default=None,
                     choices=["auto", "straight", "interp", "tma", "pipe", "grouped", "grouped_tma",
-                             "grouped_pipe", "multi"])
+                             "grouped_pipe", "multi", "gftable"])
     ap.add_argument("--stages", type=int, default=None)
     ap.add_argument("--streams", type=int, default=8, help="internal streams for grouped decode")
     ap.add_argument("--lanes", type=int, default=1)
@@ -203,6 +208,8 @@ def oracle_stripe(wl, g, s, rows_cache, synth, mx, rs):
     cost does not depend on their values)."""
     n, p, B = wl["n"], wl["p"], wl["B"]
     data = synth.stripe_data(wl["seed"], s, n, B)
+    if wl["op"] == "encode_gft" or wl.get("layout") == "byte":   # byte-wise RS (P:495-525)
+        return rs.bytewise_apply(g[n:], data)
     if wl["op"] not in DECODE:
         return rs.encode(g, n, data)
     if "erased" not in wl and "e" in wl:
@@ -284,6 +291,8 @@ def kernel_name(args, wl, stats):
         return "xslp_sl_pipe"
     if k == "multi":
         return "xslp_sl_multi"
+    if k == "gftable":
+        return "xslp_gftable_kernel"
     return "xslp_sl_batch"
 
 
@@ -298,6 +307,8 @@ def config_of(args, wl, stats):
          "parallelism": (f"blocks spread over {args.gpus} GPU(s); survivors read in place over "
                          "NVLink P2P by the decode kernel (no collective)")
          if wl["op"] == "decode_peer" else f"stripe-sharded x{args.gpus}, no collective"}
+    if wl["op"] == "encode_gft":
+        c["program"] = "none: GF(2^8) MM with nibble tables (approach (1), P:538-545)"
     if stats:
         c["slp"] = {k: stats[k] for k in ("xor_count", "mem_count", "n_instr", "nvar", "maxlive",
                                           "regs", "spill_bytes", "regs_tma", "spill_bytes_tma",
@@ -396,6 +407,10 @@ def main():
                               lane_words=args.lanes, threads=args.threads, block_bytes_hint=B,
                               stages=args.stages, groups=args.groups)
         m_out = len(erased)
+    elif wl["op"] == "encode_gft":    # approach (1): no SLP, the coefficient rows themselves
+        prog = None
+        coef_rows = np.ascontiguousarray(G[n:])
+        m_out = p
     else:
         prog = X.xslp_compile(X.xslp_encode_bitmatrix(G, n, p), compress=args.compress,
                               kernel=args.kernel, lane_words=args.lanes, threads=args.threads,
@@ -404,8 +419,8 @@ def main():
                               groups=args.groups)
         m_out = p
     compile_s = time.perf_counter() - t0
-    log(f'compiled in {compile_s:.2f} s', prog.stats())
-    stats = prog.stats()
+    stats = prog.stats() if prog is not None else None
+    log(f'compiled in {compile_s:.2f} s', stats)
 
     # ---- device buffers and seeded inputs (untimed) ----
     from paper_2108_02692_b200.shard import max_over_ranks, stripe_range
@@ -457,6 +472,8 @@ def main():
     def launch(st=stream):
         if wl["op"] == "decode_peer":
             pdec.launch(stream=st, nstreams=args.streams)
+        elif wl["op"] == "encode_gft":
+            X.xslp_gf_table_apply(coef_rows, ti, to, S, B, stream=st)
         elif wl["op"] == "decode_multi" and mode == "multi":
             X.xslp_multi_decode(multi, idx, gids, goff, ti, to, B, stream=st)
         elif wl["op"] == "decode_multi" and mode == "interp":
@@ -502,7 +519,8 @@ def main():
         # one step's launches (all per-pattern kernels, their fork/join over the internal
         # streams) captured once and replayed: removes the host launch cost, not device work
         for pr in (progs if wl["op"] in ("decode_multi", "decode_peer") else [prog]):
-            X.xslp_prepare(pr, B)
+            if pr is not None:
+                X.xslp_prepare(pr, B)
         cap = torch.cuda.Stream()
         cap.wait_stream(stream)
         graph = torch.cuda.CUDAGraph()
@@ -568,7 +586,7 @@ def main():
 
     # ---- e2e through the host-buffer C-ABI call ----
     e2e = None
-    if not args.no_e2e and wl["op"] not in ("decode_multi", "decode_peer"):
+    if not args.no_e2e and wl["op"] not in ("decode_multi", "decode_peer", "encode_gft"):
         try:
             # pinned host buffers: the full workload at N=1; at most 16 GiB over all ranks
             Se = min(S, max(1, (16 << 30) // max(1, world) // ((n + p) * B)))

@@ -257,6 +257,15 @@ int xslp_multi_info(const xslp_multi *multi, int32_t *modules, int32_t *regs, in
                     double *compile_ms);
 void xslp_multi_free(xslp_multi *multi);
 
+/* Comparison path, the paper's approach (1): byte-layout RS as MM over GF(2^8)
+ * with nibble-table field multiplication (ISA-L's method; PRMT in place of PSHUFB).
+ * coef: HOST [m][n] GF(2^8) coefficients (1 <= n <= 64, 1 <= m <= 8); output block i of
+ * each stripe = sum_j coef[i][j] * input block j, byte by byte -- the same bytes
+ * as an XSLP_LAYOUT_BYTE program of those rows.  Tables as in xslp_encode_batch; block
+ * pointers 16-byte aligned, block_bytes % 16 == 0. */
+int xslp_gf_table_apply(const uint8_t *coef, int n, int m, const uint8_t *const *d_in_tbl,
+                        uint8_t *const *d_out_tbl, int nstripes, size_t block_bytes, void *stream);
+
 /* End-to-end form with HOST buffers: h_in = [nstripes][n][block_bytes] and
  * h_out = [nstripes][m][block_bytes], contiguous (ideally pinned) host memory.
  * Stages chunks of stripes through device memory owned by the program's

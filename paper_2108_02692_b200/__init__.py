@@ -102,6 +102,8 @@ _sig = {
     "xslp_multi_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                        ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)]),
     "xslp_multi_free": (None, [_P]),
+    "xslp_gf_table_apply": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, _P, ctypes.c_int,
+                                           ctypes.c_size_t, _P]),
     "xslp_fill_random": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_size_t,
                                         ctypes.c_uint64, ctypes.c_int64, _P]),
     "xslp_launch_count": (ctypes.c_int64, []),
@@ -382,6 +384,14 @@ def xslp_multi_decode(multi, d_prog_of_stripe, d_stripe_ids, group_offsets, d_in
     _check(_lib.xslp_multi_decode(multi.handle, _ptr(d_prog_of_stripe), _ptr(d_stripe_ids),
                                   off.ctypes.data, _ptr(d_in_tbl), _ptr(d_out_tbl), block_bytes,
                                   _stream(stream)))
+
+
+def xslp_gf_table_apply(coef, d_in_tbl, d_out_tbl, nstripes, block_bytes, stream=None):
+    """Byte-wise GF(2^8) matrix apply with nibble tables (the paper's approach (1))."""
+    c = np.ascontiguousarray(coef, dtype=np.uint8)
+    m, n = c.shape
+    _check(_lib.xslp_gf_table_apply(c.ctypes.data, n, m, _ptr(d_in_tbl), _ptr(d_out_tbl), nstripes,
+                                    block_bytes, _stream(stream)))
 
 
 def group_stripes(prog_of_stripe, nprogs):

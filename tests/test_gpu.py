@@ -493,6 +493,39 @@ def test_byte_layout_encode_decode(n, p, kind, B, S):
         assert (out.cpu().numpy() == blocks[0][er]).all(), er
 
 
+@pytest.mark.parametrize("n,p,kind,B,S", [(10, 4, "isal", 4096 + 48, 3), (4, 2, "cauchy", 4096, 2),
+                                          (20, 4, "isal", 1024, 2), (6, 8, "sysvand", 160, 2)])
+def test_gf_table_kernel(n, p, kind, B, S):
+    # approach (1): byte-wise GF(2^8) MM with nibble tables, against the oracle's byte RS and
+    # against the XOR-SLP byte-layout program of the same rows
+    og = mx.coding_matrix(n, p, kind)
+    g = X.xslp_coding_matrix(n, p, kind)
+    din = dev_buf(S, n, B)
+    X.xslp_fill_random(din, S, n, B, seed=81)
+    out = torch.full((S, p, B), 0x33, dtype=torch.uint8, device="cuda")
+    X.xslp_gf_table_apply(g[n:], X.block_table(din, S, n, B), X.block_table(out, S, p, B), S, B)
+    torch.cuda.synchronize()
+    for s in range(S):
+        want = rs.bytewise_apply(og[n:], synth.stripe_data(81, s, n, B))
+        assert (out[s].cpu().numpy() == want).all(), s
+    if B % 32 == 0:
+        _, prog = compile_enc(n, p, kind, layout="byte")
+        out2 = dev_buf(S, p, B)
+        run_batch(prog, din, out2, B)
+        assert torch.equal(out, out2)
+    # decode rows (a data + a parity erasure) through the same kernel
+    er = [1, n]
+    surv, rows = mx.decode_rows(og, n, er)
+    blocks = np.stack([np.concatenate([d, rs.bytewise_apply(og[n:], d)])
+                       for d in (synth.stripe_data(81, s, n, B) for s in range(S))])
+    dsv = torch.from_numpy(np.ascontiguousarray(blocks[:, surv])).cuda()
+    rec = dev_buf(S, len(er), B)
+    X.xslp_gf_table_apply(np.array(rows, dtype=np.uint8), X.block_table(dsv, S, n, B),
+                          X.block_table(rec, S, len(er), B), S, B)
+    torch.cuda.synchronize()
+    assert (rec.cpu().numpy() == blocks[:, er]).all()
+
+
 def test_byte_layout_full_size_sampled():
     n, p, B, S = 10, 4, 1 << 20, 1024
     og = mx.coding_matrix(n, p)
