@@ -4,7 +4,7 @@
 #include <chrono>
 #include <set>
 
-#include "xslp_internal.h"
+#include "xslp_api.h"
 
 namespace xslp {
 static thread_local std::string g_err;
@@ -13,22 +13,6 @@ void set_last_error(const std::string &m) { g_err = m; }
 
 using namespace xslp;
 
-#define API_BEGIN try {
-#define API_END                                        \
-  }                                                    \
-  catch (const Error &e) {                             \
-    set_last_error(e.what());                          \
-    return e.code;                                     \
-  }                                                    \
-  catch (const std::bad_alloc &) {                     \
-    set_last_error("out of host memory");              \
-    return XSLP_ENOMEM;                                \
-  }                                                    \
-  catch (const std::exception &e) {                    \
-    set_last_error(e.what());                          \
-    return XSLP_EINVAL;                                \
-  }                                                    \
-  return XSLP_OK;
 
 extern "C" void xslp_default_opts(xslp_opts *o) {
   if (!o) return;
@@ -241,19 +225,15 @@ void check_opts(xslp_opts &o) {
 }  // namespace
 
 namespace xslp {
-// bitmatrix -> compiled program (shared by xslp_compile and the codec's memo cache)
-std::shared_ptr<Program> compile_bits(const std::vector<uint8_t> &bitv, int out_rows, int in_cols,
-                                      const xslp_opts &o) {
-  const uint8_t *bits = bitv.data();
+// bitmatrix -> compiled program, in place (xslp_compile and the codec's memo cache)
+static void build_from_bits(Program &P, const uint8_t *bits, int out_rows, int in_cols, const xslp_opts &o) {
   if (out_rows < 0 || in_cols <= 0 || in_cols > 512 || out_rows > 4096)
     throw Error(XSLP_EINVAL, "bitmatrix shape out of range");
-  if (bitv.size() < (size_t)out_rows * in_cols) throw Error(XSLP_EINVAL, "bitmatrix too short");
   auto t0 = std::chrono::steady_clock::now();
-  auto P = std::make_shared<Program>();
-  P->opts = o;
-  check_opts(P->opts);
-  P->n_const = in_cols;
-  P->n_goals = out_rows;
+  P.opts = o;
+  check_opts(P.opts);
+  P.n_const = in_cols;
+  P.n_goals = out_rows;
   std::vector<Bits> goals(out_rows, Bits(in_cols));
   for (int r = 0; r < out_rows; ++r)
     for (int c = 0; c < in_cols; ++c) {
@@ -261,12 +241,20 @@ std::shared_ptr<Program> compile_bits(const std::vector<uint8_t> &bitv, int out_
       if (b > 1) throw Error(XSLP_EINVAL, "bitmatrix entries must be 0 or 1");
       if (b) goals[r].set(c);
     }
-  if (P->opts.compress == XSLP_COMPRESS_NONE)
-    P->slp = lift(goals, in_cols, P->opts.fuse != 0);
+  if (P.opts.compress == XSLP_COMPRESS_NONE)
+    P.slp = lift(goals, in_cols, P.opts.fuse != 0);
   else
-    P->slp = compress(goals, in_cols, P->opts.compress == XSLP_COMPRESS_XORREPAIR);
-  P->stats.compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  finish(*P, &goals, true);
+    P.slp = compress(goals, in_cols, P.opts.compress == XSLP_COMPRESS_XORREPAIR);
+  P.stats.compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  finish(P, &goals, true);
+}
+
+std::shared_ptr<Program> compile_bits(const std::vector<uint8_t> &bitv, int out_rows, int in_cols,
+                                      const xslp_opts &o) {
+  if (out_rows < 0 || in_cols <= 0 || bitv.size() < (size_t)out_rows * in_cols)
+    throw Error(XSLP_EINVAL, "bitmatrix too short");
+  auto P = std::make_shared<Program>();
+  build_from_bits(*P, bitv.data(), out_rows, in_cols, o);
   return P;
 }
 }  // namespace xslp
@@ -277,27 +265,10 @@ extern "C" int xslp_compile(const uint8_t *bits, int out_rows, int in_cols, cons
   if (!out) throw Error(XSLP_EINVAL, "null out");
   *out = nullptr;
   if (!bits && out_rows * in_cols > 0) throw Error(XSLP_EINVAL, "null bitmatrix");
-  if (out_rows < 0 || in_cols <= 0 || in_cols > 512 || out_rows > 4096)
-    throw Error(XSLP_EINVAL, "bitmatrix shape out of range");
-  auto t0 = std::chrono::steady_clock::now();
+  xslp_opts o;
+  if (opts) o = *opts; else xslp_default_opts(&o);
   auto P = std::make_unique<Program>();
-  if (opts) P->opts = *opts; else xslp_default_opts(&P->opts);
-  check_opts(P->opts);
-  P->n_const = in_cols;
-  P->n_goals = out_rows;
-  std::vector<Bits> goals(out_rows, Bits(in_cols));
-  for (int r = 0; r < out_rows; ++r)
-    for (int c = 0; c < in_cols; ++c) {
-      uint8_t b = bits[(size_t)r * in_cols + c];
-      if (b > 1) throw Error(XSLP_EINVAL, "bitmatrix entries must be 0 or 1");
-      if (b) goals[r].set(c);
-    }
-  if (P->opts.compress == XSLP_COMPRESS_NONE)
-    P->slp = lift(goals, in_cols, P->opts.fuse != 0);
-  else
-    P->slp = compress(goals, in_cols, P->opts.compress == XSLP_COMPRESS_XORREPAIR);
-  P->stats.compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  finish(*P, &goals, true);
+  build_from_bits(*P, bits, out_rows, in_cols, o);
   *out = reinterpret_cast<xslp_program *>(P.release());
   API_END
 }

@@ -12,7 +12,7 @@
 #include <list>
 #include <set>
 
-#include "xslp_internal.h"
+#include "xslp_api.h"
 
 namespace xslp {
 
@@ -80,22 +80,6 @@ static std::shared_ptr<Program> decode_program(Codec &c, std::vector<int> er) {
 
 using namespace xslp;
 
-#define API_BEGIN try {
-#define API_END                                        \
-  }                                                    \
-  catch (const Error &e) {                             \
-    set_last_error(e.what());                          \
-    return e.code;                                     \
-  }                                                    \
-  catch (const std::bad_alloc &) {                     \
-    set_last_error("out of host memory");              \
-    return XSLP_ENOMEM;                                \
-  }                                                    \
-  catch (const std::exception &e) {                    \
-    set_last_error(e.what());                          \
-    return XSLP_EINVAL;                                \
-  }                                                    \
-  return XSLP_OK;
 
 static Codec *C(const xslp_codec *c) {
   if (!c) throw Error(XSLP_EINVAL, "null codec");

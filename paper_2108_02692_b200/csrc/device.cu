@@ -12,19 +12,13 @@
 #include <atomic>
 #include <cstdio>
 
-#include "xslp_internal.h"
+#include "xslp_api.h"
 
 namespace xslp {
 
 static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches++; }
 
-#define CUDA_OK(x)                                                                      \
-  do {                                                                                  \
-    cudaError_t e_ = (x);                                                               \
-    if (e_ != cudaSuccess)                                                              \
-      throw Error(XSLP_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));         \
-  } while (0)
 
 // ---------------------------------------------------------------------------------
 // Interpreter kernel (A29: "run optimized SLPs line-by-line ... in the interpreter
@@ -645,22 +639,6 @@ static void host_apply(const Program *p, const uint8_t *h_in, uint8_t *h_out, in
 // C ABI (device entry points)
 using namespace xslp;
 
-#define API_BEGIN try {
-#define API_END                                        \
-  }                                                    \
-  catch (const Error &e) {                             \
-    set_last_error(e.what());                          \
-    return e.code;                                     \
-  }                                                    \
-  catch (const std::bad_alloc &) {                     \
-    set_last_error("out of host memory");              \
-    return XSLP_ENOMEM;                                \
-  }                                                    \
-  catch (const std::exception &e) {                    \
-    set_last_error(e.what());                          \
-    return XSLP_EINVAL;                                \
-  }                                                    \
-  return XSLP_OK;
 
 static const Program *P(const xslp_program *p) {
   if (!p) throw Error(XSLP_EINVAL, "null program");

@@ -16,33 +16,11 @@
 #include <chrono>
 #include <thread>
 
-#include "xslp_internal.h"
+#include "xslp_api.h"
 
 namespace xslp {
 
-#define CUDA_OK(x)                                                                      \
-  do {                                                                                  \
-    cudaError_t e_ = (x);                                                               \
-    if (e_ != cudaSuccess)                                                              \
-      throw Error(XSLP_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));         \
-  } while (0)
 
-#define API_BEGIN try {
-#define API_END                                        \
-  }                                                    \
-  catch (const Error &e) {                             \
-    set_last_error(e.what());                          \
-    return e.code;                                     \
-  }                                                    \
-  catch (const std::bad_alloc &) {                     \
-    set_last_error("out of host memory");              \
-    return XSLP_ENOMEM;                                \
-  }                                                    \
-  catch (const std::exception &e) {                    \
-    set_last_error(e.what());                          \
-    return XSLP_EINVAL;                                \
-  }                                                    \
-  return XSLP_OK;
 
 void count_launch();  // device.cu
 
