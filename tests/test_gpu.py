@@ -197,6 +197,20 @@ def test_multi_program_decode(per_module, hint, threads):
         rows = mx.decode_rows(og, n, list(pats[s]))[1]
         want = rs.decode(rows, synth.stripe_data(72, s, n, B))
         assert (out[s].cpu().numpy() == want).all(), s
+    # the launches (two internal streams for > 1 module) captured in a CUDA graph, replayed
+    pos_d = torch.tensor(pos, dtype=torch.int32, device="cuda")
+    ids_d = torch.from_numpy(ids).cuda()
+    ti, to = X.block_table(din, S, n, B), X.block_table(out, S, 4, B)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        X.xslp_multi_decode(multi, pos_d, ids_d, off, ti, to, B)
+    X.xslp_fill_random(din, S, n, B, seed=73)
+    gr.replay()
+    torch.cuda.synchronize()
+    for s in (0, S // 2, S - 1):
+        rows = mx.decode_rows(og, n, list(pats[s]))[1]
+        assert (out[s].cpu().numpy() == rs.decode(rows, synth.stripe_data(73, s, n, B))).all(), s
     if hint:
         with pytest.raises(X.XslpError):          # kernels were built for B
             X.xslp_multi_decode(multi, torch.tensor(pos, dtype=torch.int32, device="cuda"),
