@@ -337,3 +337,21 @@ def test_decode_bitmatrix_from_matches_oracle():
         with pytest.raises(X.XslpError) as ei:                                   # > p erasures
             X.xslp_decode_bitmatrix_from(g, n, p, list(range(p + 1)), list(range(n)))
         assert ei.value.code == -3
+
+
+def test_semantic_equality_all_1002_rs10_4_slps():
+    # every optimised SLP of the paper's dataset (RS(10,4) encode + all 1001
+    # 4-erasure decodes) computes exactly the oracle's goal sets, in both the
+    # pebble form and the interpreter's slot form
+    n, p = 10, 4
+    g = X.xslp_coding_matrix(n, p)
+    og = mx.coding_matrix(n, p)
+    pats = list(itertools.combinations(range(n + p), p))
+    bits = [X.xslp_encode_bitmatrix(g, n, p)] + [X.xslp_decode_bitmatrix(g, n, p, er)[0] for er in pats]
+    progs = X.compile_many(bits, specialise=0)
+    wants = [oslp.rows_to_sets(mx.to_bitmatrix(og[n:]))]
+    wants += [oslp.rows_to_sets(mx.to_bitmatrix(mx.decode_rows(og, n, list(er))[1])) for er in pats]
+    assert len(progs) == 1002
+    for k, (prog, want) in enumerate(zip(progs, wants)):
+        assert oslp.evaluate(prog.dump()) == want, k
+        assert oslp.evaluate(prog.dump(1)) == want, k
