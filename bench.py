@@ -35,7 +35,7 @@ MiB = 1 << 20
 WORKLOADS = {
     "cfg2": dict(desc="RS(10,4) encode, 1024 stripes x 10 x 1 MiB per GPU (BASELINE configs[1])",
                  n=10, p=4, B=MiB, S=1024, op="encode", seed=2,
-                 tuned=dict(kernel="pipe", threads=256, stages=2)),
+                 tuned=dict(kernel="pipe", threads=128, lanes=2, stages=2)),
     "cfg2b": dict(desc="RS(10,4) encode in the byte-compatible layout (output = textbook byte-wise "
                        "RS, SURVEY NEXT #3), 1024 stripes x 10 x 1 MiB",
                   n=10, p=4, B=MiB, S=1024, op="encode", seed=2, layout="byte",
@@ -55,7 +55,7 @@ WORKLOADS = {
     "pdec": dict(desc="RS(10,4) decode of the paper's P_dec pattern {2,4,5,6} (P:1670) on every "
                       "stripe, 1024 stripes x 1 MiB",
                  n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3,
-                 tuned=dict(kernel="pipe", threads=256, stages=2)),
+                 tuned=dict(kernel="pipe", threads=128, lanes=2, stages=2)),
     "cfg4": dict(desc="RS(10,p) encode sweep point (BASELINE configs[3]): total data fixed at "
                       "10 GiB, stripes = 10 GiB / (n x block)",
                  n=10, p=4, B=MiB, S=1024, op="encode", seed=4,
@@ -109,7 +109,7 @@ def parse():
                              "grouped_pipe", "multi", "gftable"])
     ap.add_argument("--stages", type=int, default=None)
     ap.add_argument("--streams", type=int, default=8, help="internal streams for grouped decode")
-    ap.add_argument("--lanes", type=int, default=1)
+    ap.add_argument("--lanes", type=int, default=None)
     ap.add_argument("--groups", type=int, default=None, help="PIPE consumer groups (goal split)")
     ap.add_argument("--per-module", type=int, default=56,
                     help="programs per fused multi-program kernel (--kernel multi)")
@@ -328,6 +328,7 @@ def main():
     args.threads = args.threads or 128
     args.stages = args.stages or 2
     args.groups = args.groups or 1
+    args.lanes = args.lanes or 1
     args.graph = int(args.graph or 0)
     if args.p:
         wl["p"] = args.p

@@ -279,13 +279,15 @@ def _xor_reduce(t):
     return acc
 
 
-@pytest.mark.parametrize("kern,threads", [("straight", 128), ("tma", 128), ("pipe", 256)])
-def test_cfg2_full_size_sampled(kern, threads):
-    # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); ("pipe", 256) with 2 stages is the
-    # exact launch configuration bench.py times by default
+@pytest.mark.parametrize("kern,threads,lanes", [("straight", 128, 1), ("tma", 128, 1), ("pipe", 256, 1),
+                                                ("pipe", 128, 2)])
+def test_cfg2_full_size_sampled(kern, threads, lanes):
+    # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); ("pipe", 128, 2 lanes) with 2 stages is
+    # the exact launch configuration bench.py times by default
     n, p, B, S = 10, 4, 1 << 20, 1024
     og = mx.coding_matrix(n, p)
-    _, prog = compile_enc(n, p, block_bytes_hint=B, kernel=kern, threads=threads, stages=2)
+    _, prog = compile_enc(n, p, block_bytes_hint=B, kernel=kern, threads=threads, stages=2,
+                          lane_words=lanes)
     din = dev_buf(S, n, B)
     X.xslp_fill_random(din, S, n, B, seed=2)
     dout = dev_buf(S, p, B)
@@ -354,13 +356,15 @@ def test_cfg3_full_size_roundtrip_sampled(mode):
     torch.cuda.empty_cache()
 
 
-def test_pdec_full_size_sampled():
+@pytest.mark.parametrize("threads,lanes", [(256, 1), (128, 2)])
+def test_pdec_full_size_sampled(threads, lanes):
     # the paper's P_dec (erase {2,4,5,6}) on 1024 stripes x 1 MiB in bench's launch configuration
     n, p, B, S = 10, 4, 1 << 20, 1024
     og = mx.coding_matrix(n, p)
     g = X.xslp_coding_matrix(n, p)
     bits, surv = X.xslp_decode_bitmatrix(g, n, p, [2, 4, 5, 6])
-    dec = X.xslp_compile(bits, kernel="pipe", threads=256, stages=2, block_bytes_hint=B)
+    dec = X.xslp_compile(bits, kernel="pipe", threads=threads, lane_words=lanes, stages=2,
+                         block_bytes_hint=B)
     din = dev_buf(S, n, B)
     X.xslp_fill_random(din, S, n, B, seed=3)          # survivors: arbitrary bytes
     out = dev_buf(S, 4, B)
