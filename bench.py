@@ -111,6 +111,7 @@ def parse():
     ap.add_argument("--streams", type=int, default=8, help="internal streams for grouped decode")
     ap.add_argument("--lanes", type=int, default=None)
     ap.add_argument("--groups", type=int, default=None, help="PIPE consumer groups (goal split)")
+    ap.add_argument("--phases", type=int, default=None, help="PIPE input phases (K-split)")
     ap.add_argument("--per-module", type=int, default=56,
                     help="programs per fused multi-program kernel (--kernel multi)")
     ap.add_argument("--threads", type=int, default=None)
@@ -302,7 +303,8 @@ def config_of(args, wl, stats):
          else wl["S"] // max(1, args.gpus),
          "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": args.compress + ("+fuse" if args.fuse else "") + ("+dfs" if args.schedule else ""),
          "kernel": args.kernel, "lane_words": args.lanes, "threads": args.threads,
-         "stages": args.stages, "groups": args.groups, "cuda_graph": bool(args.graph),
+         "stages": args.stages, "groups": args.groups, "phases": args.phases,
+         "cuda_graph": bool(args.graph),
          "l2": "inputs larger than the 126 MB L2; no flush between steps",
          "parallelism": (f"blocks spread over {args.gpus} GPU(s); survivors read in place over "
                          "NVLink P2P by the decode kernel (no collective)")
@@ -329,6 +331,7 @@ def main():
     args.stages = args.stages or 2
     args.groups = args.groups or 1
     args.lanes = args.lanes or 1
+    args.phases = args.phases or 1
     args.graph = int(args.graph or 0)
     if args.p:
         wl["p"] = args.p
@@ -406,7 +409,7 @@ def main():
         bits, _surv = X.xslp_decode_bitmatrix(G, n, p, erased)
         prog = X.xslp_compile(bits, compress=args.compress, kernel=args.kernel,
                               lane_words=args.lanes, threads=args.threads, block_bytes_hint=B,
-                              stages=args.stages, groups=args.groups)
+                              stages=args.stages, groups=args.groups, phases=args.phases)
         m_out = len(erased)
     elif wl["op"] == "encode_gft":    # approach (1): no SLP, the coefficient rows themselves
         prog = None
@@ -417,7 +420,7 @@ def main():
                               kernel=args.kernel, lane_words=args.lanes, threads=args.threads,
                               block_bytes_hint=B, stages=args.stages, fuse=args.fuse,
                               schedule=args.schedule, layout=wl.get("layout", "strip"),
-                              groups=args.groups)
+                              groups=args.groups, phases=args.phases)
         m_out = p
     compile_s = time.perf_counter() - t0
     stats = prog.stats() if prog is not None else None

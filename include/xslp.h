@@ -97,6 +97,12 @@ typedef struct xslp_opts {
                               each set's sub-program (the instructions its goals reach) runs on
                               its own `threads` consumer threads over the same shared-memory
                               stage, so a wide program keeps more warps issuing per SM */
+  int32_t phases;          /* PIPE input phases (1..8; default 1): the input blocks are cut into
+                              `phases` contiguous ranges, each compiled as its own program over all
+                              goals; a tile is streamed one range at a time and the goal partials
+                              are XORed in registers, so a stage holds one range's strips (wide
+                              codes such as RS(20,4) keep more consumer threads per SM).  Not
+                              combinable with groups > 1. */
 } xslp_opts;
 
 typedef struct xslp_stats {
@@ -116,8 +122,9 @@ typedef struct xslp_stats {
   int32_t regs_pipe;  /* registers per thread of the persistent TMA pipeline kernel */
   int32_t spill_bytes_pipe; /* its spill stores */
   double compile_ms;  /* host compile time of xslp_compile (SLP passes + PTX -> cubin) */
-  int64_t group_xor;  /* PIPE consumer groups: XORs executed per word position summed over the
-                         groups (>= xor_count: shared temporaries are recomputed); 0 if groups == 1 */
+  int64_t group_xor;  /* PIPE consumer groups / input phases: XORs executed per word position
+                         summed over the groups or phases, including the phases' accumulation
+                         XORs (>= xor_count in practice); 0 if neither is used */
 } xslp_stats;
 
 typedef struct xslp_program xslp_program; /* opaque, immutable after compile, thread-safe to share */

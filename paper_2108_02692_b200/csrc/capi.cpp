@@ -30,6 +30,7 @@ extern "C" void xslp_default_opts(xslp_opts *o) {
   o->greedy_capacity = 0;
   o->layout = XSLP_LAYOUT_STRIP;
   o->groups = 1;
+  o->phases = 1;
 }
 
 extern "C" int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out) {
@@ -121,6 +122,43 @@ extern "C" int xslp_decode_bitmatrix_from(const uint8_t *g, int n, int p, const 
 
 namespace {
 
+// Input phases for the PIPE kernel: the input blocks cut into opts.phases contiguous ranges
+// (as equal as possible); each range's goal sets (columns outside it cleared) are compressed,
+// fused and DFS-scheduled as their own program over all goals, and checked by evaluation.
+void build_phases(Program &P, const std::vector<Bits> &want) {
+  const xslp_opts &o = P.opts;
+  const int nb = P.n_const / 8, np = std::min(o.phases, std::max(1, nb));
+  P.phases.clear();
+  int used_max = 1;
+  for (int k = 0; k < np; ++k) {
+    const int lo = 8 * (k * nb / np), hi = 8 * ((k + 1) * nb / np);
+    std::vector<Bits> g(want.size(), Bits(P.n_const));
+    for (size_t r = 0; r < want.size(); ++r)
+      for (int c = lo; c < hi; ++c)
+        if (want[r].get(c)) g[r].set(c);
+    Slp s = o.compress == XSLP_COMPRESS_NONE ? lift(g, P.n_const, o.fuse != 0)
+                                             : compress(g, P.n_const, o.compress == XSLP_COMPRESS_XORREPAIR);
+    if (o.fuse) fuse(s);
+    if (o.schedule != XSLP_SCHED_NONE) schedule_dfs(s, o.goal_order);
+    auto got = evaluate(s);
+    for (size_t r = 0; r < g.size(); ++r)
+      if (!(got[r] == g[r])) throw Error(XSLP_EINVAL, "internal: phase program differs from its goals");
+    std::vector<char> u(P.n_const, 0);
+    for (auto &in : s.ins) {
+      P.stats.group_xor += (int64_t)in.ops.size() - 1;
+      for (int t : in.ops)
+        if (t < P.n_const) u[t] = 1;
+    }
+    for (int t : s.goal) {
+      if (t >= 0 && t < P.n_const) u[t] = 1;
+      if (t >= 0) P.stats.group_xor += 1;  // the partial's XOR into its accumulator
+    }
+    used_max = std::max(used_max, (int)std::count(u.begin(), u.end(), 1));
+    P.phases.push_back(std::move(s));
+  }
+  P.stage_used_const = used_max;
+}
+
 void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
   auto t0 = std::chrono::steady_clock::now();
   const xslp_opts &o = P.opts;
@@ -172,6 +210,7 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
     for (int g : P.slp.goal)
       if (g >= 0 && g < P.n_const) u[g] = 1;
     P.n_used_const = (int)std::count(u.begin(), u.end(), 1);
+    P.stage_used_const = P.n_used_const;
     P.const_reads = 0;
     for (auto &in : P.slp.ins)
       for (int t : in.ops)
@@ -182,18 +221,22 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
   const bool device_ok = P.n_const % 8 == 0 && P.n_goals % 8 == 0 && P.n_const > 0 &&
                          P.n_const / 8 + P.n_goals / 8 <= 128;
   if (o.specialise && device_ok) {
+    if (o.phases > 1 && o.layout == XSLP_LAYOUT_STRIP && want) {
+      build_phases(P, *want);
+    }
     if (o.groups > 1 && o.layout == XSLP_LAYOUT_STRIP) {
       P.groups = split_goals(P.slp, o.groups);
       for (auto &g : P.groups)
         for (auto &in : g.ins) st.group_xor += (int64_t)in.ops.size() - 1;
     }
     const std::vector<Slp> *gp = P.groups.empty() ? nullptr : &P.groups;
-    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads, o.min_blocks, o.stages, o.layout, gp);
+    const std::vector<Slp> *ph = P.phases.empty() ? nullptr : &P.phases;
+    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads, o.min_blocks, o.stages, o.layout, gp, ph);
     P.cubin_generic = ptx_to_cubin(P.ptx_generic, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma, &st.regs_pipe, &st.spill_bytes_pipe);
     if (o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0) {
       P.baked_strip = o.block_bytes_hint / 8;
       P.ptx_baked = emit_ptx(P.slp, o.lane_words, P.baked_strip, o.threads, o.min_blocks, o.stages,
-                           o.layout, gp);
+                           o.layout, gp, ph);
       P.cubin_baked = ptx_to_cubin(P.ptx_baked, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma, &st.regs_pipe, &st.spill_bytes_pipe);
     }
   }
@@ -219,6 +262,8 @@ void check_opts(xslp_opts &o) {
   if (o.layout == XSLP_LAYOUT_BYTE && !o.specialise)
     throw Error(XSLP_EINVAL, "the byte layout needs specialise = 1");
   if (o.groups < 1 || o.groups > 4) throw Error(XSLP_EINVAL, "groups must be 1..4");
+  if (o.phases < 1 || o.phases > 8) throw Error(XSLP_EINVAL, "phases must be 1..8");
+  if (o.phases > 1 && o.groups > 1) throw Error(XSLP_EINVAL, "phases and groups cannot be combined");
   if (o.threads * o.groups > 992) throw Error(XSLP_EINVAL, "pipe kernel: threads * groups <= 992");
 }
 

@@ -326,7 +326,7 @@ static int auto_kernel(const Program *p, size_t block_bytes, int nstripes) {
   const uint64_t strip = block_bytes / 8;
   const int T = p->opts.threads, L = p->opts.lane_words;
   if (strip % 16 || p->opts.threads * std::max<int>(1, (int)p->groups.size()) > 992) return XSLP_KERNEL_STRAIGHT;
-  const size_t smem = 128 + (size_t)p->opts.stages * p->n_used_const * 4 * L * T;
+  const size_t smem = 128 + (size_t)p->opts.stages * p->stage_used_const * 4 * L * T;
   const uint64_t tiles = (strip / (4 * L) + T - 1) / T * (uint64_t)nstripes;
   if (smem > 227 * 1024 || p->opts.stages < 2 || tiles < 4 * 148) return XSLP_KERNEL_STRAIGHT;
   // shared-memory bytes per data byte of the pipeline (one 4-byte read per constant use,
@@ -363,7 +363,7 @@ static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *c
     uint32_t tps = (words + T - 1) / T;
     if ((uint64_t)tps * (uint64_t)nstripes > 0xffffffffull) throw Error(XSLP_EINVAL, "too many tiles");
     uint32_t ntiles = tps * (uint32_t)nstripes;
-    const size_t smem = 128 + (size_t)p->opts.stages * p->n_used_const * 4 * L * T;
+    const size_t smem = 128 + (size_t)p->opts.stages * p->stage_used_const * 4 * L * T;
     if (smem > 227 * 1024) throw Error(XSLP_EINVAL, "pipeline stages do not fit in shared memory");
     cudaKernel_t k;
     int grid;
@@ -656,7 +656,7 @@ extern "C" int xslp_prepare(const xslp_program *prog, size_t block_bytes) {
   libs_of(p);
   if (block_bytes && block_bytes % 32 == 0 && p->opts.layout != XSLP_LAYOUT_BYTE) {
     const int T = p->opts.threads, L = p->opts.lane_words;
-    const size_t smem_pipe = 128 + (size_t)p->opts.stages * p->n_used_const * 4 * L * T;
+    const size_t smem_pipe = 128 + (size_t)p->opts.stages * p->stage_used_const * 4 * L * T;
     const size_t smem_tma = 128 + (size_t)p->n_used_const * 4 * L * T;
     const int d = current_device();
     std::lock_guard<std::mutex> g(g_mu);

@@ -31,6 +31,7 @@ struct Emitter {
   const Slp *sp;                  // the program being emitted (a group's sub-program in PIPE)
   const Slp &full;                // the whole program (declarations, other entries)
   const std::vector<Slp> *groups; // PIPE consumer groups, or nullptr
+  const std::vector<Slp> *phases = nullptr; // PIPE input phases (K-split), or nullptr
   int L;
   int64_t baked;
   int threads;
@@ -458,9 +459,18 @@ struct Emitter {
   }
 
   void store(int g, const std::vector<std::string> &r, int &tmp) {
+    if (accumulate) {  // input phases: goal partials are XORed into %acc, stored after the last
+      if (r[0] == "%zero") return;
+      for (int l = 0; l < L; ++l) {
+        const std::string acc = "%acc" + std::to_string(g * L + l);
+        o << "  xor.b32 " << acc << ", " << acc << ", " << r[l] << ";\n";
+      }
+      return;
+    }
     std::string a = addr("%ob" + std::to_string(g / 8), g % 8, tmp);
     o << "  st.global" << vsuf() << " " << a << ", " << vec(r) << ";\n";
   }
+  bool accumulate = false;
 
   void decls(int ntmp_guess) {
     o << "  .reg .pred %p<5>;\n  .reg .b32 %s<8>;\n  .reg .b64 %rd<8>;\n  .reg .b64 %off;\n";
@@ -474,6 +484,7 @@ struct Emitter {
     o << "  .reg .b32 %tps, %nt, %nct, %wid, %it, %tile, %lane, %st, %ph, %fb, %eb, %tw, %dst;\n";
     o << "  .reg .pred %pids, %pprod, %p5;\n  .reg .b32 %grp, %ltid, %pk, %pfirst, %t1, %chunk;\n";
     o << "  .reg .b64 %rpm;\n";
+    if (phases) o << "  .reg .b32 %acc<" << std::max<size_t>(1, full.goal.size() * L) << ">;\n";
     o << "  .reg .b32 %tx0;\n  .reg .b32 %y<8>;\n";
     int nq = 0;
     for (auto &in : cur().ins)
@@ -610,6 +621,137 @@ struct Emitter {
     o << "$DONE:\n  ret;\n";
   }
 
+  // PIPE with input phases (K-split): the constants are cut into P contiguous block ranges,
+  // each compiled as its own program over all goals; a word-tile is streamed as P stage fills
+  // (phase k's strips only), the consumers run phase k's program on fill k and XOR its goal
+  // values into accumulators %acc that live across the phases, stored after the last one.
+  // A stage holds one phase's strips, so wide codes (RS(20,4): 160 strips) keep T=256
+  // consumers with two stages in shared memory.
+  void body_pipe_phases(int S) {
+    const int nc = full.n_const, P = (int)phases->size();
+    const int TC = threads, NCW = threads / 32;
+    std::vector<std::vector<char>> used(P, std::vector<char>(nc, 0));
+    std::vector<std::vector<int>> slot(P, std::vector<int>(nc, -1));
+    std::vector<int> nused(P, 0);
+    std::vector<std::vector<char>> blk(P, std::vector<char>(n_in, 0));
+    int maxused = 1;
+    for (int k = 0; k < P; ++k) {
+      const Slp &q = (*phases)[k];
+      for (auto &in : q.ins)
+        for (int t : in.ops)
+          if (t < nc) used[k][t] = 1;
+      for (int g : q.goal)
+        if (g >= 0 && g < nc) used[k][g] = 1;
+      for (int c = 0; c < nc; ++c)
+        if (used[k][c]) { blk[k][c / 8] = 1; slot[k][c] = nused[k]++; }
+      maxused = std::max(maxused, nused[k]);
+    }
+    const int rowb = 4 * L * TC;
+    const int64_t STAGE = (int64_t)maxused * rowb;
+    const int EB = 8 * S;
+    o << "  mov.u32 %s2, %tid.x;\n  mov.u32 %sb, dsm;\n";
+    o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
+    for (int k = 0; k < S; ++k) {
+      o << "  mbarrier.init.shared::cta.b64 [%sb+" << 8 * k << "], 1;\n";
+      o << "  mbarrier.init.shared::cta.b64 [%sb+" << EB + 8 * k << "], " << NCW << ";\n";
+    }
+    o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
+    o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
+    o << "  ld.param.u64 %rd0, [p_ids];\n  setp.ne.u64 %pids, %rd0, 0;\n";
+    o << "  mov.u32 %nct, %nctaid.x;\n";
+    if (baked <= 0) {
+      o << "  ld.param.u64 %sk1, [p_strip];\n";
+      for (int k = 2; k < 8; ++k) o << "  mul.lo.u64 %sk" << k << ", %sk1, " << k << ";\n";
+    }
+    o << "  shr.u32 %wid, %s2, 5;\n  setp.eq.u32 %pprod, %wid, " << NCW << ";\n  @%pprod bra $PROD;\n";
+    auto stripe_of = [&](const std::string &lab) {
+      o << "  div.u32 %s5, %tile, %tps;\n  rem.u32 %tw, %tile, %tps;\n";
+      o << "  @!%pids bra " << lab << ";\n";
+      o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
+      o << lab << ":\n";
+    };
+    // ---------------- consumers: per word-tile, P phases
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n  mov.u32 %lane, %laneid;\n";
+    o << "$CLOOP:\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
+    stripe_of("$CID");
+    o << "  mad.lo.u32 %s3, %tw, " << TC << ", %s2;\n";
+    o << "  setp.lt.u32 %p5, %s3, %s4;\n";  // this thread has a word in the tile
+    o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+    o << "  mul.wide.u32 %off, %s3, " << 4 * L << ";\n";
+    for (size_t g = 0; g < full.goal.size() * L; ++g) o << "  mov.b32 %acc" << g << ", 0;\n";
+    accumulate = true;
+    for (int k = 0; k < P; ++k) {
+      const std::string x = std::to_string(k);
+      o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n";
+      o << "  and.b32 %ph, %ph, 1;\n  mad.lo.u32 %fb, %st, 8, %sb;\n";
+      o << "$CW" << x << ":\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW" << x << ";\n";
+      o << "  @!%p5 bra $CSKIP" << x << ";\n";
+      o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
+      o << "  mad.lo.u32 %sth, %s2, " << 4 * L << ", %sth;\n  add.u32 %sth, %sth, 128;\n";
+      sp = &(*phases)[k];
+      int tmp = 0;
+      compute(true, 0, slot[k], used[k], tmp);
+      o << "$CSKIP" << x << ":\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT" << x << ";\n";
+      o << "  add.u32 %eb, %fb, " << EB << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
+      o << "$CNEXT" << x << ":\n  add.u32 %it, %it, 1;\n";
+    }
+    accumulate = false;
+    sp = &full;
+    {  // the goals, once per word-tile
+      o << "  @!%p5 bra $CSTORED;\n";
+      for (int i = 0; i < n_out; ++i) {
+        o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+        o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
+      }
+      int tmp = 0;
+      for (size_t g = 0; g < full.goal.size(); ++g) {
+        std::vector<std::string> r;
+        for (int l = 0; l < L; ++l) r.push_back("%acc" + std::to_string(g * L + l));
+        store((int)g, r, tmp);
+      }
+      o << "$CSTORED:\n";
+    }
+    o << "  add.u32 %tile, %tile, %nct;\n  bra.uni $CLOOP;\n";
+    // ---------------- producer: per word-tile, P stage fills
+    int tmp = 0;
+    o << "$PROD:\n  mov.u32 %lane, %laneid;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $DONE;\n";
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n";
+    o << "$PLOOP:\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
+    stripe_of("$PID");
+    o << "  mul.lo.u32 %s7, %tw, " << TC << ";\n";
+    o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << TC << ";\n  mul.lo.u32 %nb, %nb, " << 4 * L << ";\n";
+    o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
+    o << "  mul.wide.u32 %toff, %s7, " << 4 * L << ";\n";
+    for (int j = 0; j < n_in; ++j) {
+      bool any = false;
+      for (int k = 0; k < P; ++k) any |= blk[k][j] != 0;
+      if (!any) continue;
+      o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+      o << "  add.s64 %ib" << j << ", %ib" << j << ", %toff;\n";
+    }
+    for (int k = 0; k < P; ++k) {
+      const std::string x = std::to_string(k);
+      o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n";
+      o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
+      o << "  setp.lt.u32 %p3, %it, " << S << ";\n  @%p3 bra $PNW" << x << ";\n";
+      o << "  sub.u32 %ph, %ph, 1;\n  and.b32 %ph, %ph, 1;\n  add.u32 %eb, %fb, " << EB << ";\n";
+      o << "$PW" << x << ":\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%eb], %ph;\n  @!%p3 bra $PW" << x << ";\n";
+      o << "$PNW" << x << ":\n";
+      o << "  mul.lo.u32 %s6, %nb, " << nused[k] << ";\n";
+      o << "  mbarrier.arrive.expect_tx.shared::cta.b64 _, [%fb], %s6;\n";
+      o << "  mul.lo.u32 %dst, %st, " << STAGE << ";\n  add.u32 %dst, %dst, %sb;\n";
+      for (int c = 0; c < nc; ++c) {
+        if (!used[k][c]) continue;
+        std::string a = addr("%ib" + std::to_string(c / 8), c % 8, tmp);
+        o << "  cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%dst+"
+          << 128 + (int64_t)slot[k][c] * rowb << "], " << a << ", %nb, [%fb];\n";
+      }
+      o << "  add.u32 %it, %it, 1;\n";
+    }
+    o << "  add.u32 %tile, %tile, %nct;\n  bra.uni $PLOOP;\n";
+    o << "$DONE:\n  ret;\n";
+  }
+
   std::string run_multi(const std::vector<const Slp *> &progs) {
     int mv = 0, mq = 0;
     for (const Slp *q : progs) {
@@ -675,7 +817,7 @@ struct Emitter {
       << threads * (groups ? (int)groups->size() : 1) + 32 << ", 1, 1\n";
     o << "{\n";
     decls(ntmp);
-    body_pipe(stages);
+    if (phases) body_pipe_phases(stages); else body_pipe(stages);
     o << "}\n";
     return o.str();
   }
@@ -684,13 +826,15 @@ struct Emitter {
 }  // namespace
 
 std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks,
-                     int stages, int layout, const std::vector<Slp> *groups) {
+                     int stages, int layout, const std::vector<Slp> *groups,
+                     const std::vector<Slp> *phases) {
   if (s.n_const % 8 || s.goal.size() % 8)
     throw Error(XSLP_EINVAL, "device programs need whole blocks (constants and goals multiples of 8)");
   if (s.n_const / 8 + s.goal.size() / 8 > 128)
     throw Error(XSLP_EINVAL, "too many blocks for one kernel (n + m > 128)");
   if (layout == XSLP_LAYOUT_BYTE) lanes = 1;
   Emitter e(s, lanes, baked_strip, threads, min_blocks, stages, layout, groups);
+  e.phases = phases;
   return e.run();
 }
 

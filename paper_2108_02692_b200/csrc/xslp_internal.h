@@ -88,6 +88,8 @@ struct Program {
   xslp_stats stats{};
   // interpreter bytecode (uint16 words) and slot count
   std::vector<Slp> groups;         // PIPE consumer groups: goal-restricted sub-programs (opts.groups > 1)
+  std::vector<Slp> phases;         // PIPE input phases: programs over contiguous input-block ranges
+  int stage_used_const = 0;        // constants per PIPE stage fill (max over phases, or n_used_const)
   std::vector<uint16_t> code;
   int nslots = 0;
   // straight-line kernel(s): generic addressing + optional baked strip size
@@ -118,7 +120,8 @@ Slp parse_text(const std::string &text, int n_const);
 
 // PTX (ptx.cpp)
 std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks,
-                     int stages, int layout, const std::vector<Slp> *groups = nullptr);
+                     int stages, int layout, const std::vector<Slp> *groups = nullptr,
+                     const std::vector<Slp> *phases = nullptr);
 // Split the goals into k contiguous sets balanced by issue cost; each result keeps the
 // instructions its goals reach (original order and variable ids) and marks the other goals -2.
 std::vector<Slp> split_goals(const Slp &s, int k);

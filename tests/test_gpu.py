@@ -410,6 +410,34 @@ def test_pipe_consumer_groups(groups, case):
             assert (dout[s].cpu().numpy() == want).all(), (case, groups, hint, s)
 
 
+@pytest.mark.parametrize("phases,threads", [(2, 256), (3, 128), (4, 64)])
+@pytest.mark.parametrize("case", ["rs20enc", "rs20dec", "rs10dec", "cauchy42"])
+def test_pipe_input_phases(phases, threads, case):
+    # PIPE with the inputs streamed in phases (K-split) and goal partials accumulated in
+    # registers: every output byte equals the oracle; ragged last tile, baked and generic
+    n, p, kind, er = {"rs20enc": (20, 4, "isal", None), "rs20dec": (20, 4, "isal", [0, 5, 21, 23]),
+                      "rs10dec": (10, 4, "isal", [2, 4, 5, 6]), "cauchy42": (4, 2, "cauchy", None)}[case]
+    og = mx.coding_matrix(n, p, kind)
+    g = X.xslp_coding_matrix(n, p, kind)
+    B, S = 8192 + 1152, 3                     # 292 words per strip: ragged last tile
+    if er is None:
+        bits, rows, m = X.xslp_encode_bitmatrix(g, n, p), og[n:], p
+    else:
+        bits, _ = X.xslp_decode_bitmatrix(g, n, p, er)
+        rows, m = mx.decode_rows(og, n, er)[1], len(er)
+    for hint in (0, B):
+        prog = X.xslp_compile(bits, kernel="pipe", threads=threads, stages=2, phases=phases,
+                              block_bytes_hint=hint)
+        assert prog.stats()["group_xor"] >= prog.stats()["xor_count"]
+        din = dev_buf(S, n, B)
+        X.xslp_fill_random(din, S, n, B, seed=91 + phases)
+        dout = torch.full((S, m, B), 0x5C, dtype=torch.uint8, device="cuda")
+        run_batch(prog, din, dout, B)
+        for s in range(S):
+            want = rs.apply_rows(rows, synth.stripe_data(91 + phases, s, n, B))
+            assert (dout[s].cpu().numpy() == want).all(), (case, phases, hint, s)
+
+
 @pytest.mark.parametrize("kern", ["straight", "tma", "pipe"])
 def test_cfg5_rs20_reduced(kern):
     # RS(20,4) encode + one seeded 4-erasure decode; 16 stripes x 20 x 1 MiB (configs[4] shape)
