@@ -63,12 +63,12 @@ WORKLOADS = {
     "cfg5": dict(desc="RS(20,4) encode, 8192 stripes x 20 x 1 MiB sharded over the GPUs; chunks "
                       "of <=2048 stripes per launch (BASELINE configs[4])",
                  n=20, p=4, B=MiB, S=8192, op="encode_sharded", seed=5, chunk=2048,
-                 tuned=dict(kernel="pipe", threads=128, stages=2)),
+                 tuned=dict(kernel="pipe", threads=256, stages=2, phases=2)),
     "cfg5d": dict(desc="RS(20,4) decode of one seeded random 4-erasure pattern (synth.erasure_pattern"
                        "(5, 0, 24, 4)) applied to every stripe, 8192 stripes x 1 MiB sharded over the "
                        "GPUs; chunks of <=2048 stripes per launch (BASELINE configs[4], decode half)",
                   n=20, p=4, B=MiB, S=8192, op="decode_sharded", e=4, seed=5, chunk=2048,
-                  tuned=dict(kernel="pipe", threads=128, stages=2)),
+                  tuned=dict(kernel="pipe", threads=256, stages=2, phases=2)),
     "xdec": dict(desc="RS(10,4) cross-GPU decode (SURVEY NEXT #4): the 14 blocks of each stripe "
                       "spread over the GPUs (block j of stripe s on rank (s+j) mod N), rank s mod N "
                       "decodes stripe s reading its survivors in place from local and NVLink-peer "

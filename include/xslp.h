@@ -97,7 +97,8 @@ typedef struct xslp_opts {
                               each set's sub-program (the instructions its goals reach) runs on
                               its own `threads` consumer threads over the same shared-memory
                               stage, so a wide program keeps more warps issuing per SM */
-  int32_t phases;          /* PIPE input phases (1..8; default 1): the input blocks are cut into
+  int32_t phases;          /* PIPE input phases (0 = auto, the default: ceil(n/10) for n > 10 input
+                              blocks, else 1; or 1..8): the input blocks are cut into
                               `phases` contiguous ranges, each compiled as its own program over all
                               goals; a tile is streamed one range at a time and the goal partials
                               are XORed in registers, so a stage holds one range's strips (wide

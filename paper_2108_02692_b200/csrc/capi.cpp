@@ -30,7 +30,7 @@ extern "C" void xslp_default_opts(xslp_opts *o) {
   o->greedy_capacity = 0;
   o->layout = XSLP_LAYOUT_STRIP;
   o->groups = 1;
-  o->phases = 1;
+  o->phases = 0;
 }
 
 extern "C" int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out) {
@@ -221,7 +221,11 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
   const bool device_ok = P.n_const % 8 == 0 && P.n_goals % 8 == 0 && P.n_const > 0 &&
                          P.n_const / 8 + P.n_goals / 8 <= 128;
   if (o.specialise && device_ok) {
-    if (o.phases > 1 && o.layout == XSLP_LAYOUT_STRIP && want) {
+    int phases = o.phases;
+    if (phases == 0)  // auto: at most 10 input blocks (80 strips) per stage fill
+      phases = o.groups > 1 ? 1 : std::min(8, (P.n_const / 8 + 9) / 10);
+    if (phases > 1 && o.layout == XSLP_LAYOUT_STRIP && want) {
+      P.opts.phases = phases;
       build_phases(P, *want);
     }
     if (o.groups > 1 && o.layout == XSLP_LAYOUT_STRIP) {
@@ -262,7 +266,7 @@ void check_opts(xslp_opts &o) {
   if (o.layout == XSLP_LAYOUT_BYTE && !o.specialise)
     throw Error(XSLP_EINVAL, "the byte layout needs specialise = 1");
   if (o.groups < 1 || o.groups > 4) throw Error(XSLP_EINVAL, "groups must be 1..4");
-  if (o.phases < 1 || o.phases > 8) throw Error(XSLP_EINVAL, "phases must be 1..8");
+  if (o.phases < 0 || o.phases > 8) throw Error(XSLP_EINVAL, "phases must be 0 (auto) or 1..8");
   if (o.phases > 1 && o.groups > 1) throw Error(XSLP_EINVAL, "phases and groups cannot be combined");
   if (o.threads * o.groups > 992) throw Error(XSLP_EINVAL, "pipe kernel: threads * groups <= 992");
 }

@@ -466,17 +466,18 @@ def test_cfg5_rs20_reduced(kern):
 
 def test_cfg5_full_chunk_sampled():
     # RS(20,4) encode and the seeded 4-erasure decode (configs[4]) over one bench launch: a chunk
-    # of 2048 stripes x 24 x 1 MiB, PIPE T=128 S=2 (bench.py cfg5 / cfg5d launch configuration)
+    # of 2048 stripes x 24 x 1 MiB, PIPE T=256 S=2 with 2 input phases (bench.py cfg5 / cfg5d
+    # launch configuration)
     n, p, B, S = 20, 4, 1 << 20, 2048
     og = mx.coding_matrix(n, p)
-    g, enc = compile_enc(n, p, block_bytes_hint=B, kernel="pipe", threads=128, stages=2)
+    g, enc = compile_enc(n, p, block_bytes_hint=B, kernel="pipe", threads=256, stages=2, phases=2)
     allb = dev_buf(S, n + p, B)
     X.xslp_fill_random(allb, S, n + p, B, seed=5)   # data words do not depend on nblocks
     ti = X.block_table(allb, S, n + p, B).view(S, n + p)
     X.xslp_encode_batch(enc, ti[:, :n].contiguous(), ti[:, n:].contiguous(), S, B)
     er = synth.erasure_pattern(5, 0, n + p, 4)
     bits, surv = X.xslp_decode_bitmatrix(g, n, p, er)
-    dec = X.xslp_compile(bits, block_bytes_hint=B, kernel="pipe", threads=128, stages=2)
+    dec = X.xslp_compile(bits, block_bytes_hint=B, kernel="pipe", threads=256, stages=2, phases=2)
     out = dev_buf(S, 4, B)
     X.xslp_encode_batch(dec, ti[:, torch.as_tensor(surv, dtype=torch.long)].contiguous(),
                         X.block_table(out, S, 4, B), S, B)
