@@ -9,6 +9,7 @@
 // (interpreter) standing in for the paper's L1-resident blocks.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 
@@ -225,7 +226,10 @@ static std::shared_ptr<Program::Dev> dev_of(const Program *p) {
   return e;
 }
 
+static void drop_pools_of(const Program *p);  // below: pools that contain p's bytecode
+
 Program::~Program() {
+  drop_pools_of(this);  // a later program at the same address must not find this one's pool
   {
     std::lock_guard<std::mutex> g(g_mu);
     auto it = g_libs.find(this);
@@ -501,6 +505,24 @@ static Pool pool_of(const Program *const *progs, int np) {
   CUDA_OK(cudaMemcpy(P.off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
   g_pools[{d, key}] = P;
   return P;
+}
+
+static void drop_pools_of(const Program *p) {
+  std::lock_guard<std::mutex> g(g_mu);
+  for (auto it = g_pools.begin(); it != g_pools.end();) {
+    const auto &progs = it->first.second;
+    if (std::find(progs.begin(), progs.end(), p) != progs.end()) {
+      int cur = -1;
+      const bool have = cudaGetDevice(&cur) == cudaSuccess;
+      cudaSetDevice(it->first.first);
+      cudaFree(it->second.code);
+      cudaFree(it->second.off);
+      if (have) cudaSetDevice(cur);
+      it = g_pools.erase(it);
+    } else {
+      ++it;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------

@@ -218,6 +218,33 @@ def test_multi_program_decode(per_module, hint, threads):
                                 X.block_table(out, S, 4, B), B - 128)
 
 
+def test_program_lifetime_no_stale_interpreter_pool():
+    # heterogeneous interpreter launches cache a device pool of the programs' bytecode keyed by
+    # the programs; freed programs must not leave a pool a new program at a recycled address
+    # would pick up (compare every round with the oracle)
+    import gc
+    n, p, B, S = 10, 4, 4096, 6
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    din = dev_buf(S, n, B)
+    X.xslp_fill_random(din, S, n, B, seed=101)
+    data = din.cpu().numpy()
+    for rnd in range(4):
+        pats = [tuple(synth.erasure_pattern(200 + rnd, s, n + p, 4)) for s in range(S)]
+        uniq = sorted(set(pats))
+        progs = [X.xslp_compile(X.xslp_decode_bitmatrix(g, n, p, er)[0], specialise=0) for er in uniq]
+        idx = torch.tensor([uniq.index(er) for er in pats], dtype=torch.int32, device="cuda")
+        out = torch.zeros((S, 4, B), dtype=torch.uint8, device="cuda")
+        X.xslp_decode_batch_multi(progs, idx, X.block_table(din, S, n, B), X.block_table(out, S, 4, B),
+                                  S, B)
+        torch.cuda.synchronize()
+        for s in range(S):
+            rows = mx.decode_rows(og, n, list(pats[s]))[1]
+            assert (out[s].cpu().numpy() == rs.decode(rows, data[s])).all(), (rnd, s)
+        del progs
+        gc.collect()
+
+
 def test_edge_cases():
     n, p = 4, 2
     _, prog = compile_enc(n, p, "cauchy")
