@@ -437,9 +437,9 @@ def test_pipe_consumer_groups(groups, case):
             assert (dout[s].cpu().numpy() == want).all(), (case, groups, hint, s)
 
 
-@pytest.mark.parametrize("phases,threads", [(2, 256), (3, 128), (4, 64)])
+@pytest.mark.parametrize("phases,threads,lanes", [(2, 256, 1), (3, 128, 1), (4, 64, 1), (2, 128, 2)])
 @pytest.mark.parametrize("case", ["rs20enc", "rs20dec", "rs10dec", "cauchy42"])
-def test_pipe_input_phases(phases, threads, case):
+def test_pipe_input_phases(phases, threads, lanes, case):
     # PIPE with the inputs streamed in phases (K-split) and goal partials accumulated in
     # registers: every output byte equals the oracle; ragged last tile, baked and generic
     n, p, kind, er = {"rs20enc": (20, 4, "isal", None), "rs20dec": (20, 4, "isal", [0, 5, 21, 23]),
@@ -454,7 +454,7 @@ def test_pipe_input_phases(phases, threads, case):
         rows, m = mx.decode_rows(og, n, er)[1], len(er)
     for hint in (0, B):
         prog = X.xslp_compile(bits, kernel="pipe", threads=threads, stages=2, phases=phases,
-                              block_bytes_hint=hint)
+                              lane_words=lanes, block_bytes_hint=hint)
         assert prog.stats()["group_xor"] >= prog.stats()["xor_count"]
         din = dev_buf(S, n, B)
         X.xslp_fill_random(din, S, n, B, seed=91 + phases)
@@ -520,6 +520,29 @@ def test_cfg5_full_chunk_sampled():
         assert (out[s].cpu().numpy() == rs.decode(rows, blocks[osurv])).all(), s
     del allb, out
     torch.cuda.empty_cache()
+
+
+def test_rs20_heterogeneous_grouped_pipe_with_phases():
+    # RS(20,4) per-stripe erasure patterns through the grouped path with PIPE kernels, whose
+    # default (auto) input phases read stripes through the stripe-id lists
+    n, p, B, S = 20, 4, 16384, 12
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    pats = [tuple(synth.erasure_pattern(111, s, n + p, 4)) for s in range(S)]
+    uniq = sorted(set(pats))
+    progs = X.compile_many([X.xslp_decode_bitmatrix(g, n, p, er)[0] for er in uniq],
+                           kernel="pipe", threads=128, stages=2, block_bytes_hint=B)
+    din = dev_buf(S, n, B)
+    X.xslp_fill_random(din, S, n, B, seed=112)
+    out = torch.zeros((S, 4, B), dtype=torch.uint8, device="cuda")
+    ids, off = X.group_stripes([uniq.index(er) for er in pats], len(progs))
+    X.xslp_decode_batch_grouped(progs, torch.from_numpy(ids).cuda(), off,
+                                X.block_table(din, S, n, B), X.block_table(out, S, 4, B), B,
+                                nstreams=4)
+    torch.cuda.synchronize()
+    for s in range(S):
+        rows = mx.decode_rows(og, n, list(pats[s]))[1]
+        assert (out[s].cpu().numpy() == rs.decode(rows, synth.stripe_data(112, s, n, B))).all(), s
 
 
 def test_shards_equal_single_run():
