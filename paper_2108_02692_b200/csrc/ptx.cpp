@@ -541,6 +541,10 @@ struct Emitter {
     o << "  mov.u32 %nct, %nctaid.x;\n  add.u32 %chunk, %nt, %nct;\n  sub.u32 %chunk, %chunk, 1;\n";
     o << "  div.u32 %chunk, %chunk, %nct;\n  mov.u32 %s0, %ctaid.x;\n";
     o << "  mul.lo.u32 %s1, %s0, %chunk;\n  add.u32 %t1, %s1, %chunk;\n  min.u32 %t1, %t1, %nt;\n";
+    // (a strided tile order -- tile = ctaid + i * nctaid, the PIPE kernel's -- measured 0.61
+    // here against 0.96: neighbouring CTAs then run different programs and instruction fetch
+    // thrashes; profiles/r01_s2_heterogeneous_and_groups.md)
+    const char *step = "1";
     if (baked <= 0) {
       o << "  ld.param.u64 %sk1, [p_strip];\n";
       for (int k = 2; k < 8; ++k) o << "  mul.lo.u64 %sk" << k << ", %sk1, " << k << ";\n";
@@ -577,7 +581,7 @@ struct Emitter {
     sp = &full;
     o << "$CSKIP:\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT;\n";
     o << "  add.u32 %eb, %fb, " << EB << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
-    o << "$CNEXT:\n  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, 1;\n  bra.uni $CLOOP;\n";
+    o << "$CNEXT:\n  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, " << step << ";\n  bra.uni $CLOOP;\n";
     // ---------------- producer
     int tmp = 0;
     o << "$PROD:\n  mov.u32 %lane, %laneid;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $DONE;\n";
@@ -617,7 +621,7 @@ struct Emitter {
       o << "  cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%dst+"
         << ROWS + (int64_t)slot[c] * rowb << "], " << a << ", %nb, [%fb];\n";
     }
-    o << "  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, 1;\n  bra.uni $PLOOP;\n";
+    o << "  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, " << step << ";\n  bra.uni $PLOOP;\n";
     o << "$DONE:\n  ret;\n";
   }
 
