@@ -534,6 +534,9 @@ struct Emitter {
       o << "  mbarrier.init.shared::cta.b64 [%sb+" << EB + 8 * k << "], " << NCW << ";\n";
     }
     o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
+    // programmatic dependent launch: once every CTA of this grid is resident the next module's
+    // grid (which touches other stripes) may be scheduled onto SMs as ours retire
+    o << "  griddepcontrol.launch_dependents;\n";
     o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
     o << "  ld.param.u64 %rd0, [p_ids];\n";
     o << "  ld.param.u64 %rpm, [p_pos];\n  ld.param.u32 %pfirst, [p_first];\n";
