@@ -65,7 +65,8 @@ extern "C" {
 #define XSLP_LAYOUT_STRIP 0 /* a block is 8 contiguous strips; the paper's layout */
 #define XSLP_LAYOUT_BYTE 1  /* a block is plain bytes; outputs equal textbook byte-wise RS
                                 via in-register bit-plane transposes; block_bytes % 32
-                               == 0, block pointers 32-byte aligned; straight-line kernel only */
+                               == 0, block pointers 32-byte aligned; straight-line (LDG) or PIPE
+                               kernel */
 
 #define XSLP_KERNEL_AUTO 0     /* batched calls: PIPE when its stages fit and there are >= 4 tiles per
                                   SM, else STRAIGHT; interpreter when nothing was compiled */

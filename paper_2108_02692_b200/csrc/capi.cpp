@@ -211,6 +211,15 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
       if (g >= 0 && g < P.n_const) u[g] = 1;
     P.n_used_const = (int)std::count(u.begin(), u.end(), 1);
     P.stage_used_const = P.n_used_const;
+    if (o.layout == XSLP_LAYOUT_BYTE) {  // PIPE stages hold whole 32-byte chunks of used blocks
+      int nub = 0;
+      for (int j = 0; j < P.n_const / 8; ++j) {
+        bool any = false;
+        for (int k = 0; k < 8; ++k) any |= u[8 * j + k] != 0;
+        nub += any;
+      }
+      P.stage_used_const = 8 * std::max(1, nub);
+    }
     P.const_reads = 0;
     for (auto &in : P.slp.ins)
       for (int t : in.ops)
@@ -260,9 +269,8 @@ void check_opts(xslp_opts &o) {
   if (o.min_blocks < 0 || o.min_blocks > 32) throw Error(XSLP_EINVAL, "bad min_blocks");
   if (o.stages < 1 || o.stages > 8) throw Error(XSLP_EINVAL, "stages must be 1..8");
   if (o.layout != XSLP_LAYOUT_STRIP && o.layout != XSLP_LAYOUT_BYTE) throw Error(XSLP_EINVAL, "bad layout");
-  if (o.layout == XSLP_LAYOUT_BYTE && (o.kernel == XSLP_KERNEL_INTERP || o.kernel == XSLP_KERNEL_TMA ||
-                                       o.kernel == XSLP_KERNEL_PIPE))
-    throw Error(XSLP_EINVAL, "the byte layout runs on the straight-line (LDG) kernel only");
+  if (o.layout == XSLP_LAYOUT_BYTE && (o.kernel == XSLP_KERNEL_INTERP || o.kernel == XSLP_KERNEL_TMA))
+    throw Error(XSLP_EINVAL, "the byte layout runs on the straight-line (LDG) or PIPE kernels only");
   if (o.layout == XSLP_LAYOUT_BYTE && !o.specialise)
     throw Error(XSLP_EINVAL, "the byte layout needs specialise = 1");
   if (o.groups < 1 || o.groups > 4) throw Error(XSLP_EINVAL, "groups must be 1..4");

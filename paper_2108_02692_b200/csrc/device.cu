@@ -362,8 +362,10 @@ static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *c
   if (straight && kind == XSLP_KERNEL_PIPE) {
     const int T = p->opts.threads, L = p->opts.lane_words;
     uint64_t strip = block_bytes / 8;
-    if (strip % 16) throw Error(XSLP_EINVAL, "TMA staging needs block_bytes % 128 == 0");
-    uint32_t words = (uint32_t)(strip / (4 * L));
+    const bool bytel = p->opts.layout == XSLP_LAYOUT_BYTE;
+    if (!bytel && strip % 16) throw Error(XSLP_EINVAL, "TMA staging needs block_bytes % 128 == 0");
+    // byte layout: a "word" is a thread's 32-byte chunk of every block
+    uint32_t words = bytel ? (uint32_t)(block_bytes / 32) : (uint32_t)(strip / (4 * L));
     uint32_t tps = (words + T - 1) / T;
     if ((uint64_t)tps * (uint64_t)nstripes > 0xffffffffull) throw Error(XSLP_EINVAL, "too many tiles");
     uint32_t ntiles = tps * (uint32_t)nstripes;
@@ -676,7 +678,7 @@ extern "C" int xslp_prepare(const xslp_program *prog, size_t block_bytes) {
   dev_of(p);  // interpreter bytecode
   set_smem_attr();
   libs_of(p);
-  if (block_bytes && block_bytes % 32 == 0 && p->opts.layout != XSLP_LAYOUT_BYTE) {
+  if (block_bytes && block_bytes % 32 == 0) {
     const int T = p->opts.threads, L = p->opts.lane_words;
     const size_t smem_pipe = 128 + (size_t)p->opts.stages * p->stage_used_const * 4 * L * T;
     const size_t smem_tma = 128 + (size_t)p->n_used_const * 4 * L * T;

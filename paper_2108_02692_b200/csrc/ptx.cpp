@@ -16,6 +16,7 @@
 //   xslp_sl_one(ptrs[128], strip_bytes, words)
 //     one stripe, pointers passed by value (in[0..n_in), out[n_in..n_in+n_out))
 // With a baked strip size the 8 strips of a block are addressed by immediate offsets.
+#include <functional>
 #include <map>
 #include <sstream>
 
@@ -293,44 +294,33 @@ struct Emitter {
       }
   }
 
-  void body_byte(bool one) {
+  // constants read by the program: per input block, any of its 8 planes used
+  std::vector<char> byte_blocks_used() {
     const int nc = cur().n_const;
-    std::vector<char> used(nc, 0);
+    std::vector<char> used(nc, 0), blk(n_in, 0);
     for (auto &in : cur().ins)
       for (int t : in.ops)
         if (t < nc) used[t] = 1;
     for (int g : cur().goal)
       if (g >= 0 && g < nc) used[g] = 1;
-    o << "  mov.u32 %s0, %ctaid.x;\n  mov.u32 %s1, %ntid.x;\n  mov.u32 %s2, %tid.x;\n";
-    o << "  mad.lo.u32 %s3, %s0, %s1, %s2;\n  ld.param.u32 %s4, [p_words];\n";
-    o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $DONE;\n  mul.wide.u32 %off, %s3, 32;\n";
-    if (!one) {
-      o << "  mov.u32 %s5, %ctaid.y;\n  ld.param.u32 %s6, [p_base];\n  add.u32 %s5, %s5, %s6;\n";
-      o << "  ld.param.u64 %rd0, [p_ids];\n  setp.eq.u64 %p1, %rd0, 0;\n  @%p1 bra $NOIDS;\n";
-      o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n";
-      o << "  ld.global.nc.u32 %s5, [%rd1];\n$NOIDS:\n";
-      o << "  ld.param.u64 %rd2, [p_in];\n  ld.param.u64 %rd3, [p_out];\n";
-      o << "  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
-      o << "  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
-    }
+    for (int c = 0; c < nc; ++c)
+      if (used[c]) blk[c / 8] = 1;
+    return blk;
+  }
+
+  // The byte-layout program on one 32-byte chunk of every block: `load(j, w)` brings block
+  // j's 8 words into registers w; they are transposed into bit-planes, the SLP runs, and each
+  // output block is transposed back and stored (256-bit) once its 8 goals exist.  %ob<i> must
+  // address the thread's chunk of output block i.
+  void byte_compute(const std::function<void(int, const std::vector<std::string> &)> &load) {
+    const int nc = cur().n_const;
+    auto blk = byte_blocks_used();
     for (int j = 0; j < n_in; ++j) {
-      bool any = false;
-      for (int k = 0; k < 8; ++k) any |= used[8 * j + k] != 0;
-      if (!any) continue;
-      if (one) o << "  ld.param.u64 %ib" << j << ", [p_ptrs+" << 8 * j << "];\n";
-      else o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
-      o << "  add.s64 %ib" << j << ", %ib" << j << ", %off;\n";
+      if (!blk[j]) continue;
       std::vector<std::string> w;
       for (int k = 0; k < 8; ++k) w.push_back(creg(8 * j + k, 0));
-      o << "  ld.global.nc.L1::no_allocate.v8.u32 {";
-      for (int k = 0; k < 8; ++k) o << (k ? ", " : "") << w[k];
-      o << "}, [%ib" << j << "];\n";
+      load(j, w);
       transpose8(w);
-    }
-    for (int i = 0; i < n_out; ++i) {
-      if (one) o << "  ld.param.u64 %ob" << i << ", [p_ptrs+" << 8 * (n_in + i) << "];\n";
-      else o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
-      o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
     }
     // when is each output block complete?
     std::vector<int> ready_at(n_out, -1);  // instruction index after which all 8 goals exist
@@ -376,6 +366,123 @@ struct Emitter {
       for (int b = 0; b < n_out; ++b)
         if (ready_at[b] == (int)k) store_block(b);
     }
+  }
+
+  void body_byte(bool one) {
+    o << "  mov.u32 %s0, %ctaid.x;\n  mov.u32 %s1, %ntid.x;\n  mov.u32 %s2, %tid.x;\n";
+    o << "  mad.lo.u32 %s3, %s0, %s1, %s2;\n  ld.param.u32 %s4, [p_words];\n";
+    o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $DONE;\n  mul.wide.u32 %off, %s3, 32;\n";
+    if (!one) {
+      o << "  mov.u32 %s5, %ctaid.y;\n  ld.param.u32 %s6, [p_base];\n  add.u32 %s5, %s5, %s6;\n";
+      o << "  ld.param.u64 %rd0, [p_ids];\n  setp.eq.u64 %p1, %rd0, 0;\n  @%p1 bra $NOIDS;\n";
+      o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n";
+      o << "  ld.global.nc.u32 %s5, [%rd1];\n$NOIDS:\n";
+      o << "  ld.param.u64 %rd2, [p_in];\n  ld.param.u64 %rd3, [p_out];\n";
+      o << "  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
+      o << "  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+    }
+    auto blk = byte_blocks_used();
+    for (int j = 0; j < n_in; ++j) {
+      if (!blk[j]) continue;
+      if (one) o << "  ld.param.u64 %ib" << j << ", [p_ptrs+" << 8 * j << "];\n";
+      else o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+      o << "  add.s64 %ib" << j << ", %ib" << j << ", %off;\n";
+    }
+    for (int i = 0; i < n_out; ++i) {
+      if (one) o << "  ld.param.u64 %ob" << i << ", [p_ptrs+" << 8 * (n_in + i) << "];\n";
+      else o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+      o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
+    }
+    byte_compute([&](int j, const std::vector<std::string> &w) {
+      o << "  ld.global.nc.L1::no_allocate.v8.u32 {";
+      for (int k = 0; k < 8; ++k) o << (k ? ", " : "") << w[k];
+      o << "}, [%ib" << j << "];\n";
+    });
+    o << "$DONE:\n  ret;\n";
+  }
+
+  // Byte layout through the TMA pipeline (entry xslp_sl_pipe of a byte-layout module): the
+  // producer warp copies the tile's T 32-byte chunks of every used input block (one bulk copy
+  // per block) into a stage row; consumers read their chunk with two 128-bit shared loads and
+  // run byte_compute.  "words" are 32-byte chunks here.
+  void body_pipe_byte(int S) {
+    const int TC = threads, NCW = threads / 32;
+    auto blk = byte_blocks_used();
+    std::vector<int> bslot(n_in, -1);
+    int nub = 0;
+    for (int j = 0; j < n_in; ++j)
+      if (blk[j]) bslot[j] = nub++;
+    const int ROWB = 32 * TC;
+    const int64_t STAGE = (int64_t)std::max(1, nub) * ROWB;
+    const int EB = 8 * S;
+    o << "  mov.u32 %s2, %tid.x;\n  mov.u32 %sb, dsm;\n";
+    o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
+    for (int k = 0; k < S; ++k) {
+      o << "  mbarrier.init.shared::cta.b64 [%sb+" << 8 * k << "], 1;\n";
+      o << "  mbarrier.init.shared::cta.b64 [%sb+" << EB + 8 * k << "], " << NCW << ";\n";
+    }
+    o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
+    o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
+    o << "  ld.param.u64 %rd0, [p_ids];\n  setp.ne.u64 %pids, %rd0, 0;\n";
+    o << "  mov.u32 %nct, %nctaid.x;\n";
+    o << "  shr.u32 %wid, %s2, 5;\n  setp.eq.u32 %pprod, %wid, " << NCW << ";\n  @%pprod bra $PROD;\n";
+    auto stripe_of = [&](const std::string &lab) {
+      o << "  div.u32 %s5, %tile, %tps;\n  rem.u32 %tw, %tile, %tps;\n";
+      o << "  @!%pids bra " << lab << ";\n";
+      o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
+      o << lab << ":\n";
+    };
+    // ---------------- consumers
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n  mov.u32 %lane, %laneid;\n";
+    o << "$CLOOP:\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
+    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n  and.b32 %ph, %ph, 1;\n";
+    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
+    o << "$CW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW;\n";
+    stripe_of("$CID");
+    o << "  mad.lo.u32 %s3, %tw, " << TC << ", %s2;\n";
+    o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $CSKIP;\n";
+    o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
+    o << "  mad.lo.u32 %sth, %s2, 32, %sth;\n  add.u32 %sth, %sth, 128;\n";
+    o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+    o << "  mul.wide.u32 %off, %s3, 32;\n";
+    for (int i = 0; i < n_out; ++i) {
+      o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+      o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
+    }
+    byte_compute([&](int j, const std::vector<std::string> &w) {
+      const int64_t at = (int64_t)bslot[j] * ROWB;
+      o << "  ld.shared.v4.u32 {" << w[0] << ", " << w[1] << ", " << w[2] << ", " << w[3] << "}, [%sth+" << at << "];\n";
+      o << "  ld.shared.v4.u32 {" << w[4] << ", " << w[5] << ", " << w[6] << ", " << w[7] << "}, [%sth+" << at + 16 << "];\n";
+    });
+    o << "$CSKIP:\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT;\n";
+    o << "  add.u32 %eb, %fb, " << EB << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
+    o << "$CNEXT:\n  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, %nct;\n  bra.uni $CLOOP;\n";
+    // ---------------- producer
+    o << "$PROD:\n  mov.u32 %lane, %laneid;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $DONE;\n";
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n";
+    o << "$PLOOP:\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
+    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n";
+    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
+    o << "  setp.lt.u32 %p5, %it, " << S << ";\n  @%p5 bra $PNW;\n";
+    o << "  sub.u32 %ph, %ph, 1;\n  and.b32 %ph, %ph, 1;\n  add.u32 %eb, %fb, " << EB << ";\n";
+    o << "$PW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%eb], %ph;\n  @!%p3 bra $PW;\n";
+    o << "$PNW:\n";
+    stripe_of("$PID");
+    o << "  mul.lo.u32 %s7, %tw, " << TC << ";\n";
+    o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << TC << ";\n  mul.lo.u32 %nb, %nb, 32;\n";
+    o << "  mul.lo.u32 %s6, %nb, " << nub << ";\n";
+    o << "  mbarrier.arrive.expect_tx.shared::cta.b64 _, [%fb], %s6;\n";
+    o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
+    o << "  mul.wide.u32 %toff, %s7, 32;\n";
+    o << "  mul.lo.u32 %dst, %st, " << STAGE << ";\n  add.u32 %dst, %dst, %sb;\n";
+    for (int j = 0; j < n_in; ++j) {
+      if (!blk[j]) continue;
+      o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+      o << "  add.s64 %ib" << j << ", %ib" << j << ", %toff;\n";
+      o << "  cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%dst+"
+        << 128 + (int64_t)bslot[j] * ROWB << "], [%ib" << j << "], %nb, [%fb];\n";
+    }
+    o << "  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, %nct;\n  bra.uni $PLOOP;\n";
     o << "$DONE:\n  ret;\n";
   }
 
@@ -808,7 +915,16 @@ struct Emitter {
     decls(ntmp);
     if (layout == XSLP_LAYOUT_BYTE) body_byte(true); else body(1);
     o << "}\n\n";
-    if (layout == XSLP_LAYOUT_BYTE) return o.str();  // no TMA variants for the byte layout
+    if (layout == XSLP_LAYOUT_BYTE) {  // byte layout: the TMA pipeline only (no xslp_sl_tma)
+      o << ".visible .entry xslp_sl_pipe(\n  .param .u64 p_in,\n  .param .u64 p_out,\n"
+           "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
+           "  .param .u32 p_tps,\n  .param .u32 p_ntiles)\n.maxntid "
+        << threads + 32 << ", 1, 1\n{\n";
+      decls(ntmp);
+      body_pipe_byte(stages);
+      o << "}\n";
+      return o.str();
+    }
     o << ".visible .entry xslp_sl_tma(\n  .param .u64 p_in,\n  .param .u64 p_out,\n"
          "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
          "  .param .u32 p_base)\n.maxntid "

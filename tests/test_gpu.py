@@ -564,11 +564,12 @@ def test_shards_equal_single_run():
 
 # ---- byte-compatible layout: outputs = textbook byte-wise RS -------
 
+@pytest.mark.parametrize("kern", ["straight", "pipe"])
 @pytest.mark.parametrize("n,p,kind,B,S", [(10, 4, "isal", 8224, 3), (4, 2, "cauchy", 4096, 2),
                                           (20, 4, "isal", 1 << 16, 2)])
-def test_byte_layout_encode_decode(n, p, kind, B, S):
+def test_byte_layout_encode_decode(n, p, kind, B, S, kern):
     og = mx.coding_matrix(n, p, kind)
-    g, prog = compile_enc(n, p, kind, layout="byte")
+    g, prog = compile_enc(n, p, kind, layout="byte", kernel=kern)
     data = host_data(31, range(S), n, B)
     din = torch.from_numpy(data).cuda()
     dout = torch.full((S, p, B), 0x77, dtype=torch.uint8, device="cuda")
@@ -623,10 +624,11 @@ def test_gf_table_kernel(n, p, kind, B, S):
     assert (rec.cpu().numpy() == blocks[:, er]).all()
 
 
-def test_byte_layout_full_size_sampled():
+@pytest.mark.parametrize("kern,threads", [("straight", 128), ("pipe", 128), ("pipe", 256)])
+def test_byte_layout_full_size_sampled(kern, threads):
     n, p, B, S = 10, 4, 1 << 20, 1024
     og = mx.coding_matrix(n, p)
-    _, prog = compile_enc(n, p, layout="byte", block_bytes_hint=B)
+    _, prog = compile_enc(n, p, layout="byte", block_bytes_hint=B, kernel=kern, threads=threads)
     din = dev_buf(S, n, B)
     X.xslp_fill_random(din, S, n, B, seed=2)
     dout = dev_buf(S, p, B)
