@@ -39,7 +39,7 @@ WORKLOADS = {
     "cfg2b": dict(desc="RS(10,4) encode in the byte-compatible layout (output = textbook byte-wise "
                        "RS, SURVEY NEXT #3), 1024 stripes x 10 x 1 MiB",
                   n=10, p=4, B=MiB, S=1024, op="encode", seed=2, layout="byte",
-                  tuned=dict(kernel="straight", threads=128, stages=2)),
+                  tuned=dict(kernel="pipe", threads=256, stages=2)),
     "cfg2t": dict(desc="RS(10,4) encode in the byte layout with the paper's approach (1) on the GPU: "
                        "byte-wise GF(2^8) MM with nibble-table multiplication (PRMT), the comparison "
                        "point for cfg2b's XOR program, 1024 stripes x 10 x 1 MiB",

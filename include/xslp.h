@@ -69,7 +69,9 @@ extern "C" {
                                kernel */
 
 #define XSLP_KERNEL_AUTO 0     /* batched calls: PIPE when its stages fit and there are >= 4 tiles per
-                                  SM, else STRAIGHT; interpreter when nothing was compiled */
+                                  SM (and, strip layout, the program reads <= ~6 shared-memory
+                                  bytes per data byte), else STRAIGHT; interpreter when nothing
+                                  was compiled */
 #define XSLP_KERNEL_STRAIGHT 1 /* the JIT-compiled straight-line specialisation */
 #define XSLP_KERNEL_INTERP 2   /* the generic SLP interpreter kernel */
 #define XSLP_KERNEL_TMA 3      /* straight-line kernel with TMA (cp.async.bulk) staging of the

@@ -326,7 +326,14 @@ static bool can_straight(const Program *p, size_t block_bytes, bool &baked) {
 // enough tiles to keep every SM busy (measured fastest: profiles/r01_*), otherwise the
 // register-resident LDG kernel.
 static int auto_kernel(const Program *p, size_t block_bytes, int nstripes) {
-  if (p->opts.layout == XSLP_LAYOUT_BYTE) return XSLP_KERNEL_STRAIGHT;
+  if (p->opts.layout == XSLP_LAYOUT_BYTE) {  // 32-byte chunks staged once, read once
+    const int T = p->opts.threads;
+    const size_t smem = 128 + (size_t)p->opts.stages * p->stage_used_const * 4 * T;
+    const uint64_t tiles = (block_bytes / 32 + T - 1) / T * (uint64_t)nstripes;
+    if (smem > 227 * 1024 || p->opts.stages < 2 || tiles < 4 * 148 || T > 992)
+      return XSLP_KERNEL_STRAIGHT;
+    return XSLP_KERNEL_PIPE;
+  }
   const uint64_t strip = block_bytes / 8;
   const int T = p->opts.threads, L = p->opts.lane_words;
   if (strip % 16 || p->opts.threads * std::max<int>(1, (int)p->groups.size()) > 992) return XSLP_KERNEL_STRAIGHT;
