@@ -47,7 +47,7 @@ WORKLOADS = {
                   tuned=dict(kernel="gftable", threads=256, stages=2)),
     "cfg3": dict(desc="RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures, "
                       "the distinct patterns' programs fused into persistent multi-program pipeline kernels "
-                      "(branch table per stripe, 56 programs per kernel); --kernel grouped: one "
+                      "(branch table per stripe, 20 programs per kernel); --kernel grouped: one "
                       "straight-line kernel per pattern over internal streams; --kernel interp: "
                       "one interpreter launch (BASELINE configs[2])",
                  n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3,
@@ -112,7 +112,7 @@ def parse():
     ap.add_argument("--lanes", type=int, default=None)
     ap.add_argument("--groups", type=int, default=None, help="PIPE consumer groups (goal split)")
     ap.add_argument("--phases", type=int, default=None, help="PIPE input phases (K-split)")
-    ap.add_argument("--per-module", type=int, default=56,
+    ap.add_argument("--per-module", type=int, default=20,
                     help="programs per fused multi-program kernel (--kernel multi)")
     ap.add_argument("--threads", type=int, default=None)
     ap.add_argument("--block-bytes", type=int, default=0, help="override block size")

@@ -41,3 +41,17 @@ for copies, pm in ((56, 56), (128, 128), (256, 256), (56, 28), (56, 14), (56, 5)
     ids, off = X.group_stripes([s % copies for s in range(S)], copies)
     ids = torch.from_numpy(ids).cuda()
     print("multi copies", copies, "per module", pm, m.info()["modules"], "modules", round(timeit(lambda: X.xslp_multi_decode(m, pos, ids, off, ti, to, B)), 1))
+
+# real decode programs (the first 56 cfg3 patterns), each owning ~18 stripes, one module;
+# then the same 56 programs with stripes assigned round-robin in runs of 1 stripe
+import synth  # noqa: E402
+pats = sorted(set(tuple(synth.erasure_pattern(3, s, n + p, 4)) for s in range(1024)))[:56]
+progs = X.compile_many([X.xslp_decode_bitmatrix(g, n, p, er)[0] for er in pats], specialise=0)
+m = X.Multi(progs, per_module=56, threads=256, stages=2, block_bytes_hint=B)
+print("real programs", m.info())
+for label, posl in (("18-stripe runs", [s * 56 // S for s in range(S)]),
+                    ("1-stripe runs", [s % 56 for s in range(S)])):
+    pos = torch.tensor(posl, dtype=torch.int32, device="cuda")
+    ids, off = X.group_stripes(posl, 56)
+    ids = torch.from_numpy(ids).cuda()
+    print("real 56 programs,", label, round(timeit(lambda: X.xslp_multi_decode(m, pos, ids, off, ti, to, B)), 1))
