@@ -246,7 +246,7 @@ int xslp_decode_batch_grouped(const xslp_program *const *progs, int nprogs,
  * producer warp streams the union of its programs' constant strips through `opts->stages`
  * shared-memory stages by TMA; each consumer warp reads its stripe's program index and jumps
  * to that program's straight-line code (a branch table), so a kernel serves many erasure
- * patterns.  Programs are packed per_module (<= 0: 64) to a module; modules compile in
+ * patterns.  Programs are packed per_module (<= 0: 20) to a module; modules compile in
  * parallel host threads.  opts: threads (consumer threads, <= 992), stages (2..8),
  * lane_words, block_bytes_hint (> 0: bake that block size in; launches must then use it).
  * The programs must stay alive while the multi is used.  Free with xslp_multi_free. */

@@ -352,7 +352,7 @@ def xslp_decode_batch_grouped(progs, d_stripe_ids, group_offsets, d_in_tbl, d_ou
 class Multi:
     """Programs fused into persistent multi-program pipeline kernels (xslp_multi_*)."""
 
-    def __init__(self, progs, per_module=64, opts=None, **kw):
+    def __init__(self, progs, per_module=20, opts=None, **kw):
         self._progs = list(progs)          # keep the programs alive
         o = opts if opts is not None else default_opts(**kw)
         arr = (ctypes.c_void_p * len(self._progs))(*[p.handle for p in self._progs])

@@ -133,7 +133,7 @@ extern "C" int xslp_multi_create(const xslp_program *const *progs, int nprogs, i
   if (o.threads < 32 || o.threads > 992 || o.threads % 32) throw Error(XSLP_EINVAL, "bad threads");
   if (o.stages < 2 || o.stages > 8) throw Error(XSLP_EINVAL, "stages must be 2..8");
   if (o.lane_words != 1 && o.lane_words != 2 && o.lane_words != 4) throw Error(XSLP_EINVAL, "bad lane_words");
-  if (per_module <= 0) per_module = 64;
+  if (per_module <= 0) per_module = 20;  // measured optimum for RS(10,4) decode (profiles)
   per_module = std::min(per_module, 256);
   auto t0 = std::chrono::steady_clock::now();
   auto M = std::make_unique<Multi>();
