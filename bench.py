@@ -450,7 +450,13 @@ def main():
         torch.cuda.synchronize()
         if dist:
             dist.barrier()                # every rank's storage written before any peer read
-        pdec = peer.PeerDecoder(X, pl, din, dout, plan, progs, dist=dist)
+        pmulti = None
+        if world == 1 and len(progs) > 1:   # all blocks local: the fused multi-program kernels
+            pmulti = X.Multi(X.compile_many([X.xslp_decode_bitmatrix_from(G, n, p, er, sv)
+                                             for er, sv in plan.keys], specialise=0),
+                             per_module=args.per_module, threads=256, stages=2, block_bytes_hint=B)
+            args.kernel, args.threads = "multi", 256
+        pdec = peer.PeerDecoder(X, pl, din, dout, plan, progs, dist=dist, multi=pmulti)
         remote_blocks, all_blocks = plan.remote_reads()
     elif wl["op"] in ("decode_one", "decode_sharded"):
         # whole codewords (data from the generator, parity by the encode program, untimed);

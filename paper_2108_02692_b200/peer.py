@@ -171,9 +171,15 @@ class PeerDecoder:
     stripes straight from local + peer memory (one grouped launch, or a single batch launch
     when all home stripes share one program)."""
 
-    def __init__(self, X, placement, storage, out, plan, progs, dist=None, group=None):
+    def __init__(self, X, placement, storage, out, plan, progs, dist=None, group=None, multi=None):
+        """multi: optional X.Multi over `progs` (fused multi-program kernels); used for local
+        data only -- peer blocks are read by the LDG straight-line kernels, whose plain loads
+        are what P2P mappings are exercised with here (TMA bulk copies from peer memory are not)."""
         import torch
         self.X, self.pl, self.plan, self.progs = X, placement, plan, progs
+        if multi is not None and placement.world > 1:
+            raise ValueError("the fused multi-program kernels are used for local blocks only")
+        self.multi = multi
         B = storage.shape[-1]
         self.B = B
         world = placement.world
@@ -198,6 +204,7 @@ class PeerDecoder:
         ids, off = plan.groups()
         self.ids = torch.from_numpy(ids).to(storage.device)
         self.off = off
+        self.pos = torch.tensor(plan.key_of, dtype=torch.int32).to(storage.device)
         self.S = len(plan.stripes)
 
     def launch(self, stream=None, nstreams=8):
@@ -206,6 +213,9 @@ class PeerDecoder:
             return
         if len(self.progs) == 1:
             X.xslp_encode_batch(self.progs[0], self.in_tbl, self.out_tbl, self.S, self.B, stream=stream)
+        elif self.multi is not None:
+            X.xslp_multi_decode(self.multi, self.pos, self.ids, self.off, self.in_tbl, self.out_tbl,
+                                self.B, stream=stream)
         else:
             X.xslp_decode_batch_grouped(self.progs, self.ids, self.off, self.in_tbl, self.out_tbl,
                                         self.B, nstreams=nstreams, stream=stream)

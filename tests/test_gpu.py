@@ -796,6 +796,14 @@ def test_peer_decode_emulated_ranks(world, e):
         ids, off = plan.groups()
         X.xslp_decode_batch_grouped(progs, torch.from_numpy(ids).cuda(), off, tin, tout, B, nstreams=4)
         torch.cuda.synchronize()
+        if world == 2:   # the same tables through the fused multi-program kernels
+            out2 = torch.zeros_like(out)
+            m = X.Multi(progs, per_module=3, threads=128, stages=2, block_bytes_hint=B)
+            X.xslp_multi_decode(m, torch.tensor(plan.key_of, dtype=torch.int32, device="cuda"),
+                                torch.from_numpy(ids).cuda(), off, tin,
+                                torch.from_numpy(plan.out_table(out2.data_ptr(), B).reshape(-1)).cuda(), B)
+            torch.cuda.synchronize()
+            assert torch.equal(out2, out)
         for i, s in enumerate(plan.stripes):
             erased, surv = plan.keys[plan.key_of[i]]
             d = synth.stripe_data(51, s, n, B)
