@@ -643,12 +643,15 @@ def test_byte_layout_full_size_sampled(kern, threads):
 
 # ---- CUDA graphs: launches are capturable after xslp_prepare -----------------------------
 
-@pytest.mark.parametrize("kern", ["pipe", "straight", "interp"])
+@pytest.mark.parametrize("kern", ["pipe", "straight", "interp", "pipe_phases", "pipe_byte"])
 def test_cuda_graph_capture(kern):
-    n, p, B, S = 10, 4, 65536, 64
+    n, p, B, S = (20, 4, 65536, 32) if kern == "pipe_phases" else (10, 4, 65536, 64)
     og = mx.coding_matrix(n, p)
-    _, prog = compile_enc(n, p, kernel=kern, threads=256 if kern == "pipe" else 128,
-                          block_bytes_hint=B)
+    if kern == "pipe_byte":
+        _, prog = compile_enc(n, p, kernel="pipe", threads=128, layout="byte", block_bytes_hint=B)
+    else:
+        _, prog = compile_enc(n, p, kernel=kern.split("_")[0], threads=256 if kern.startswith("pipe") else 128,
+                              block_bytes_hint=B, phases=2 if kern == "pipe_phases" else 1)
     X.xslp_prepare(prog, B)
     din = dev_buf(S, n, B)
     X.xslp_fill_random(din, S, n, B, seed=44)
@@ -661,12 +664,13 @@ def test_cuda_graph_capture(kern):
     assert not dout.any()                       # capture does not execute
     g.replay()
     torch.cuda.synchronize()
+    enc = (lambda d: rs.bytewise_apply(og[n:], d)) if kern == "pipe_byte" else (lambda d: rs.encode(og, n, d))
     for s in (0, S - 1):
-        assert (dout[s].cpu().numpy() == rs.encode(og, n, synth.stripe_data(44, s, n, B))).all()
+        assert (dout[s].cpu().numpy() == enc(synth.stripe_data(44, s, n, B))).all()
     X.xslp_fill_random(din, S, n, B, seed=45)   # replay on new inputs
     g.replay()
     torch.cuda.synchronize()
-    assert (dout[3].cpu().numpy() == rs.encode(og, n, synth.stripe_data(45, 3, n, B))).all()
+    assert (dout[3].cpu().numpy() == enc(synth.stripe_data(45, 3, n, B))).all()
 
 
 def test_cuda_graph_grouped_decode():
