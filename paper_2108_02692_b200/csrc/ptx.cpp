@@ -153,6 +153,46 @@ struct Emitter {
     o << "$DONE:\n  ret;\n";
   }
 
+  // ---- pieces shared by the pipelined kernels (a producer warp + consumer warps) ----------
+  // Shared memory [0, 8S): full barriers (one arrival: the producer's expect_tx, completed by
+  // the TMA bytes); [8S, 16S): empty barriers (one arrival per consumer warp).  Stage use %it
+  // of a CTA lives in stage %it % S with phase parity (%it / S) & 1.
+  void pipe_barriers(int S, int consumer_warps) {
+    o << "  mov.u32 %s2, %tid.x;\n  mov.u32 %sb, dsm;\n";
+    o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
+    for (int k = 0; k < S; ++k) {
+      o << "  mbarrier.init.shared::cta.b64 [%sb+" << 8 * k << "], 1;\n";
+      o << "  mbarrier.init.shared::cta.b64 [%sb+" << 8 * S + 8 * k << "], " << consumer_warps << ";\n";
+    }
+    o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
+  }
+  // %st, %ph (raw phase count) and %fb (full barrier) of stage use %it
+  void stage_regs(int S) {
+    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n";
+    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
+  }
+  // consumer: wait until the producer's fill of this stage use has landed
+  void consumer_wait(int S, const std::string &x) {
+    stage_regs(S);
+    o << "  and.b32 %ph, %ph, 1;\n";
+    o << "$CW" << x << ":\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW" << x << ";\n";
+  }
+  // consumer: $CSKIP<x> (threads without a word jump here), then one arrival per warp on the
+  // stage's empty barrier; ends at $CNEXT<x>
+  void consumer_release(int S, const std::string &x) {
+    o << "$CSKIP" << x << ":\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT" << x << ";\n";
+    o << "  add.u32 %eb, %fb, " << 8 * S << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
+    o << "$CNEXT" << x << ":\n";
+  }
+  // producer (after stage_regs): from the second round on, wait until the consumers drained
+  // the stage's previous fill
+  void producer_wait(int S, const std::string &x) {
+    o << "  setp.lt.u32 %p5, %it, " << S << ";\n  @%p5 bra $PNW" << x << ";\n";
+    o << "  sub.u32 %ph, %ph, 1;\n  and.b32 %ph, %ph, 1;\n  add.u32 %eb, %fb, " << 8 * S << ";\n";
+    o << "$PW" << x << ":\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%eb], %ph;\n  @!%p3 bra $PW" << x << ";\n";
+    o << "$PNW" << x << ":\n";
+  }
+
   // Persistent, warp-specialised TMA pipeline (entry xslp_sl_pipe).  threads = consumer
   // threads TC (NCW warps) plus one producer warp.  Each CTA walks tiles
   // tile = ctaid.x + i*nctaid.x (tile -> stripe = tile / tps, tw = tile % tps; a tile is
@@ -177,14 +217,7 @@ struct Emitter {
       if (used[c]) { blk_used[c / 8] = 1; slot[c] = nused++; }
     const int rowb = 4 * L * TC;
     const int64_t STAGE = (int64_t)nused * rowb;
-    const int EB = 8 * S;  // empty barriers follow the full barriers
-    o << "  mov.u32 %s2, %tid.x;\n  mov.u32 %sb, dsm;\n";
-    o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
-    for (int k = 0; k < S; ++k) {
-      o << "  mbarrier.init.shared::cta.b64 [%sb+" << 8 * k << "], 1;\n";
-      o << "  mbarrier.init.shared::cta.b64 [%sb+" << EB + 8 * k << "], " << G * NCW << ";\n";
-    }
-    o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
+    pipe_barriers(S, G * NCW);
     o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
     o << "  ld.param.u64 %rd0, [p_ids];\n  setp.ne.u64 %pids, %rd0, 0;\n";
     o << "  mov.u32 %nct, %nctaid.x;\n";
@@ -212,9 +245,7 @@ struct Emitter {
       o << "$C" << x << "START:\n";
       o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n  mov.u32 %lane, %laneid;\n";
       o << "$CLOOP" << x << ":\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
-      o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n  and.b32 %ph, %ph, 1;\n";
-      o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
-      o << "$CW" << x << ":\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW" << x << ";\n";
+      consumer_wait(S, x);
       stripe_of(("$CID" + x).c_str());
       o << "  mad.lo.u32 %s3, %tw, " << TC << ", %ltid;\n";
       o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $CSKIP" << x << ";\n";
@@ -232,9 +263,8 @@ struct Emitter {
       }
       int tmp = 0;
       compute(true, 0, slot, used, tmp);
-      o << "$CSKIP" << x << ":\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT" << x << ";\n";
-      o << "  add.u32 %eb, %fb, " << EB << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
-      o << "$CNEXT" << x << ":\n  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, %nct;\n  bra.uni $CLOOP" << x << ";\n";
+      consumer_release(S, x);
+      o << "  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, %nct;\n  bra.uni $CLOOP" << x << ";\n";
     }
     sp = &full;
     int tmp = 0;
@@ -242,12 +272,8 @@ struct Emitter {
     o << "$PROD:\n  mov.u32 %lane, %laneid;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $DONE;\n";
     o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n";
     o << "$PLOOP:\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
-    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n";
-    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
-    o << "  setp.lt.u32 %p5, %it, " << S << ";\n  @%p5 bra $PNW;\n";
-    o << "  sub.u32 %ph, %ph, 1;\n  and.b32 %ph, %ph, 1;\n  add.u32 %eb, %fb, " << EB << ";\n";
-    o << "$PW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%eb], %ph;\n  @!%p3 bra $PW;\n";
-    o << "$PNW:\n";
+    stage_regs(S);
+    producer_wait(S, "");
     stripe_of("$PID");
     o << "  mul.lo.u32 %s7, %tw, " << TC << ";\n";
     o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << TC << ";\n  mul.lo.u32 %nb, %nb, " << 4 * L << ";\n";
@@ -414,14 +440,7 @@ struct Emitter {
       if (blk[j]) bslot[j] = nub++;
     const int ROWB = 32 * TC;
     const int64_t STAGE = (int64_t)std::max(1, nub) * ROWB;
-    const int EB = 8 * S;
-    o << "  mov.u32 %s2, %tid.x;\n  mov.u32 %sb, dsm;\n";
-    o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
-    for (int k = 0; k < S; ++k) {
-      o << "  mbarrier.init.shared::cta.b64 [%sb+" << 8 * k << "], 1;\n";
-      o << "  mbarrier.init.shared::cta.b64 [%sb+" << EB + 8 * k << "], " << NCW << ";\n";
-    }
-    o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
+    pipe_barriers(S, NCW);
     o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
     o << "  ld.param.u64 %rd0, [p_ids];\n  setp.ne.u64 %pids, %rd0, 0;\n";
     o << "  mov.u32 %nct, %nctaid.x;\n";
@@ -435,9 +454,7 @@ struct Emitter {
     // ---------------- consumers
     o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n  mov.u32 %lane, %laneid;\n";
     o << "$CLOOP:\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
-    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n  and.b32 %ph, %ph, 1;\n";
-    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
-    o << "$CW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW;\n";
+    consumer_wait(S, "");
     stripe_of("$CID");
     o << "  mad.lo.u32 %s3, %tw, " << TC << ", %s2;\n";
     o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $CSKIP;\n";
@@ -454,19 +471,14 @@ struct Emitter {
       o << "  ld.shared.v4.u32 {" << w[0] << ", " << w[1] << ", " << w[2] << ", " << w[3] << "}, [%sth+" << at << "];\n";
       o << "  ld.shared.v4.u32 {" << w[4] << ", " << w[5] << ", " << w[6] << ", " << w[7] << "}, [%sth+" << at + 16 << "];\n";
     });
-    o << "$CSKIP:\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT;\n";
-    o << "  add.u32 %eb, %fb, " << EB << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
-    o << "$CNEXT:\n  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, %nct;\n  bra.uni $CLOOP;\n";
+    consumer_release(S, "");
+    o << "  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, %nct;\n  bra.uni $CLOOP;\n";
     // ---------------- producer
     o << "$PROD:\n  mov.u32 %lane, %laneid;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $DONE;\n";
     o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %ctaid.x;\n";
     o << "$PLOOP:\n  setp.ge.u32 %p0, %tile, %nt;\n  @%p0 bra $DONE;\n";
-    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n";
-    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
-    o << "  setp.lt.u32 %p5, %it, " << S << ";\n  @%p5 bra $PNW;\n";
-    o << "  sub.u32 %ph, %ph, 1;\n  and.b32 %ph, %ph, 1;\n  add.u32 %eb, %fb, " << EB << ";\n";
-    o << "$PW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%eb], %ph;\n  @!%p3 bra $PW;\n";
-    o << "$PNW:\n";
+    stage_regs(S);
+    producer_wait(S, "");
     stripe_of("$PID");
     o << "  mul.lo.u32 %s7, %tw, " << TC << ";\n";
     o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << TC << ";\n  mul.lo.u32 %nb, %nb, 32;\n";
@@ -632,15 +644,8 @@ struct Emitter {
       if (used[c]) { blk_used[c / 8] = 1; slot[c] = nused++; }
     const int rowb = 4 * L * TC;
     const int64_t STAGE = (int64_t)nused * rowb;
-    const int EB = 8 * S;
     const int HS = multi_hs(n_out), ROWS = multi_rows(S, n_out);
-    o << "  mov.u32 %s2, %tid.x;\n  mov.u32 %sb, dsm;\n";
-    o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
-    for (int k = 0; k < S; ++k) {
-      o << "  mbarrier.init.shared::cta.b64 [%sb+" << 8 * k << "], 1;\n";
-      o << "  mbarrier.init.shared::cta.b64 [%sb+" << EB + 8 * k << "], " << NCW << ";\n";
-    }
-    o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
+    pipe_barriers(S, NCW);
     // programmatic dependent launch: once every CTA of this grid is resident the next module's
     // grid (which touches other stripes) may be scheduled onto SMs as ours retire
     o << "  griddepcontrol.launch_dependents;\n";
@@ -663,9 +668,7 @@ struct Emitter {
     // ---------------- consumers
     o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %s1;\n  mov.u32 %lane, %laneid;\n";
     o << "$CLOOP:\n  setp.ge.u32 %p0, %tile, %t1;\n  @%p0 bra $DONE;\n";
-    o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n  and.b32 %ph, %ph, 1;\n";
-    o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
-    o << "$CW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW;\n";
+    consumer_wait(S, "");
     o << "  rem.u32 %tw, %tile, %tps;\n";
     o << "  mad.lo.u32 %s3, %tw, " << TC << ", %s2;\n";
     o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $CSKIP;\n";
@@ -689,9 +692,8 @@ struct Emitter {
       o << "  bra.uni $CSKIP;\n";
     }
     sp = &full;
-    o << "$CSKIP:\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT;\n";
-    o << "  add.u32 %eb, %fb, " << EB << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
-    o << "$CNEXT:\n  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, " << step << ";\n  bra.uni $CLOOP;\n";
+    consumer_release(S, "");
+    o << "  add.u32 %it, %it, 1;\n  add.u32 %tile, %tile, " << step << ";\n  bra.uni $CLOOP;\n";
     // ---------------- producer
     int tmp = 0;
     o << "$PROD:\n  mov.u32 %lane, %laneid;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $DONE;\n";
@@ -714,10 +716,7 @@ struct Emitter {
       o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
       o << "  add.s64 %ib" << j << ", %ib" << j << ", %toff;\n";
     }
-    o << "  setp.lt.u32 %p5, %it, " << S << ";\n  @%p5 bra $PNW;\n";
-    o << "  sub.u32 %ph, %ph, 1;\n  and.b32 %ph, %ph, 1;\n  add.u32 %eb, %fb, " << EB << ";\n";
-    o << "$PW:\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%eb], %ph;\n  @!%p3 bra $PW;\n";
-    o << "$PNW:\n";
+    producer_wait(S, "");
     o << "  mad.lo.u32 %dst, %st, " << HS << ", %sb;\n  add.u32 %dst, %dst, 128;\n";
     o << "  st.shared.u32 [%dst], %s5;\n  st.shared.u32 [%dst+4], %pk;\n";
     for (int i = 0; i < n_out; ++i) o << "  st.shared.u64 [%dst+" << 8 + 8 * i << "], %ob" << i << ";\n";
@@ -762,14 +761,7 @@ struct Emitter {
     }
     const int rowb = 4 * L * TC;
     const int64_t STAGE = (int64_t)maxused * rowb;
-    const int EB = 8 * S;
-    o << "  mov.u32 %s2, %tid.x;\n  mov.u32 %sb, dsm;\n";
-    o << "  setp.ne.u32 %p2, %s2, 0;\n  @%p2 bra $INIT;\n";
-    for (int k = 0; k < S; ++k) {
-      o << "  mbarrier.init.shared::cta.b64 [%sb+" << 8 * k << "], 1;\n";
-      o << "  mbarrier.init.shared::cta.b64 [%sb+" << EB + 8 * k << "], " << NCW << ";\n";
-    }
-    o << "  fence.mbarrier_init.release.cluster;\n$INIT:\n  bar.sync 0;\n";
+    pipe_barriers(S, NCW);
     o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
     o << "  ld.param.u64 %rd0, [p_ids];\n  setp.ne.u64 %pids, %rd0, 0;\n";
     o << "  mov.u32 %nct, %nctaid.x;\n";
@@ -796,18 +788,15 @@ struct Emitter {
     accumulate = true;
     for (int k = 0; k < P; ++k) {
       const std::string x = std::to_string(k);
-      o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n";
-      o << "  and.b32 %ph, %ph, 1;\n  mad.lo.u32 %fb, %st, 8, %sb;\n";
-      o << "$CW" << x << ":\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%fb], %ph;\n  @!%p3 bra $CW" << x << ";\n";
+      consumer_wait(S, x);
       o << "  @!%p5 bra $CSKIP" << x << ";\n";
       o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
       o << "  mad.lo.u32 %sth, %s2, " << 4 * L << ", %sth;\n  add.u32 %sth, %sth, 128;\n";
       sp = &(*phases)[k];
       int tmp = 0;
       compute(true, 0, slot[k], used[k], tmp);
-      o << "$CSKIP" << x << ":\n  bar.warp.sync -1;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $CNEXT" << x << ";\n";
-      o << "  add.u32 %eb, %fb, " << EB << ";\n  mbarrier.arrive.shared::cta.b64 _, [%eb];\n";
-      o << "$CNEXT" << x << ":\n  add.u32 %it, %it, 1;\n";
+      consumer_release(S, x);
+      o << "  add.u32 %it, %it, 1;\n";
     }
     accumulate = false;
     sp = &full;
@@ -845,12 +834,8 @@ struct Emitter {
     }
     for (int k = 0; k < P; ++k) {
       const std::string x = std::to_string(k);
-      o << "  rem.u32 %st, %it, " << S << ";\n  div.u32 %ph, %it, " << S << ";\n";
-      o << "  mad.lo.u32 %fb, %st, 8, %sb;\n";
-      o << "  setp.lt.u32 %p3, %it, " << S << ";\n  @%p3 bra $PNW" << x << ";\n";
-      o << "  sub.u32 %ph, %ph, 1;\n  and.b32 %ph, %ph, 1;\n  add.u32 %eb, %fb, " << EB << ";\n";
-      o << "$PW" << x << ":\n  mbarrier.try_wait.parity.shared::cta.b64 %p3, [%eb], %ph;\n  @!%p3 bra $PW" << x << ";\n";
-      o << "$PNW" << x << ":\n";
+      stage_regs(S);
+      producer_wait(S, x);
       o << "  mul.lo.u32 %s6, %nb, " << nused[k] << ";\n";
       o << "  mbarrier.arrive.expect_tx.shared::cta.b64 _, [%fb], %s6;\n";
       o << "  mul.lo.u32 %dst, %st, " << STAGE << ";\n  add.u32 %dst, %dst, %sb;\n";
