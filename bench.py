@@ -109,6 +109,9 @@ def parse():
                              "grouped_pipe", "multi", "gftable"])
     ap.add_argument("--stages", type=int, default=None)
     ap.add_argument("--streams", type=int, default=8, help="internal streams for grouped decode")
+    ap.add_argument("--xmode", default="peer", choices=["peer", "staged"],
+                    help="cross-GPU decode: read survivors in place over NVLink (peer), or the "
+                         "baseline: NCCL point-to-point into a staging buffer, then decode (staged)")
     ap.add_argument("--lanes", type=int, default=None)
     ap.add_argument("--groups", type=int, default=None, help="PIPE consumer groups (goal split)")
     ap.add_argument("--phases", type=int, default=None, help="PIPE input phases (K-split)")
@@ -307,7 +310,9 @@ def config_of(args, wl, stats):
          "cuda_graph": bool(args.graph),
          "l2": "inputs larger than the 126 MB L2; no flush between steps",
          "parallelism": (f"blocks spread over {args.gpus} GPU(s); survivors read in place over "
-                         "NVLink P2P by the decode kernel (no collective)")
+                         "NVLink P2P by the decode kernel (no collective)" if args.xmode == "peer" else
+                         f"blocks spread over {args.gpus} GPU(s); baseline: remote survivors "
+                         "gathered by NCCL point-to-point into a staging buffer, then a local decode")
          if wl["op"] == "decode_peer" else f"stripe-sharded x{args.gpus}, no collective"}
     if wl["op"] == "encode_gft":
         c["program"] = "none: GF(2^8) MM with nibble tables (approach (1), P:538-545)"
@@ -458,6 +463,11 @@ def main():
             args.kernel, args.threads = "multi", 256
         pdec = peer.PeerDecoder(X, pl, din, dout, plan, progs, dist=dist, multi=pmulti)
         remote_blocks, all_blocks = plan.remote_reads()
+        if args.xmode == "staged":        # baseline: gather the survivors, then a local decode
+            staging = torch.empty((len(plan.stripes), n, B), dtype=torch.uint8, device="cuda")
+            st_in = X.block_table(staging, len(plan.stripes), n, B)
+            sids, soff = plan.groups()
+            sids = torch.from_numpy(sids).cuda()
     elif wl["op"] in ("decode_one", "decode_sharded"):
         # whole codewords (data from the generator, parity by the encode program, untimed);
         # the decode program reads the n survivors of each stripe through the pointer table
@@ -480,7 +490,16 @@ def main():
         gids = torch.from_numpy(gids).cuda()
 
     def launch(st=stream):
-        if wl["op"] == "decode_peer":
+        if wl["op"] == "decode_peer" and args.xmode == "staged":
+            peer.staged_gather(pl, plan, din, staging, erasures, dist)
+            if len(progs) == 1:
+                X.xslp_encode_batch(progs[0], st_in, pdec.out_tbl, S, B, stream=st)
+            elif pmulti is not None:
+                X.xslp_multi_decode(pmulti, pdec.pos, sids, soff, st_in, pdec.out_tbl, B, stream=st)
+            else:
+                X.xslp_decode_batch_grouped(progs, sids, soff, st_in, pdec.out_tbl, B,
+                                            nstreams=args.streams, stream=st)
+        elif wl["op"] == "decode_peer":
             pdec.launch(stream=st, nstreams=args.streams)
         elif wl["op"] == "encode_gft":
             X.xslp_gf_table_apply(coef_rows, ti, to, S, B, stream=st)
