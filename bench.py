@@ -468,6 +468,7 @@ def main():
             st_in = X.block_table(staging, len(plan.stripes), n, B)
             sids, soff = plan.groups()
             sids = torch.from_numpy(sids).cuda()
+            sgather = peer.StagedGather(pl, plan, din, staging, erasures, X=X)
     elif wl["op"] in ("decode_one", "decode_sharded"):
         # whole codewords (data from the generator, parity by the encode program, untimed);
         # the decode program reads the n survivors of each stripe through the pointer table
@@ -491,7 +492,7 @@ def main():
 
     def launch(st=stream):
         if wl["op"] == "decode_peer" and args.xmode == "staged":
-            peer.staged_gather(pl, plan, din, staging, erasures, dist)
+            sgather.run(dist, stream=st)
             if len(progs) == 1:
                 X.xslp_encode_batch(progs[0], st_in, pdec.out_tbl, S, B, stream=st)
             elif pmulti is not None:

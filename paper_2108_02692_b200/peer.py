@@ -141,29 +141,56 @@ def exchange_lists(placement, rank, erasures):
     return send, recv
 
 
+class StagedGather:
+    """Baseline: copy every survivor of a rank's home stripes into staging [S_home][n][B]
+    (local ones by one device gather, remote ones by NCCL / gloo point-to-point), so a local
+    decode can follow.  The index lists are built once; `run()` moves one step's bytes."""
+
+    def __init__(self, placement, plan, storage, staging, erasures, X=None):
+        """X: the binding; when given, local survivors are copied by an identity program
+        (one 8-strip block in, the same block out) over block pointer tables -- one launch."""
+        import numpy as np
+        import torch
+        pl, rank = placement, plan.rank
+        self.pl, self.storage, self.staging, self.X = pl, storage, staging, X
+        row = {s: i for i, s in enumerate(plan.stripes)}
+        col = {}
+        src, dst = [], []
+        n = staging.shape[1]
+        for i, (s, k) in enumerate(zip(plan.stripes, plan.key_of)):
+            for c, j in enumerate(plan.keys[k][1]):
+                col[(s, j)] = c
+                if pl.owner(s, j) == rank:
+                    src.append(s * pl.slots + pl.slot(s, j))
+                    dst.append(i * n + c)
+        self.src = torch.tensor(src, dtype=torch.long, device=storage.device)
+        self.dst = torch.tensor(dst, dtype=torch.long, device=staging.device)
+        if X is not None and src:
+            B = staging.shape[-1]
+            self.copy = X.xslp_compile(np.eye(8, dtype=np.uint8), kernel="straight", threads=128,
+                                       block_bytes_hint=B)
+            self.tin = self.src * B + storage.data_ptr()
+            self.tout = self.dst * B + staging.data_ptr()
+        send, recv = exchange_lists(pl, rank, erasures)
+        self.sends = [(q, storage[s, pl.slot(s, j)]) for q, lst in send.items() for (s, j) in lst]
+        self.recvs = [(q, staging[row[s], col[(s, j)]]) for q, lst in recv.items() for (s, j) in lst]
+
+    def run(self, dist, group=None, stream=None):
+        B = self.staging.shape[-1]
+        if len(self.src) and self.X is not None:
+            self.X.xslp_encode_batch(self.copy, self.tin, self.tout, len(self.src), B, stream=stream)
+        elif len(self.src):
+            self.staging.view(-1, B)[self.dst] = self.storage.view(-1, B)[self.src]
+        ops = [dist.P2POp(dist.isend, t, q, group) for q, t in self.sends]
+        ops += [dist.P2POp(dist.irecv, t, q, group) for q, t in self.recvs]
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+
 def staged_gather(placement, plan, storage, staging, erasures, dist, group=None):
-    """Baseline: copy every survivor of rank's home stripes into staging [S_home][n][B]
-    (local ones by a device copy, remote ones by NCCL / gloo point-to-point), so a local
-    decode can follow.  storage: [S][slots][B] tensor of this rank."""
-    pl, rank = placement, plan.rank
-    row = {s: i for i, s in enumerate(plan.stripes)}
-    col = {}
-    for i, (s, k) in enumerate(zip(plan.stripes, plan.key_of)):
-        for c, j in enumerate(plan.keys[k][1]):
-            col[(s, j)] = c
-            if pl.owner(s, j) == rank:
-                staging[i, c].copy_(storage[s, pl.slot(s, j)])
-    send, recv = exchange_lists(pl, rank, erasures)
-    ops = []
-    for q, lst in send.items():
-        for (s, j) in lst:
-            ops.append(dist.P2POp(dist.isend, storage[s, pl.slot(s, j)], q, group))
-    for q, lst in recv.items():
-        for (s, j) in lst:
-            ops.append(dist.P2POp(dist.irecv, staging[row[s], col[(s, j)]], q, group))
-    if ops:
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
+    """One-shot form of StagedGather."""
+    StagedGather(placement, plan, storage, staging, erasures).run(dist, group)
 
 
 class PeerDecoder:
