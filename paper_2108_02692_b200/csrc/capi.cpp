@@ -373,6 +373,10 @@ extern "C" int64_t xslp_program_dump(const xslp_program *prog, int form, char *b
       s = dump_slots(P.code, P.n_const);
     } else if (form == 2) {
       s = P.ptx_baked.empty() ? P.ptx_generic : P.ptx_baked;
+    } else if (form == 3) {
+      // the pipelined interpreter's micro-op code for T = opts.threads
+      auto w = build_code32(P.code, P.opts.threads);
+      for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");
     } else {
       throw Error(XSLP_EINVAL, "bad dump form");
     }

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 
 #include "xslp_api.h"
 
@@ -19,6 +20,9 @@ namespace xslp {
 
 static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches++; }
+bool interp_pipe_launch(const Program *const *progs, int np, const int32_t *d_pos,
+                        const int32_t *d_ids, const uint8_t *const *in, uint8_t *const *out,
+                        int nstripes, size_t B, cudaStream_t st, int want_T);  // interp.cu
 
 
 // ---------------------------------------------------------------------------------
@@ -228,8 +232,11 @@ static std::shared_ptr<Program::Dev> dev_of(const Program *p) {
 
 static void drop_pools_of(const Program *p);  // below: pools that contain p's bytecode
 
+void drop_code32_of(const Program *p);  // interp.cu
+
 Program::~Program() {
   drop_pools_of(this);  // a later program at the same address must not find this one's pool
+  drop_code32_of(this);
   {
     std::lock_guard<std::mutex> g(g_mu);
     auto it = g_libs.find(this);
@@ -438,6 +445,12 @@ static void apply_batch(const Program *p, const uint8_t *const *d_in, uint8_t *c
       g_launches++;
     }
     return;
+  }
+  {  // the pipelined interpreter (interp.cu) when it applies, else the one-tile interpreter
+    const Program *ps1[1] = {p};
+    if (interp_pipe_launch(ps1, 1, nullptr, d_ids, d_in, d_out, nstripes, block_bytes, st,
+                           p->opts.threads))
+      return;
   }
   if (d_ids) throw Error(XSLP_EINVAL, "stripe id lists need the straight-line kernel");
   auto D = dev_of(p);
@@ -679,10 +692,16 @@ static const Program *P(const xslp_program *p) {
 // Load everything a launch of `prog` may need on the current device (JIT libraries,
 // shared-memory attributes, pipeline occupancy, interpreter bytecode) so later launches do
 // no allocation or synchronous copy and can be captured into a CUDA graph.
+namespace xslp {
+bool interp_pipe_prepare(const Program *p, size_t B);  // interp.cu
+}
+
 extern "C" int xslp_prepare(const xslp_program *prog, size_t block_bytes) {
   API_BEGIN
   const Program *p = P(prog);
   dev_of(p);  // interpreter bytecode
+  if (block_bytes && block_bytes % 32 == 0)
+    interp_pipe_prepare(p, block_bytes);  // the pipelined interpreter's code pool
   set_smem_attr();
   libs_of(p);
   if (block_bytes && block_bytes % 32 == 0) {
@@ -748,6 +767,9 @@ extern "C" int xslp_decode_batch_multi(const xslp_program *const *progs, int npr
     if (!d_prog_of_stripe || !d_in_tbl || !d_out_tbl) throw Error(XSLP_EINVAL, "null table");
     if (nstripes < 0) throw Error(XSLP_EINVAL, "nstripes < 0");
     if (nstripes == 0 || block_bytes == 0) return XSLP_OK;
+    if (interp_pipe_launch(ps.data(), nprogs, d_prog_of_stripe, nullptr, d_in_tbl, d_out_tbl,
+                           nstripes, block_bytes, (cudaStream_t)stream, ps[0]->opts.threads))
+      return XSLP_OK;
     Pool pool = pool_of(ps.data(), nprogs);
     int nsl = 1;
     for (auto q : ps) nsl = std::max(nsl, q->nslots);

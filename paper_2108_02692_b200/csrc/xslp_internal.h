@@ -125,6 +125,8 @@ std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, 
 // Split the goals into k contiguous sets balanced by issue cost; each result keeps the
 // instructions its goals reach (original order and variable ids) and marks the other goals -2.
 std::vector<Slp> split_goals(const Slp &s, int k);
+// Micro-op code of the pipelined interpreter for consumer width T (interp.cu).
+std::vector<uint32_t> build_code32(const std::vector<uint16_t> &code, int T);
 // One persistent pipeline kernel (entry xslp_sl_multi) over several programs with the same
 // constants/goals, dispatching per stripe through a branch table.
 std::string emit_ptx_multi(const std::vector<const Slp *> &progs, int lanes, int64_t baked_strip,

@@ -355,3 +355,52 @@ def test_semantic_equality_all_1002_rs10_4_slps():
     for k, (prog, want) in enumerate(zip(progs, wants)):
         assert oslp.evaluate(prog.dump()) == want, k
         assert oslp.evaluate(prog.dump(1)) == want, k
+
+
+def _emulate_microops(words, T, strips, n_goals):
+    """Plain host emulation of the pipelined interpreter's micro-op code (interp.cu)."""
+    w = np.array(words, dtype=np.int64)
+    nl, nm, _, nslots = (int(x) for x in w[:4])
+    row = T * 4
+    slots = np.zeros((nslots + 1, strips.shape[1]), dtype=np.uint32)   # + the zero row
+    for i in range(nl):
+        slots[w[5 + 2 * i] // row] = strips[w[4 + 2 * i]]
+    start = (4 + 2 * nl + 7) & ~7
+    out = np.full((n_goals, strips.shape[1]), 0xDEADBEEF, dtype=np.uint32)
+    acc = np.zeros(strips.shape[1], dtype=np.uint32)
+    for m in range(nm):
+        o = w[start + 8 * m:start + 8 * m + 8]
+        if o[4] & 1:
+            acc = np.zeros_like(acc)
+        for u in range(4):
+            acc = acc ^ slots[o[u] // row]
+        if o[4] & 2:
+            slots[o[5] // row] = acc
+        if o[4] & 4:
+            out[o[6]] = acc
+    return out
+
+
+@pytest.mark.parametrize("n,p,comp,er,T", [(10, 3, "none", None, 128), (10, 4, "xorrepair", None, 256),
+                                           (10, 2, "repair", None, 64), (4, 2, "none", None, 32),
+                                           (10, 4, "xorrepair", (2, 4, 5, 6), 128),
+                                           (20, 4, "xorrepair", (0, 5, 21, 23), 96)])
+def test_interpreter_microops_compute_the_oracle_result(n, p, comp, er, T):
+    # the host re-encoding of the bytecode for the pipelined interpreter (dump form 3), run by a
+    # plain emulator, reproduces the oracle's RS bytes on the strip layout
+    import synth
+    from oracle import rs
+    kind = "cauchy" if (n, p) == (4, 2) else "isal"
+    og = mx.coding_matrix(n, p, kind)
+    g = X.xslp_coding_matrix(n, p, kind)
+    if er is None:
+        bits, rows = X.xslp_encode_bitmatrix(g, n, p), og[n:]
+    else:
+        bits, rows = X.xslp_decode_bitmatrix(g, n, p, er)[0], mx.decode_rows(og, n, list(er))[1]
+    prog = X.xslp_compile(bits, compress=comp, specialise=0, threads=T)
+    words = [int(x) for x in prog.dump(3).split()]
+    B = 128
+    data = synth.stripe_data(9, 1, n, B)
+    got = _emulate_microops(words, T, data.reshape(8 * n, B // 8).view(np.uint32), bits.shape[0])
+    want = rs.apply_rows(rows, data).reshape(bits.shape[0], B // 8).view(np.uint32)
+    assert (got == want).all()
