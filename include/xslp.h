@@ -258,9 +258,9 @@ int xslp_multi_create(const xslp_program *const *progs, int nprogs, int per_modu
  * stripe; d_stripe_ids / group_offsets: the stripes of program i are d_stripe_ids[
  * group_offsets[i] .. group_offsets[i+1]) (DEVICE ids, HOST offsets, as in
  * xslp_decode_batch_grouped, which must agree with d_prog_of_stripe).  One launch per module
- * that has stripes, in order on `stream`, with programmatic dependent launch so a module's
- * grid starts as the previous one retires (capturable in a CUDA graph).  block_bytes % 128
- * == 0.  Tables as in xslp_encode_batch. */
+ * that has stripes; consecutive modules alternate between two internal streams forked from
+ * and joined back into `stream` (capturable in a CUDA graph).  block_bytes % 128 == 0.
+ * Tables as in xslp_encode_batch. */
 int xslp_multi_decode(const xslp_multi *multi, const int32_t *d_prog_of_stripe,
                       const int32_t *d_stripe_ids, const int32_t *group_offsets,
                       const uint8_t *const *d_in_tbl, uint8_t *const *d_out_tbl,

@@ -53,10 +53,16 @@ static int cur_dev() {
   return d;
 }
 
-// Modules launch in order on the caller's stream with programmatic dependent launch: each
-// kernel signals griddepcontrol.launch_dependents once its CTAs are resident, so the next
-// module's CTAs take SMs as this one's retire (tails overlap) while dispatch stays ordered --
-// unlike two concurrent streams, whose persistent grids can split the SMs between them.
+// Two internal streams per device: consecutive modules alternate between them (forked from
+// and joined back into the caller's stream with events), so the tail of one module's
+// persistent launch overlaps the start of the next.
+struct MultiStreams {
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+};
+static std::mutex g_ms_mu;
+static std::map<int, MultiStreams> g_ms;
+
 static void multi_launch(Multi &M, const int32_t *d_pos, const int32_t *d_ids, const int32_t *off,
                          const uint8_t *const *d_in, uint8_t *const *d_out, size_t B,
                          cudaStream_t user) {
@@ -71,6 +77,24 @@ static void multi_launch(Multi &M, const int32_t *d_pos, const int32_t *d_ids, c
   const int d = cur_dev();
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+  int active = 0;
+  for (auto &m : M.mods) active += off[m.first + m.count] > off[m.first];
+  MultiStreams *P = nullptr;
+  std::unique_lock<std::mutex> lk(g_ms_mu, std::defer_lock);
+  if (active > 1) {
+    lk.lock();
+    P = &g_ms[d];
+    if (!P->fork) {
+      for (int k = 0; k < 2; ++k) {
+        CUDA_OK(cudaStreamCreateWithFlags(&P->st[k], cudaStreamNonBlocking));
+        CUDA_OK(cudaEventCreateWithFlags(&P->join[k], cudaEventDisableTiming));
+      }
+      CUDA_OK(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
+    }
+    CUDA_OK(cudaEventRecord(P->fork, user));
+    for (int k = 0; k < 2; ++k) CUDA_OK(cudaStreamWaitEvent(P->st[k], P->fork, 0));
+  }
+  int launched = 0;
   for (auto &m : M.mods) {
     const int a = m.first, b = m.first + m.count;
     if (off[b] < off[a]) throw Error(XSLP_EINVAL, "group offsets must be non-decreasing");
@@ -104,19 +128,16 @@ static void multi_launch(Multi &M, const int32_t *d_pos, const int32_t *d_ids, c
     uint32_t first = (uint32_t)a;
     void *args[] = {(void *)&d_in, (void *)&d_out, (void *)&ids, &strip, &words, &tps, &ntiles,
                     (void *)&d_pos, &first};
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(T + 32);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = user;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CUDA_OK(cudaLaunchKernelExC(&cfg, (const void *)m.k, args));
+    cudaStream_t st = P ? P->st[launched % 2] : user;
+    CUDA_OK(cudaLaunchKernel((const void *)m.k, dim3(grid), dim3(T + 32), args, smem, st));
     count_launch();
+    ++launched;
   }
+  if (P)
+    for (int k = 0; k < 2; ++k) {
+      CUDA_OK(cudaEventRecord(P->join[k], P->st[k]));
+      CUDA_OK(cudaStreamWaitEvent(user, P->join[k], 0));
+    }
 }
 
 }  // namespace xslp

@@ -646,9 +646,6 @@ struct Emitter {
     const int64_t STAGE = (int64_t)nused * rowb;
     const int HS = multi_hs(n_out), ROWS = multi_rows(S, n_out);
     pipe_barriers(S, NCW);
-    // programmatic dependent launch: once every CTA of this grid is resident the next module's
-    // grid (which touches other stripes) may be scheduled onto SMs as ours retire
-    o << "  griddepcontrol.launch_dependents;\n";
     o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
     o << "  ld.param.u64 %rd0, [p_ids];\n";
     o << "  ld.param.u64 %rpm, [p_pos];\n  ld.param.u32 %pfirst, [p_first];\n";
