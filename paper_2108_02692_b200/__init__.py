@@ -21,7 +21,7 @@ _LIBPATH = os.path.join(_HERE, "libxslp.so")
 
 if not os.path.exists(_LIBPATH):
     raise ImportError(
-        f"{_LIBPATH} is missing: build it with `python -m paper_2108_02692_b200.build` "
+        f"{_LIBPATH} is missing: build it with `python paper_2108_02692_b200/build.py` "
         "(there is no CPU fallback)")
 
 _lib = ctypes.CDLL(_LIBPATH)
