@@ -404,3 +404,13 @@ def test_interpreter_microops_compute_the_oracle_result(n, p, comp, er, T):
     got = _emulate_microops(words, T, data.reshape(8 * n, B // 8).view(np.uint32), bits.shape[0])
     want = rs.apply_rows(rows, data).reshape(bits.shape[0], B // 8).view(np.uint32)
     assert (got == want).all()
+
+
+def test_no_goal_program():
+    # RS(n, 0): no parity blocks -- the program has no goals and no work
+    g = X.xslp_coding_matrix(4, 0)
+    bits = X.xslp_encode_bitmatrix(g, 4, 0)
+    assert bits.shape == (0, 32)
+    prog = X.xslp_compile(bits, specialise=0)
+    assert prog.stats()["n_goals"] == 0 and prog.stats()["xor_count"] == 0
+    assert oslp.evaluate(prog.dump()) == []

@@ -282,6 +282,40 @@ def test_copy_and_zero_goals_on_device():
         assert (out.cpu().numpy() == want).all()
 
 
+@pytest.mark.parametrize("kern", ["straight", "tma", "pipe", "interp", "multi"])
+def test_copy_and_zero_goals_batched(kern):
+    # degenerate goals through the batched kernels (identity rows, all-zero rows, a full row),
+    # several stripes, ragged tiles: copies and zeros must be written like any other goal
+    rng = np.random.default_rng(1)
+    bits = np.zeros((16, 24), dtype=np.uint8)
+    bits[0, 3] = 1
+    bits[1, 17] = 1
+    bits[2, [1, 2, 5]] = 1
+    bits[5, :] = 1
+    bits[9:, :] = rng.integers(0, 2, size=(7, 24))
+    B, S = 2048 + 640, 3                         # 84 words per strip: ragged at every T
+    data = host_data(9, range(S), 3, B)
+    din = torch.from_numpy(data).cuda()
+    out = torch.full((S, 2, B), 0x5A, dtype=torch.uint8, device="cuda")
+    ti, to = X.block_table(din, S, 3, B), X.block_table(out, S, 2, B)
+    if kern == "multi":
+        bits2 = rng.integers(0, 2, size=(16, 24)).astype(np.uint8)
+        progs = [X.xslp_compile(b, specialise=0) for b in (bits, bits2)]
+        m = X.Multi(progs, per_module=1, threads=64, stages=2)
+        pos = [s % 2 for s in range(S)]
+        ids, off = X.group_stripes(pos, 2)
+        X.xslp_multi_decode(m, torch.tensor(pos, dtype=torch.int32, device="cuda"),
+                            torch.from_numpy(ids).cuda(), off, ti, to, B)
+        wants = [rs.bitmatrix_apply(bits if s % 2 == 0 else bits2, data[s]) for s in range(S)]
+    else:
+        prog = X.xslp_compile(bits, kernel=kern, threads=64, specialise=0 if kern == "interp" else 1)
+        X.xslp_encode_batch(prog, ti, to, S, B)
+        wants = [rs.bitmatrix_apply(bits, data[s]) for s in range(S)]
+    torch.cuda.synchronize()
+    for s in range(S):
+        assert (out[s].cpu().numpy() == wants[s]).all(), (kern, s)
+
+
 def test_host_buffer_path():
     n, p, B, S = 10, 4, 65536, 40
     og = mx.coding_matrix(n, p)
