@@ -69,6 +69,11 @@ WORKLOADS = {
                        "GPUs; chunks of <=2048 stripes per launch (BASELINE configs[4], decode half)",
                   n=20, p=4, B=MiB, S=8192, op="decode_sharded", e=4, seed=5, chunk=2048,
                   tuned=dict(kernel="pipe", threads=256, stages=2, phases=2)),
+    "cfg5h": dict(desc="RS(20,4) decode with per-stripe seeded 4-of-24 erasures (the secondary "
+                       "reading of BASELINE configs[4]), 1024 stripes x 1 MiB per GPU: the patterns' "
+                       "programs fused into multi-program kernels with 2 input phases",
+                  n=20, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=5,
+                  tuned=dict(kernel="multi", threads=256, stages=2)),
     "xdec": dict(desc="RS(10,4) cross-GPU decode (SURVEY NEXT #4): the 14 blocks of each stripe "
                       "spread over the GPUs (block j of stripe s on rank (s+j) mod N), rank s mod N "
                       "decodes stripe s reading its survivors in place from local and NVLink-peer "
@@ -344,7 +349,8 @@ def config_of(args, wl, stats):
          else wl["S"] // max(1, args.gpus),
          "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": args.compress + ("+fuse" if args.fuse else "") + ("+dfs" if args.schedule else ""),
          "kernel": args.kernel, "lane_words": args.lanes, "threads": args.threads,
-         "stages": args.stages, "groups": args.groups, "phases": args.phases,
+         "stages": args.stages, "groups": args.groups,
+         "phases": args.phases or (-(-wl["n"] // 10) if wl["n"] > 10 else 1),
          "cuda_graph": bool(args.graph),
          "l2": "inputs larger than the 126 MB L2; no flush between steps",
          "parallelism": (f"blocks spread over {args.gpus} GPU(s); survivors read in place over "
@@ -374,7 +380,8 @@ def main():
     args.stages = args.stages or 2
     args.groups = args.groups or 1
     args.lanes = args.lanes or 1
-    args.phases = args.phases or 1
+    if args.phases is None:            # 0 = the library's auto: ceil(n/10) input phases if n > 10
+        args.phases = 0
     args.graph = int(args.graph or 0)
     if args.p:
         wl["p"] = args.p
@@ -418,7 +425,8 @@ def main():
             progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,
                                    threads=args.threads)
             multi = X.Multi(progs, per_module=args.per_module, threads=args.threads,
-                            stages=args.stages, lane_words=args.lanes, block_bytes_hint=B)
+                            stages=args.stages, lane_words=args.lanes, block_bytes_hint=B,
+                            phases=args.phases)
             log("multi", multi.info())
         elif mode == "interp":
             progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,

@@ -249,7 +249,9 @@ int xslp_decode_batch_grouped(const xslp_program *const *progs, int nprogs,
  * to that program's straight-line code (a branch table), so a kernel serves many erasure
  * patterns.  Programs are packed per_module (<= 0: 20) to a module; modules compile in
  * parallel host threads.  opts: threads (consumer threads, <= 992), stages (2..8),
- * lane_words, block_bytes_hint (> 0: bake that block size in; launches must then use it).
+ * lane_words, block_bytes_hint (> 0: bake that block size in; launches must then use it),
+ * phases (input phases as for the PIPE kernel; 0 = ceil(n/10) for codes wider than 10 blocks:
+ * each program is recompiled per input-block range and a tile is streamed range by range).
  * The programs must stay alive while the multi is used.  Free with xslp_multi_free. */
 typedef struct xslp_multi xslp_multi;
 int xslp_multi_create(const xslp_program *const *progs, int nprogs, int per_module,

@@ -120,41 +120,51 @@ extern "C" int xslp_decode_bitmatrix_from(const uint8_t *g, int n, int p, const 
   API_END
 }
 
-namespace {
-
-// Input phases for the PIPE kernel: the input blocks cut into opts.phases contiguous ranges
-// (as equal as possible); each range's goal sets (columns outside it cleared) are compressed,
-// fused and DFS-scheduled as their own program over all goals, and checked by evaluation.
-void build_phases(Program &P, const std::vector<Bits> &want) {
-  const xslp_opts &o = P.opts;
-  const int nb = P.n_const / 8, np = std::min(o.phases, std::max(1, nb));
-  P.phases.clear();
-  int used_max = 1;
+namespace xslp {
+// Input-phase programs: the goal sets restricted to each of `nphases` contiguous input-block
+// ranges (as equal as possible), each compressed, fused and DFS-scheduled as its own program
+// over all goals, checked by evaluation.  xor_total (if given) accumulates the XORs the phases
+// execute per word position, including each nonzero partial's XOR into its accumulator.
+std::vector<Slp> phase_programs(const std::vector<Bits> &want, int n_const, int nphases,
+                                const xslp_opts &o, int64_t *xor_total) {
+  const int nb = n_const / 8, np = std::min(nphases, std::max(1, nb));
+  std::vector<Slp> out;
   for (int k = 0; k < np; ++k) {
     const int lo = 8 * (k * nb / np), hi = 8 * ((k + 1) * nb / np);
-    std::vector<Bits> g(want.size(), Bits(P.n_const));
+    std::vector<Bits> g(want.size(), Bits(n_const));
     for (size_t r = 0; r < want.size(); ++r)
       for (int c = lo; c < hi; ++c)
         if (want[r].get(c)) g[r].set(c);
-    Slp s = o.compress == XSLP_COMPRESS_NONE ? lift(g, P.n_const, o.fuse != 0)
-                                             : compress(g, P.n_const, o.compress == XSLP_COMPRESS_XORREPAIR);
+    Slp s = o.compress == XSLP_COMPRESS_NONE ? lift(g, n_const, o.fuse != 0)
+                                             : compress(g, n_const, o.compress == XSLP_COMPRESS_XORREPAIR);
     if (o.fuse) fuse(s);
     if (o.schedule != XSLP_SCHED_NONE) schedule_dfs(s, o.goal_order);
     auto got = evaluate(s);
     for (size_t r = 0; r < g.size(); ++r)
       if (!(got[r] == g[r])) throw Error(XSLP_EINVAL, "internal: phase program differs from its goals");
+    if (xor_total) {
+      for (auto &in : s.ins) *xor_total += (int64_t)in.ops.size() - 1;
+      for (int t : s.goal) *xor_total += t >= 0;
+    }
+    out.push_back(std::move(s));
+  }
+  return out;
+}
+}  // namespace xslp
+
+namespace {
+
+void build_phases(Program &P, const std::vector<Bits> &want) {
+  P.phases = phase_programs(want, P.n_const, P.opts.phases, P.opts, &P.stats.group_xor);
+  int used_max = 1;
+  for (auto &s : P.phases) {
     std::vector<char> u(P.n_const, 0);
-    for (auto &in : s.ins) {
-      P.stats.group_xor += (int64_t)in.ops.size() - 1;
+    for (auto &in : s.ins)
       for (int t : in.ops)
         if (t < P.n_const) u[t] = 1;
-    }
-    for (int t : s.goal) {
+    for (int t : s.goal)
       if (t >= 0 && t < P.n_const) u[t] = 1;
-      if (t >= 0) P.stats.group_xor += 1;  // the partial's XOR into its accumulator
-    }
     used_max = std::max(used_max, (int)std::count(u.begin(), u.end(), 1));
-    P.phases.push_back(std::move(s));
   }
   P.stage_used_const = used_max;
 }

@@ -35,7 +35,7 @@ struct MultiModule {
 };
 
 struct Multi {
-  int n_const = 0, n_goals = 0, threads = 128, stages = 2, lanes = 1;
+  int n_const = 0, n_goals = 0, threads = 128, stages = 2, lanes = 1, phases = 1;
   int64_t baked_strip = 0;
   int nprogs = 0;
   std::vector<MultiModule> mods;
@@ -173,19 +173,61 @@ extern "C" int xslp_multi_create(const xslp_program *const *progs, int nprogs, i
   M->lanes = o.lane_words;
   M->nprogs = nprogs;
   M->baked_strip = o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0 ? o.block_bytes_hint / 8 : 0;
+  // input phases for wide codes (as the PIPE kernel's opts.phases; 0 = ceil(n/10) for n > 10)
+  int nph = o.phases == 0 ? std::min(8, (M->n_const / 8 + 9) / 10) : std::max(1, o.phases);
+  nph = std::min(nph, std::max(1, M->n_const / 8));
+  M->phases = nph;
+  std::vector<std::vector<Slp>> phased;  // phased[k][ph]
+  if (nph > 1) {
+    phased.resize(nprogs);
+    std::atomic<int> nx{0};
+    std::vector<std::string> perr(nprogs);
+    auto pwork = [&]() {
+      for (;;) {
+        int k = nx++;
+        if (k >= nprogs) return;
+        try {
+          phased[k] = phase_programs(evaluate(ps[k]->slp), M->n_const, nph, ps[k]->opts, nullptr);
+        } catch (const std::exception &e) {
+          perr[k] = e.what();
+        }
+      }
+    };
+    const int nt = (int)std::min<size_t>(nprogs, std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) th.emplace_back(pwork);
+    for (auto &t : th) t.join();
+    for (auto &e : perr)
+      if (!e.empty()) throw Error(XSLP_ECOMPILE, e);
+  }
   for (int a = 0; a < nprogs; a += per_module) {
     MultiModule m;
     m.first = a;
     m.count = std::min(per_module, nprogs - a);
-    std::vector<char> u(M->n_const, 0);
-    for (int i = a; i < a + m.count; ++i) {
-      for (auto &in : ps[i]->slp.ins)
-        for (int t : in.ops)
-          if (t < M->n_const) u[t] = 1;
-      for (int g : ps[i]->slp.goal)
-        if (g >= 0 && g < M->n_const) u[g] = 1;
+    // constants per stage fill: the union over the module's programs (per phase: the max)
+    auto count_used = [&](const std::vector<const Slp *> &v) {
+      std::vector<char> u(M->n_const, 0);
+      for (const Slp *q : v) {
+        for (auto &in : q->ins)
+          for (int t : in.ops)
+            if (t < M->n_const) u[t] = 1;
+        for (int g : q->goal)
+          if (g >= 0 && g < M->n_const) u[g] = 1;
+      }
+      return (int)std::count(u.begin(), u.end(), 1);
+    };
+    if (nph > 1) {
+      m.nused = 1;
+      for (int ph = 0; ph < nph; ++ph) {
+        std::vector<const Slp *> v;
+        for (int i = a; i < a + m.count; ++i) v.push_back(&phased[i][ph]);
+        m.nused = std::max(m.nused, count_used(v));
+      }
+    } else {
+      std::vector<const Slp *> v;
+      for (int i = a; i < a + m.count; ++i) v.push_back(&ps[i]->slp);
+      m.nused = count_used(v);
     }
-    m.nused = (int)std::count(u.begin(), u.end(), 1);
     M->mods.push_back(std::move(m));
   }
   // compile the modules on host threads
@@ -197,9 +239,19 @@ extern "C" int xslp_multi_create(const xslp_program *const *progs, int nprogs, i
       if (i >= (int)M->mods.size()) return;
       auto &m = M->mods[i];
       try {
-        std::vector<const Slp *> v;
-        for (int k = m.first; k < m.first + m.count; ++k) v.push_back(&ps[k]->slp);
-        std::string ptx = emit_ptx_multi(v, M->lanes, M->baked_strip, M->threads, M->stages);
+        std::string ptx;
+        if (nph > 1) {
+          std::vector<std::vector<const Slp *>> v;
+          for (int k = m.first; k < m.first + m.count; ++k) {
+            v.emplace_back();
+            for (auto &q : phased[k]) v.back().push_back(&q);
+          }
+          ptx = emit_ptx_multi_phases(v, M->lanes, M->baked_strip, M->threads, M->stages);
+        } else {
+          std::vector<const Slp *> v;
+          for (int k = m.first; k < m.first + m.count; ++k) v.push_back(&ps[k]->slp);
+          ptx = emit_ptx_multi(v, M->lanes, M->baked_strip, M->threads, M->stages);
+        }
         m.cubin = ptx_to_cubin(ptx, nullptr, nullptr, nullptr, nullptr, &m.regs, &m.spill);
       } catch (const std::exception &e) {
         errs[i] = e.what();

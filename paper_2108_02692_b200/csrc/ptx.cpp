@@ -590,6 +590,7 @@ struct Emitter {
     o << "  st.global" << vsuf() << " " << a << ", " << vec(r) << ";\n";
   }
   bool accumulate = false;
+  bool multi_acc = false;  // phased multi-program kernel: declare the accumulators
 
   void decls(int ntmp_guess) {
     o << "  .reg .pred %p<5>;\n  .reg .b32 %s<8>;\n  .reg .b64 %rd<8>;\n  .reg .b64 %off;\n";
@@ -603,7 +604,8 @@ struct Emitter {
     o << "  .reg .b32 %tps, %nt, %nct, %wid, %it, %tile, %lane, %st, %ph, %fb, %eb, %tw, %dst;\n";
     o << "  .reg .pred %pids, %pprod, %p5;\n  .reg .b32 %grp, %ltid, %pk, %pfirst, %t1, %chunk;\n";
     o << "  .reg .b64 %rpm;\n";
-    if (phases) o << "  .reg .b32 %acc<" << std::max<size_t>(1, full.goal.size() * L) << ">;\n";
+    if (phases || multi_acc)
+      o << "  .reg .b32 %acc<" << std::max<size_t>(1, full.goal.size() * L) << ">;\n";
     o << "  .reg .b32 %tx0;\n  .reg .b32 %y<8>;\n";
     int nq = 0;
     for (auto &in : cur().ins)
@@ -848,9 +850,148 @@ struct Emitter {
     o << "$DONE:\n  ret;\n";
   }
 
-  std::string run_multi(const std::vector<const Slp *> &progs) {
+  // Multi-program pipeline with input phases (wide codes): program k is given as P phase
+  // programs progs[k][ph] over contiguous input-block ranges.  A word-tile is streamed as P
+  // stage fills (phase ph's strips only); on each fill the consumers jump through phase ph's
+  // branch table to their stripe's phase program and XOR the goal partials into %acc, stored
+  // after the last phase.  The program index and output pointers are taken from the header of
+  // the tile's first fill into registers (that stage may be refilled before the last phase).
+  void body_multi_phases(int S, const std::vector<std::vector<const Slp *>> &progs) {
+    const int nc = full.n_const, P = (int)progs[0].size();
+    const int TC = threads, NCW = threads / 32;
+    std::vector<std::vector<char>> used(P, std::vector<char>(nc, 0));
+    std::vector<std::vector<int>> slot(P, std::vector<int>(nc, -1));
+    std::vector<int> nused(P, 0);
+    std::vector<char> blk(n_in, 0);
+    int maxused = 1;
+    for (int ph = 0; ph < P; ++ph) {
+      for (auto &pk : progs) {
+        const Slp *q = pk[ph];
+        for (auto &in : q->ins)
+          for (int t : in.ops)
+            if (t < nc) used[ph][t] = 1;
+        for (int g : q->goal)
+          if (g >= 0 && g < nc) used[ph][g] = 1;
+      }
+      for (int c = 0; c < nc; ++c)
+        if (used[ph][c]) { blk[c / 8] = 1; slot[ph][c] = nused[ph]++; }
+      maxused = std::max(maxused, nused[ph]);
+    }
+    const int rowb = 4 * L * TC;
+    const int64_t STAGE = (int64_t)maxused * rowb;
+    const int HS = multi_hs(n_out), ROWS = multi_rows(S, n_out);
+    pipe_barriers(S, NCW);
+    o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
+    o << "  ld.param.u64 %rd0, [p_ids];\n";
+    o << "  ld.param.u64 %rpm, [p_pos];\n  ld.param.u32 %pfirst, [p_first];\n";
+    // contiguous tile range of this CTA (see body_multi)
+    o << "  mov.u32 %nct, %nctaid.x;\n  add.u32 %chunk, %nt, %nct;\n  sub.u32 %chunk, %chunk, 1;\n";
+    o << "  div.u32 %chunk, %chunk, %nct;\n  mov.u32 %s0, %ctaid.x;\n";
+    o << "  mul.lo.u32 %s1, %s0, %chunk;\n  add.u32 %t1, %s1, %chunk;\n  min.u32 %t1, %t1, %nt;\n";
+    if (baked <= 0) {
+      o << "  ld.param.u64 %sk1, [p_strip];\n";
+      for (int k = 2; k < 8; ++k) o << "  mul.lo.u64 %sk" << k << ", %sk1, " << k << ";\n";
+    }
+    o << "  shr.u32 %wid, %s2, 5;\n  setp.eq.u32 %pprod, %wid, " << NCW << ";\n  @%pprod bra $PROD;\n";
+    // ---------------- consumers
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %s1;\n  mov.u32 %lane, %laneid;\n";
+    o << "$CLOOP:\n  setp.ge.u32 %p0, %tile, %t1;\n  @%p0 bra $DONE;\n";
+    o << "  rem.u32 %tw, %tile, %tps;\n  mad.lo.u32 %s3, %tw, " << TC << ", %s2;\n";
+    o << "  setp.lt.u32 %p5, %s3, %s4;\n  mul.wide.u32 %off, %s3, " << 4 * L << ";\n";
+    for (size_t g = 0; g < full.goal.size() * L; ++g) o << "  mov.b32 %acc" << g << ", 0;\n";
+    accumulate = true;
+    for (int ph = 0; ph < P; ++ph) {
+      const std::string x = std::to_string(ph);
+      consumer_wait(S, x);
+      if (ph == 0) {  // tile metadata from the first fill's header
+        o << "  mad.lo.u32 %dst, %st, " << HS << ", %sb;\n  add.u32 %dst, %dst, 128;\n";
+        o << "  ld.shared.u32 %pk, [%dst+4];\n";
+        for (int i = 0; i < n_out; ++i) {
+          o << "  ld.shared.u64 %ob" << i << ", [%dst+" << 8 + 8 * i << "];\n";
+          o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
+        }
+      }
+      o << "  @!%p5 bra $CSKIP" << x << ";\n";
+      o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
+      o << "  mad.lo.u32 %sth, %s2, " << 4 * L << ", %sth;\n";
+      o << "  $TBL" << x << ": .branchtargets ";
+      for (size_t k = 0; k < progs.size(); ++k) o << (k ? ", " : "") << "$K" << k << "_" << x;
+      o << ";\n  brx.idx %pk, $TBL" << x << ";\n";
+      for (size_t k = 0; k < progs.size(); ++k) {
+        sp = progs[k][ph];
+        o << "$K" << k << "_" << x << ":\n";
+        int tmp = 0;
+        compute(true, ROWS, slot[ph], used[ph], tmp);
+        o << "  bra.uni $CSKIP" << x << ";\n";
+      }
+      consumer_release(S, x);
+      o << "  add.u32 %it, %it, 1;\n";
+    }
+    accumulate = false;
+    sp = &full;
+    {
+      o << "  @!%p5 bra $CSTORED;\n";
+      int tmp = 0;
+      for (size_t g = 0; g < full.goal.size(); ++g) {
+        std::vector<std::string> r;
+        for (int l = 0; l < L; ++l) r.push_back("%acc" + std::to_string(g * L + l));
+        store((int)g, r, tmp);
+      }
+      o << "$CSTORED:\n";
+    }
+    o << "  add.u32 %tile, %tile, 1;\n  bra.uni $CLOOP;\n";
+    // ---------------- producer
+    int tmp = 0;
+    o << "$PROD:\n  mov.u32 %lane, %laneid;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $DONE;\n";
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %s1;\n";
+    o << "$PLOOP:\n  setp.ge.u32 %p0, %tile, %t1;\n  @%p0 bra $DONE;\n";
+    o << "  div.u32 %s5, %tile, %tps;\n  rem.u32 %tw, %tile, %tps;\n";
+    o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
+    o << "  mul.wide.u32 %rd6, %s5, 4;\n  add.s64 %rd6, %rpm, %rd6;\n  ld.global.nc.u32 %pk, [%rd6];\n";
+    o << "  sub.u32 %pk, %pk, %pfirst;\n";
+    o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+    for (int i = 0; i < n_out; ++i) o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+    o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
+    o << "  mul.lo.u32 %s7, %tw, " << TC << ";\n";
+    o << "  mul.wide.u32 %toff, %s7, " << 4 * L << ";\n";
+    for (int j = 0; j < n_in; ++j) {
+      if (!blk[j]) continue;
+      o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+      o << "  add.s64 %ib" << j << ", %ib" << j << ", %toff;\n";
+    }
+    o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << TC << ";\n  mul.lo.u32 %nb, %nb, " << 4 * L << ";\n";
+    for (int ph = 0; ph < P; ++ph) {
+      const std::string x = std::to_string(ph);
+      stage_regs(S);
+      producer_wait(S, "P" + x);
+      if (ph == 0) {
+        o << "  mad.lo.u32 %dst, %st, " << HS << ", %sb;\n  add.u32 %dst, %dst, 128;\n";
+        o << "  st.shared.u32 [%dst], %s5;\n  st.shared.u32 [%dst+4], %pk;\n";
+        for (int i = 0; i < n_out; ++i) o << "  st.shared.u64 [%dst+" << 8 + 8 * i << "], %ob" << i << ";\n";
+      }
+      o << "  mul.lo.u32 %s6, %nb, " << nused[ph] << ";\n";
+      o << "  mbarrier.arrive.expect_tx.shared::cta.b64 _, [%fb], %s6;\n";
+      o << "  mul.lo.u32 %dst, %st, " << STAGE << ";\n  add.u32 %dst, %dst, %sb;\n";
+      for (int c = 0; c < nc; ++c) {
+        if (!used[ph][c]) continue;
+        std::string a = addr("%ib" + std::to_string(c / 8), c % 8, tmp);
+        o << "  cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%dst+"
+          << ROWS + (int64_t)slot[ph][c] * rowb << "], " << a << ", %nb, [%fb];\n";
+      }
+      o << "  add.u32 %it, %it, 1;\n";
+    }
+    o << "  add.u32 %tile, %tile, 1;\n  bra.uni $PLOOP;\n";
+    o << "$DONE:\n  ret;\n";
+  }
+
+  // progs: one program per table entry; with input phases (phased non-empty) the entries'
+  // phase programs are phased[k][ph] and progs is unused by the body.
+  std::string run_multi(const std::vector<const Slp *> &progs,
+                        const std::vector<std::vector<const Slp *>> &phased = {}) {
     int mv = 0, mq = 0;
-    for (const Slp *q : progs) {
+    std::vector<const Slp *> all(progs);
+    for (auto &pk : phased) all.insert(all.end(), pk.begin(), pk.end());
+    for (const Slp *q : all) {
       mv = std::max(mv, q->n_vars);
       int nq = 0;
       for (auto &in : q->ins)
@@ -860,6 +1001,7 @@ struct Emitter {
     }
     decl_vars = mv;
     decl_nq = mq;
+    multi_acc = !phased.empty();
     o << "//\n// xslp multi-program pipeline kernel: " << progs.size() << " programs, "
       << full.n_const << " constants, " << full.goal.size() << " goals, lanes=" << L << "\n//\n";
     o << ".version 8.8\n.target sm_100a\n.address_size 64\n\n";
@@ -870,7 +1012,7 @@ struct Emitter {
          "  .param .u32 p_first)\n.maxntid "
       << threads + 32 << ", 1, 1\n{\n";
     decls(full.n_const + (int)full.goal.size() + 8);
-    body_multi(stages, progs);
+    if (phased.empty()) body_multi(stages, progs); else body_multi_phases(stages, phased);
     o << "}\n";
     return o.str();
   }
@@ -954,6 +1096,22 @@ std::string emit_ptx_multi(const std::vector<const Slp *> &progs, int lanes, int
     throw Error(XSLP_EINVAL, "device programs need whole blocks (n + m <= 128)");
   Emitter e(f, lanes, baked_strip, threads, 0, stages, XSLP_LAYOUT_STRIP, nullptr);
   return e.run_multi(progs);
+}
+
+std::string emit_ptx_multi_phases(const std::vector<std::vector<const Slp *>> &phased, int lanes,
+                                  int64_t baked_strip, int threads, int stages) {
+  if (phased.empty() || phased[0].empty()) throw Error(XSLP_EINVAL, "no programs");
+  const Slp &f = *phased[0][0];
+  for (auto &pk : phased) {
+    if (pk.size() != phased[0].size()) throw Error(XSLP_EINVAL, "programs disagree on phases");
+    for (const Slp *q : pk)
+      if (q->n_const != f.n_const || q->goal.size() != f.goal.size())
+        throw Error(XSLP_EINVAL, "programs disagree on constants/goals");
+  }
+  if (f.n_const % 8 || f.goal.size() % 8 || f.n_const / 8 + f.goal.size() / 8 > 128)
+    throw Error(XSLP_EINVAL, "device programs need whole blocks (n + m <= 128)");
+  Emitter e(f, lanes, baked_strip, threads, 0, stages, XSLP_LAYOUT_STRIP, nullptr);
+  return e.run_multi({}, phased);
 }
 
 std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, int *regs_tma,

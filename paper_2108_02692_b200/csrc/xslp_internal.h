@@ -127,10 +127,16 @@ std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, 
 std::vector<Slp> split_goals(const Slp &s, int k);
 // Micro-op code of the pipelined interpreter for consumer width T (interp.cu).
 std::vector<uint32_t> build_code32(const std::vector<uint16_t> &code, int T);
+// Input-phase programs of a goal set (capi.cpp; PIPE input phases and the phased multi kernel).
+std::vector<Slp> phase_programs(const std::vector<Bits> &want, int n_const, int nphases,
+                                const xslp_opts &o, int64_t *xor_total);
 // One persistent pipeline kernel (entry xslp_sl_multi) over several programs with the same
 // constants/goals, dispatching per stripe through a branch table.
 std::string emit_ptx_multi(const std::vector<const Slp *> &progs, int lanes, int64_t baked_strip,
                            int threads, int stages);
+// The same with input phases: phased[k][ph] = phase ph's program of table entry k.
+std::string emit_ptx_multi_phases(const std::vector<std::vector<const Slp *>> &phased, int lanes,
+                                  int64_t baked_strip, int threads, int stages);
 std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, int *regs_tma,
                                int *spill_tma, int *regs_pipe, int *spill_pipe);
 

@@ -245,6 +245,31 @@ def test_program_lifetime_no_stale_interpreter_pool():
         gc.collect()
 
 
+@pytest.mark.parametrize("phases,threads", [(0, 256), (1, 128), (3, 128)])
+def test_multi_program_decode_wide_code_phases(phases, threads):
+    # RS(20,4) per-stripe erasure patterns through the fused multi-program kernels, with input
+    # phases (auto = 2 for 20 blocks, or 3) and without; ragged last tile; against the oracle
+    n, p, B, S = 20, 4, 8192 + 1152, 14
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    pats = [tuple(synth.erasure_pattern(121, s, n + p, 4)) for s in range(S)]
+    uniq = sorted(set(pats))
+    progs = X.compile_many([X.xslp_decode_bitmatrix(g, n, p, er)[0] for er in uniq], specialise=0)
+    multi = X.Multi(progs, per_module=5, threads=threads, stages=2, phases=phases)
+    pos = [uniq.index(er) for er in pats]
+    ids, off = X.group_stripes(pos, len(progs))
+    din = dev_buf(S, n, B)
+    X.xslp_fill_random(din, S, n, B, seed=122)
+    out = torch.full((S, 4, B), 0x3C, dtype=torch.uint8, device="cuda")
+    X.xslp_multi_decode(multi, torch.tensor(pos, dtype=torch.int32, device="cuda"),
+                        torch.from_numpy(ids).cuda(), off, X.block_table(din, S, n, B),
+                        X.block_table(out, S, 4, B), B)
+    torch.cuda.synchronize()
+    for s in range(S):
+        rows = mx.decode_rows(og, n, list(pats[s]))[1]
+        assert (out[s].cpu().numpy() == rs.decode(rows, synth.stripe_data(122, s, n, B))).all(), s
+
+
 def test_edge_cases():
     n, p = 4, 2
     _, prog = compile_enc(n, p, "cauchy")
