@@ -73,7 +73,7 @@ WORKLOADS = {
                        "reading of BASELINE configs[4]), 1024 stripes x 1 MiB per GPU: the patterns' "
                        "programs fused into multi-program kernels with 2 input phases",
                   n=20, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=5,
-                  tuned=dict(kernel="multi", threads=256, stages=2)),
+                  tuned=dict(kernel="multi", threads=256, stages=2, per_module=8)),
     "xdec": dict(desc="RS(10,4) cross-GPU decode (SURVEY NEXT #4): the 14 blocks of each stripe "
                       "spread over the GPUs (block j of stripe s on rank (s+j) mod N), rank s mod N "
                       "decodes stripe s reading its survivors in place from local and NVLink-peer "
@@ -120,7 +120,7 @@ def parse():
     ap.add_argument("--lanes", type=int, default=None)
     ap.add_argument("--groups", type=int, default=None, help="PIPE consumer groups (goal split)")
     ap.add_argument("--phases", type=int, default=None, help="PIPE input phases (K-split)")
-    ap.add_argument("--per-module", type=int, default=20,
+    ap.add_argument("--per-module", type=int, default=None,
                     help="programs per fused multi-program kernel (--kernel multi)")
     ap.add_argument("--threads", type=int, default=None)
     ap.add_argument("--block-bytes", type=int, default=0, help="override block size")
@@ -380,6 +380,7 @@ def main():
     args.stages = args.stages or 2
     args.groups = args.groups or 1
     args.lanes = args.lanes or 1
+    args.per_module = args.per_module or 20
     if args.phases is None:            # 0 = the library's auto: ceil(n/10) input phases if n > 10
         args.phases = 0
     args.graph = int(args.graph or 0)
