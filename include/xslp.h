@@ -163,6 +163,15 @@ int xslp_decode_bitmatrix(const uint8_t *gf, int n, int p, const int32_t *erased
 int xslp_decode_bitmatrix_from(const uint8_t *gf, int n, int p, const int32_t *erased, int ne,
                                const int32_t *survivors, uint8_t *bits_out);
 
+/* Syndrome-form decode (a GPU restructuring of P:526-530, csrc/syndrome.cpp): with the
+ * parity-check matrix H = [R | I_p] of the systematic code, s = H c' over the codeword whose
+ * erased blocks are replaced by zero blocks equals H_E c_E, and c_E = H_E[J]^-1 s_J for e rows J
+ * of H with H_E[J] invertible.  syn_bits (may be NULL): (8p) x (8(n+p)), the lowering of H;
+ * solve_bits (may be NULL): (8ne) x (8p), the erased blocks (ascending) as XORs of the
+ * syndrome words.  gf must be systematic ([I_n; R]).  Errors as xslp_decode_bitmatrix. */
+int xslp_syndrome_bitmatrices(const uint8_t *gf, int n, int p, const int32_t *erased, int ne,
+                              uint8_t *syn_bits, uint8_t *solve_bits);
+
 /* ---- compile (host, untimed) ------------------------------------------------------- */
 
 /* bits: out_rows x in_cols (in_cols a multiple of 8, out_rows a multiple of 8, in_cols <= 512).

@@ -75,6 +75,8 @@ _sig = {
     "xslp_decode_bitmatrix": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int, _P, _P]),
     "xslp_decode_bitmatrix_from": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int,
                                                   _P, _P]),
+    "xslp_syndrome_bitmatrices": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int,
+                                                 _P, _P]),
     "xslp_peer_export": (ctypes.c_int, [_P, _P]),
     "xslp_peer_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "xslp_peer_close": (ctypes.c_int, [_P]),
@@ -258,6 +260,17 @@ def xslp_decode_bitmatrix_from(gf, n, p, erased, survivors):
     _check(_lib.xslp_decode_bitmatrix_from(gf.ctypes.data, n, p, er.ctypes.data if len(er) else None,
                                            len(er), sv.ctypes.data, out.ctypes.data))
     return out
+
+
+def xslp_syndrome_bitmatrices(gf, n, p, erased):
+    """(syndrome bitmatrix 8p x 8(n+p), solve bitmatrix 8e x 8p) of the syndrome-form decode."""
+    gf = np.ascontiguousarray(gf, dtype=np.uint8)
+    er = np.ascontiguousarray(list(erased), dtype=np.int32)
+    syn = np.zeros((8 * p, 8 * (n + p)), dtype=np.uint8)
+    sol = np.zeros((8 * len(er), 8 * p), dtype=np.uint8)
+    _check(_lib.xslp_syndrome_bitmatrices(gf.ctypes.data, n, p, er.ctypes.data, len(er),
+                                          syn.ctypes.data, sol.ctypes.data))
+    return syn, sol
 
 
 # ---- peer memory (cross-GPU decode) ---------------------------------------------------

@@ -414,3 +414,42 @@ def test_no_goal_program():
     prog = X.xslp_compile(bits, specialise=0)
     assert prog.stats()["n_goals"] == 0 and prog.stats()["xor_count"] == 0
     assert oslp.evaluate(prog.dump()) == []
+
+
+@pytest.mark.parametrize("n,p,kind", [(4, 2, "cauchy"), (10, 4, "isal"), (20, 4, "isal"), (8, 3, "sysvand")])
+def test_syndrome_decode_math_matches_the_codeword(n, p, kind):
+    # syndrome-form decode (csrc/syndrome.cpp): zero the erased blocks of an oracle codeword,
+    # apply the syndrome bitmatrix then the solve bitmatrix (plain GF(2) applies, oracle side):
+    # the erased blocks come back, for every erasure count 1..p and sampled patterns
+    from oracle import rs
+    import synth
+    g = X.xslp_coding_matrix(n, p, kind)
+    og = mx.coding_matrix(n, p, kind)
+    B = 64
+    data = synth.stripe_data(17, 0, n, B)
+    cw = np.concatenate([data, rs.encode(og, n, data)])
+    rng = np.random.default_rng(n * 31 + p)
+    for e in range(1, p + 1):
+        pats = list(itertools.combinations(range(n + p), e))
+        for er in [pats[i] for i in rng.choice(len(pats), min(40, len(pats)), replace=False)]:
+            syn, sol = X.xslp_syndrome_bitmatrices(g, n, p, er)
+            z = cw.copy()
+            z[list(er)] = 0
+            s = rs.bitmatrix_apply(syn, z)                 # 8p strips of syndrome
+            assert s.shape == (p, B)
+            got = rs.bitmatrix_apply(sol, s)
+            assert (got == cw[list(er)]).all(), er
+    with pytest.raises(X.XslpError):
+        X.xslp_syndrome_bitmatrices(g, n, p, list(range(p + 1)))
+
+
+def test_syndrome_of_a_codeword_is_zero():
+    from oracle import rs
+    import synth
+    n, p = 10, 4
+    g = X.xslp_coding_matrix(n, p)
+    og = mx.coding_matrix(n, p)
+    data = synth.stripe_data(18, 0, n, 128)
+    cw = np.concatenate([data, rs.encode(og, n, data)])
+    syn, _ = X.xslp_syndrome_bitmatrices(g, n, p, [0])
+    assert not rs.bitmatrix_apply(syn, cw).any()
