@@ -276,6 +276,17 @@ int xslp_multi_decode(const xslp_multi *multi, const int32_t *d_prog_of_stripe,
                       const int32_t *d_stripe_ids, const int32_t *group_offsets,
                       const uint8_t *const *d_in_tbl, uint8_t *const *d_out_tbl,
                       size_t block_bytes, void *stream);
+/* Heterogeneous decode in syndrome form (see xslp_syndrome_bitmatrices): one shared syndrome
+ * program over all n+p blocks of a stripe (compiled once, streamed in opts->phases input
+ * phases; 0 = ceil((n+p)/10)) followed by the stripe's pattern's small solve program, fused
+ * in the multi-program kernels; the result is a multi usable with xslp_multi_decode,
+ * xslp_multi_info and xslp_multi_free.  patterns: npat x ne erased block indices (each row any
+ * order, the outputs are the erased blocks ascending).  For xslp_multi_decode, d_in_tbl is
+ * [stripes][n+p]: every block of the stripe, the ERASED ones pointing at a zero block of
+ * block_bytes (any readable all-zero device buffer); d_out_tbl is [stripes][ne].  Same bytes
+ * as the M^-1 decode (the solution is unique).  gf must be systematic. */
+int xslp_syndrome_create(const uint8_t *gf, int n, int p, const int32_t *patterns, int npat, int ne,
+                         int per_module, const xslp_opts *opts, xslp_multi **out);
 /* modules, max registers / spill bytes per thread over the modules, host compile time. */
 int xslp_multi_info(const xslp_multi *multi, int32_t *modules, int32_t *regs, int32_t *spill_bytes,
                     double *compile_ms);

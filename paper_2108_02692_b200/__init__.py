@@ -102,6 +102,9 @@ _sig = {
     "xslp_multi_create": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(xslp_opts),
                                          ctypes.POINTER(_P)]),
     "xslp_multi_decode": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "xslp_syndrome_create": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int,
+                                            ctypes.c_int, ctypes.c_int, ctypes.POINTER(xslp_opts),
+                                            ctypes.POINTER(_P)]),
     "xslp_multi_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                        ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)]),
     "xslp_multi_free": (None, [_P]),
@@ -390,6 +393,22 @@ class Multi:
         if h and lib is not None:
             lib.xslp_multi_free(h)
             self._h = None
+
+
+class SyndromeDecoder(Multi):
+    """Heterogeneous decode in syndrome form (xslp_syndrome_create): the shared syndrome program
+    plus one small solve program per erasure pattern, fused; decode with xslp_multi_decode on
+    an input table of all n+p blocks per stripe (erased entries -> a zero block)."""
+
+    def __init__(self, gf, n, p, patterns, per_module=64, opts=None, **kw):   # noqa: super
+        self._progs = []
+        pats = np.ascontiguousarray([sorted(er) for er in patterns], dtype=np.int32)
+        g = np.ascontiguousarray(gf, dtype=np.uint8)
+        o = opts if opts is not None else default_opts(**kw)
+        h = _P()
+        _check(_lib.xslp_syndrome_create(g.ctypes.data, n, p, pats.ctypes.data, pats.shape[0],
+                                         pats.shape[1], per_module, ctypes.byref(o), ctypes.byref(h)))
+        self._h = h.value
 
 
 def xslp_multi_decode(multi, d_prog_of_stripe, d_stripe_ids, group_offsets, d_in_tbl, d_out_tbl,

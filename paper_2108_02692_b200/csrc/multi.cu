@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <set>
 #include <thread>
 
 #include "xslp_api.h"
@@ -252,6 +253,114 @@ extern "C" int xslp_multi_create(const xslp_program *const *progs, int nprogs, i
           for (int k = m.first; k < m.first + m.count; ++k) v.push_back(&ps[k]->slp);
           ptx = emit_ptx_multi(v, M->lanes, M->baked_strip, M->threads, M->stages);
         }
+        m.cubin = ptx_to_cubin(ptx, nullptr, nullptr, nullptr, nullptr, &m.regs, &m.spill);
+      } catch (const std::exception &e) {
+        errs[i] = e.what();
+      }
+    }
+  };
+  const int nt = (int)std::min<size_t>(M->mods.size(), std::max(1u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) th.emplace_back(work);
+  for (auto &t : th) t.join();
+  for (auto &e : errs)
+    if (!e.empty()) throw Error(XSLP_ECOMPILE, e);
+  M->compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  *out = reinterpret_cast<xslp_multi *>(M.release());
+  API_END
+}
+
+extern "C" int xslp_syndrome_create(const uint8_t *gf, int n, int p, const int32_t *patterns,
+                                    int npat, int ne, int per_module, const xslp_opts *opts,
+                                    xslp_multi **out) {
+  API_BEGIN
+  if (!out || !gf || !patterns || npat <= 0 || n < 1 || p < 1 || n + p > 255 || ne < 1)
+    throw Error(XSLP_EINVAL, "bad arguments");
+  if (ne > p) throw Error(XSLP_EUNRECOVERABLE, "more erasures than parity blocks");
+  *out = nullptr;
+  xslp_opts o;
+  if (opts) o = *opts; else xslp_default_opts(&o);
+  if (o.threads < 32 || o.threads > 992 || o.threads % 32) throw Error(XSLP_EINVAL, "bad threads");
+  if (o.stages < 2 || o.stages > 8) throw Error(XSLP_EINVAL, "stages must be 2..8");
+  if (o.lane_words != 1 && o.lane_words != 2 && o.lane_words != 4) throw Error(XSLP_EINVAL, "bad lane_words");
+  if (per_module <= 0) per_module = 64;  // solve programs are small: many per module
+  per_module = std::min(per_module, 256);
+  auto t0 = std::chrono::steady_clock::now();
+  auto M = std::make_unique<Multi>();
+  const int nb = n + p;
+  M->n_const = 8 * nb;
+  M->n_goals = 8 * ne;
+  M->threads = o.threads;
+  M->stages = o.stages;
+  M->lanes = o.lane_words;
+  M->nprogs = npat;
+  M->baked_strip = o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0 ? o.block_bytes_hint / 8 : 0;
+  int nph = o.phases == 0 ? std::min(8, (nb + 9) / 10) : std::max(1, o.phases);
+  nph = std::min(nph, nb);
+  M->phases = nph;
+  // the shared syndrome program (H over all n+p blocks), in input phases
+  auto h = parity_check(gf, n, p);
+  auto hb = gf::to_bits(h, p, nb);
+  std::vector<Bits> sgoals(8 * p, Bits(8 * nb));
+  for (int r = 0; r < 8 * p; ++r)
+    for (int c = 0; c < 8 * nb; ++c)
+      if (hb[(size_t)r * 8 * nb + c]) sgoals[r].set(c);
+  xslp_opts so = o;
+  so.specialise = 0;
+  auto syn = phase_programs(sgoals, 8 * nb, nph, so, nullptr);
+  // per-pattern solve programs (8e x 8p bitmatrices over the syndrome words)
+  std::vector<std::shared_ptr<Program>> solve(npat);
+  {
+    std::atomic<int> nx{0};
+    std::vector<std::string> perr(npat);
+    auto work = [&]() {
+      for (;;) {
+        int k = nx++;
+        if (k >= npat) return;
+        try {
+          std::set<int> es(patterns + (size_t)k * ne, patterns + (size_t)(k + 1) * ne);
+          if ((int)es.size() != ne || *es.begin() < 0 || *es.rbegin() >= nb)
+            throw Error(XSLP_EINVAL, "bad erasure pattern");
+          auto x = solve_rows(h, n, p, std::vector<int>(es.begin(), es.end()));
+          solve[k] = compile_bits(gf::to_bits(x, ne, p), 8 * ne, 8 * p, so);
+        } catch (const std::exception &e) {
+          perr[k] = e.what();
+        }
+      }
+    };
+    const int nt = (int)std::min<size_t>(npat, std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) th.emplace_back(work);
+    for (auto &t : th) t.join();
+    for (auto &e : perr)
+      if (!e.empty()) throw Error(XSLP_EINVAL, e);
+  }
+  int nused = 1;
+  for (auto &q : syn) {
+    std::vector<char> u(8 * nb, 0);
+    for (auto &in : q.ins)
+      for (int t : in.ops)
+        if (t < 8 * nb) u[t] = 1;
+    nused = std::max(nused, (int)std::count(u.begin(), u.end(), 1));
+  }
+  for (int a = 0; a < npat; a += per_module) {
+    MultiModule m;
+    m.first = a;
+    m.count = std::min(per_module, npat - a);
+    m.nused = nused;
+    M->mods.push_back(std::move(m));
+  }
+  std::atomic<int> next{0};
+  std::vector<std::string> errs(M->mods.size());
+  auto work = [&]() {
+    for (;;) {
+      int i = next++;
+      if (i >= (int)M->mods.size()) return;
+      auto &m = M->mods[i];
+      try {
+        std::vector<const Slp *> v;
+        for (int k = m.first; k < m.first + m.count; ++k) v.push_back(&solve[k]->slp);
+        std::string ptx = emit_ptx_syndrome(syn, v, ne, M->lanes, M->baked_strip, M->threads, M->stages);
         m.cubin = ptx_to_cubin(ptx, nullptr, nullptr, nullptr, nullptr, &m.regs, &m.spill);
       } catch (const std::exception &e) {
         errs[i] = e.what();

@@ -50,7 +50,11 @@ struct Emitter {
   const Slp &cur() const { return *sp; }
   int decl_vars = -1, decl_nq = -1;  // register declaration sizes when several programs share a body
 
-  std::string creg(int c, int l) { return "%c" + std::to_string(c * L + l); }
+  std::string creg(int c, int l) {
+    if (acc_consts) return "%acc" + std::to_string(c * L + l);  // syndrome solve: constants = %acc
+    return "%c" + std::to_string(c * L + l);
+  }
+  bool acc_consts = false;
   std::string vreg(int v, int l) { return "%v" + std::to_string(v * L + l); }
   std::string treg(int t, int l) { return t < cur().n_const ? creg(t, l) : vreg(t - cur().n_const, l); }
 
@@ -507,6 +511,7 @@ struct Emitter {
     const int rowb = 4 * L * threads;
     std::vector<char> loaded(nc, 0);
     auto need = [&](int c) {  // make constant c available in registers
+      if (acc_consts) return;   // already in %acc
       if (loaded[c]) return;
       loaded[c] = 1;
       std::vector<std::string> r;
@@ -984,6 +989,166 @@ struct Emitter {
     o << "$DONE:\n  ret;\n";
   }
 
+  // Syndrome-form decode (csrc/syndrome.cpp): every stripe runs the ONE syndrome program over
+  // all n+p blocks (erased ones read from a zero block), streamed in input phases with the
+  // syndrome words accumulated in %acc, then jumps through a branch table to its pattern's
+  // small solve program, whose constants are the %acc registers and whose goals (the erased
+  // blocks) are stored.  The shared code stays hot in the instruction cache; per pattern only
+  // the solve code (~e x p GF entries) differs.
+  void body_syndrome(int S, const std::vector<Slp> &syn, const std::vector<const Slp *> &solves) {
+    const int nc = full.n_const, P = (int)syn.size();
+    const int TC = threads, NCW = threads / 32;
+    std::vector<std::vector<char>> used(P, std::vector<char>(nc, 0));
+    std::vector<std::vector<int>> slot(P, std::vector<int>(nc, -1));
+    std::vector<int> nused(P, 0);
+    std::vector<char> blk(n_in, 0);
+    int maxused = 1;
+    for (int ph = 0; ph < P; ++ph) {
+      for (auto &in : syn[ph].ins)
+        for (int t : in.ops)
+          if (t < nc) used[ph][t] = 1;
+      for (int g : syn[ph].goal)
+        if (g >= 0 && g < nc) used[ph][g] = 1;
+      for (int c = 0; c < nc; ++c)
+        if (used[ph][c]) { blk[c / 8] = 1; slot[ph][c] = nused[ph]++; }
+      maxused = std::max(maxused, nused[ph]);
+    }
+    const int rowb = 4 * L * TC;
+    const int64_t STAGE = (int64_t)maxused * rowb;
+    const int HS = multi_hs(n_out), ROWS = multi_rows(S, n_out);
+    const int nsyn = (int)full.goal.size();  // syndrome words (8p)
+    pipe_barriers(S, NCW);
+    o << "  ld.param.u32 %s4, [p_words];\n  ld.param.u32 %tps, [p_tps];\n  ld.param.u32 %nt, [p_ntiles];\n";
+    o << "  ld.param.u64 %rd0, [p_ids];\n";
+    o << "  ld.param.u64 %rpm, [p_pos];\n  ld.param.u32 %pfirst, [p_first];\n";
+    o << "  mov.u32 %nct, %nctaid.x;\n  add.u32 %chunk, %nt, %nct;\n  sub.u32 %chunk, %chunk, 1;\n";
+    o << "  div.u32 %chunk, %chunk, %nct;\n  mov.u32 %s0, %ctaid.x;\n";
+    o << "  mul.lo.u32 %s1, %s0, %chunk;\n  add.u32 %t1, %s1, %chunk;\n  min.u32 %t1, %t1, %nt;\n";
+    if (baked <= 0) {
+      o << "  ld.param.u64 %sk1, [p_strip];\n";
+      for (int k = 2; k < 8; ++k) o << "  mul.lo.u64 %sk" << k << ", %sk1, " << k << ";\n";
+    }
+    o << "  shr.u32 %wid, %s2, 5;\n  setp.eq.u32 %pprod, %wid, " << NCW << ";\n  @%pprod bra $PROD;\n";
+    // ---------------- consumers
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %s1;\n  mov.u32 %lane, %laneid;\n";
+    o << "$CLOOP:\n  setp.ge.u32 %p0, %tile, %t1;\n  @%p0 bra $DONE;\n";
+    o << "  rem.u32 %tw, %tile, %tps;\n  mad.lo.u32 %s3, %tw, " << TC << ", %s2;\n";
+    o << "  setp.lt.u32 %p5, %s3, %s4;\n  mul.wide.u32 %off, %s3, " << 4 * L << ";\n";
+    for (int g = 0; g < nsyn * L; ++g) o << "  mov.b32 %acc" << g << ", 0;\n";
+    accumulate = true;
+    for (int ph = 0; ph < P; ++ph) {
+      const std::string x = std::to_string(ph);
+      consumer_wait(S, x);
+      if (ph == 0) {
+        o << "  mad.lo.u32 %dst, %st, " << HS << ", %sb;\n  add.u32 %dst, %dst, 128;\n";
+        o << "  ld.shared.u32 %pk, [%dst+4];\n";
+        for (int i = 0; i < n_out; ++i) {
+          o << "  ld.shared.u64 %ob" << i << ", [%dst+" << 8 + 8 * i << "];\n";
+          o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
+        }
+      }
+      o << "  @!%p5 bra $CSKIP" << x << ";\n";
+      o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
+      o << "  mad.lo.u32 %sth, %s2, " << 4 * L << ", %sth;\n";
+      sp = &syn[ph];
+      int tmp = 0;
+      compute(true, ROWS, slot[ph], used[ph], tmp);
+      consumer_release(S, x);
+      o << "  add.u32 %it, %it, 1;\n";
+    }
+    accumulate = false;
+    // the pattern's solve program on the syndrome words
+    o << "  @!%p5 bra $CSOLVED;\n";
+    o << "  $TBL: .branchtargets ";
+    for (size_t k = 0; k < solves.size(); ++k) o << (k ? ", " : "") << "$K" << k;
+    o << ";\n  brx.idx %pk, $TBL;\n";
+    acc_consts = true;
+    for (size_t k = 0; k < solves.size(); ++k) {
+      sp = solves[k];
+      o << "$K" << k << ":\n";
+      int tmp = 0;
+      std::vector<int> noslot(nsyn, -1);
+      std::vector<char> nouse(nsyn, 0);
+      compute(false, 0, noslot, nouse, tmp);
+      o << "  bra.uni $CSOLVED;\n";
+    }
+    acc_consts = false;
+    sp = &full;
+    o << "$CSOLVED:\n  add.u32 %tile, %tile, 1;\n  bra.uni $CLOOP;\n";
+    // ---------------- producer
+    int tmp = 0;
+    o << "$PROD:\n  mov.u32 %lane, %laneid;\n  setp.ne.u32 %p4, %lane, 0;\n  @%p4 bra $DONE;\n";
+    o << "  mov.u32 %it, 0;\n  mov.u32 %tile, %s1;\n";
+    o << "$PLOOP:\n  setp.ge.u32 %p0, %tile, %t1;\n  @%p0 bra $DONE;\n";
+    o << "  div.u32 %s5, %tile, %tps;\n  rem.u32 %tw, %tile, %tps;\n";
+    o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
+    o << "  mul.wide.u32 %rd6, %s5, 4;\n  add.s64 %rd6, %rpm, %rd6;\n  ld.global.nc.u32 %pk, [%rd6];\n";
+    o << "  sub.u32 %pk, %pk, %pfirst;\n";
+    o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+    for (int i = 0; i < n_out; ++i) o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+    o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
+    o << "  mul.lo.u32 %s7, %tw, " << TC << ";\n";
+    o << "  mul.wide.u32 %toff, %s7, " << 4 * L << ";\n";
+    for (int j = 0; j < n_in; ++j) {
+      if (!blk[j]) continue;
+      o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+      o << "  add.s64 %ib" << j << ", %ib" << j << ", %toff;\n";
+    }
+    o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << TC << ";\n  mul.lo.u32 %nb, %nb, " << 4 * L << ";\n";
+    for (int ph = 0; ph < P; ++ph) {
+      const std::string x = std::to_string(ph);
+      stage_regs(S);
+      producer_wait(S, "P" + x);
+      if (ph == 0) {
+        o << "  mad.lo.u32 %dst, %st, " << HS << ", %sb;\n  add.u32 %dst, %dst, 128;\n";
+        o << "  st.shared.u32 [%dst], %s5;\n  st.shared.u32 [%dst+4], %pk;\n";
+        for (int i = 0; i < n_out; ++i) o << "  st.shared.u64 [%dst+" << 8 + 8 * i << "], %ob" << i << ";\n";
+      }
+      o << "  mul.lo.u32 %s6, %nb, " << nused[ph] << ";\n";
+      o << "  mbarrier.arrive.expect_tx.shared::cta.b64 _, [%fb], %s6;\n";
+      o << "  mul.lo.u32 %dst, %st, " << STAGE << ";\n  add.u32 %dst, %dst, %sb;\n";
+      for (int c = 0; c < nc; ++c) {
+        if (!used[ph][c]) continue;
+        std::string a = addr("%ib" + std::to_string(c / 8), c % 8, tmp);
+        o << "  cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%dst+"
+          << ROWS + (int64_t)slot[ph][c] * rowb << "], " << a << ", %nb, [%fb];\n";
+      }
+      o << "  add.u32 %it, %it, 1;\n";
+    }
+    o << "  add.u32 %tile, %tile, 1;\n  bra.uni $PLOOP;\n";
+    o << "$DONE:\n  ret;\n";
+  }
+
+  std::string run_syndrome(const std::vector<Slp> &syn, const std::vector<const Slp *> &solves) {
+    int mv = 0, mq = 0;
+    std::vector<const Slp *> all(solves);
+    for (auto &q : syn) all.push_back(&q);
+    for (const Slp *q : all) {
+      mv = std::max(mv, q->n_vars);
+      int nq = 0;
+      for (auto &in : q->ins)
+        for (int t : in.ops)
+          if (t < q->n_const) ++nq;
+      mq = std::max(mq, nq);
+    }
+    decl_vars = mv;
+    decl_nq = mq;
+    multi_acc = true;
+    o << "//\n// xslp syndrome-form decode kernel: " << solves.size() << " patterns, "
+      << full.n_const << " constants, " << full.goal.size() << " syndrome words\n//\n";
+    o << ".version 8.8\n.target sm_100a\n.address_size 64\n\n";
+    o << ".extern .shared .align 128 .b8 dsm[];\n\n";
+    o << ".visible .entry xslp_sl_multi(\n  .param .u64 p_in,\n  .param .u64 p_out,\n"
+         "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
+         "  .param .u32 p_tps,\n  .param .u32 p_ntiles,\n  .param .u64 p_pos,\n"
+         "  .param .u32 p_first)\n.maxntid "
+      << threads + 32 << ", 1, 1\n{\n";
+    decls(full.n_const + (int)full.goal.size() + 8);
+    body_syndrome(stages, syn, solves);
+    o << "}\n";
+    return o.str();
+  }
+
   // progs: one program per table entry; with input phases (phased non-empty) the entries'
   // phase programs are phased[k][ph] and progs is unused by the body.
   std::string run_multi(const std::vector<const Slp *> &progs,
@@ -1112,6 +1277,19 @@ std::string emit_ptx_multi_phases(const std::vector<std::vector<const Slp *>> &p
     throw Error(XSLP_EINVAL, "device programs need whole blocks (n + m <= 128)");
   Emitter e(f, lanes, baked_strip, threads, 0, stages, XSLP_LAYOUT_STRIP, nullptr);
   return e.run_multi({}, phased);
+}
+
+std::string emit_ptx_syndrome(const std::vector<Slp> &syn, const std::vector<const Slp *> &solves,
+                              int n_out, int lanes, int64_t baked_strip, int threads, int stages) {
+  if (syn.empty() || solves.empty()) throw Error(XSLP_EINVAL, "no programs");
+  for (const Slp *q : solves)
+    if (q->n_const != (int)syn[0].goal.size() || (int)q->goal.size() != 8 * n_out)
+      throw Error(XSLP_EINVAL, "solve programs do not match the syndrome");
+  if (syn[0].n_const % 8 || syn[0].goal.size() % 8 || syn[0].n_const / 8 + n_out > 128)
+    throw Error(XSLP_EINVAL, "device programs need whole blocks (n + p + e <= 128)");
+  Emitter e(syn[0], lanes, baked_strip, threads, 0, stages, XSLP_LAYOUT_STRIP, nullptr);
+  e.n_out = n_out;  // outputs are the erased blocks, not the syndrome
+  return e.run_syndrome(syn, solves);
 }
 
 std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, int *regs_tma,

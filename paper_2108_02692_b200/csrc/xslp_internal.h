@@ -134,6 +134,16 @@ std::vector<Slp> phase_programs(const std::vector<Bits> &want, int n_const, int 
 // constants/goals, dispatching per stripe through a branch table.
 std::string emit_ptx_multi(const std::vector<const Slp *> &progs, int lanes, int64_t baked_strip,
                            int threads, int stages);
+// bitmatrix -> compiled program (capi.cpp)
+std::shared_ptr<Program> compile_bits(const std::vector<uint8_t> &bits, int out_rows, int in_cols,
+                                      const xslp_opts &o);
+// syndrome-form decode math (syndrome.cpp)
+std::vector<uint8_t> parity_check(const uint8_t *g, int n, int p);
+std::vector<uint8_t> solve_rows(const std::vector<uint8_t> &h, int n, int p, const std::vector<int> &er);
+// Syndrome-form decode kernel (entry xslp_sl_multi): the shared syndrome program in input
+// phases `syn`, then per-pattern solve programs (constants = the 8p syndrome words).
+std::string emit_ptx_syndrome(const std::vector<Slp> &syn, const std::vector<const Slp *> &solves,
+                              int n_out, int lanes, int64_t baked_strip, int threads, int stages);
 // The same with input phases: phased[k][ph] = phase ph's program of table entry k.
 std::string emit_ptx_multi_phases(const std::vector<std::vector<const Slp *>> &phased, int lanes,
                                   int64_t baked_strip, int threads, int stages);

@@ -270,6 +270,45 @@ def test_multi_program_decode_wide_code_phases(phases, threads):
         assert (out[s].cpu().numpy() == rs.decode(rows, synth.stripe_data(122, s, n, B))).all(), s
 
 
+@pytest.mark.parametrize("n,p,kind,e,phases", [(10, 4, "isal", 4, 0), (20, 4, "isal", 4, 0),
+                                                (4, 2, "cauchy", 2, 0), (10, 4, "isal", 2, 0),
+                                                (10, 4, "isal", 4, 1), (8, 3, "sysvand", 3, 3)])
+def test_syndrome_form_decode(n, p, kind, e, phases):
+    # heterogeneous decode in syndrome form: every stripe's full block table (erased entries ->
+    # one zero block), the shared syndrome program then the pattern's solve program; the erased
+    # blocks of real codewords come back, and the bytes equal the oracle's decode
+    B, S = 8192 + 1152, 11
+    og = mx.coding_matrix(n, p, kind)
+    g = X.xslp_coding_matrix(n, p, kind)
+    pats = [tuple(synth.erasure_pattern(131 + e, s, n + p, e)) for s in range(S)]
+    uniq = sorted(set(pats))
+    dec = X.SyndromeDecoder(g, n, p, uniq, per_module=4, threads=128, stages=2, phases=phases)
+    allb = dev_buf(S, n + p, B)
+    X.xslp_fill_random(allb, S, n + p, B, seed=132)
+    _, enc = compile_enc(n, p, kind)
+    t = X.block_table(allb, S, n + p, B).view(S, n + p)
+    X.xslp_encode_batch(enc, t[:, :n].contiguous(), t[:, n:].contiguous(), S, B)
+    zero = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    tin = t.clone()
+    for s, er in enumerate(pats):
+        for j in er:
+            tin[s, j] = zero.data_ptr()
+    out = torch.full((S, e, B), 0x66, dtype=torch.uint8, device="cuda")
+    pos = [uniq.index(er) for er in pats]
+    ids, off = X.group_stripes(pos, len(uniq))
+    X.xslp_multi_decode(dec, torch.tensor(pos, dtype=torch.int32, device="cuda"),
+                        torch.from_numpy(ids).cuda(), off, tin.reshape(-1),
+                        X.block_table(out, S, e, B), B)
+    torch.cuda.synchronize()
+    for s, er in enumerate(pats):
+        assert torch.equal(out[s], allb[s, list(er)]), (s, er)
+    for s in (0, S - 1):                       # the oracle's decode of the same survivors
+        d = synth.stripe_data(132, s, n, B)
+        blocks = np.concatenate([d, rs.encode(og, n, d)])
+        surv, rows = mx.decode_rows(og, n, list(pats[s]))
+        assert (out[s].cpu().numpy() == rs.decode(rows, blocks[surv])).all()
+
+
 def test_edge_cases():
     n, p = 4, 2
     _, prog = compile_enc(n, p, "cauchy")
