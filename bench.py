@@ -111,7 +111,7 @@ def parse():
     ap.add_argument("--compress", default="xorrepair", choices=["none", "repair", "xorrepair"])
     ap.add_argument("--kernel", default=None,
                     choices=["auto", "straight", "interp", "tma", "pipe", "grouped", "grouped_tma",
-                             "grouped_pipe", "multi", "gftable"])
+                             "grouped_pipe", "multi", "gftable", "syndrome"])
     ap.add_argument("--stages", type=int, default=None)
     ap.add_argument("--streams", type=int, default=8, help="internal streams for grouped decode")
     ap.add_argument("--xmode", default="peer", choices=["peer", "staged"],
@@ -336,7 +336,7 @@ def kernel_name(args, wl, stats):
         return "xslp_sl_tma"
     if k in ("pipe", "grouped_pipe"):
         return "xslp_sl_pipe"
-    if k == "multi":
+    if k in ("multi", "syndrome"):
         return "xslp_sl_multi"
     if k == "gftable":
         return "xslp_gftable_kernel"
@@ -380,6 +380,7 @@ def main():
     args.stages = args.stages or 2
     args.groups = args.groups or 1
     args.lanes = args.lanes or 1
+    args.per_module_raw = args.per_module
     args.per_module = args.per_module or 20
     if args.phases is None:            # 0 = the library's auto: ceil(n/10) input phases if n > 10
         args.phases = 0
@@ -422,7 +423,13 @@ def main():
         uniq = sorted(set(pats))
         dec = [X.xslp_decode_bitmatrix(G, n, p, er) for er in uniq]
         mode = "grouped" if args.kernel == "auto" else args.kernel
-        if mode == "multi":     # fused multi-program pipeline kernels (branch table per stripe)
+        if mode == "syndrome":  # shared syndrome program + per-pattern solve programs, fused
+            progs = uniq
+            multi = X.SyndromeDecoder(G, n, p, uniq, per_module=args.per_module_raw or 64,
+                                      threads=args.threads, stages=args.stages,
+                                      lane_words=args.lanes, block_bytes_hint=B, phases=args.phases)
+            log("syndrome", multi.info())
+        elif mode == "multi":   # fused multi-program pipeline kernels (branch table per stripe)
             progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,
                                    threads=args.threads)
             multi = X.Multi(progs, per_module=args.per_module, threads=args.threads,
@@ -527,6 +534,19 @@ def main():
                             stream=stream)
         ti = tall[:, torch.as_tensor(_surv, dtype=torch.long)].contiguous().view(-1)
         erased_idx = torch.as_tensor(erased, dtype=torch.long)
+    elif wl["op"] == "decode_multi" and mode == "syndrome":
+        # whole codewords [S][n+p] (untimed encode); erased entries of the table -> a zero block
+        din = torch.empty((S, n + p, B), dtype=torch.uint8, device="cuda")
+        X.xslp_fill_random(din, S, n + p, B, seed=wl["seed"], stripe0=stripe0)
+        tall = X.block_table(din, S, n + p, B).view(S, n + p)
+        enc = X.xslp_compile(X.xslp_encode_bitmatrix(G, n, p), block_bytes_hint=B)
+        X.xslp_encode_batch(enc, tall[:, :n].contiguous(), tall[:, n:].contiguous(), S, B,
+                            stream=stream)
+        zero_block = torch.zeros(B, dtype=torch.uint8, device="cuda")
+        th = tall.cpu().numpy().copy()
+        for s_, er in enumerate(pats):
+            th[s_, list(er)] = zero_block.data_ptr()
+        ti = torch.from_numpy(th.reshape(-1)).cuda()
     else:
         din = torch.empty((S, n_in, B), dtype=torch.uint8, device="cuda")
         X.xslp_fill_random(din, S, n_in, B, seed=wl["seed"], stripe0=stripe0)
@@ -551,7 +571,7 @@ def main():
             pdec.launch(stream=st, nstreams=args.streams)
         elif wl["op"] == "encode_gft":
             X.xslp_gf_table_apply(coef_rows, ti, to, S, B, stream=st)
-        elif wl["op"] == "decode_multi" and mode == "multi":
+        elif wl["op"] == "decode_multi" and mode in ("multi", "syndrome"):
             X.xslp_multi_decode(multi, idx, gids, goff, ti, to, B, stream=st)
         elif wl["op"] == "decode_multi" and mode == "interp":
             X.xslp_decode_batch_multi(progs, idx, ti, to, S, B, stream=st)
@@ -578,6 +598,10 @@ def main():
     elif wl["op"] in ("decode_one", "decode_sharded"):
         if not torch.equal(dout, din[:, erased_idx]):
             raise SystemExit("sanity check failed: decoded blocks != the erased blocks")
+    elif wl["op"] == "decode_multi" and mode == "syndrome":
+        for s_ in (0, S // 2, S - 1):
+            if not torch.equal(dout[s_], din[s_, list(pats[s_])]):
+                raise SystemExit(f"sanity check failed: syndrome decode of stripe {s_}")
     elif wl["op"] == "decode_peer":       # regenerate a few home codewords locally and compare
         chk = plan.stripes[:2] + plan.stripes[-2:]
         full = torch.empty((1, n + p, B), dtype=torch.uint8, device="cuda")
@@ -709,9 +733,10 @@ def main():
                 "scaling": "strong" if wl["op"] in SHARDED else "weak", "vs_baseline": None,
                 "dtype": "u32", "data": "synthetic",
                 "config": dict(config_of(args, wl, stats),
-                               **({"multi": multi.info(), "per_module": args.per_module,
-                                   "patterns": len(progs)}
-                                  if wl["op"] == "decode_multi" and mode == "multi" else {})),
+                               **({"multi": multi.info(), "patterns": len(progs),
+                                   "per_module": args.per_module_raw or (64 if mode == "syndrome" else 20)}
+                                  if wl["op"] == "decode_multi" and mode in ("multi", "syndrome")
+                                  else {})),
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
                 "compile_s": round(compile_s, 3),
