@@ -46,12 +46,13 @@ WORKLOADS = {
                   n=10, p=4, B=MiB, S=1024, op="encode_gft", seed=2,
                   tuned=dict(kernel="gftable", threads=256, stages=2)),
     "cfg3": dict(desc="RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures, "
-                      "the distinct patterns' programs fused into persistent multi-program pipeline kernels "
-                      "(branch table per stripe, 20 programs per kernel); --kernel grouped: one "
-                      "straight-line kernel per pattern over internal streams; --kernel interp: "
-                      "one interpreter launch (BASELINE configs[2])",
+                      "syndrome form: one shared syndrome program over all 14 blocks (erased ones read from a "
+                      "zero block) + a small solve program per pattern, fused with a branch table "
+                      "(32 patterns per kernel); --kernel multi: the patterns' M^-1 programs fused; "
+                      "--kernel grouped: one straight-line kernel per pattern; --kernel interp "
+                      "(BASELINE configs[2])",
                  n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3,
-                 tuned=dict(kernel="multi", threads=256, stages=2)),
+                 tuned=dict(kernel="syndrome", threads=256, stages=2, per_module=32)),
     "pdec": dict(desc="RS(10,4) decode of the paper's P_dec pattern {2,4,5,6} (P:1670) on every "
                       "stripe, 1024 stripes x 1 MiB",
                  n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3,
@@ -70,10 +71,11 @@ WORKLOADS = {
                   n=20, p=4, B=MiB, S=8192, op="decode_sharded", e=4, seed=5, chunk=2048,
                   tuned=dict(kernel="pipe", threads=256, stages=2, phases=2)),
     "cfg5h": dict(desc="RS(20,4) decode with per-stripe seeded 4-of-24 erasures (the secondary "
-                       "reading of BASELINE configs[4]), 1024 stripes x 1 MiB per GPU: the patterns' "
-                       "programs fused into multi-program kernels with 2 input phases",
+                       "reading of BASELINE configs[4]), 1024 stripes x 1 MiB per GPU: syndrome form (shared "
+                       "syndrome program over 24 blocks in 3 input phases + per-pattern solve "
+                       "programs, 16 per kernel); --kernel multi: the M^-1 programs fused",
                   n=20, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=5,
-                  tuned=dict(kernel="multi", threads=256, stages=2, per_module=8)),
+                  tuned=dict(kernel="syndrome", threads=128, stages=2, per_module=16)),
     "xdec": dict(desc="RS(10,4) cross-GPU decode (SURVEY NEXT #4): the 14 blocks of each stripe "
                       "spread over the GPUs (block j of stripe s on rank (s+j) mod N), rank s mod N "
                       "decodes stripe s reading its survivors in place from local and NVLink-peer "
@@ -350,7 +352,8 @@ def config_of(args, wl, stats):
          "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": args.compress + ("+fuse" if args.fuse else "") + ("+dfs" if args.schedule else ""),
          "kernel": args.kernel, "lane_words": args.lanes, "threads": args.threads,
          "stages": args.stages, "groups": args.groups,
-         "phases": args.phases or (-(-wl["n"] // 10) if wl["n"] > 10 else 1),
+         "phases": args.phases or (-(-(wl["n"] + wl["p"]) // 10) if args.kernel == "syndrome" else
+                                   (-(-wl["n"] // 10) if wl["n"] > 10 else 1)),
          "cuda_graph": bool(args.graph),
          "l2": "inputs larger than the 126 MB L2; no flush between steps",
          "parallelism": (f"blocks spread over {args.gpus} GPU(s); survivors read in place over "
@@ -446,7 +449,7 @@ def main():
                                    stages=args.stages,
                                    kernel={"tma": "tma", "grouped_tma": "tma", "pipe": "pipe",
                                            "grouped_pipe": "pipe"}.get(mode, "straight"))
-        prog = progs[0]
+        prog = progs[0] if mode != "syndrome" else None
         m_out = wl["e"]
     elif wl["op"] == "decode_peer":
         import synth
@@ -461,7 +464,7 @@ def main():
         progs = peer.compile_plan(X, G, plan, compress=args.compress, threads=args.threads,
                                   lane_words=args.lanes, block_bytes_hint=B, stages=args.stages,
                                   kernel="straight")
-        prog = progs[0]
+        prog = progs[0] if mode != "syndrome" else None
         m_out = plan.e
     elif wl["op"] in ("decode_one", "decode_sharded"):
         erased = erased_of(wl)
