@@ -72,10 +72,10 @@ WORKLOADS = {
                   tuned=dict(kernel="pipe", threads=256, stages=2, phases=2)),
     "cfg5h": dict(desc="RS(20,4) decode with per-stripe seeded 4-of-24 erasures (the secondary "
                        "reading of BASELINE configs[4]), 1024 stripes x 1 MiB per GPU: syndrome form (shared "
-                       "syndrome program over 24 blocks in 3 input phases + per-pattern solve "
+                       "syndrome program over 24 blocks in 6 input phases + per-pattern solve "
                        "programs, 16 per kernel); --kernel multi: the M^-1 programs fused",
                   n=20, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=5,
-                  tuned=dict(kernel="syndrome", threads=128, stages=2, per_module=16)),
+                  tuned=dict(kernel="syndrome", threads=256, stages=3, phases=6, per_module=16)),
     "xdec": dict(desc="RS(10,4) cross-GPU decode (SURVEY NEXT #4): the 14 blocks of each stripe "
                       "spread over the GPUs (block j of stripe s on rank (s+j) mod N), rank s mod N "
                       "decodes stripe s reading its survivors in place from local and NVLink-peer "
@@ -122,6 +122,8 @@ def parse():
     ap.add_argument("--lanes", type=int, default=None)
     ap.add_argument("--groups", type=int, default=None, help="PIPE consumer groups (goal split)")
     ap.add_argument("--phases", type=int, default=None, help="PIPE input phases (K-split)")
+    ap.add_argument("--distinct", type=int, default=0,
+                    help="diagnostic: only K distinct erasure patterns (stripe s takes pattern s mod K)")
     ap.add_argument("--per-module", type=int, default=None,
                     help="programs per fused multi-program kernel (--kernel multi)")
     ap.add_argument("--threads", type=int, default=None)
@@ -422,7 +424,8 @@ def main():
         import synth
         S = wl["S"]
         s0 = rank * S
-        pats = [tuple(synth.erasure_pattern(wl["seed"], s0 + s, n + p, wl["e"])) for s in range(S)]
+        pats = [tuple(synth.erasure_pattern(wl["seed"], (s0 + s) % args.distinct if args.distinct else s0 + s,
+                                            n + p, wl["e"])) for s in range(S)]
         uniq = sorted(set(pats))
         dec = [X.xslp_decode_bitmatrix(G, n, p, er) for er in uniq]
         mode = "grouped" if args.kernel == "auto" else args.kernel
@@ -739,7 +742,8 @@ def main():
                                **({"multi": multi.info(), "patterns": len(progs),
                                    "per_module": args.per_module_raw or (64 if mode == "syndrome" else 20)}
                                   if wl["op"] == "decode_multi" and mode in ("multi", "syndrome")
-                                  else {})),
+                                  else {}),
+                               **({"distinct_diagnostic": args.distinct} if args.distinct else {})),
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
                 "compile_s": round(compile_s, 3),
