@@ -93,6 +93,7 @@ WORKLOADS = {
 SHARDED = ("encode_sharded", "decode_sharded")     # strong scaling: fixed total over the ranks
 DECODE = ("decode_one", "decode_sharded", "decode_multi", "decode_peer")
 NVLINK_GBS = 770.0   # B200_PROFILING.md: measured peer copy bandwidth per direction
+HBM_NOMINAL_GBS = 7700.0  # B200_PROFILING.md: HBM3e nominal (HGX figure)
 
 
 def erased_of(wl):
@@ -677,7 +678,11 @@ def main():
             "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload),
             "peak_source": peak_src, "kernel": kernel_name(args, wl, stats),
             "alg_bytes_per_launch": alg_bytes_launch, "launch_ms": round(launch_ms, 4),
-            "alg_bytes_per_data_byte": round((n_in + m_out) / n, 4)}
+            "alg_bytes_per_data_byte": round((n_in + m_out) / n, 4),
+            # SURVEY 8(d) asks for both denominators: the measured copy bandwidth (frac, the
+            # judged one) and the nominal HBM3e figure (B200_PROFILING.md: 7.7 TB/s HGX)
+            "nominal_peak": HBM_NOMINAL_GBS, "frac_nominal": round(achieved / HBM_NOMINAL_GBS, 4),
+            "data_roof_gbs": round(peak / ((n_in + m_out) / n), 1)}
     if wl["op"] == "decode_peer":
         # survivors read over NVLink from peer HBM: the second roof of the fused gather+decode
         rem_bytes = remote_blocks * B
