@@ -94,6 +94,8 @@ SHARDED = ("encode_sharded", "decode_sharded")     # strong scaling: fixed total
 DECODE = ("decode_one", "decode_sharded", "decode_multi", "decode_peer")
 NVLINK_GBS = 770.0   # B200_PROFILING.md: measured peer copy bandwidth per direction
 HBM_NOMINAL_GBS = 7700.0  # B200_PROFILING.md: HBM3e nominal (HGX figure)
+ALU_LANE_OPS_PER_CLK_SM = 64  # measured: scripts/alu_probe.cu (LOP3 and PRMT alike)
+NUM_SMS = 148
 
 
 def erased_of(wl):
@@ -683,6 +685,21 @@ def main():
             # judged one) and the nominal HBM3e figure (B200_PROFILING.md: 7.7 TB/s HGX)
             "nominal_peak": HBM_NOMINAL_GBS, "frac_nominal": round(achieved / HBM_NOMINAL_GBS, 4),
             "data_roof_gbs": round(peak / ((n_in + m_out) / n), 1)}
+    if wl["op"] == "encode_gft":
+        # approach (1) is bound by the ALU pipe, not HBM (profiles/r01_s2_gftable.md): report its
+        # design op count against the ALU pipe's measured 64 lane-ops / clk / SM
+        # (scripts/alu_probe.cu, profiles/r01_s2_alu_probe.md) at the median SM clock under load
+        sm_mhz = clk.summary()["sm_mhz"] or 1965
+        ops_b = (6 + 4.5 * m_out + m_out / n) / 4      # ALU lane-ops per data byte (csrc/gftable.cu)
+        a_ops = S * n * B * ops_b / (launch_ms / 1e3) / 1e12
+        a_peak = ALU_LANE_OPS_PER_CLK_SM * NUM_SMS * sm_mhz * 1e6 / 1e12
+        roof = {"bound": "alu", "achieved": round(a_ops, 3), "peak": round(a_peak, 3),
+                "unit": "T ALU lane-ops/s", "frac": round(a_ops / a_peak, 4),
+                "traffic": ncu_traffic(args.workload), "kernel": roof["kernel"],
+                "peak_source": f"ALU pipe {ALU_LANE_OPS_PER_CLK_SM} lane-ops/clk/SM (alu_probe, "
+                               f"B300_MICROARCH rt=2) x {NUM_SMS} SMs x median SM clock {sm_mhz} MHz",
+                "alu_ops_per_data_byte": round(ops_b, 4), "launch_ms": roof["launch_ms"],
+                "hbm": {"achieved": roof["achieved"], "peak": peak, "unit": "GB/s", "frac": roof["frac"]}}
     if wl["op"] == "decode_peer":
         # survivors read over NVLink from peer HBM: the second roof of the fused gather+decode
         rem_bytes = remote_blocks * B
