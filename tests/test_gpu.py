@@ -7,6 +7,8 @@ BASELINE-size cases run in the bench's launch configuration and compare sampled
 stripes with the oracle, plus properties checked over all stripes.
 """
 import itertools
+import sys
+import os
 
 import numpy as np
 import pytest
@@ -307,6 +309,54 @@ def test_syndrome_form_decode(n, p, kind, e, phases):
         blocks = np.concatenate([d, rs.encode(og, n, d)])
         surv, rows = mx.decode_rows(og, n, list(pats[s]))
         assert (out[s].cpu().numpy() == rs.decode(rows, blocks[surv])).all()
+
+
+@pytest.mark.parametrize("wname", ["cfg3", "cfg5h"])
+def test_syndrome_full_size_bench_config(wname):
+    # the heterogeneous decode workloads at full size (1024 stripes x 1 MiB, per-stripe seeded
+    # 4-erasures) in exactly the launch configuration bench.py times (read from its table):
+    # roundtrip on every stripe, the oracle's decode on sampled stripes
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    wl, t = bench.WORKLOADS[wname], bench.WORKLOADS[wname]["tuned"]
+    assert t["kernel"] == "syndrome"
+    n, p, B, S, e, seed = wl["n"], wl["p"], wl["B"], wl["S"], wl["e"], wl["seed"]
+    phases = t.get("phases") or -(-(n + p) // 10)      # bench.py's default for the syndrome form
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    pats = [tuple(synth.erasure_pattern(seed, s, n + p, e)) for s in range(S)]
+    uniq = sorted(set(pats))
+    dec = X.SyndromeDecoder(g, n, p, uniq, per_module=t["per_module"], threads=t["threads"],
+                            stages=t["stages"], phases=phases, block_bytes_hint=B)
+    _, enc = compile_enc(n, p, block_bytes_hint=B)
+    allb = dev_buf(S, n + p, B)
+    data = dev_buf(S, n, B)
+    X.xslp_fill_random(data, S, n, B, seed=seed)
+    allb[:, :n] = data
+    ti = X.block_table(allb, S, n + p, B).view(S, n + p)
+    X.xslp_encode_batch(enc, ti[:, :n].contiguous(), ti[:, n:].contiguous(), S, B)
+    zero = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    tin = ti.clone()
+    for s_, er in enumerate(pats):
+        for j in er:
+            tin[s_, j] = zero.data_ptr()
+    out = dev_buf(S, e, B)
+    pos = [uniq.index(er) for er in pats]
+    ids, off = X.group_stripes(pos, len(uniq))
+    X.xslp_multi_decode(dec, torch.tensor(pos, dtype=torch.int32, device="cuda"),
+                        torch.from_numpy(ids).cuda(), off, tin.reshape(-1),
+                        X.block_table(out, S, e, B), B)
+    torch.cuda.synchronize()
+    for s_, er in enumerate(pats):                    # every stripe: the erased blocks come back
+        assert torch.equal(out[s_], allb[s_, list(er)]), (s_, er)
+    for s_ in (0, 613, S - 1):                         # the oracle's blocks and decode
+        d = synth.stripe_data(seed, s_, n, B)
+        blocks = np.concatenate([d, rs.encode(og, n, d)])
+        assert (allb[s_].cpu().numpy() == blocks).all(), s_
+        surv, rows = mx.decode_rows(og, n, list(pats[s_]))
+        assert (out[s_].cpu().numpy() == rs.decode(rows, blocks[surv])).all(), s_
+    del allb, data, out, tin
+    torch.cuda.empty_cache()
 
 
 def test_edge_cases():
@@ -720,6 +770,25 @@ def test_gf_table_kernel(n, p, kind, B, S):
                           X.block_table(rec, S, len(er), B), S, B)
     torch.cuda.synchronize()
     assert (rec.cpu().numpy() == blocks[:, er]).all()
+
+
+def test_gf_table_full_size_sampled():
+    # approach (1) at bench cfg2t's size: RS(10,4) byte-wise encode of 1024 stripes x 10 x 1 MiB;
+    # row 0 of [I; 2^(ij)] is all ones, so parity 0 = XOR of the data on every stripe
+    n, p, B, S = 10, 4, 1 << 20, 1024
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    din = dev_buf(S, n, B)
+    X.xslp_fill_random(din, S, n, B, seed=2)
+    out = dev_buf(S, p, B)
+    X.xslp_gf_table_apply(g[n:], X.block_table(din, S, n, B), X.block_table(out, S, p, B), S, B)
+    torch.cuda.synchronize()
+    assert torch.equal(out[:, 0], _xor_reduce(din))
+    for s in (0, 401, 1023):
+        want = rs.bytewise_apply(og[n:], synth.stripe_data(2, s, n, B))
+        assert (out[s].cpu().numpy() == want).all(), s
+    del din, out
+    torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("kern,threads", [("straight", 128), ("pipe", 128), ("pipe", 256)])
