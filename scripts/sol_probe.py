@@ -59,3 +59,18 @@ a = din.view(-1)[: hbm // 2]
 b = torch.empty_like(a)
 ms = timeit(lambda: b.copy_(a))
 report("torch copy 7 GiB -> 7 GiB", ms, 0, hbm)
+
+# HBM throughput against the write share: m goal strips per stripe (goal r = XOR of the input
+# strips c = r mod m), same launch; m = 32 is the traffic above (the batched API needs whole output blocks: m a multiple of 8)
+if "--mix" in sys.argv:
+    for m in (8, 16, 32, 48, 64):
+        bits = np.zeros((m, 8 * n), dtype=np.uint8)
+        for c in range(8 * n):
+            bits[c % m, c] = 1
+        o = torch.empty((S, (m + 7) // 8, B), dtype=torch.uint8, device="cuda")
+        prog = X.xslp_compile(bits, kernel="pipe", threads=128, lane_words=2, stages=2,
+                              block_bytes_hint=B)
+        to_m = X.block_table(o, S, (m + 7) // 8, B)
+        ms = timeit(lambda: X.xslp_encode_batch(prog, ti, to_m, S, B))
+        report(f"mix m={m} goal strips (write {m / 8:.3g} blocks per 10 read)", ms, data,
+               S * n * B + S * m * (B // 8))
