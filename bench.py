@@ -125,6 +125,8 @@ def parse():
     ap.add_argument("--lanes", type=int, default=None)
     ap.add_argument("--groups", type=int, default=None, help="PIPE consumer groups (goal split)")
     ap.add_argument("--phases", type=int, default=None, help="PIPE input phases (K-split)")
+    ap.add_argument("--reuse", type=int, default=0,
+                    help="constant register reuse window (xslp_opts.reuse): 0 auto, -1 off")
     ap.add_argument("--distinct", type=int, default=0,
                     help="diagnostic: only K distinct erasure patterns (stripe s takes pattern s mod K)")
     ap.add_argument("--per-module", type=int, default=None,
@@ -359,6 +361,9 @@ def config_of(args, wl, stats):
          "stages": args.stages, "groups": args.groups,
          "phases": args.phases or (-(-(wl["n"] + wl["p"]) // 10) if args.kernel == "syndrome" else
                                    (-(-wl["n"] // 10) if wl["n"] > 10 else 1)),
+         "const_reuse": (args.reuse if args.reuse else
+                         ("auto: 16 (fused kernels)" if args.kernel in ("multi", "syndrome")
+                          else "auto: 64")) if args.kernel not in ("gftable", "interp") else None,
          "cuda_graph": bool(args.graph),
          "l2": "inputs larger than the 126 MB L2; no flush between steps",
          "parallelism": (f"blocks spread over {args.gpus} GPU(s); survivors read in place over "
@@ -436,14 +441,15 @@ def main():
             progs = uniq
             multi = X.SyndromeDecoder(G, n, p, uniq, per_module=args.per_module_raw or 64,
                                       threads=args.threads, stages=args.stages,
-                                      lane_words=args.lanes, block_bytes_hint=B, phases=args.phases)
+                                      lane_words=args.lanes, block_bytes_hint=B, phases=args.phases,
+                                      reuse=args.reuse)
             log("syndrome", multi.info())
         elif mode == "multi":   # fused multi-program pipeline kernels (branch table per stripe)
             progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,
                                    threads=args.threads)
             multi = X.Multi(progs, per_module=args.per_module, threads=args.threads,
                             stages=args.stages, lane_words=args.lanes, block_bytes_hint=B,
-                            phases=args.phases)
+                            phases=args.phases, reuse=args.reuse)
             log("multi", multi.info())
         elif mode == "interp":
             progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,
@@ -477,7 +483,8 @@ def main():
         bits, _surv = X.xslp_decode_bitmatrix(G, n, p, erased)
         prog = X.xslp_compile(bits, compress=args.compress, kernel=args.kernel,
                               lane_words=args.lanes, threads=args.threads, block_bytes_hint=B,
-                              stages=args.stages, groups=args.groups, phases=args.phases)
+                              stages=args.stages, groups=args.groups, phases=args.phases,
+                              reuse=args.reuse)
         m_out = len(erased)
     elif wl["op"] == "encode_gft":    # approach (1): no SLP, the coefficient rows themselves
         prog = None
@@ -488,7 +495,7 @@ def main():
                               kernel=args.kernel, lane_words=args.lanes, threads=args.threads,
                               block_bytes_hint=B, stages=args.stages, fuse=args.fuse,
                               schedule=args.schedule, layout=wl.get("layout", "strip"),
-                              groups=args.groups, phases=args.phases)
+                              groups=args.groups, phases=args.phases, reuse=args.reuse)
         m_out = p
     compile_s = time.perf_counter() - t0
     stats = prog.stats() if prog is not None else None

@@ -107,6 +107,13 @@ typedef struct xslp_opts {
                               are XORed in registers, so a stage holds one range's strips (wide
                               codes such as RS(20,4) keep more consumer threads per SM).  Not
                               combinable with groups > 1. */
+  int32_t reuse;           /* constant register reuse window of the TMA-staged kernels (PIPE, TMA,
+                              fused multi-program / syndrome): a constant read from shared memory
+                              within the last `reuse` instructions keeps its register instead of
+                              a fresh read; 0 = auto (the default: 64 for single-program kernels,
+                              which run one CTA per SM, 16 for the fused kernels, which keep two
+                              CTAs per SM), -1 = a fresh shared-memory read at every use, or
+                              1..4096 */
 } xslp_opts;
 
 typedef struct xslp_stats {

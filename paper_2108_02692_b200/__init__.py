@@ -49,7 +49,8 @@ class xslp_opts(ctypes.Structure):
                 ("goal_order", ctypes.c_int32), ("min_blocks", ctypes.c_int32),
                 ("stages", ctypes.c_int32), ("greedy_capacity", ctypes.c_int32),
                 ("layout", ctypes.c_int32), ("groups", ctypes.c_int32),
-                ("phases", ctypes.c_int32)]
+                ("phases", ctypes.c_int32),
+                ("reuse", ctypes.c_int32)]
 
 
 class xslp_stats(ctypes.Structure):

@@ -31,6 +31,7 @@ extern "C" void xslp_default_opts(xslp_opts *o) {
   o->layout = XSLP_LAYOUT_STRIP;
   o->groups = 1;
   o->phases = 0;
+  o->reuse = 0;
 }
 
 extern "C" int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out) {
@@ -254,12 +255,13 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
     }
     const std::vector<Slp> *gp = P.groups.empty() ? nullptr : &P.groups;
     const std::vector<Slp> *ph = P.phases.empty() ? nullptr : &P.phases;
-    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads, o.min_blocks, o.stages, o.layout, gp, ph);
+    P.ptx_generic = emit_ptx(P.slp, o.lane_words, 0, o.threads, o.min_blocks, o.stages, o.layout, gp, ph,
+                             reuse_window(o.reuse, 64));
     P.cubin_generic = ptx_to_cubin(P.ptx_generic, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma, &st.regs_pipe, &st.spill_bytes_pipe);
     if (o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0) {
       P.baked_strip = o.block_bytes_hint / 8;
       P.ptx_baked = emit_ptx(P.slp, o.lane_words, P.baked_strip, o.threads, o.min_blocks, o.stages,
-                           o.layout, gp, ph);
+                           o.layout, gp, ph, reuse_window(o.reuse, 64));
       P.cubin_baked = ptx_to_cubin(P.ptx_baked, &st.regs, &st.spill_bytes, &st.regs_tma, &st.spill_bytes_tma, &st.regs_pipe, &st.spill_bytes_pipe);
     }
   }
@@ -286,6 +288,7 @@ void check_opts(xslp_opts &o) {
   if (o.groups < 1 || o.groups > 4) throw Error(XSLP_EINVAL, "groups must be 1..4");
   if (o.phases < 0 || o.phases > 8) throw Error(XSLP_EINVAL, "phases must be 0 (auto) or 1..8");
   if (o.phases > 1 && o.groups > 1) throw Error(XSLP_EINVAL, "phases and groups cannot be combined");
+  if (o.reuse < -1 || o.reuse > 4096) throw Error(XSLP_EINVAL, "reuse must be -1, 0 (auto) or 1..4096");
   if (o.threads * o.groups > 992) throw Error(XSLP_EINVAL, "pipe kernel: threads * groups <= 992");
 }
 

@@ -36,7 +36,7 @@ struct MultiModule {
 };
 
 struct Multi {
-  int n_const = 0, n_goals = 0, threads = 128, stages = 2, lanes = 1, phases = 1;
+  int n_const = 0, n_goals = 0, threads = 128, stages = 2, lanes = 1, phases = 1, reuse = 16;
   int64_t baked_strip = 0;
   int nprogs = 0;
   std::vector<MultiModule> mods;
@@ -172,6 +172,7 @@ extern "C" int xslp_multi_create(const xslp_program *const *progs, int nprogs, i
   M->threads = o.threads;
   M->stages = o.stages;
   M->lanes = o.lane_words;
+  M->reuse = reuse_window(o.reuse, 16);
   M->nprogs = nprogs;
   M->baked_strip = o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0 ? o.block_bytes_hint / 8 : 0;
   // input phases for wide codes (as the PIPE kernel's opts.phases; 0 = ceil(n/10) for n > 10)
@@ -247,11 +248,11 @@ extern "C" int xslp_multi_create(const xslp_program *const *progs, int nprogs, i
             v.emplace_back();
             for (auto &q : phased[k]) v.back().push_back(&q);
           }
-          ptx = emit_ptx_multi_phases(v, M->lanes, M->baked_strip, M->threads, M->stages);
+          ptx = emit_ptx_multi_phases(v, M->lanes, M->baked_strip, M->threads, M->stages, M->reuse);
         } else {
           std::vector<const Slp *> v;
           for (int k = m.first; k < m.first + m.count; ++k) v.push_back(&ps[k]->slp);
-          ptx = emit_ptx_multi(v, M->lanes, M->baked_strip, M->threads, M->stages);
+          ptx = emit_ptx_multi(v, M->lanes, M->baked_strip, M->threads, M->stages, M->reuse);
         }
         m.cubin = ptx_to_cubin(ptx, nullptr, nullptr, nullptr, nullptr, &m.regs, &m.spill);
       } catch (const std::exception &e) {
@@ -293,6 +294,7 @@ extern "C" int xslp_syndrome_create(const uint8_t *gf, int n, int p, const int32
   M->threads = o.threads;
   M->stages = o.stages;
   M->lanes = o.lane_words;
+  M->reuse = reuse_window(o.reuse, 16);
   M->nprogs = npat;
   M->baked_strip = o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0 ? o.block_bytes_hint / 8 : 0;
   int nph = o.phases == 0 ? std::min(8, (nb + 9) / 10) : std::max(1, o.phases);
@@ -360,7 +362,8 @@ extern "C" int xslp_syndrome_create(const uint8_t *gf, int n, int p, const int32
       try {
         std::vector<const Slp *> v;
         for (int k = m.first; k < m.first + m.count; ++k) v.push_back(&solve[k]->slp);
-        std::string ptx = emit_ptx_syndrome(syn, v, ne, M->lanes, M->baked_strip, M->threads, M->stages);
+        std::string ptx = emit_ptx_syndrome(syn, v, ne, M->lanes, M->baked_strip, M->threads, M->stages,
+                                            M->reuse);
         m.cubin = ptx_to_cubin(ptx, nullptr, nullptr, nullptr, nullptr, &m.regs, &m.spill);
       } catch (const std::exception &e) {
         errs[i] = e.what();

@@ -541,13 +541,23 @@ struct Emitter {
     }
     // the program
     int qn = 0;
+    // TMA: a constant read within the last `reuse` instructions keeps its register instead of
+    // a fresh shared-memory read (0 = a fresh read at every use)
+    std::map<int, std::pair<int, int>> lastq;  // constant -> (register index, last use)
     for (size_t k = 0; k < cur().ins.size(); ++k) {
       const auto &in = cur().ins[k];
       const auto &ops = in.ops;
-      std::map<int, int> q;  // TMA: constant -> fresh register for this instruction
+      std::map<int, int> q;  // TMA: constant -> register for this instruction
       for (int t : ops) {
         if (t >= nc) continue;
         if (!tma) { need(t); continue; }
+        auto lq = lastq.find(t);
+        if (reuse > 0 && lq != lastq.end() && (int)k - lq->second.second <= reuse) {
+          q[t] = lq->second.first;
+          lq->second.second = (int)k;
+          continue;
+        }
+        lastq[t] = {qn, (int)k};
         q[t] = qn;
         std::vector<std::string> r;
         for (int l = 0; l < L; ++l) r.push_back("%q" + std::to_string(qn * L + l));
@@ -596,6 +606,7 @@ struct Emitter {
   }
   bool accumulate = false;
   bool multi_acc = false;  // phased multi-program kernel: declare the accumulators
+  int reuse = 0;   // constant register reuse window in instructions (xslp_opts.reuse)
 
   void decls(int ntmp_guess) {
     o << "  .reg .pred %p<5>;\n  .reg .b32 %s<8>;\n  .reg .b64 %rd<8>;\n  .reg .b64 %off;\n";
@@ -1239,7 +1250,7 @@ struct Emitter {
 
 std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks,
                      int stages, int layout, const std::vector<Slp> *groups,
-                     const std::vector<Slp> *phases) {
+                     const std::vector<Slp> *phases, int reuse) {
   if (s.n_const % 8 || s.goal.size() % 8)
     throw Error(XSLP_EINVAL, "device programs need whole blocks (constants and goals multiples of 8)");
   if (s.n_const / 8 + s.goal.size() / 8 > 128)
@@ -1247,11 +1258,12 @@ std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, 
   if (layout == XSLP_LAYOUT_BYTE) lanes = 1;
   Emitter e(s, lanes, baked_strip, threads, min_blocks, stages, layout, groups);
   e.phases = phases;
+  e.reuse = reuse;
   return e.run();
 }
 
 std::string emit_ptx_multi(const std::vector<const Slp *> &progs, int lanes, int64_t baked_strip,
-                           int threads, int stages) {
+                           int threads, int stages, int reuse) {
   if (progs.empty()) throw Error(XSLP_EINVAL, "no programs");
   const Slp &f = *progs[0];
   for (const Slp *q : progs)
@@ -1260,11 +1272,12 @@ std::string emit_ptx_multi(const std::vector<const Slp *> &progs, int lanes, int
   if (f.n_const % 8 || f.goal.size() % 8 || f.n_const / 8 + f.goal.size() / 8 > 128)
     throw Error(XSLP_EINVAL, "device programs need whole blocks (n + m <= 128)");
   Emitter e(f, lanes, baked_strip, threads, 0, stages, XSLP_LAYOUT_STRIP, nullptr);
+  e.reuse = reuse;
   return e.run_multi(progs);
 }
 
 std::string emit_ptx_multi_phases(const std::vector<std::vector<const Slp *>> &phased, int lanes,
-                                  int64_t baked_strip, int threads, int stages) {
+                                  int64_t baked_strip, int threads, int stages, int reuse) {
   if (phased.empty() || phased[0].empty()) throw Error(XSLP_EINVAL, "no programs");
   const Slp &f = *phased[0][0];
   for (auto &pk : phased) {
@@ -1276,11 +1289,13 @@ std::string emit_ptx_multi_phases(const std::vector<std::vector<const Slp *>> &p
   if (f.n_const % 8 || f.goal.size() % 8 || f.n_const / 8 + f.goal.size() / 8 > 128)
     throw Error(XSLP_EINVAL, "device programs need whole blocks (n + m <= 128)");
   Emitter e(f, lanes, baked_strip, threads, 0, stages, XSLP_LAYOUT_STRIP, nullptr);
+  e.reuse = reuse;
   return e.run_multi({}, phased);
 }
 
 std::string emit_ptx_syndrome(const std::vector<Slp> &syn, const std::vector<const Slp *> &solves,
-                              int n_out, int lanes, int64_t baked_strip, int threads, int stages) {
+                              int n_out, int lanes, int64_t baked_strip, int threads, int stages,
+                              int reuse) {
   if (syn.empty() || solves.empty()) throw Error(XSLP_EINVAL, "no programs");
   for (const Slp *q : solves)
     if (q->n_const != (int)syn[0].goal.size() || (int)q->goal.size() != 8 * n_out)
@@ -1289,6 +1304,7 @@ std::string emit_ptx_syndrome(const std::vector<Slp> &syn, const std::vector<con
     throw Error(XSLP_EINVAL, "device programs need whole blocks (n + p + e <= 128)");
   Emitter e(syn[0], lanes, baked_strip, threads, 0, stages, XSLP_LAYOUT_STRIP, nullptr);
   e.n_out = n_out;  // outputs are the erased blocks, not the syndrome
+  e.reuse = reuse;
   return e.run_syndrome(syn, solves);
 }
 

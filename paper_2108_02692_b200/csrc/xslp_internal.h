@@ -118,10 +118,13 @@ int lru_ccap(const Slp &s, const std::vector<int> &peb);
 std::string dump_slots(const std::vector<uint16_t> &code, int n_const);
 Slp parse_text(const std::string &text, int n_const);
 
-// PTX (ptx.cpp)
+// PTX (ptx.cpp).  `reuse`: constant register reuse window of the TMA-staged kernels in
+// instructions (0 = a fresh shared-memory read at every use); see xslp_opts.reuse.
 std::string emit_ptx(const Slp &s, int lanes, int64_t baked_strip, int threads, int min_blocks,
                      int stages, int layout, const std::vector<Slp> *groups = nullptr,
-                     const std::vector<Slp> *phases = nullptr);
+                     const std::vector<Slp> *phases = nullptr, int reuse = 0);
+// xslp_opts.reuse -> window: 0 = auto (the kernel family's default), -1 = off
+inline int reuse_window(int opt, int auto_window) { return opt == 0 ? auto_window : opt < 0 ? 0 : opt; }
 // Split the goals into k contiguous sets balanced by issue cost; each result keeps the
 // instructions its goals reach (original order and variable ids) and marks the other goals -2.
 std::vector<Slp> split_goals(const Slp &s, int k);
@@ -133,7 +136,7 @@ std::vector<Slp> phase_programs(const std::vector<Bits> &want, int n_const, int 
 // One persistent pipeline kernel (entry xslp_sl_multi) over several programs with the same
 // constants/goals, dispatching per stripe through a branch table.
 std::string emit_ptx_multi(const std::vector<const Slp *> &progs, int lanes, int64_t baked_strip,
-                           int threads, int stages);
+                           int threads, int stages, int reuse = 0);
 // bitmatrix -> compiled program (capi.cpp)
 std::shared_ptr<Program> compile_bits(const std::vector<uint8_t> &bits, int out_rows, int in_cols,
                                       const xslp_opts &o);
@@ -143,10 +146,11 @@ std::vector<uint8_t> solve_rows(const std::vector<uint8_t> &h, int n, int p, con
 // Syndrome-form decode kernel (entry xslp_sl_multi): the shared syndrome program in input
 // phases `syn`, then per-pattern solve programs (constants = the 8p syndrome words).
 std::string emit_ptx_syndrome(const std::vector<Slp> &syn, const std::vector<const Slp *> &solves,
-                              int n_out, int lanes, int64_t baked_strip, int threads, int stages);
+                              int n_out, int lanes, int64_t baked_strip, int threads, int stages,
+                              int reuse = 0);
 // The same with input phases: phased[k][ph] = phase ph's program of table entry k.
 std::string emit_ptx_multi_phases(const std::vector<std::vector<const Slp *>> &phased, int lanes,
-                                  int64_t baked_strip, int threads, int stages);
+                                  int64_t baked_strip, int threads, int stages, int reuse = 0);
 std::vector<char> ptx_to_cubin(const std::string &ptx, int *regs, int *spill, int *regs_tma,
                                int *spill_tma, int *regs_pipe, int *spill_pipe);
 

@@ -16,6 +16,10 @@ sys.path.insert(0, ".")
 import paper_2108_02692_b200 as X  # noqa: E402
 
 n, p, B, S = 10, 4, 1 << 20, 1024
+if "--rs20" in sys.argv:        # the cfg5 code: RS(20,4), 2 input phases (bench's cfg5 launch)
+    n = 20
+PH = 2 if n > 10 else 0
+LAUNCHES = ((256, 1),) if n > 10 else ((128, 2), (256, 1))
 din = torch.empty((S, n, B), dtype=torch.uint8, device="cuda")
 X.xslp_fill_random(din, S, n, B, seed=2)
 out = torch.empty((S, p, B), dtype=torch.uint8, device="cuda")
@@ -48,12 +52,13 @@ for r in range(8 * p):
         thin[r, c] = 1
 data, hbm = S * n * B, S * (n + p) * B
 for label, bits in (("rs10_4_encode", rs_bits), ("min_compute_same_traffic", thin)):
-    for threads, lanes in ((128, 2), (256, 1)):
+    for threads, lanes in LAUNCHES:
         prog = X.xslp_compile(bits, kernel="pipe", threads=threads, lane_words=lanes, stages=2,
-                              block_bytes_hint=B)
+                              block_bytes_hint=B, phases=PH)
         st = prog.stats()
         ms = timeit(lambda: X.xslp_encode_batch(prog, ti, to, S, B))
-        report(f"{label} pipe T={threads} L={lanes} xor={st['xor_count']}", ms, data, hbm)
+        report(f"RS({n},{p}) {label} pipe T={threads} L={lanes} phases={PH} xor={st['xor_count']}",
+               ms, data, hbm)
 # plain copies for scale: torch's copy kernel over the same byte count (read 7 GiB + write 7 GiB)
 a = din.view(-1)[: hbm // 2]
 b = torch.empty_like(a)

@@ -64,6 +64,26 @@ def test_decode_bitmatrix_errors():
     assert e.value.code == X.XSLP_EINVAL
 
 
+def test_const_reuse_window_codegen():
+    # xslp_opts.reuse only changes how often the TMA-staged code re-reads a constant from
+    # shared memory: off (-1) reads at every use, a wider window reads less; out of range is
+    # EINVAL.  (PTX is emitted and compiled for sm_100a in-process: no GPU needed.)
+    g = X.xslp_coding_matrix(20, 4)
+    bits = X.xslp_encode_bitmatrix(g, 20, 4)
+    counts = {}
+    for r in (-1, 16, 64):
+        prog = X.xslp_compile(bits, kernel="pipe", threads=256, phases=2, block_bytes_hint=1 << 20,
+                              reuse=r)
+        counts[r] = prog.dump(2).count("ld.volatile.shared")
+    assert counts[-1] > counts[16] > counts[64] > 0
+    auto = X.xslp_compile(bits, kernel="pipe", threads=256, phases=2, block_bytes_hint=1 << 20)
+    assert auto.dump(2).count("ld.volatile.shared") == counts[64]    # auto = 64 (single program)
+    for bad in (-2, 4097):
+        with pytest.raises(X.XslpError) as e:
+            X.xslp_compile(bits, kernel="pipe", reuse=bad)
+        assert e.value.code == X.XSLP_EINVAL
+
+
 def test_singular_matrix():
     g = np.array([[1, 0], [0, 1], [1, 1], [2, 2]], dtype=np.uint8)  # rows 2 and 3 dependent
     with pytest.raises(X.XslpError) as e:

@@ -613,6 +613,54 @@ def test_pipe_input_phases(phases, threads, lanes, case):
             assert (dout[s].cpu().numpy() == want).all(), (case, phases, hint, s)
 
 
+@pytest.mark.parametrize("reuse", [-1, 1, 3, 16, 64, 4096])
+@pytest.mark.parametrize("kern", ["pipe", "tma", "syndrome"])
+def test_const_reuse_window(reuse, kern):
+    # the constant register reuse window only changes which shared-memory reads the emitted
+    # code repeats: every window gives the oracle's bytes (PIPE with input phases, the TMA
+    # kernel, the syndrome-form decode), ragged last tile
+    n, p = 20, 4
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    B, S = 8192 + 1152, 3
+    if kern == "syndrome":
+        pats = [(0, 5, 21, 23), (1, 2, 3, 4), (20, 21, 22, 23)]
+        dec = X.SyndromeDecoder(g, n, p, pats, per_module=2, threads=128, stages=2, reuse=reuse)
+        allb = dev_buf(S, n + p, B)
+        X.xslp_fill_random(allb, S, n + p, B, seed=97)
+        _, enc = compile_enc(n, p)
+        t = X.block_table(allb, S, n + p, B).view(S, n + p)
+        X.xslp_encode_batch(enc, t[:, :n].contiguous(), t[:, n:].contiguous(), S, B)
+        zero = torch.zeros(B, dtype=torch.uint8, device="cuda")
+        tin = t.clone()
+        for s_, er in enumerate(pats):
+            for j in er:
+                tin[s_, j] = zero.data_ptr()
+        out = torch.full((S, 4, B), 0x5C, dtype=torch.uint8, device="cuda")
+        pos = list(range(S))
+        ids, off = X.group_stripes(pos, S)
+        X.xslp_multi_decode(dec, torch.tensor(pos, dtype=torch.int32, device="cuda"),
+                            torch.from_numpy(ids).cuda(), off, tin.reshape(-1),
+                            X.block_table(out, S, 4, B), B)
+        torch.cuda.synchronize()
+        for s_, er in enumerate(pats):
+            d = synth.stripe_data(97, s_, n, B)
+            blocks = np.concatenate([d, rs.encode(og, n, d)])
+            assert (out[s_].cpu().numpy() == blocks[list(er)]).all(), (reuse, s_)
+        return
+    er = [0, 5, 21, 23]
+    bits, _ = X.xslp_decode_bitmatrix(g, n, p, er)
+    rows = mx.decode_rows(og, n, er)[1]
+    prog = X.xslp_compile(bits, kernel=kern, threads=128, stages=2, block_bytes_hint=B, reuse=reuse)
+    din = dev_buf(S, n, B)
+    X.xslp_fill_random(din, S, n, B, seed=98)
+    dout = torch.full((S, 4, B), 0x5C, dtype=torch.uint8, device="cuda")
+    run_batch(prog, din, dout, B)
+    for s_ in range(S):
+        want = rs.apply_rows(rows, synth.stripe_data(98, s_, n, B))
+        assert (dout[s_].cpu().numpy() == want).all(), (kern, reuse, s_)
+
+
 @pytest.mark.parametrize("kern", ["straight", "tma", "pipe"])
 def test_cfg5_rs20_reduced(kern):
     # RS(20,4) encode + one seeded 4-erasure decode; 16 stripes x 20 x 1 MiB (configs[4] shape)
