@@ -35,7 +35,7 @@ MiB = 1 << 20
 WORKLOADS = {
     "cfg2": dict(desc="RS(10,4) encode, 1024 stripes x 10 x 1 MiB per GPU (BASELINE configs[1])",
                  n=10, p=4, B=MiB, S=1024, op="encode", seed=2,
-                 tuned=dict(kernel="pipe", threads=128, lanes=2, stages=2)),
+                 tuned=dict(kernel="pipe", threads=128, lanes=2, stages=2, reuse=32)),
     "cfg2b": dict(desc="RS(10,4) encode in the byte-compatible layout (output = textbook byte-wise "
                        "RS, SURVEY NEXT #3), 1024 stripes x 10 x 1 MiB",
                   n=10, p=4, B=MiB, S=1024, op="encode", seed=2, layout="byte",
@@ -52,7 +52,7 @@ WORKLOADS = {
                       "--kernel grouped: one straight-line kernel per pattern; --kernel interp "
                       "(BASELINE configs[2])",
                  n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3,
-                 tuned=dict(kernel="syndrome", threads=256, stages=2, per_module=32)),
+                 tuned=dict(kernel="syndrome", threads=256, stages=2, per_module=32, reuse=40)),
     "pdec": dict(desc="RS(10,4) decode of the paper's P_dec pattern {2,4,5,6} (P:1670) on every "
                       "stripe, 1024 stripes x 1 MiB",
                  n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3,
@@ -125,7 +125,7 @@ def parse():
     ap.add_argument("--lanes", type=int, default=None)
     ap.add_argument("--groups", type=int, default=None, help="PIPE consumer groups (goal split)")
     ap.add_argument("--phases", type=int, default=None, help="PIPE input phases (K-split)")
-    ap.add_argument("--reuse", type=int, default=0,
+    ap.add_argument("--reuse", type=int, default=None,
                     help="constant register reuse window (xslp_opts.reuse): 0 auto, -1 off")
     ap.add_argument("--distinct", type=int, default=0,
                     help="diagnostic: only K distinct erasure patterns (stripe s takes pattern s mod K)")
@@ -394,6 +394,7 @@ def main():
     args.groups = args.groups or 1
     args.lanes = args.lanes or 1
     args.per_module_raw = args.per_module
+    args.reuse = args.reuse or 0
     args.per_module = args.per_module or 20
     if args.phases is None:            # 0 = the library's auto: ceil(n/10) input phases if n > 10
         args.phases = 0

@@ -327,7 +327,8 @@ def test_syndrome_full_size_bench_config(wname):
     pats = [tuple(synth.erasure_pattern(seed, s, n + p, e)) for s in range(S)]
     uniq = sorted(set(pats))
     dec = X.SyndromeDecoder(g, n, p, uniq, per_module=t["per_module"], threads=t["threads"],
-                            stages=t["stages"], phases=phases, block_bytes_hint=B)
+                            stages=t["stages"], phases=phases, block_bytes_hint=B,
+                            reuse=t.get("reuse", 0))
     _, enc = compile_enc(n, p, block_bytes_hint=B)
     allb = dev_buf(S, n + p, B)
     data = dev_buf(S, n, B)
@@ -454,15 +455,21 @@ def _xor_reduce(t):
     return acc
 
 
-@pytest.mark.parametrize("kern,threads,lanes", [("straight", 128, 1), ("tma", 128, 1), ("pipe", 256, 1),
-                                                ("pipe", 128, 2)])
-def test_cfg2_full_size_sampled(kern, threads, lanes):
-    # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); ("pipe", 128, 2 lanes) with 2 stages is
-    # the exact launch configuration bench.py times by default
+@pytest.mark.parametrize("kern,threads,lanes,reuse", [("straight", 128, 1, 0), ("tma", 128, 1, 0),
+                                                      ("pipe", 256, 1, 0), ("pipe", 128, 2, "bench")])
+def test_cfg2_full_size_sampled(kern, threads, lanes, reuse):
+    # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); ("pipe", 128, 2 lanes) with 2 stages and
+    # bench's reuse window is the exact launch configuration bench.py times by default
     n, p, B, S = 10, 4, 1 << 20, 1024
+    if reuse == "bench":
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+        t = bench.WORKLOADS["cfg2"]["tuned"]
+        assert (t["kernel"], t["threads"], t["lanes"], t["stages"]) == (kern, threads, lanes, 2)
+        reuse = t.get("reuse", 0)
     og = mx.coding_matrix(n, p)
     _, prog = compile_enc(n, p, block_bytes_hint=B, kernel=kern, threads=threads, stages=2,
-                          lane_words=lanes)
+                          lane_words=lanes, reuse=reuse)
     din = dev_buf(S, n, B)
     X.xslp_fill_random(din, S, n, B, seed=2)
     dout = dev_buf(S, p, B)
