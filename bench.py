@@ -48,11 +48,11 @@ WORKLOADS = {
     "cfg3": dict(desc="RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures, "
                       "syndrome form: one shared syndrome program over all 14 blocks (erased ones read from a "
                       "zero block) + a small solve program per pattern, fused with a branch table "
-                      "(32 patterns per kernel); --kernel multi: the patterns' M^-1 programs fused; "
+                      "(16 patterns per kernel); --kernel multi: the patterns' M^-1 programs fused; "
                       "--kernel grouped: one straight-line kernel per pattern; --kernel interp "
                       "(BASELINE configs[2])",
                  n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3,
-                 tuned=dict(kernel="syndrome", threads=256, stages=2, per_module=32, reuse=40)),
+                 tuned=dict(kernel="syndrome", threads=256, stages=2, per_module=16, reuse=40)),
     "pdec": dict(desc="RS(10,4) decode of the paper's P_dec pattern {2,4,5,6} (P:1670) on every "
                       "stripe, 1024 stripes x 1 MiB",
                  n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3,
@@ -73,9 +73,9 @@ WORKLOADS = {
     "cfg5h": dict(desc="RS(20,4) decode with per-stripe seeded 4-of-24 erasures (the secondary "
                        "reading of BASELINE configs[4]), 1024 stripes x 1 MiB per GPU: syndrome form (shared "
                        "syndrome program over 24 blocks in 6 input phases + per-pattern solve "
-                       "programs, 16 per kernel); --kernel multi: the M^-1 programs fused",
+                       "programs, 10 per kernel); --kernel multi: the M^-1 programs fused",
                   n=20, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=5,
-                  tuned=dict(kernel="syndrome", threads=256, stages=3, phases=6, per_module=16)),
+                  tuned=dict(kernel="syndrome", threads=256, stages=3, phases=6, per_module=10)),
     "xdec": dict(desc="RS(10,4) cross-GPU decode (SURVEY NEXT #4): the 14 blocks of each stripe "
                       "spread over the GPUs (block j of stripe s on rank (s+j) mod N), rank s mod N "
                       "decodes stripe s reading its survivors in place from local and NVLink-peer "
