@@ -440,7 +440,7 @@ def main():
         mode = "grouped" if args.kernel == "auto" else args.kernel
         if mode == "syndrome":  # shared syndrome program + per-pattern solve programs, fused
             progs = uniq
-            multi = X.SyndromeDecoder(G, n, p, uniq, per_module=args.per_module_raw or 64,
+            multi = X.SyndromeDecoder(G, n, p, uniq, per_module=args.per_module_raw or 0,
                                       threads=args.threads, stages=args.stages,
                                       lane_words=args.lanes, block_bytes_hint=B, phases=args.phases,
                                       reuse=args.reuse)
@@ -770,7 +770,7 @@ def main():
                 "dtype": "u32", "data": "synthetic",
                 "config": dict(config_of(args, wl, stats),
                                **({"multi": multi.info(), "patterns": len(progs),
-                                   "per_module": args.per_module_raw or (64 if mode == "syndrome" else 20)}
+                                   "per_module": args.per_module_raw or (16 if mode == "syndrome" else 20)}
                                   if wl["op"] == "decode_multi" and mode in ("multi", "syndrome")
                                   else {}),
                                **({"distinct_diagnostic": args.distinct} if args.distinct else {})),

@@ -291,7 +291,8 @@ int xslp_multi_decode(const xslp_multi *multi, const int32_t *d_prog_of_stripe,
  * order, the outputs are the erased blocks ascending).  For xslp_multi_decode, d_in_tbl is
  * [stripes][n+p]: every block of the stripe, the ERASED ones pointing at a zero block of
  * block_bytes (any readable all-zero device buffer); d_out_tbl is [stripes][ne].  Same bytes
- * as the M^-1 decode (the solution is unique).  gf must be systematic. */
+ * as the M^-1 decode (the solution is unique).  gf must be systematic.  Patterns are packed
+ * per_module (<= 0: 16) to a module. */
 int xslp_syndrome_create(const uint8_t *gf, int n, int p, const int32_t *patterns, int npat, int ne,
                          int per_module, const xslp_opts *opts, xslp_multi **out);
 /* modules, max registers / spill bytes per thread over the modules, host compile time. */

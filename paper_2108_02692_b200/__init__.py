@@ -401,7 +401,7 @@ class SyndromeDecoder(Multi):
     plus one small solve program per erasure pattern, fused; decode with xslp_multi_decode on
     an input table of all n+p blocks per stripe (erased entries -> a zero block)."""
 
-    def __init__(self, gf, n, p, patterns, per_module=64, opts=None, **kw):   # noqa: super
+    def __init__(self, gf, n, p, patterns, per_module=0, opts=None, **kw):   # noqa: super
         self._progs = []
         pats = np.ascontiguousarray([sorted(er) for er in patterns], dtype=np.int32)
         g = np.ascontiguousarray(gf, dtype=np.uint8)

@@ -284,7 +284,7 @@ extern "C" int xslp_syndrome_create(const uint8_t *gf, int n, int p, const int32
   if (o.threads < 32 || o.threads > 992 || o.threads % 32) throw Error(XSLP_EINVAL, "bad threads");
   if (o.stages < 2 || o.stages > 8) throw Error(XSLP_EINVAL, "stages must be 2..8");
   if (o.lane_words != 1 && o.lane_words != 2 && o.lane_words != 4) throw Error(XSLP_EINVAL, "bad lane_words");
-  if (per_module <= 0) per_module = 64;  // solve programs are small: many per module
+  if (per_module <= 0) per_module = 16;  // measured optimum for RS(10,4) / RS(20,4) (profiles/r01_s2_reuse.md)
   per_module = std::min(per_module, 256);
   auto t0 = std::chrono::steady_clock::now();
   auto M = std::make_unique<Multi>();
