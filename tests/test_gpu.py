@@ -397,6 +397,97 @@ def test_copy_and_zero_goals_on_device():
         assert (out.cpu().numpy() == want).all()
 
 
+@pytest.mark.parametrize("case", range(96))
+def test_random_programs_and_launches(case):
+    # seeded fuzz over program shape and launch knobs: a random bitmatrix (1-24 input blocks,
+    # 1-6 output blocks, random density incl. empty and full rows) through a random launch of
+    # the straight-line / TMA / PIPE kernels (threads, words per thread, stages, input phases,
+    # reuse window, ragged block size, stripes) must give the oracle's bytes; launches the
+    # library rejects as not fitting (EINVAL) are skipped, and most cases must run
+    rng = np.random.default_rng(7000 + case)
+    n_in, m_out = int(rng.integers(1, 25)), int(rng.integers(1, 7))
+    dens = float(rng.choice([0.02, 0.1, 0.3, 0.5, 0.9]))
+    bits = (rng.random((8 * m_out, 8 * n_in)) < dens).astype(np.uint8)
+    bits[int(rng.integers(0, 8 * m_out))] = 0                      # an all-zero goal
+    if case % 3 == 0:
+        bits[int(rng.integers(0, 8 * m_out))] = 1                  # a full goal
+    kern = ["straight", "tma", "pipe", "pipe"][case % 4]
+    kw = dict(kernel=kern, threads=int(rng.choice([32, 64, 128, 256])),
+              reuse=int(rng.choice([-1, 0, 1, 7, 32, 128])))
+    if kern != "tma":
+        kw["lane_words"] = int(rng.choice([1, 2]))
+    if kern == "pipe":
+        kw["stages"] = int(rng.integers(1, 5))
+        kw["phases"] = int(rng.integers(0, min(4, n_in) + 1))
+    B = 128 * int(rng.integers(1, 40))
+    S = int(rng.integers(1, 5))
+    if rng.random() < 0.5:
+        kw["block_bytes_hint"] = B
+    try:
+        prog = X.xslp_compile(bits, **kw)
+        data = host_data(7000 + case, range(S), n_in, B)
+        din = torch.from_numpy(data).cuda()
+        out = torch.full((S, m_out, B), 0xA5, dtype=torch.uint8, device="cuda")
+        run_batch(prog, din, out, B)
+        torch.cuda.synchronize()
+    except X.XslpError as e:
+        assert e.code == X.XSLP_EINVAL, (case, kw, str(e))
+        pytest.skip(f"launch rejected: {e}")
+    for s_ in range(S):
+        assert (out[s_].cpu().numpy() == rs.bitmatrix_apply(bits, data[s_])).all(), (case, kw, B, s_)
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_random_heterogeneous_decode(case):
+    # seeded fuzz of the fused heterogeneous decode: a random code (n, p, matrix kind), random
+    # per-stripe erasure patterns (1..p erasures, data and parity mixed), the syndrome form or
+    # the M^-1 programs fused, random launch knobs; the erased blocks of real codewords come back
+    rng = np.random.default_rng(8000 + case)
+    kind = ["isal", "cauchy", "sysvand"][case % 3]
+    n, p = int(rng.integers(2, 17)), int(rng.integers(1, 5))
+    e = int(rng.integers(1, p + 1))
+    S = int(rng.integers(2, 9))
+    B = 128 * int(rng.integers(1, 40))
+    og = mx.coding_matrix(n, p, kind)
+    g = X.xslp_coding_matrix(n, p, kind)
+    pats = [tuple(sorted(rng.choice(n + p, size=e, replace=False).tolist())) for _ in range(S)]
+    uniq = sorted(set(pats))
+    pos = [uniq.index(er) for er in pats]
+    mode = "syndrome" if case % 2 == 0 else "multi"
+    kw = dict(threads=int(rng.choice([64, 128, 256])), stages=int(rng.integers(2, 4)),
+              reuse=int(rng.choice([-1, 0, 5, 16, 40])))          # fused kernels: 2..8 stages
+    pm = int(rng.integers(1, 5))
+    data = host_data(8000 + case, range(S), n, B)
+    blocks = np.stack([np.concatenate([d, rs.encode(og, n, d)]) for d in data])
+    allb = torch.from_numpy(blocks).cuda()
+    t = X.block_table(allb, S, n + p, B).view(S, n + p)
+    out = torch.full((S, e, B), 0x3C, dtype=torch.uint8, device="cuda")
+    try:
+        if mode == "syndrome":
+            dec = X.SyndromeDecoder(g, n, p, uniq, per_module=pm, phases=int(rng.integers(0, 3)), **kw)
+            zero = torch.zeros(B, dtype=torch.uint8, device="cuda")
+            tin = t.clone()
+            for s_, er in enumerate(pats):
+                for j in er:
+                    tin[s_, j] = zero.data_ptr()
+            tin = tin.reshape(-1)
+        else:
+            survs = {er: X.xslp_decode_bitmatrix(g, n, p, list(er)) for er in uniq}
+            progs = X.compile_many([survs[er][0] for er in uniq], specialise=0)
+            dec = X.Multi(progs, per_module=pm, **kw)
+            tin = torch.stack([t[s_, torch.as_tensor(survs[pats[s_]][1], dtype=torch.long)]
+                               for s_ in range(S)]).contiguous()
+        ids, off = X.group_stripes(pos, len(uniq))
+        X.xslp_multi_decode(dec, torch.tensor(pos, dtype=torch.int32, device="cuda"),
+                            torch.from_numpy(ids).cuda(), off, tin, X.block_table(out, S, e, B), B)
+        torch.cuda.synchronize()
+    except X.XslpError as ex:
+        assert ex.code == X.XSLP_EINVAL, (case, mode, kw, str(ex))
+        pytest.skip(f"launch rejected: {ex}")
+    for s_, er in enumerate(pats):
+        assert (out[s_].cpu().numpy() == blocks[s_, list(er)]).all(), (case, mode, kw, n, p, er)
+
+
 @pytest.mark.parametrize("kern", ["straight", "tma", "pipe", "interp", "multi"])
 def test_copy_and_zero_goals_batched(kern):
     # degenerate goals through the batched kernels (identity rows, all-zero rows, a full row),
