@@ -417,11 +417,22 @@ def main():
     import torch
     import paper_2108_02692_b200 as X
 
+    # XSLP_BENCH_SHARED_GPU=1: a control-flow check of the N>1 path on a one-GPU box -- every
+    # rank on cuda:0, gloo for the barriers and the max over ranks (the ranks' kernels never wait
+    # on one another); its numbers are not throughput claims
+    shared_gpu = os.environ.get("XSLP_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
+    red_dev = "cuda"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+            red_dev = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     n, p, B = wl["n"], wl["p"], wl["B"]
     G = X.xslp_coding_matrix(n, p)
@@ -675,7 +686,7 @@ def main():
     torch.cuda.synchronize()
     per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
-    total_ms = max_over_ranks(total_ms, dist, device="cuda")
+    total_ms = max_over_ranks(total_ms, dist, device=red_dev)
     data_bytes_step = S * nchunks * n * B * world
     value = data_bytes_step * args.steps / (total_ms / 1e3) / 1e9
 
@@ -743,7 +754,7 @@ def main():
             for _ in range(args.e2e_steps):
                 X.xslp_encode_host(prog, h_in, h_out, Se, B, stream=stream)
             torch.cuda.synchronize()
-            et = max_over_ranks(time.perf_counter() - e0, dist, device="cuda")
+            et = max_over_ranks(time.perf_counter() - e0, dist, device=red_dev)
             ok = bool(torch.equal(h_out.cuda(), want))
             del want
             e2e = {"value": round(Se * n * B * world * args.e2e_steps / et / 1e9, 3),
