@@ -166,10 +166,16 @@ def _ptr(x):
     raise TypeError(f"cannot take the address of {type(x)}")
 
 
+_CUDA_OK = None
+
+
 def _stream(s):
+    global _CUDA_OK
     if s is None:
         import torch
-        return torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else 0
+        if _CUDA_OK is None:                 # cached: is_available() costs microseconds per call
+            _CUDA_OK = torch.cuda.is_available()
+        return torch.cuda.current_stream().cuda_stream if _CUDA_OK else 0
     if isinstance(s, int):
         return s
     return s.cuda_stream
@@ -325,8 +331,15 @@ def xslp_compile_text(text, n_const, opts=None, **kw):
 
 # ---- device -------------------------------------------------------------------------
 def _ptr_array(ptrs):
-    arr = (ctypes.c_void_p * max(1, len(ptrs)))(*[_ptr(p) for p in ptrs])
-    return arr
+    if isinstance(ptrs, ctypes.Array):       # a prebuilt pointer array (see block_ptrs)
+        return ptrs
+    return (ctypes.c_void_p * max(1, len(ptrs)))(*[_ptr(p) for p in ptrs])
+
+
+def block_ptrs(blocks):
+    """A reusable pointer array for xslp_encode / xslp_decode (skips the per-call conversion
+    of a list of tensors; the caller keeps the tensors alive)."""
+    return _ptr_array(list(blocks))
 
 
 def xslp_prepare(prog, block_bytes=0):
