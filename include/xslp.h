@@ -301,7 +301,8 @@ int xslp_multi_info(const xslp_multi *multi, int32_t *modules, int32_t *regs, in
 void xslp_multi_free(xslp_multi *multi);
 
 /* Comparison path, the paper's approach (1): byte-layout RS as MM over GF(2^8)
- * with nibble-table field multiplication (ISA-L's method; PRMT in place of PSHUFB).
+ * with table-driven field multiplication (ISA-L splits bytes into nibbles for PSHUFB; here
+ * each byte is split into bit groups [0,3), [3,6), [6,8) looked up in 8-entry tables by PRMT).
  * coef: HOST [m][n] GF(2^8) coefficients (1 <= n <= 64, 1 <= m <= 8); output block i of
  * each stripe = sum_j coef[i][j] * input block j, byte by byte -- the same bytes
  * as an XSLP_LAYOUT_BYTE program of those rows.  Tables as in xslp_encode_batch; block

@@ -434,7 +434,7 @@ def xslp_multi_decode(multi, d_prog_of_stripe, d_stripe_ids, group_offsets, d_in
 
 
 def xslp_gf_table_apply(coef, d_in_tbl, d_out_tbl, nstripes, block_bytes, stream=None):
-    """Byte-wise GF(2^8) matrix apply with nibble tables (the paper's approach (1))."""
+    """Byte-wise GF(2^8) matrix apply with PRMT lookup tables (the paper's approach (1))."""
     c = np.ascontiguousarray(coef, dtype=np.uint8)
     m, n = c.shape
     _check(_lib.xslp_gf_table_apply(c.ctypes.data, n, m, _ptr(d_in_tbl), _ptr(d_out_tbl), nstripes,
