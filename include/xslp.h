@@ -136,6 +136,9 @@ typedef struct xslp_stats {
   int64_t group_xor;  /* PIPE consumer groups / input phases: XORs executed per word position
                          summed over the groups or phases, including the phases' accumulation
                          XORs (>= xor_count in practice); 0 if neither is used */
+  int64_t smem_reads; /* shared-memory reads of constants per word position that the
+                         TMA-staged kernels issue under opts.reuse (single program, no phases):
+                         #constant operand uses with reuse off, down to n_const */
 } xslp_stats;
 
 typedef struct xslp_program xslp_program; /* opaque, immutable after compile, thread-safe to share */

@@ -62,7 +62,8 @@ class xslp_stats(ctypes.Structure):
                 ("spill_bytes", ctypes.c_int32), ("regs_tma", ctypes.c_int32),
                 ("spill_bytes_tma", ctypes.c_int32), ("regs_pipe", ctypes.c_int32),
                 ("spill_bytes_pipe", ctypes.c_int32), ("compile_ms", ctypes.c_double),
-                ("group_xor", ctypes.c_int64)]
+                ("group_xor", ctypes.c_int64),
+                ("smem_reads", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -231,12 +231,21 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
       }
       P.stage_used_const = 8 * std::max(1, nub);
     }
+    // shared-memory reads of constants per word position in the TMA-staged kernels: the
+    // emitter's rule (ptx.cpp compute) -- a constant used within the reuse window of its
+    // previous use keeps its register, otherwise it is read again
     P.const_reads = 0;
-    for (auto &in : P.slp.ins)
-      for (int t : in.ops)
-        if (t < P.n_const) P.const_reads++;
+    const int W = reuse_window(o.reuse, 64);
+    std::vector<int> last(P.n_const, -1);
+    for (size_t k = 0; k < P.slp.ins.size(); ++k)
+      for (int t : P.slp.ins[k].ops) {
+        if (t >= P.n_const) continue;
+        if (W <= 0 || last[t] < 0 || (int)k - last[t] > W) P.const_reads++;
+        last[t] = (int)k;
+      }
   }
   st.regs = st.spill_bytes = st.regs_tma = st.spill_bytes_tma = st.regs_pipe = st.spill_bytes_pipe = 0;
+  st.smem_reads = P.const_reads;
   st.group_xor = 0;
   const bool device_ok = P.n_const % 8 == 0 && P.n_goals % 8 == 0 && P.n_const > 0 &&
                          P.n_const / 8 + P.n_goals / 8 <= 128;

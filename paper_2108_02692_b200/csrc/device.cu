@@ -347,9 +347,10 @@ static int auto_kernel(const Program *p, size_t block_bytes, int nstripes) {
   const size_t smem = 128 + (size_t)p->opts.stages * p->stage_used_const * 4 * L * T;
   const uint64_t tiles = (strip / (4 * L) + T - 1) / T * (uint64_t)nstripes;
   if (smem > 227 * 1024 || p->opts.stages < 2 || tiles < 4 * 148) return XSLP_KERNEL_STRAIGHT;
-  // shared-memory bytes per data byte of the pipeline (one 4-byte read per constant use,
-  // 32n data bytes per word position): above ~6 the pipeline is smem-bound (uncompressed
-  // programs, profiles/r01_cfg4_sweep.md) and the register-resident kernel wins
+  // shared-memory bytes per data byte of the pipeline (one 4-byte read per constant read
+  // the emitted code issues under the reuse window, 32n data bytes per word position): above
+  // ~6 the pipeline was smem-bound (uncompressed programs without the reuse window,
+  // profiles/r01_cfg4_sweep.md) and the register-resident kernel wins
   if (p->const_reads * 4.0 / (4.0 * p->n_const) > 6.0) return XSLP_KERNEL_STRAIGHT;
   return XSLP_KERNEL_PIPE;
 }

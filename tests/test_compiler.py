@@ -78,6 +78,21 @@ def test_const_reuse_window_codegen():
     assert counts[-1] > counts[16] > counts[64] > 0
     auto = X.xslp_compile(bits, kernel="pipe", threads=256, phases=2, block_bytes_hint=1 << 20)
     assert auto.dump(2).count("ld.volatile.shared") == counts[64]    # auto = 64 (single program)
+    # the host's count of those reads (AUTO's shared-memory estimate) follows the same rule as
+    # the emitter: one read per constant operand with the window off, each constant once when
+    # every reuse distance is inside the window; PTX = the TMA and the PIPE kernel bodies
+    g10 = X.xslp_coding_matrix(10, 4)
+    for compress in ("none", "xorrepair"):
+        uses = None
+        for r in (-1, 16, 4096):
+            prog = X.xslp_compile(X.xslp_encode_bitmatrix(g10, 10, 4), compress=compress, threads=256,
+                                  block_bytes_hint=1 << 20, reuse=r)
+            st = prog.stats()
+            assert 2 * st["smem_reads"] == prog.dump(2).count("ld.volatile.shared")
+            if r == -1:
+                uses = st["smem_reads"]      # every constant operand of every instruction
+                assert st["n_instr"] < uses <= st["mem_count"] - st["n_instr"]
+        assert st["smem_reads"] == 80 < uses                      # window 4096: each constant once
     for bad in (-2, 4097):
         with pytest.raises(X.XslpError) as e:
             X.xslp_compile(bits, kernel="pipe", reuse=bad)
