@@ -538,6 +538,11 @@ def main():
         if dist:
             dist.barrier()                # every rank's storage written before any peer read
         pmulti = None
+        if world == 1 and len(progs) == 1:  # all blocks local: the TMA pipeline (peer tables keep
+            # the LDG kernel: TMA bulk copies from peer memory are not validated on this pool)
+            progs = peer.compile_plan(X, G, plan, compress=args.compress, threads=128, lane_words=2,
+                                      block_bytes_hint=B, stages=2, kernel="pipe")
+            args.kernel, args.threads, args.lanes = "pipe", 128, 2
         if world == 1 and len(progs) > 1:   # all blocks local: the fused multi-program kernels
             pmulti = X.Multi(X.compile_many([X.xslp_decode_bitmatrix_from(G, n, p, er, sv)
                                              for er, sv in plan.keys], specialise=0),
