@@ -45,24 +45,44 @@ def main():
     er = synth.erasure_pattern(5, 0, 24, 4)
     cases = [
         ("cfg2 RS(10,4) enc, PIPE T=128 x 2 words (default line)",
-         X.xslp_encode_bitmatrix(g10, 10, 4), dict(kernel="pipe", threads=128, lane_words=2), "xslp_sl_pipe"),
+         X.xslp_encode_bitmatrix(g10, 10, 4), dict(kernel="pipe", threads=128, lane_words=2, reuse=32),
+         "xslp_sl_pipe"),
+        ("cfg2, same launch, reuse window off",
+         X.xslp_encode_bitmatrix(g10, 10, 4), dict(kernel="pipe", threads=128, lane_words=2, reuse=-1),
+         "xslp_sl_pipe"),
         ("cfg5 RS(20,4) enc, PIPE T=256, 2 input phases",
          X.xslp_encode_bitmatrix(g20, 20, 4), dict(kernel="pipe", threads=256, phases=2), "xslp_sl_pipe"),
+        ("cfg5, same launch, reuse window off",
+         X.xslp_encode_bitmatrix(g20, 20, 4), dict(kernel="pipe", threads=256, phases=2, reuse=-1),
+         "xslp_sl_pipe"),
         ("cfg5d RS(20,4) dec, PIPE T=256, 2 input phases",
          X.xslp_decode_bitmatrix(g20, 20, 4, er)[0], dict(kernel="pipe", threads=256, phases=2), "xslp_sl_pipe"),
         ("cfg2b RS(10,4) enc, byte layout, PIPE T=256",
          X.xslp_encode_bitmatrix(g10, 10, 4), dict(kernel="pipe", threads=256, layout="byte"), "xslp_sl_pipe"),
     ]
     print("# SASS instruction mix (round 1, session 2) -- `scripts/sass_evidence.py`\n")
-    print("PTX from `prog.dump(2)` assembled with `ptxas -arch=sm_100a`, counted with `cuobjdump -sass`.\n")
-    print("| program / launch | entry | SASS | LDS | LOP3 | UBLKCP | SYNCS | LDG | STG | SHF | regs |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|")
+    print("PTX from `prog.dump(2)` assembled with `ptxas -arch=sm_100a`, counted with `cuobjdump -sass`;")
+    print("`reuse` = the constant register reuse window (`xslp_opts.reuse`, auto = 64).\n")
+    print("| program / launch | entry | reuse | SASS | LDS | LOP3 | UBLKCP | SYNCS | LDG | STG | SHF | regs |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|")
     for label, bits, kw, entry in cases:
         p = X.xslp_compile(bits, block_bytes_hint=B, stages=2, **kw)
         m = mix(sass_of(p.dump(2)), entry)
         st = p.stats()
-        print(f"| {label} | `{entry}` | {m['total']} | {m['LDS']} | {m['LOP3']} | {m['UBLKCP']} | "
-              f"{m['SYNCS']} | {m['LDG']} | {m['STG']} | {m['SHF']} | {st['regs_pipe']} |")
+        r = kw.get("reuse", 0)
+        print(f"| {label} | `{entry}` | {'auto (64)' if r == 0 else 'off' if r < 0 else r} | {m['total']} | "
+              f"{m['LDS']} | {m['LOP3']} | {m['UBLKCP']} | {m['SYNCS']} | {m['LDG']} | {m['STG']} | "
+              f"{m['SHF']} | {st['regs_pipe']} |")
+    # the library's precompiled kernels (approach (1)): SASS straight from libxslp.so
+    lib = os.path.join(os.path.dirname(X.__file__), "libxslp.so")
+    sass = subprocess.run([os.path.join(CUDA, "bin", "cuobjdump"), "-sass", lib], check=True,
+                          capture_output=True, text=True).stdout
+    ent = re.search(r"Function : (\S*xslp_gftable_kernelILi4ELi2E\S*)", sass)
+    if ent:
+        m = mix(sass, re.escape(ent.group(1)))
+        print(f"\nApproach (1), `xslp_gftable_kernel<4, 2>` (RS(10,4) rows, 2 x 16 B per thread): "
+              f"{m['total']} SASS, PRMT {m['PRMT']}, LOP3 {m['LOP3']}, SHF {m['SHF']}, LDS {m['LDS']} "
+              f"(the two-block main loop body plus the odd-block tail and the table build).")
     print("\nNo `HMMA`/`UTC*MMA`: the path is bitwise XOR over HBM streams, not a contraction.")
 
 
