@@ -4,7 +4,6 @@ import os
 import re
 import sys
 
-import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -35,4 +34,3 @@ def test_readme_usage_block():
     assert ns["dec"].stats()["n_goals"] == 32
     del data, par, ns
     torch.cuda.empty_cache()
-    assert np.__version__
