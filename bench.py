@@ -362,7 +362,7 @@ def config_of(args, wl, stats):
          "phases": args.phases or (-(-(wl["n"] + wl["p"]) // 10) if args.kernel == "syndrome" else
                                    (-(-wl["n"] // 10) if wl["n"] > 10 else 1)),
          "const_reuse": (args.reuse if args.reuse else
-                         ("auto: 16 (fused kernels)" if args.kernel in ("multi", "syndrome")
+                         ("auto: 16 (syndrome-form kernels)" if args.kernel == "syndrome"
                           else "auto: 64")) if args.kernel not in ("gftable", "interp") else None,
          "cuda_graph": bool(args.graph),
          "l2": "inputs larger than the 126 MB L2; no flush between steps",
@@ -546,7 +546,8 @@ def main():
         if world == 1 and len(progs) > 1:   # all blocks local: the fused multi-program kernels
             pmulti = X.Multi(X.compile_many([X.xslp_decode_bitmatrix_from(G, n, p, er, sv)
                                              for er, sv in plan.keys], specialise=0),
-                             per_module=args.per_module, threads=256, stages=2, block_bytes_hint=B)
+                             per_module=args.per_module, threads=256, stages=2, block_bytes_hint=B,
+                             reuse=args.reuse)
             args.kernel, args.threads = "multi", 256
         pdec = peer.PeerDecoder(X, pl, din, dout, plan, progs, dist=dist, multi=pmulti)
         remote_blocks, all_blocks = plan.remote_reads()

@@ -110,10 +110,10 @@ typedef struct xslp_opts {
   int32_t reuse;           /* constant register reuse window of the TMA-staged kernels (PIPE, TMA,
                               fused multi-program / syndrome): a constant read from shared memory
                               within the last `reuse` instructions keeps its register instead of
-                              a fresh read; 0 = auto (the default: 64 for single-program kernels,
-                              which run one CTA per SM, 16 for the fused kernels, which keep two
-                              CTAs per SM), -1 = a fresh shared-memory read at every use, or
-                              1..4096 */
+                              a fresh read; 0 = auto (the default: 64 for single-program kernels
+                              and the fused M^-1 multi-program kernels, which run one CTA per
+                              SM, 16 for the syndrome-form kernels, which keep two CTAs per SM),
+                              -1 = a fresh shared-memory read at every use, or 1..4096 */
 } xslp_opts;
 
 typedef struct xslp_stats {

@@ -172,7 +172,7 @@ extern "C" int xslp_multi_create(const xslp_program *const *progs, int nprogs, i
   M->threads = o.threads;
   M->stages = o.stages;
   M->lanes = o.lane_words;
-  M->reuse = reuse_window(o.reuse, 16);
+  M->reuse = reuse_window(o.reuse, 64);   // full M^-1 programs: one CTA per SM, registers to spare
   M->nprogs = nprogs;
   M->baked_strip = o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0 ? o.block_bytes_hint / 8 : 0;
   // input phases for wide codes (as the PIPE kernel's opts.phases; 0 = ceil(n/10) for n > 10)
@@ -294,7 +294,7 @@ extern "C" int xslp_syndrome_create(const uint8_t *gf, int n, int p, const int32
   M->threads = o.threads;
   M->stages = o.stages;
   M->lanes = o.lane_words;
-  M->reuse = reuse_window(o.reuse, 16);
+  M->reuse = reuse_window(o.reuse, 16);   // 96 registers keep two CTAs per SM; 24+ drops to one
   M->nprogs = npat;
   M->baked_strip = o.block_bytes_hint > 0 && o.block_bytes_hint % 32 == 0 ? o.block_bytes_hint / 8 : 0;
   int nph = o.phases == 0 ? std::min(8, (nb + 9) / 10) : std::max(1, o.phases);
