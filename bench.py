@@ -52,7 +52,7 @@ WORKLOADS = {
                       "--kernel grouped: one straight-line kernel per pattern; --kernel interp "
                       "(BASELINE configs[2])",
                  n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3,
-                 tuned=dict(kernel="syndrome", threads=256, stages=2, per_module=16, reuse=40)),
+                 tuned=dict(kernel="syndrome", threads=256, stages=2, per_module=16, reuse=40, graph=1)),
     "pdec": dict(desc="RS(10,4) decode of the paper's P_dec pattern {2,4,5,6} (P:1670) on every "
                       "stripe, 1024 stripes x 1 MiB",
                  n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3,
@@ -75,7 +75,7 @@ WORKLOADS = {
                        "syndrome program over 24 blocks in 6 input phases + per-pattern solve "
                        "programs, 10 per kernel); --kernel multi: the M^-1 programs fused",
                   n=20, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=5,
-                  tuned=dict(kernel="syndrome", threads=256, stages=3, phases=6, per_module=10)),
+                  tuned=dict(kernel="syndrome", threads=256, stages=3, phases=6, per_module=10, graph=1)),
     "xdec": dict(desc="RS(10,4) cross-GPU decode (SURVEY NEXT #4): the 14 blocks of each stripe "
                       "spread over the GPUs (block j of stripe s on rank (s+j) mod N), rank s mod N "
                       "decodes stripe s reading its survivors in place from local and NVLink-peer "
@@ -654,7 +654,7 @@ def main():
         # one step's launches (all per-pattern kernels, their fork/join over the internal
         # streams) captured once and replayed: removes the host launch cost, not device work
         for pr in (progs if wl["op"] in ("decode_multi", "decode_peer") else [prog]):
-            if pr is not None:
+            if isinstance(pr, X.Program):    # (the syndrome form's entries are patterns)
                 X.xslp_prepare(pr, B)
         cap = torch.cuda.Stream()
         cap.wait_stream(stream)
