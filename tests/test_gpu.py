@@ -1021,6 +1021,46 @@ def test_cuda_graph_grouped_decode():
             assert (out[s].cpu().numpy() == want).all(), (seed, s)
 
 
+def test_cuda_graph_syndrome_decode():
+    # the syndrome-form heterogeneous decode (several modules over the two internal streams)
+    # captured into one graph, as bench.py's cfg3 / cfg5h replay it; replays on two codeword
+    # sets recover the erased blocks
+    n, p, B, S = 10, 4, 16384, 48
+    g = X.xslp_coding_matrix(n, p)
+    pats = [tuple(synth.erasure_pattern(49, s, n + p, 4)) for s in range(S)]
+    uniq = sorted(set(pats))
+    dec = X.SyndromeDecoder(g, n, p, uniq, per_module=8, threads=256, reuse=40, block_bytes_hint=B)
+    assert dec.info()["modules"] >= 3
+    _, enc = compile_enc(n, p, block_bytes_hint=B)
+    allb = dev_buf(S, n + p, B)
+    t = X.block_table(allb, S, n + p, B).view(S, n + p)
+    zero = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    tin = t.clone()
+    for s_, er in enumerate(pats):
+        for j in er:
+            tin[s_, j] = zero.data_ptr()
+    tin = tin.reshape(-1).contiguous()
+    out = torch.zeros((S, 4, B), dtype=torch.uint8, device="cuda")
+    to = X.block_table(out, S, 4, B)
+    pos = [uniq.index(er) for er in pats]
+    ids, off = X.group_stripes(pos, len(uniq))
+    posd, idsd = torch.tensor(pos, dtype=torch.int32, device="cuda"), torch.from_numpy(ids).cuda()
+    X.xslp_multi_decode(dec, posd, idsd, off, tin, to, B)        # internal streams created
+    torch.cuda.synchronize()
+    out.zero_()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        X.xslp_multi_decode(dec, posd, idsd, off, tin, to, B, stream=torch.cuda.current_stream())
+    assert not out.any()
+    for seed in (50, 51):
+        X.xslp_fill_random(allb, S, n + p, B, seed=seed)
+        X.xslp_encode_batch(enc, t[:, :n].contiguous(), t[:, n:].contiguous(), S, B)
+        gr.replay()
+        torch.cuda.synchronize()
+        for s_, er in enumerate(pats):
+            assert torch.equal(out[s_], allb[s_, list(er)]), (seed, s_, er)
+
+
 # ---- size edges: the 65535 grid-row limit and the widest supported code ------------------
 
 @pytest.mark.parametrize("kern", ["straight", "tma", "pipe", "interp"])
