@@ -170,6 +170,7 @@ class ClockSampler:
 
     def __init__(self, dev_index):
         self.samples, self.reasons, self.ok = [], set(), False
+        self.power, self.limit_w = [], None
         self.stop = threading.Event()
         try:
             import pynvml
@@ -178,6 +179,10 @@ class ClockSampler:
             self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
             self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
+            try:
+                self.limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0
+            except Exception:
+                pass
         except Exception:
             self.max = None
 
@@ -197,6 +202,7 @@ class ClockSampler:
                 for k, bit in names.items():
                     if r & bit:
                         self.reasons.add(k)
+                self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
             except Exception:
                 pass
             time.sleep(0.005)
@@ -215,8 +221,11 @@ class ClockSampler:
     def summary(self):
         s = sorted(self.samples)
         med = s[len(s) // 2] if s else None
+        pw = sorted(self.power)
         return {"sm_mhz": med, "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
-                "samples": len(s), "source": "nvml" if self.ok else "unavailable"}
+                "samples": len(s), "source": "nvml" if self.ok else "unavailable",
+                "power_w": round(pw[len(pw) // 2], 1) if pw else None,
+                "power_limit_w": self.limit_w}
 
 
 # ------------------------------------------------------------------------------------------
