@@ -104,3 +104,33 @@ def test_product_arm_fails_loudly_without_gpu():
     r = _run([sys.executable, "bench.py", "--steps", "1", "--warmup", "0"], timeout=300)
     assert r.returncode != 0
     assert not _json_lines(r.stdout)   # no number printed from a fallback
+
+
+@pytest.mark.gpu
+def test_product_arm_json_contract_on_gpu():
+    # the default line's full contract: metric / value / roofline (bound, achieved, peak, unit,
+    # frac, traffic), cpu_baseline, e2e with the copied bytes, clocks, gpu_launches
+    r = _run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3"], timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = _json_lines(r.stdout)
+    assert len(lines) == 1
+    d = lines[0]
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "roofline",
+              "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
+    assert d["config"]["workload"].startswith("cfg2") and "l2" in d["config"]
+    ro = d["roofline"]
+    assert ro["bound"] == "hbm" and ro["unit"] == "GB/s" and ro["peak"] > 0
+    assert abs(ro["frac"] - ro["achieved"] / ro["peak"]) < 1e-3
+    assert ro["traffic"] is None or ro["traffic"] > 0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["unit"] == "GB/s"
+    assert e["h2d_bytes_per_step"] == 1024 * 10 * (1 << 20)
+    assert e["d2h_bytes_per_step"] == 1024 * 4 * (1 << 20)
+    assert d["gpu_launches"] >= 3
+    c = d["clocks"]
+    assert c["sm_mhz"] and c["sm_max_mhz"] and isinstance(c["reasons"], list)
