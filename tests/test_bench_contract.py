@@ -1,7 +1,7 @@
 """bench.py's driver contract, checked on the CPU: the reference arm (the oracle timed on the
 host cores, `--impl reference`) prints the JSON line the driver parses, alone on rank 0 under
 torchrun; the workload table is consistent; the product arm fails loudly without a GPU
-instead of falling back to anything."""
+instead of falling back to anything.  On a GPU (`-m gpu`): the default line's full contract."""
 import json
 import os
 import socket
