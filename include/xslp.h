@@ -196,6 +196,8 @@ int xslp_compile(const uint8_t *bits, int out_rows, int in_cols, const xslp_opts
  * needs a multiple of 8). */
 int xslp_compile_text(const char *text, int n_const, const xslp_opts *opts, xslp_program **out);
 
+/* The program's metrics (xslp_stats above: #xor, #M, NVar, registers of the JIT kernels, ...)
+ * into *stats (caller-owned).  XSLP_EINVAL on NULL arguments. */
 int xslp_program_stats(const xslp_program *prog, xslp_stats *stats);
 
 /* Text of the program.  form 0: the scheduled MultiSLP with the paper's pebble
@@ -215,6 +217,9 @@ int64_t xslp_program_dump(const xslp_program *prog, int form, char *buf, size_t 
  * (capacity is ignored when iocost is NULL).  Host-side analysis; not on the device path. */
 int xslp_program_cache(const xslp_program *prog, int capacity, int64_t *iocost, int32_t *ccap);
 
+/* Release a program and every device resource cached for it (JIT libraries, bytecode and
+ * micro-op pools).  The caller must not free a program while launches using it are queued on
+ * a stream it has not synchronised.  NULL is a no-op. */
 void xslp_free(xslp_program *prog);
 
 /* ---- device application (timed hot path) ---------------------------------------- */
@@ -372,7 +377,9 @@ int xslp_peer_enable(int peer_device);
 typedef struct xslp_codec xslp_codec;
 int xslp_codec_create(int n, int p, int kind, const xslp_opts *opts, int cache_entries,
                       xslp_codec **out);
-void xslp_codec_free(xslp_codec *codec);
+void xslp_codec_free(xslp_codec *codec);   /* also frees its memoised programs; NULL is a no-op */
+/* Block (shard) size B for len bytes of data: ceil(len / n) rounded up to a multiple of 128,
+ * at least 128; negative (XSLP_EINVAL) for len < 0. */
 int64_t xslp_codec_block_bytes(const xslp_codec *codec, int64_t len);
 /* d_data: len device bytes -> d_shards: (n+p) x B (data copied + padded, parity computed). */
 int xslp_codec_encode(const xslp_codec *codec, const uint8_t *d_data, int64_t len, uint8_t *d_shards,
