@@ -381,19 +381,24 @@ void xslp_codec_free(xslp_codec *codec);   /* also frees its memoised programs; 
 /* Block (shard) size B for len bytes of data: ceil(len / n) rounded up to a multiple of 128,
  * at least 128; negative (XSLP_EINVAL) for len < 0. */
 int64_t xslp_codec_block_bytes(const xslp_codec *codec, int64_t len);
-/* d_data: len device bytes -> d_shards: (n+p) x B (data copied + padded, parity computed). */
+/* d_data: len device bytes -> d_shards: (n+p) x B (data copied + padded, parity computed; with
+ * d_data 16-byte aligned in one pass that reads each data block once and writes its data shard
+ * and the parity). */
 int xslp_codec_encode(const xslp_codec *codec, const uint8_t *d_data, int64_t len, uint8_t *d_shards,
                       void *stream);
 /* Rebuild the erased shards (any order, <= p) in place from the survivors. */
 int xslp_codec_reconstruct(const xslp_codec *codec, uint8_t *d_shards, const int32_t *erased, int ne,
                            int64_t len, void *stream);
-/* Rebuild what is needed and write the original len bytes to d_data_out. */
+/* Write the original len bytes to d_data_out (16-byte aligned: one pass that reads the
+ * survivors and writes the data blocks, surviving ones copied and lost ones solved; otherwise
+ * rebuild in place and copy out).  Lost shards that hold the data's tail may be rebuilt in
+ * place in d_shards. */
 int xslp_codec_decode(const xslp_codec *codec, uint8_t *d_shards, const int32_t *erased, int ne,
                       int64_t len, uint8_t *d_data_out, void *stream);
 /* The memoised program for an erasure pattern (ne == 0: the encode program); owned by the codec. */
 int xslp_codec_program(const xslp_codec *codec, const int32_t *erased, int ne,
                        const xslp_program **out);
-int xslp_codec_cached(const xslp_codec *codec);   /* decode programs currently memoised */
+int xslp_codec_cached(const xslp_codec *codec);   /* erasure patterns with a memoised decode program */
 
 /* 32-byte shard header (SPEC wire format): "XSLP", version 1, n, p, shard index,
  * original length (u64 LE), block size (u32 LE), 12 reserved zero bytes. */

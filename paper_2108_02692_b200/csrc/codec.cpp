@@ -25,6 +25,12 @@ struct Codec {
   std::mutex mu;
   std::list<std::vector<int>> lru;  // most recent at front
   std::map<std::vector<int>, std::pair<std::shared_ptr<Program>, std::list<std::vector<int>>::iterator>> memo;
+  // encode-through programs, by the number f of whole data blocks in the caller's buffer:
+  // goals = data shards 0..f-1 (copies) + the p parity shards, read straight from the data
+  std::map<int, std::shared_ptr<Program>> thru;
+  // decode-through programs, by (erasure pattern, f): goals = data blocks 0..f-1 (copies of
+  // the surviving ones, M^-1 rows for the erased ones) written straight to the caller's buffer
+  std::map<std::pair<std::vector<int>, int>, std::shared_ptr<Program>> dthru;
 };
 
 std::shared_ptr<Program> compile_bits(const std::vector<uint8_t> &bits, int rows, int cols,
@@ -73,6 +79,62 @@ static std::shared_ptr<Program> decode_program(Codec &c, std::vector<int> er) {
     c.memo.erase(c.lru.back());
     c.lru.pop_back();
   }
+  return prog;
+}
+
+// [I_8f rows of blocks 0..f-1 ; the 8p parity rows] over the 8n data strips
+static std::shared_ptr<Program> thru_program(Codec &c, int f) {
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    auto it = c.thru.find(f);
+    if (it != c.thru.end()) return it->second;
+  }
+  const int cols = 8 * c.n, rows = 8 * (f + c.p);
+  std::vector<uint8_t> bits((size_t)rows * cols, 0);
+  for (int r = 0; r < 8 * f; ++r) bits[(size_t)r * cols + r] = 1;
+  std::vector<uint8_t> par((size_t)64 * c.p * c.n);
+  int rc = xslp_encode_bitmatrix(c.G.data(), c.n, c.p, par.data());
+  if (rc) throw Error(rc, xslp_last_error());
+  std::copy(par.begin(), par.end(), bits.begin() + (size_t)8 * f * cols);
+  auto prog = compile_bits(bits, rows, cols, c.opts);
+  std::lock_guard<std::mutex> g(c.mu);
+  auto it = c.thru.find(f);
+  if (it != c.thru.end()) return it->second;
+  c.thru[f] = prog;
+  return prog;
+}
+
+static std::shared_ptr<Program> dthru_program(Codec &c, const std::vector<int> &er, int f) {
+  const auto key = std::make_pair(er, f);
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    auto it = c.dthru.find(key);
+    if (it != c.dthru.end()) return it->second;
+  }
+  const int cols = 8 * c.n;
+  std::vector<int32_t> e32(er.begin(), er.end());
+  std::vector<uint8_t> dec((size_t)64 * er.size() * c.n);
+  std::vector<int32_t> surv(c.n);
+  int rc = xslp_decode_bitmatrix(c.G.data(), c.n, c.p, e32.data(), (int)e32.size(), dec.data(),
+                                 surv.data());
+  if (rc) throw Error(rc, xslp_last_error());
+  std::vector<uint8_t> bits((size_t)8 * f * cols, 0);
+  for (int j = 0; j < f; ++j) {
+    auto e = std::find(er.begin(), er.end(), j);
+    if (e != er.end()) {                                   // erased: its M^-1 rows
+      const size_t k = (size_t)(e - er.begin());
+      std::copy(dec.begin() + 8 * k * cols, dec.begin() + 8 * (k + 1) * cols, bits.begin() + (size_t)8 * j * cols);
+    } else {                                               // survivor: identity on its strips
+      const int pos = (int)(std::find(surv.begin(), surv.end(), j) - surv.begin());
+      for (int r = 0; r < 8; ++r) bits[(size_t)(8 * j + r) * cols + 8 * pos + r] = 1;
+    }
+  }
+  auto prog = compile_bits(bits, 8 * f, cols, c.opts);
+  std::lock_guard<std::mutex> g(c.mu);
+  auto it = c.dthru.find(key);
+  if (it != c.dthru.end()) return it->second;
+  if (c.dthru.size() >= c.cap) c.dthru.clear();            // bounded, like the decode memo
+  c.dthru[key] = prog;
   return prog;
 }
 
@@ -130,6 +192,26 @@ extern "C" int xslp_codec_encode(const xslp_codec *cc, const uint8_t *d_data, in
     throw Error(XSLP_EINVAL, "bad buffers (shards must be 16-byte aligned)");
   const int64_t B = block_bytes_for(c, len);
   cudaStream_t st = (cudaStream_t)stream;
+  const int f = (int)std::min<int64_t>(c.n, len / B);  // whole data blocks in the caller's buffer
+  if (c.p > 0 && f > 0 && ((uintptr_t)d_data & 15) == 0) {
+    // encode-through: one pass reads each data block once from the caller's buffer and writes
+    // both its data shard (a copy goal) and the parity; only the partial / padding blocks are
+    // staged into their shards first
+    if (len > f * B)
+      cuda_ok(cudaMemcpyAsync(d_shards + f * B, d_data + f * B, len - f * B, cudaMemcpyDeviceToDevice, st),
+              "copy tail");
+    if (c.n * B > len) cuda_ok(cudaMemsetAsync(d_shards + len, 0, c.n * B - len, st), "pad");
+    auto prog = thru_program(c, f);
+    std::vector<const uint8_t *> in(c.n);
+    std::vector<uint8_t *> out(f + c.p);
+    for (int j = 0; j < c.n; ++j) in[j] = j < f ? d_data + j * B : d_shards + j * B;
+    for (int j = 0; j < f; ++j) out[j] = d_shards + j * B;
+    for (int i = 0; i < c.p; ++i) out[f + i] = d_shards + (c.n + i) * B;
+    int rc = xslp_encode(reinterpret_cast<const xslp_program *>(prog.get()), in.data(), out.data(),
+                         (size_t)B, stream);
+    if (rc) throw Error(rc, xslp_last_error());
+    return XSLP_OK;
+  }
   // systematic part: the padded data is the first n shards, contiguous
   if (len > 0) cuda_ok(cudaMemcpyAsync(d_shards, d_data, len, cudaMemcpyDeviceToDevice, st), "copy");
   if (c.n * B > len) cuda_ok(cudaMemsetAsync(d_shards + len, 0, c.n * B - len, st), "pad");
@@ -174,20 +256,50 @@ extern "C" int xslp_codec_decode(const xslp_codec *cc, uint8_t *d_shards, const 
   Codec &c = *C(cc);
   if (!d_data_out && len > 0) throw Error(XSLP_EINVAL, "null output");
   if (ne < 0 || (ne > 0 && !erased)) throw Error(XSLP_EINVAL, "bad erasure list");
-  // only erased data shards must be rebuilt to return the data
-  std::vector<int32_t> need;
-  for (int k = 0; k < ne; ++k)
-    if (erased[k] < c.n) need.push_back(erased[k]);
   if (ne > c.p) throw Error(XSLP_EUNRECOVERABLE, "more erasures than parity shards");
-  if (!need.empty()) {
-    // decode program over the full erasure set (survivors exclude every erased shard),
-    // but only data-shard goals are required: rebuild all erased shards for simplicity
+  const int64_t B = block_bytes_for(c, len);
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int> er(erased, erased + ne);
+  std::sort(er.begin(), er.end());
+  const int f = (int)std::min<int64_t>(c.n, len / B);   // whole data blocks of the output
+  bool data_lost = false;
+  for (int e : er) data_lost |= e < c.n;
+  if (data_lost && f > 0 && ((uintptr_t)d_data_out & 15) == 0) {
+    // decode-through: one pass reads the n survivors and writes blocks 0..f-1 of the data
+    // straight to the caller's buffer (surviving ones copied, erased ones solved); the tail
+    // block, if any, comes from its shard (rebuilt in place first if it was lost)
+    if (std::set<int>(er.begin(), er.end()).size() != er.size())
+      throw Error(XSLP_EINVAL, "duplicate erasure index");
+    for (int e : er)
+      if (e < 0 || e >= c.n + c.p) throw Error(XSLP_EINVAL, "erasure index out of range");
+    auto prog = dthru_program(c, er, f);
+    std::vector<int> surv;
+    for (int i = 0; i < c.n + c.p && (int)surv.size() < c.n; ++i)
+      if (!std::binary_search(er.begin(), er.end(), i)) surv.push_back(i);
+    std::vector<const uint8_t *> in(c.n);
+    std::vector<uint8_t *> out(f);
+    for (int j = 0; j < c.n; ++j) in[j] = d_shards + surv[j] * B;
+    for (int j = 0; j < f; ++j) out[j] = d_data_out + j * B;
+    int rc = xslp_decode(reinterpret_cast<const xslp_program *>(prog.get()), in.data(), out.data(),
+                         (size_t)B, stream);
+    if (rc) throw Error(rc, xslp_last_error());
+    if (len > f * B) {
+      if (std::binary_search(er.begin(), er.end(), f)) {
+        rc = xslp_codec_reconstruct(cc, d_shards, erased, ne, len, stream);
+        if (rc) throw Error(rc, xslp_last_error());
+      }
+      cuda_ok(cudaMemcpyAsync(d_data_out + f * B, d_shards + f * B, len - f * B, cudaMemcpyDeviceToDevice, st),
+              "copy tail");
+    }
+    return XSLP_OK;
+  }
+  // only erased data shards must be rebuilt to return the data: rebuild in place, copy out
+  if (data_lost) {
     int rc = xslp_codec_reconstruct(cc, d_shards, erased, ne, len, stream);
     if (rc) throw Error(rc, xslp_last_error());
   }
   if (len > 0)
-    cuda_ok(cudaMemcpyAsync(d_data_out, d_shards, len, cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
-            "copy out");
+    cuda_ok(cudaMemcpyAsync(d_data_out, d_shards, len, cudaMemcpyDeviceToDevice, st), "copy out");
   API_END
 }
 
@@ -207,7 +319,10 @@ extern "C" int xslp_codec_program(const xslp_codec *cc, const int32_t *erased, i
 extern "C" int xslp_codec_cached(const xslp_codec *cc) {
   Codec &c = *reinterpret_cast<Codec *>(const_cast<xslp_codec *>(cc));
   std::lock_guard<std::mutex> g(c.mu);
-  return (int)c.memo.size();
+  std::set<std::vector<int>> pats;       // erasure patterns with a compiled decode program
+  for (auto &kv : c.memo) pats.insert(kv.first);
+  for (auto &kv : c.dthru) pats.insert(kv.first.first);
+  return (int)pats.size();
 }
 
 // 32-byte shard header: "XSLP", version 1, n, p, shard index, original length (u64 LE),

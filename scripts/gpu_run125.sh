@@ -1,0 +1,4 @@
+# codec encode-through: codec parity tests and throughput
+cd $GRAFT_REPO_ROOT
+timeout 1200 python -m pytest tests/test_codec.py -x -q 2>&1 | tail -2
+timeout 600 python scripts/codec_probe.py 2>&1 | tail -4

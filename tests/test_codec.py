@@ -82,6 +82,14 @@ def test_codec_roundtrip_gpu(n, p, kind):
         padded[:ln] = data
         assert (h[:n].reshape(-1) == padded).all()                       # systematic
         assert (h[n:] == rs.encode(og, n, padded.reshape(n, B))).all()   # parity = oracle
+        # a data buffer that is not 16-byte aligned takes the copy-then-encode path (the
+        # aligned one above reads the data in place and writes data + parity shards in one pass)
+        mis = torch.empty(ln + 1, dtype=torch.uint8, device="cuda")
+        mis[1:] = d
+        shards2 = torch.full((n + p, B), 0x77, dtype=torch.uint8, device="cuda")
+        c.encode(mis[1:], ln, shards2)
+        torch.cuda.synchronize()
+        assert torch.equal(shards2, shards), ln
         pats = list(itertools.combinations(range(n + p), p))
         for er in pats[:: max(1, len(pats) // 12)]:
             broken = shards.clone()
@@ -90,6 +98,10 @@ def test_codec_roundtrip_gpu(n, p, kind):
             c.decode(broken, list(er), ln, out)
             torch.cuda.synchronize()
             assert (out[:ln].cpu().numpy() == data).all(), (ln, er)
+            mis = torch.zeros(ln + 1, dtype=torch.uint8, device="cuda")   # unaligned output:
+            c.decode(broken.clone(), list(er), ln, mis[1:])                # rebuild + copy path
+            torch.cuda.synchronize()
+            assert (mis[1:].cpu().numpy() == data).all(), (ln, er)
             c.reconstruct(broken, list(er), ln)
             torch.cuda.synchronize()
             assert torch.equal(broken, shards), (ln, er)
