@@ -179,10 +179,12 @@ struct Program::Dev {
 
 struct JitLib {
   cudaLibrary_t lib = nullptr;
-  cudaKernel_t batch = nullptr, one = nullptr, tma = nullptr, pipe = nullptr;
+  cudaKernel_t batch = nullptr, one = nullptr, tma = nullptr, pipe = nullptr, pipe_one = nullptr;
   std::map<int, int> smem_set;       // device -> max dynamic smem configured for `tma`
   std::map<int, int> smem_set_pipe;  // same for `pipe`
   std::map<int, int> pipe_occ;       // device -> resident pipe CTAs per SM (at smem_set_pipe)
+  std::map<int, int> smem_set_one;   // same two for `pipe_one`
+  std::map<int, int> one_occ;
 };
 
 // Libraries are context independent (cudaLibraryLoadData); keyed by program serial.
@@ -197,6 +199,8 @@ static void load_lib(const std::vector<char> &cubin, JitLib &L) {
   // the byte layout has no TMA variants
   if (cudaLibraryGetKernel(&L.tma, L.lib, "xslp_sl_tma") != cudaSuccess) L.tma = nullptr;
   if (cudaLibraryGetKernel(&L.pipe, L.lib, "xslp_sl_pipe") != cudaSuccess) L.pipe = nullptr;
+  // single-stripe pipeline (strip layout without phases or consumer groups)
+  if (cudaLibraryGetKernel(&L.pipe_one, L.lib, "xslp_sl_pipe_one") != cudaSuccess) L.pipe_one = nullptr;
   cudaGetLastError();
 }
 
@@ -483,6 +487,52 @@ static void apply_one(const Program *p, const uint8_t *const *in, uint8_t *const
   bool straight = kind != XSLP_KERNEL_INTERP && can_straight(p, block_bytes, baked);
   if (kind == XSLP_KERNEL_STRAIGHT && !straight)
     throw Error(XSLP_EINVAL, "straight-line kernel unavailable for this block size / program");
+  if (straight && kind == XSLP_KERNEL_PIPE && p->opts.layout == XSLP_LAYOUT_STRIP &&
+      p->groups.empty() && p->phases.empty()) {
+    // kernel = PIPE: one stripe through the persistent TMA pipeline with the block pointers
+    // passed by value (xslp_sl_pipe_one), no pointer table upload.  AUTO keeps the
+    // register-resident kernel for single stripes: on one stripe of 16-107 MiB blocks the two
+    // measure the same (4.2-4.35 TB/s, profiles/r01_s2_codec.md) and the LDG form wins for the
+    // codec's copy-goal programs
+    const int T = p->opts.threads, L = p->opts.lane_words;
+    uint64_t strip = block_bytes / 8;
+    const size_t smem = 128 + (size_t)p->opts.stages * p->stage_used_const * 4 * L * T;
+    cudaKernel_t k = nullptr;
+    int grid = 0;
+    uint32_t words = (uint32_t)(strip / (4 * L)), tps = (words + T - 1) / T, ntiles = tps;
+    if (strip % 16 == 0 && smem <= 227 * 1024) {
+      libs_of(p);
+      std::lock_guard<std::mutex> g(g_mu);
+      JitLib &J = baked ? g_libs[p].second : g_libs[p].first;
+      k = J.pipe_one;
+      if (k) {
+        const int d = current_device();
+        if (J.smem_set_one[d] < (int)smem) {
+          CUDA_OK(cudaKernelSetAttributeForDevice(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem, d));
+          J.smem_set_one[d] = (int)smem;
+          J.one_occ.erase(d);
+        }
+        int sms = 148, per = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+        auto it = J.one_occ.find(d);
+        if (it != J.one_occ.end()) {
+          per = it->second;
+        } else {
+          CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)k, pipe_block(p), smem));
+          J.one_occ[d] = per;
+        }
+        grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms * std::max(1, per));
+      }
+    }
+    if (k) {
+      const int32_t *no_ids = nullptr;
+      void *args[] = {&one, (void *)&no_ids, &strip, &words, &tps, &ntiles};
+      CUDA_OK(cudaLaunchKernel((const void *)k, dim3(grid), dim3(pipe_block(p)), args, smem, st));
+      g_launches++;
+      return;
+    }
+    // otherwise (phases, consumer groups, misaligned strips): the register-resident kernel
+  }
   if (straight) {
     auto libs = libs_of(p);
     const JitLib &L = baked ? libs.second : libs.first;

@@ -255,14 +255,17 @@ struct Emitter {
       o << "  setp.ge.u32 %p0, %s3, %s4;\n  @%p0 bra $CSKIP" << x << ";\n";
       o << "  mul.lo.u32 %sth, %st, " << STAGE << ";\n  add.u32 %sth, %sth, %sb;\n";
       o << "  mad.lo.u32 %sth, %ltid, " << 4 * L << ", %sth;\n  add.u32 %sth, %sth, 128;\n";
-      o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
+      if (pipe_one)   // single stripe: the block pointers are kernel parameters (p_ptrs)
+        o << "  mov.u64 %rd3, p_ptrs;\n  cvta.param.u64 %rd3, %rd3;\n  add.s64 %rd3, %rd3, " << 8 * n_in << ";\n";
+      else
+        o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
       o << "  mul.wide.u32 %off, %s3, " << 4 * L << ";\n";
       std::vector<char> oused(n_out, 0);
       for (int q = 0; q < (int)cur().goal.size(); ++q)
         if (cur().goal[q] != -2) oused[q / 8] = 1;
       for (int i = 0; i < n_out; ++i) {
         if (!oused[i]) continue;
-        o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
+        o << (pipe_one ? "  ld.u64 %ob" : "  ld.global.nc.u64 %ob") << i << ", [%rd3+" << 8 * i << "];\n";
         o << "  add.s64 %ob" << i << ", %ob" << i << ", %off;\n";
       }
       int tmp = 0;
@@ -283,11 +286,14 @@ struct Emitter {
     o << "  sub.u32 %nb, %s4, %s7;\n  min.u32 %nb, %nb, " << TC << ";\n  mul.lo.u32 %nb, %nb, " << 4 * L << ";\n";
     o << "  mul.lo.u32 %s6, %nb, " << nused << ";\n";
     o << "  mbarrier.arrive.expect_tx.shared::cta.b64 _, [%fb], %s6;\n";
-    o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
+    if (pipe_one)
+      o << "  mov.u64 %rd2, p_ptrs;\n  cvta.param.u64 %rd2, %rd2;\n";
+    else
+      o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
     o << "  mul.wide.u32 %toff, %s7, " << 4 * L << ";\n";
     for (int j = 0; j < n_in; ++j) {
       if (!blk_used[j]) continue;
-      o << "  ld.global.nc.u64 %ib" << j << ", [%rd2+" << 8 * j << "];\n";
+      o << (pipe_one ? "  ld.u64 %ib" : "  ld.global.nc.u64 %ib") << j << ", [%rd2+" << 8 * j << "];\n";
       o << "  add.s64 %ib" << j << ", %ib" << j << ", %toff;\n";
     }
     o << "  mul.lo.u32 %dst, %st, " << STAGE << ";\n  add.u32 %dst, %dst, %sb;\n";
@@ -605,6 +611,7 @@ struct Emitter {
     o << "  st.global" << vsuf() << " " << a << ", " << vec(r) << ";\n";
   }
   bool accumulate = false;
+  bool pipe_one = false;   // body_pipe for one stripe: block pointers in the p_ptrs parameter
   bool multi_acc = false;  // phased multi-program kernel: declare the accumulators
   int reuse = 0;   // constant register reuse window in instructions (xslp_opts.reuse)
 
@@ -1242,6 +1249,17 @@ struct Emitter {
     decls(ntmp);
     if (phases) body_pipe_phases(stages); else body_pipe(stages);
     o << "}\n";
+    if (!phases && !groups) {  // one stripe, pointers by value (xslp_encode / xslp_decode)
+      o << "\n.visible .entry xslp_sl_pipe_one(\n  .param .align 8 .b8 p_ptrs[1024],\n"
+           "  .param .u64 p_ids,\n  .param .u64 p_strip,\n  .param .u32 p_words,\n"
+           "  .param .u32 p_tps,\n  .param .u32 p_ntiles)\n.maxntid "
+        << threads + 32 << ", 1, 1\n{\n";
+      decls(ntmp);
+      pipe_one = true;
+      body_pipe(stages);
+      pipe_one = false;
+      o << "}\n";
+    }
     return o.str();
   }
 };

@@ -360,6 +360,34 @@ def test_syndrome_full_size_bench_config(wname):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("n,p,kind,er,B,kern", [(10, 4, "isal", None, (16 << 20) + 1152, "auto"),
+                                                (10, 4, "isal", (2, 4, 5, 6), 16 << 20, "pipe"),
+                                                (4, 2, "cauchy", None, 8 << 20, "pipe"),
+                                                (20, 4, "isal", None, 4 << 20, "auto")])
+def test_single_stripe_large_blocks(n, p, kind, er, B, kern):
+    # one stripe through xslp_encode / xslp_decode (block pointers as kernel arguments): large
+    # blocks take the TMA pipeline's single-stripe entry (xslp_sl_pipe_one; RS(20,4) has input
+    # phases and keeps the register-resident kernel); every byte equals the oracle's
+    og = mx.coding_matrix(n, p, kind)
+    g = X.xslp_coding_matrix(n, p, kind)
+    data = synth.stripe_data(61, 0, n, B)
+    if er is None:
+        bits, rows, ins = X.xslp_encode_bitmatrix(g, n, p), og[n:], data
+    else:
+        bits, surv = X.xslp_decode_bitmatrix(g, n, p, list(er))
+        blocks = np.concatenate([data, rs.encode(og, n, data)])
+        osurv, rows = mx.decode_rows(og, n, list(er))
+        assert list(surv) == osurv
+        ins = blocks[osurv]
+    prog = X.xslp_compile(bits, kernel=kern, threads=128, lane_words=2 if n <= 10 else 1)
+    din = torch.from_numpy(np.ascontiguousarray(ins)).cuda()
+    m = bits.shape[0] // 8
+    out = torch.full((m, B), 0x3C, dtype=torch.uint8, device="cuda")
+    X.xslp_encode(prog, [din[j] for j in range(n)], [out[i] for i in range(m)], B)
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy() == rs.apply_rows(rows, ins)).all()
+
+
 def test_edge_cases():
     n, p = 4, 2
     _, prog = compile_enc(n, p, "cauchy")
