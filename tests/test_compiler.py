@@ -80,7 +80,7 @@ def test_const_reuse_window_codegen():
     assert auto.dump(2).count("ld.volatile.shared") == counts[64]    # auto = 64 (single program)
     # the host's count of those reads (AUTO's shared-memory estimate) follows the same rule as
     # the emitter: one read per constant operand with the window off, each constant once when
-    # every reuse distance is inside the window; PTX = the TMA and the PIPE kernel bodies
+    # every reuse distance is inside the window; PTX = the TMA, PIPE and single-stripe PIPE bodies
     g10 = X.xslp_coding_matrix(10, 4)
     for compress in ("none", "xorrepair"):
         uses = None
@@ -88,7 +88,9 @@ def test_const_reuse_window_codegen():
             prog = X.xslp_compile(X.xslp_encode_bitmatrix(g10, 10, 4), compress=compress, threads=256,
                                   block_bytes_hint=1 << 20, reuse=r)
             st = prog.stats()
-            assert 2 * st["smem_reads"] == prog.dump(2).count("ld.volatile.shared")
+            ptx = prog.dump(2)
+            bodies = sum(ptx.count(f".entry {e}(") for e in ("xslp_sl_tma", "xslp_sl_pipe", "xslp_sl_pipe_one"))
+            assert bodies == 3 and bodies * st["smem_reads"] == ptx.count("ld.volatile.shared")
             if r == -1:
                 uses = st["smem_reads"]      # every constant operand of every instruction
                 assert st["n_instr"] < uses <= st["mem_count"] - st["n_instr"]
