@@ -430,8 +430,8 @@ def test_random_programs_and_launches(case):
     # seeded fuzz over program shape and launch knobs: a random bitmatrix (1-24 input blocks,
     # 1-6 output blocks, random density incl. empty and full rows) through a random launch of
     # the straight-line / TMA / PIPE kernels (threads, words per thread, stages, input phases,
-    # reuse window, ragged block size, stripes) must give the oracle's bytes; launches the
-    # library rejects as not fitting (EINVAL) are skipped, and most cases must run
+    # reuse window, ragged block size, stripes; every fifth case the single-stripe call) must
+    # give the oracle's bytes; launches the library rejects as not fitting (EINVAL) are skipped
     rng = np.random.default_rng(7000 + case)
     n_in, m_out = int(rng.integers(1, 25)), int(rng.integers(1, 7))
     dens = float(rng.choice([0.02, 0.1, 0.3, 0.5, 0.9]))
@@ -451,12 +451,18 @@ def test_random_programs_and_launches(case):
     S = int(rng.integers(1, 5))
     if rng.random() < 0.5:
         kw["block_bytes_hint"] = B
+    one = case % 5 == 0                 # the single-stripe call (block pointers by value)
+    if one:
+        S = 1
     try:
         prog = X.xslp_compile(bits, **kw)
         data = host_data(7000 + case, range(S), n_in, B)
         din = torch.from_numpy(data).cuda()
         out = torch.full((S, m_out, B), 0xA5, dtype=torch.uint8, device="cuda")
-        run_batch(prog, din, out, B)
+        if one:
+            X.xslp_encode(prog, [din[0, j] for j in range(n_in)], [out[0, i] for i in range(m_out)], B)
+        else:
+            run_batch(prog, din, out, B)
         torch.cuda.synchronize()
     except X.XslpError as e:
         assert e.code == X.XSLP_EINVAL, (case, kw, str(e))
