@@ -770,6 +770,15 @@ extern "C" int xslp_prepare(const xslp_program *prog, size_t block_bytes) {
         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)J->pipe, pipe_block(p), smem_pipe));
         J->pipe_occ[d] = per;
       }
+      if (J->pipe_one && smem_pipe <= 227 * 1024 && J->smem_set_one[d] < (int)smem_pipe) {
+        CUDA_OK(cudaKernelSetAttributeForDevice(J->pipe_one, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem_pipe, d));
+        J->smem_set_one[d] = (int)smem_pipe;
+        int per = 0;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)J->pipe_one, pipe_block(p),
+                                                              smem_pipe));
+        J->one_occ[d] = per;
+      }
       if (J->tma && smem_tma <= 227 * 1024 && J->smem_set[d] < (int)smem_tma) {
         CUDA_OK(cudaKernelSetAttributeForDevice(J->tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)smem_tma, d));
