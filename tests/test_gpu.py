@@ -1020,6 +1020,27 @@ def test_cuda_graph_capture(kern):
     assert (dout[3].cpu().numpy() == enc(synth.stripe_data(45, 3, n, B))).all()
 
 
+def test_cuda_graph_single_stripe_pipeline():
+    # the single-stripe pipeline entry (pointers as kernel parameters) captured after
+    # xslp_prepare; the graph replays on new data in the same buffers
+    n, p, B = 10, 4, 4 << 20
+    og = mx.coding_matrix(n, p)
+    _, prog = compile_enc(n, p, kernel="pipe", threads=128, lane_words=2)
+    X.xslp_prepare(prog, B)
+    din = dev_buf(1, n, B)
+    out = torch.zeros((p, B), dtype=torch.uint8, device="cuda")
+    ins, outs = X.block_ptrs([din[0, j] for j in range(n)]), X.block_ptrs([out[i] for i in range(p)])
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        X.xslp_encode(prog, ins, outs, B)
+    for seed in (71, 72):
+        X.xslp_fill_random(din, 1, n, B, seed=seed)
+        g.replay()
+        torch.cuda.synchronize()
+        assert (out.cpu().numpy() == rs.encode(og, n, synth.stripe_data(seed, 0, n, B))).all(), seed
+
+
 def test_cuda_graph_grouped_decode():
     # heterogeneous decode (per-pattern kernels forked over internal streams) captured into one
     # graph (bench.py cfg3 --graph 1); replays equal the oracle's decode, also on new inputs
