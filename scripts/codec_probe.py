@@ -25,7 +25,8 @@ def timed(fn, iters=20):
     return e0.elapsed_time(e1) / iters
 
 
-c = X.Codec(10, 4)
+T = int(sys.argv[1]) if len(sys.argv) > 1 else 128     # consumer threads of the codec's programs
+c = X.Codec(10, 4, threads=T)
 for length in (10 << 20, 100 << 20, 1 << 30):
     B = c.block_bytes(length)
     data = torch.empty(length, dtype=torch.uint8, device="cuda")
@@ -39,7 +40,7 @@ for length in (10 << 20, 100 << 20, 1 << 30):
     assert torch.equal(shards, ref)
     ms_d = timed(lambda: c.decode(shards, er, length, out))
     assert torch.equal(out, data)
-    print(json.dumps({"probe": "codec RS(10,4)", "bytes": length, "block_bytes": B,
+    print(json.dumps({"probe": "codec RS(10,4)", "threads": T, "bytes": length, "block_bytes": B,
                       "encode_gbs": round(length / ms_e / 1e6, 1),
                       "reconstruct4_gbs": round(length / ms_r / 1e6, 1),
                       "decode4_gbs": round(length / ms_d / 1e6, 1)}), flush=True)
