@@ -130,7 +130,7 @@ def parse():
     ap.add_argument("--distinct", type=int, default=0,
                     help="diagnostic: only K distinct erasure patterns (stripe s takes pattern s mod K)")
     ap.add_argument("--per-module", type=int, default=None,
-                    help="programs per fused multi-program kernel (--kernel multi)")
+                    help="programs (or erasure patterns) per fused kernel (--kernel multi / syndrome)")
     ap.add_argument("--threads", type=int, default=None)
     ap.add_argument("--block-bytes", type=int, default=0, help="override block size")
     ap.add_argument("--p", type=int, default=0, help="override parity count (cfg4 sweep)")
