@@ -35,7 +35,7 @@ MiB = 1 << 20
 WORKLOADS = {
     "cfg2": dict(desc="RS(10,4) encode, 1024 stripes x 10 x 1 MiB per GPU (BASELINE configs[1])",
                  n=10, p=4, B=MiB, S=1024, op="encode", seed=2,
-                 tuned=dict(kernel="pipe", threads=128, lanes=2, stages=2, reuse=32)),
+                 tuned=dict(kernel="pipe", threads=128, lanes=2, stages=3, phases=2, reuse=32)),
     "cfg2b": dict(desc="RS(10,4) encode in the byte-compatible layout (output = textbook byte-wise "
                        "RS, SURVEY NEXT #3), 1024 stripes x 10 x 1 MiB",
                   n=10, p=4, B=MiB, S=1024, op="encode", seed=2, layout="byte",

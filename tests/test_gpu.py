@@ -583,18 +583,20 @@ def _xor_reduce(t):
 @pytest.mark.parametrize("kern,threads,lanes,reuse", [("straight", 128, 1, 0), ("tma", 128, 1, 0),
                                                       ("pipe", 256, 1, 0), ("pipe", 128, 2, "bench")])
 def test_cfg2_full_size_sampled(kern, threads, lanes, reuse):
-    # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); ("pipe", 128, 2 lanes) with 2 stages and
-    # bench's reuse window is the exact launch configuration bench.py times by default
+    # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); ("pipe", 128, 2 lanes) with bench's
+    # stages, input phases and reuse window is the exact launch configuration bench.py times
     n, p, B, S = 10, 4, 1 << 20, 1024
     if reuse == "bench":
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         import bench
         t = bench.WORKLOADS["cfg2"]["tuned"]
-        assert (t["kernel"], t["threads"], t["lanes"], t["stages"]) == (kern, threads, lanes, 2)
-        reuse = t.get("reuse", 0)
+        assert (t["kernel"], t["threads"], t["lanes"]) == (kern, threads, lanes)
+        reuse, stages, phases = t.get("reuse", 0), t.get("stages", 2), t.get("phases", 0)
+    else:
+        stages, phases = 2, 0
     og = mx.coding_matrix(n, p)
-    _, prog = compile_enc(n, p, block_bytes_hint=B, kernel=kern, threads=threads, stages=2,
-                          lane_words=lanes, reuse=reuse)
+    _, prog = compile_enc(n, p, block_bytes_hint=B, kernel=kern, threads=threads, stages=stages,
+                          lane_words=lanes, reuse=reuse, phases=phases)
     din = dev_buf(S, n, B)
     X.xslp_fill_random(din, S, n, B, seed=2)
     dout = dev_buf(S, p, B)
