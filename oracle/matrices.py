@@ -66,7 +66,12 @@ def gf_invert(m):
 
 
 def vandermonde(n, p):
-    """(n+p) x n, row i (i = 1..n+p) = (1, a^i, (a^i)^2, ...), a = 0x02."""
+    """(n+p) x n, row i (i = 1..n+p) = (1, a^i, (a^i)^2, ...), a = 0x02.
+
+    Pinned through coding_matrix(kind="sysvand"): M V^-1 equals the Lagrange closed form
+    L_j(y_k) computed without Gauss-Jordan and without this module's field tables
+    (tests/test_oracle_gf.py::test_sysvand_equals_lagrange_closed_form, RS(2,1) by hand).
+    """
     rows = []
     for i in range(1, n + p + 1):
         ai = gf_pow(2, i)

@@ -121,6 +121,92 @@ def test_sysvand_is_systematic_and_text_construction():
     assert mx.gf_matmul(g, v[:10]) == v
 
 
+def _mul_long_division(a, b):
+    """a*b mod x^8+x^4+x^3+x^2+1 (P:1378) by carry-less product then long division;
+    no tables and no oracle code, so the Lagrange pin below is independent of gf256."""
+    prod = 0
+    for k in range(8):
+        if (b >> k) & 1:
+            prod ^= a << k
+    for deg in range(14, 7, -1):
+        if (prod >> deg) & 1:
+            prod ^= 0x11D << (deg - 8)
+    return prod
+
+
+def _inv_by_search(a):
+    return next(x for x in range(1, 256) if _mul_long_division(a, x) == 1)
+
+
+def _alpha_pow(e):
+    x = 1
+    for _ in range(e):
+        x = _mul_long_division(x, 2)
+    return x
+
+
+def _lagrange_rows(n, p, first_exp=1, nodes=None):
+    """Rows of M V^-1 in closed form, without Gauss-Jordan.
+
+    V stacks rows (1, x, x^2, ..., x^{n-1}) at the nodes x_i = alpha^{first_exp + i},
+    i = 0..n+p-1 (or the given nodes); the top n nodes form V, the last p form M.  Row
+    (1, y, ..., y^{n-1}) of M is the interpolation of the monomials at y:
+    sum_j L_j(y) * (row of node x_j), so
+    (M V^-1)[k][j] = L_j(y_k) = prod_{m != j} (y_k - x_m) / (x_j - x_m), with - = xor.
+    """
+    xs = nodes if nodes is not None else [_alpha_pow(first_exp + i) for i in range(n + p)]
+    top, ys = xs[:n], xs[n:]
+    rows = []
+    for y in ys:
+        row = []
+        for j in range(n):
+            num, den = 1, 1
+            for m in range(n):
+                if m != j:
+                    num = _mul_long_division(num, y ^ top[m])
+                    den = _mul_long_division(den, top[j] ^ top[m])
+            row.append(_mul_long_division(num, _inv_by_search(den)))
+        rows.append(row)
+    return rows
+
+
+@pytest.mark.parametrize("n,p", [(2, 1), (4, 2), (10, 4), (20, 4)])
+def test_sysvand_equals_lagrange_closed_form(n, p):
+    # The text's Vandermonde has rows i = 1..n+p with node alpha^i (P:1385-1388: the first
+    # row is (1, alpha, ..., alpha^9), the last (1, alpha^14, ...)), reduced to [I; M V^-1]
+    # (P:1398-1402).  The closed form replaces Gauss-Jordan and the matrix product.
+    g = mx.coding_matrix(n, p, "sysvand")
+    want = _lagrange_rows(n, p)
+    assert g[n:] == want
+    # Shifting every node by the same power of alpha scales column j of V by alpha^{sj} on
+    # both V and M, which cancels in M V^-1: nodes alpha^0..alpha^{n+p-1} give the SAME
+    # matrix (so that "mistake" is not one).  Mistakes that do change it:
+    assert _lagrange_rows(n, p, first_exp=0) == want
+    #  * integer nodes 1..n+p instead of powers of alpha,
+    assert _lagrange_rows(n, p, nodes=list(range(1, n + p + 1))) != want
+    #  * parity rows taken from the top of V instead of the bottom (M = first p rows),
+    xs = [_alpha_pow(1 + i) for i in range(n + p)]
+    assert _lagrange_rows(n, p, nodes=xs[p:] + xs[:p]) != want
+    #  * rows (x, x^2, ..., x^n) (exponents from 1): row k of M V^-1 scales by y_k / x_j.
+    shifted = [[_mul_long_division(_mul_long_division(v, xs[n + k]), _inv_by_search(xs[j]))
+                for j, v in enumerate(row)] for k, row in enumerate(want)]
+    assert shifted != want
+    # each row of M V^-1 interpolates the constant 1: sum_j L_j(y) = 1
+    for row in want:
+        s = 0
+        for v in row:
+            s ^= v
+        assert s == 1
+
+
+def test_sysvand_rs21_by_hand():
+    # RS(2,1): nodes x1 = alpha = 2, x2 = alpha^2 = 4, y = alpha^3 = 8 (P:1385-1388).
+    # L_1(8) = (8+4)/(2+4) = 0x0C/0x06 = 2 (since 2*6 = 0x0C, no reduction);
+    # L_2(8) = (8+2)/(4+2) = 0x0A/0x06 = 3 (since 3*6 = 0x0A: 6 ^ 0x0C).
+    g = mx.coding_matrix(2, 1, "sysvand")
+    assert g == [[1, 0], [0, 1], [2, 3]]
+
+
 def test_isal_raid5_row_and_values():
     g = mx.coding_matrix(10, 4, "isal")
     assert g[10] == [1] * 10                      # (2^0)^j = 1
