@@ -286,7 +286,10 @@ int xslp_multi_create(const xslp_program *const *progs, int nprogs, int per_modu
  * xslp_decode_batch_grouped, which must agree with d_prog_of_stripe).  One launch per module
  * that has stripes; consecutive modules alternate between two internal streams forked from
  * and joined back into `stream` (capturable in a CUDA graph).  block_bytes % 128 == 0.
- * Tables as in xslp_encode_batch. */
+ * Tables as in xslp_encode_batch.  group_offsets must hold nprogs + 1 non-decreasing entries
+ * (XSLP_EINVAL otherwise; the library reads exactly that many).  A d_prog_of_stripe entry
+ * outside the module that owns the stripe makes that launch trap (a CUDA error reported at
+ * the next synchronisation) rather than branch outside the module's code. */
 int xslp_multi_decode(const xslp_multi *multi, const int32_t *d_prog_of_stripe,
                       const int32_t *d_stripe_ids, const int32_t *group_offsets,
                       const uint8_t *const *d_in_tbl, uint8_t *const *d_out_tbl,
@@ -329,7 +332,9 @@ int xslp_encode_host(const xslp_program *prog, const uint8_t *h_in, uint8_t *h_o
 /* Seeded synthetic input on the device (same counter-based generator as the
  * repo's synth module; no coding arithmetic): d_buf = [nstripes][nblocks][block_bytes],
  * block j of global stripe s word i = splitmix64(seed*0x9E3779B97F4A7C15 +
- * ((s*64 + j) << 40) + i), s = stripe0 + local index.  block_bytes % 8 == 0. */
+ * ((s*64 + j) << 40) + i), s = stripe0 + local index.  block_bytes % 8 == 0.
+ * XSLP_EINVAL unless nblocks <= 64 and 0 <= stripe0, stripe0 + nstripes <= 2^18 (the range
+ * in which the counter keys of distinct words are distinct). */
 int xslp_fill_random(uint8_t *d_buf, int nstripes, int nblocks, size_t block_bytes,
                      uint64_t seed, int64_t stripe0, void *stream);
 

@@ -385,6 +385,7 @@ class Multi:
 
     def __init__(self, progs, per_module=20, opts=None, **kw):
         self._progs = list(progs)          # keep the programs alive
+        self.nprogs = len(self._progs)
         o = opts if opts is not None else default_opts(**kw)
         arr = (ctypes.c_void_p * len(self._progs))(*[p.handle for p in self._progs])
         h = _P()
@@ -418,6 +419,7 @@ class SyndromeDecoder(Multi):
     def __init__(self, gf, n, p, patterns, per_module=0, opts=None, **kw):   # noqa: super
         self._progs = []
         pats = np.ascontiguousarray([sorted(er) for er in patterns], dtype=np.int32)
+        self.nprogs = pats.shape[0]
         g = np.ascontiguousarray(gf, dtype=np.uint8)
         o = opts if opts is not None else default_opts(**kw)
         h = _P()
@@ -429,6 +431,8 @@ class SyndromeDecoder(Multi):
 def xslp_multi_decode(multi, d_prog_of_stripe, d_stripe_ids, group_offsets, d_in_tbl, d_out_tbl,
                       block_bytes, stream=None):
     off = np.ascontiguousarray(group_offsets, dtype=np.int32)
+    if len(off) != multi.nprogs + 1:
+        raise ValueError("group_offsets needs nprogs + 1 entries")
     _check(_lib.xslp_multi_decode(multi.handle, _ptr(d_prog_of_stripe), _ptr(d_stripe_ids),
                                   off.ctypes.data, _ptr(d_in_tbl), _ptr(d_out_tbl), block_bytes,
                                   _stream(stream)))

@@ -869,6 +869,10 @@ extern "C" int xslp_fill_random(uint8_t *d_buf, int nstripes, int nblocks, size_
   API_BEGIN
   if (!d_buf || nstripes < 0 || nblocks < 0 || block_bytes % 8 || ((uintptr_t)d_buf & 7))
     throw Error(XSLP_EINVAL, "bad fill arguments");
+  // the counter key ((s*64 + j) << 40) + i is distinct only for j < 64, s < 2^18, i < 2^40
+  if (nblocks > 64 || stripe0 < 0 || stripe0 + (int64_t)nstripes > (int64_t(1) << 18) ||
+      block_bytes / 8 >= (uint64_t(1) << 40))
+    throw Error(XSLP_EINVAL, "fill key range: need nblocks <= 64 and stripes < 2^18");
   const uint64_t wpb = block_bytes / 8;
   const uint64_t total = wpb * (uint64_t)nblocks * (uint64_t)nstripes;
   if (total == 0) return XSLP_OK;

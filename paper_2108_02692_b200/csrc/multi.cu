@@ -389,6 +389,12 @@ extern "C" int xslp_multi_decode(const xslp_multi *multi, const int32_t *d_prog_
   if (!multi || !d_prog_of_stripe || !d_stripe_ids || !group_offsets || !d_in_tbl || !d_out_tbl)
     throw Error(XSLP_EINVAL, "null argument");
   if (group_offsets[0] < 0) throw Error(XSLP_EINVAL, "negative group offset");
+  {
+    const Multi &M = *reinterpret_cast<const Multi *>(multi);
+    for (int i = 0; i < M.nprogs; ++i)
+      if (group_offsets[i + 1] < group_offsets[i])
+        throw Error(XSLP_EINVAL, "group offsets must be non-decreasing (nprogs + 1 entries)");
+  }
   if (block_bytes == 0) return XSLP_OK;
   Multi &M = *reinterpret_cast<Multi *>(const_cast<xslp_multi *>(multi));
   multi_launch(M, d_prog_of_stripe, d_stripe_ids, group_offsets, d_in_tbl, d_out_tbl, block_bytes,

@@ -728,6 +728,9 @@ struct Emitter {
     o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
     o << "  mul.wide.u32 %rd6, %s5, 4;\n  add.s64 %rd6, %rpm, %rd6;\n  ld.global.nc.u32 %pk, [%rd6];\n";
     o << "  sub.u32 %pk, %pk, %pfirst;\n";
+    // a table entry outside this module would send brx.idx out of its branch table: trap
+    // (the launch fails with an error) instead of jumping to an arbitrary address
+    o << "  setp.ge.u32 %p0, %pk, " << progs.size() << ";\n  @%p0 trap;\n";
     o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
     for (int i = 0; i < n_out; ++i) o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
     o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
@@ -972,6 +975,9 @@ struct Emitter {
     o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
     o << "  mul.wide.u32 %rd6, %s5, 4;\n  add.s64 %rd6, %rpm, %rd6;\n  ld.global.nc.u32 %pk, [%rd6];\n";
     o << "  sub.u32 %pk, %pk, %pfirst;\n";
+    // a table entry outside this module would send brx.idx out of its branch table: trap
+    // (the launch fails with an error) instead of jumping to an arbitrary address
+    o << "  setp.ge.u32 %p0, %pk, " << progs.size() << ";\n  @%p0 trap;\n";
     o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
     for (int i = 0; i < n_out; ++i) o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
     o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";
@@ -1102,6 +1108,9 @@ struct Emitter {
     o << "  mul.wide.u32 %rd1, %s5, 4;\n  add.s64 %rd1, %rd0, %rd1;\n  ld.global.nc.u32 %s5, [%rd1];\n";
     o << "  mul.wide.u32 %rd6, %s5, 4;\n  add.s64 %rd6, %rpm, %rd6;\n  ld.global.nc.u32 %pk, [%rd6];\n";
     o << "  sub.u32 %pk, %pk, %pfirst;\n";
+    // a table entry outside this module would send brx.idx out of its branch table: trap
+    // (the launch fails with an error) instead of jumping to an arbitrary address
+    o << "  setp.ge.u32 %p0, %pk, " << solves.size() << ";\n  @%p0 trap;\n";
     o << "  ld.param.u64 %rd3, [p_out];\n  mul.wide.u32 %rd5, %s5, " << 8 * n_out << ";\n  add.s64 %rd3, %rd3, %rd5;\n";
     for (int i = 0; i < n_out; ++i) o << "  ld.global.nc.u64 %ob" << i << ", [%rd3+" << 8 * i << "];\n";
     o << "  ld.param.u64 %rd2, [p_in];\n  mul.wide.u32 %rd4, %s5, " << 8 * n_in << ";\n  add.s64 %rd2, %rd2, %rd4;\n";

@@ -39,6 +39,9 @@ def block_bytes(seed, stripe, block, nbytes):
     """Bytes of data block ``block`` of global stripe ``stripe`` (nbytes % 8 == 0)."""
     if nbytes % 8:
         raise ValueError("nbytes must be a multiple of 8")
+    # the key ((s*64 + j) << 40) + i is distinct only for j < 64, s < 2^18, i < 2^40
+    if not (0 <= block < 64 and 0 <= stripe < (1 << 18)):
+        raise ValueError("fill key range: need block < 64 and stripe < 2^18")
     base = (seed * GOLDEN + ((stripe * 64 + block) << 40)) & M64
     with np.errstate(over="ignore"):
         idx = np.arange(nbytes // 8, dtype=np.uint64) + np.uint64(base)
