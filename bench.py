@@ -349,7 +349,7 @@ def run_reference(args, wl, rank, world):
 def kernel_name(args, wl, stats):
     k = args.kernel
     if k == "interp":
-        return "xslp_interp_kernel"
+        return "xslp_interp_pipe"
     if k in ("tma", "grouped_tma"):
         return "xslp_sl_tma"
     if k in ("pipe", "grouped_pipe"):
@@ -474,7 +474,8 @@ def main():
             log("multi", multi.info())
         elif mode == "interp":
             progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,
-                                   threads=args.threads)
+                                   threads=args.threads, lane_words=args.lanes,
+                                   stages=args.stages)
         else:   # one JIT straight-line (or TMA) kernel per distinct erasure pattern
             progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=1,
                                    threads=args.threads, lane_words=args.lanes,

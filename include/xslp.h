@@ -203,8 +203,9 @@ int xslp_program_stats(const xslp_program *prog, xslp_stats *stats);
 /* Text of the program.  form 0: the scheduled MultiSLP with the paper's pebble
  * names and a final "return" line; form 1: the interpreter's slot program
  * (initial "s<k> = c<j>" loads, slot instructions, "out <g> = ..." stores);
- * form 2: the straight-line kernel's PTX; form 3: the pipelined interpreter's micro-op code for
- * T = opts.threads, as decimal 32-bit words (layout in csrc/interp.cu build_code32).  Format: one statement per line,
+ * form 2: the straight-line kernel's PTX; form 3: the pipelined interpreter's paired micro-op
+ * code (stage-0 variant) for T = opts.threads, L = opts.lane_words, S = opts.stages, as decimal
+ * 32-bit words (layout in csrc/interp.cu emit_variant).  Forms 0/1 format: one statement per line,
  * "<var> = <term> ^ <term> ...", "out <g> = <term>", "return <term> ...", terms
  * c<j> (constant), 0 (empty set) or a variable name; statements are sequential.
  * Writes at most cap bytes including the NUL; returns the full length needed

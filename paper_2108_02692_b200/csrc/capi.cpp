@@ -396,8 +396,9 @@ extern "C" int64_t xslp_program_dump(const xslp_program *prog, int form, char *b
     } else if (form == 2) {
       s = P.ptx_baked.empty() ? P.ptx_generic : P.ptx_baked;
     } else if (form == 3) {
-      // the pipelined interpreter's micro-op code for T = opts.threads
-      auto w = build_code32(P.code, P.opts.threads);
+      // the pipelined interpreter's micro-op code (stage-0 variant) for this program's opts
+      const int L = P.opts.lane_words == 2 || P.opts.lane_words == 4 ? P.opts.lane_words : 1;
+      auto w = interp_code_dump(P.slp, P.opts.threads, L, P.opts.stages);
       for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");
     } else {
       throw Error(XSLP_EINVAL, "bad dump form");

@@ -128,8 +128,9 @@ inline int reuse_window(int opt, int auto_window) { return opt == 0 ? auto_windo
 // Split the goals into k contiguous sets balanced by issue cost; each result keeps the
 // instructions its goals reach (original order and variable ids) and marks the other goals -2.
 std::vector<Slp> split_goals(const Slp &s, int k);
-// Micro-op code of the pipelined interpreter for consumer width T (interp.cu).
-std::vector<uint32_t> build_code32(const std::vector<uint16_t> &code, int T);
+// Paired micro-op code of the pipelined interpreter (interp.cu): the stage-0 code variant of
+// this program alone for T consumers, L words per thread, S stages (xslp_program_dump form 3).
+std::vector<uint32_t> interp_code_dump(const Slp &s, int T, int L, int S);
 // Input-phase programs of a goal set (capi.cpp; PIPE input phases and the phased multi kernel).
 std::vector<Slp> phase_programs(const std::vector<Bits> &want, int n_const, int nphases,
                                 const xslp_opts &o, int64_t *xor_total);

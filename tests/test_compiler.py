@@ -394,37 +394,69 @@ def test_semantic_equality_all_1002_rs10_4_slps():
         assert oslp.evaluate(prog.dump(1)) == want, k
 
 
-def _emulate_microops(words, T, strips, n_goals):
-    """Plain host emulation of the pipelined interpreter's micro-op code (interp.cu)."""
+def _emulate_microops(words, strips, n_goals):
+    """Plain host emulation of the pipelined interpreter's paired micro-op code (interp.cu
+    emit_variant), in the kernel's order: the operands of pair q+1 are loaded before pair q
+    computes and stores, and both mops of a pair load before either stores -- so a schedule that
+    reads a variable too early reads stale data here.  Shared memory is a map from row byte
+    offset to the row; variable rows start as garbage, row 0 of them is the zero row."""
     w = np.array(words, dtype=np.int64)
-    nl, nm, _, nslots = (int(x) for x in w[:4])
-    row = T * 4
-    slots = np.zeros((nslots + 1, strips.shape[1]), dtype=np.uint32)   # + the zero row
+    nl, npairs, total, nvrows, rb, var0, const0, start = (int(x) for x in w[:8])
+    assert total == len(w) and start == 8 and npairs % 3 == 0
+    width = strips.shape[1]
+    rng = np.random.default_rng(0)
+    smem = {var0 + r * rb: rng.integers(0, 2**32, width, dtype=np.uint32) for r in range(1, nvrows)}
+    smem[var0] = np.zeros(width, dtype=np.uint32)
+    loads = w[start + 12 * (npairs + 2):start + 12 * (npairs + 2) + 2 * nl]
     for i in range(nl):
-        slots[w[5 + 2 * i] // row] = strips[w[4 + 2 * i]]
-    start = (4 + 2 * nl + 7) & ~7
-    out = np.full((n_goals, strips.shape[1]), 0xDEADBEEF, dtype=np.uint32)
-    acc = np.zeros(strips.shape[1], dtype=np.uint32)
-    for m in range(nm):
-        o = w[start + 8 * m:start + 8 * m + 8]
-        if o[4] & 1:
-            acc = np.zeros_like(acc)
-        for u in range(4):
-            acc = acc ^ slots[o[u] // row]
-        if o[4] & 2:
-            slots[o[5] // row] = acc
-        if o[4] & 4:
-            out[o[6]] = acc
+        assert const0 <= loads[2 * i + 1] < const0 + nl * rb
+        smem[int(loads[2 * i + 1])] = strips[loads[2 * i]].copy()
+
+    def pair(q):
+        c = w[start + 12 * q:start + 12 * q + 12]
+        return [(c[0:4], int(c[8]), int(c[9])), (c[4:8], int(c[10]), int(c[11]))]
+
+    def load(q):
+        vals = []
+        for ops, _, ctl in pair(q):
+            hi = (ctl >> 27) & 1
+            vals.append([smem[int(ops[u])].copy() if u < 2 or hi else None for u in range(4)])
+        return vals
+
+    out = np.full((n_goals, width), 0xDEADBEEF, dtype=np.uint32)
+    acc = np.zeros(width, dtype=np.uint32)
+    cur = load(0)
+    for q in range(npairs):
+        nxt = load(q + 1)                                     # before pair q stores (slack ok)
+        for (ops, dst, ctl), v in zip(pair(q), cur):
+            flags = (ctl >> 24) & 0xF
+            if flags & 1:
+                acc = np.zeros_like(acc)
+            acc = acc ^ v[0] ^ v[1]
+            if flags & 8:
+                acc = acc ^ v[2] ^ v[3]
+            if flags & 2:
+                assert var0 < dst < var0 + nvrows * rb        # a variable row, never 0 or a constant
+                smem[dst] = acc.copy()
+            if flags & 4:
+                g = ((ctl & 0xFFFF) - 16) // 8 * 8 + ((ctl >> 16) & 7)
+                out[g] = acc
+        cur = nxt
+    assert not smem[var0].any()
     return out
 
 
-@pytest.mark.parametrize("n,p,comp,er,T", [(10, 3, "none", None, 128), (10, 4, "xorrepair", None, 256),
-                                           (10, 2, "repair", None, 64), (4, 2, "none", None, 32),
-                                           (10, 4, "xorrepair", (2, 4, 5, 6), 128),
-                                           (20, 4, "xorrepair", (0, 5, 21, 23), 96)])
-def test_interpreter_microops_compute_the_oracle_result(n, p, comp, er, T):
-    # the host re-encoding of the bytecode for the pipelined interpreter (dump form 3), run by a
-    # plain emulator, reproduces the oracle's RS bytes on the strip layout
+@pytest.mark.parametrize("n,p,comp,er,T,L,sched", [
+    (10, 3, "none", None, 128, 1, 1), (10, 4, "xorrepair", None, 256, 1, 1),
+    (10, 2, "repair", None, 64, 2, 1), (4, 2, "none", None, 32, 4, 1),
+    (10, 4, "xorrepair", (2, 4, 5, 6), 128, 2, 1),
+    (20, 4, "xorrepair", (0, 5, 21, 23), 96, 1, 1),
+    (10, 4, "xorrepair", None, 128, 2, 2), (10, 4, "xorrepair", (2, 4, 5, 6), 64, 4, 2),
+    (20, 4, "xorrepair", (0, 5, 21, 23), 128, 1, 2), (10, 4, "none", (0, 1, 12, 13), 128, 1, 0)])
+def test_interpreter_microops_compute_the_oracle_result(n, p, comp, er, T, L, sched):
+    # the host's paired micro-op code for the pipelined interpreter (dump form 3), run by a
+    # plain emulator with the kernel's pair semantics, reproduces the oracle's RS bytes on the
+    # strip layout -- for DFS (1), capacity-bounded greedy (2) and unscheduled (0) programs
     import synth
     from oracle import rs
     kind = "cauchy" if (n, p) == (4, 2) else "isal"
@@ -434,11 +466,12 @@ def test_interpreter_microops_compute_the_oracle_result(n, p, comp, er, T):
         bits, rows = X.xslp_encode_bitmatrix(g, n, p), og[n:]
     else:
         bits, rows = X.xslp_decode_bitmatrix(g, n, p, er)[0], mx.decode_rows(og, n, list(er))[1]
-    prog = X.xslp_compile(bits, compress=comp, specialise=0, threads=T)
+    prog = X.xslp_compile(bits, compress=comp, specialise=0, threads=T, lane_words=L,
+                          schedule=sched, greedy_capacity=32)
     words = [int(x) for x in prog.dump(3).split()]
     B = 128
     data = synth.stripe_data(9, 1, n, B)
-    got = _emulate_microops(words, T, data.reshape(8 * n, B // 8).view(np.uint32), bits.shape[0])
+    got = _emulate_microops(words, data.reshape(8 * n, B // 8).view(np.uint32), bits.shape[0])
     want = rs.apply_rows(rows, data).reshape(bits.shape[0], B // 8).view(np.uint32)
     assert (got == want).all()
 
