@@ -229,118 +229,97 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------
-def oracle_stripe(wl, g, s, rows_cache, synth, mx, rs):
-    """One stripe of the workload through the oracle: encode, or decode of that stripe's
-    erasure pattern (the survivor bytes are the stripe's seeded data blocks: the oracle's
-    cost does not depend on their values)."""
-    n, p, B = wl["n"], wl["p"], wl["B"]
-    data = synth.stripe_data(wl["seed"], s, n, B)
-    if wl["op"] == "encode_gft" or wl.get("layout") == "byte":   # byte-wise RS (P:495-525)
-        return rs.bytewise_apply(g[n:], data)
+def oracle_rows(wl, g, s, rows_cache, synth, mx):
+    """GF rows the workload applies to stripe s: the parity rows R (encode), or the decode
+    rows of that stripe's erasure pattern (the oracle's cost does not depend on the
+    survivor bytes, so the stripe's seeded blocks stand in for them)."""
+    n, p = wl["n"], wl["p"]
     if wl["op"] not in DECODE:
-        return rs.encode(g, n, data)
+        return g[n:]
     if "erased" not in wl and "e" in wl:
         er = tuple(synth.erasure_pattern(wl["seed"], s, n + p, wl["e"]))
     else:
-        er = erased_of(wl)
+        er = tuple(erased_of(wl))
     if er not in rows_cache:
-        rows_cache[er] = mx.decode_rows(g, n, list(er))
-    return rs.decode(rows_cache[er][1], data)
+        rows_cache[er] = mx.decode_rows(g, n, list(er))[1]
+    return rows_cache[er]
 
 
-def oracle_baseline(wl, budget_s=12.0):
-    """The CPU oracle as it stands (oracle/rs.py, numpy, one core) on a bounded sample."""
-    import numpy as np
-    import synth
-    from oracle import matrices as mx
-    from oracle import rs
-    n, p, B = wl["n"], wl["p"], wl["B"]
-    g = mx.coding_matrix(n, p)
-    done, t0, s = 0, time.perf_counter(), 0
-    rows_cache = {}
-    while True:
-        oracle_stripe(wl, g, s, rows_cache, synth, mx, rs)
-        done += 1
-        s += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    out = {"value": round(done * n * B / dt / 1e9, 6), "unit": "GB/s", "cores": 1,
-           "kind": "oracle",
-           "sample": f"{done} stripe(s) of the workload ({n} x {B} B data each), oracle/rs.py "
-                     f"table-driven RS on the bit-transposed view, numpy single thread, "
-                     f"{dt:.1f} s"}
-    try:
-        out["all_cores"] = oracle_all_cores(wl, budget_s=min(10.0, budget_s))
-    except Exception as ex:  # report, do not hide
-        out["all_cores"] = {"error": str(ex)[:200]}
-    return out
+class OracleSample:
+    """A bounded sample of the workload for the C oracle (oracle/rs_oracle.c): K stripes'
+    inputs generated up front (untimed) and their per-stripe rows; run() applies them on
+    `threads` host threads -- the table-free naive bitmatrix product on the strip layout, or
+    the textbook byte-wise product for the byte layout / approach (1)."""
+
+    def __init__(self, wl, k):
+        import numpy as np
+        import synth
+        from oracle import matrices as mx
+        from oracle import native as nat
+        self.nat = nat
+        n, p, B = wl["n"], wl["p"], wl["B"]
+        g = mx.coding_matrix(n, p)
+        self.k = max(1, min(k, wl["S"]))
+        cache = {}
+        self.rows = np.array([oracle_rows(wl, g, s, cache, synth, mx) for s in range(self.k)],
+                             dtype=np.uint8)
+        self.x = np.stack([nat.fill(wl["seed"], s, n, B) for s in range(self.k)])
+        self.bytewise = wl["op"] == "encode_gft" or wl.get("layout") == "byte"
+        self.bytes = self.k * n * B
+
+    def run(self, threads):
+        self.nat.apply_each(self.rows, self.x, threads=threads, bytewise=self.bytewise)
 
 
-def _oracle_worker(job):
-    """One process of the all-cores oracle baseline: stripes s0, s0+k, ... for budget_s."""
-    wl, s0, k, budget_s = job
-    import synth
-    from oracle import matrices as mx
-    from oracle import rs
-    g = mx.coding_matrix(wl["n"], wl["p"])
-    rows_cache, done, s, t0 = {}, 0, s0, time.perf_counter()
-    while time.perf_counter() - t0 < budget_s:
-        oracle_stripe(wl, g, s, rows_cache, synth, mx, rs)
-        done += 1
-        s += k
-    return done, time.perf_counter() - t0
-
-
-def oracle_all_cores(wl, budget_s=10.0):
-    """The same oracle, one process per host core over disjoint stripes (BASELINE §2: an
-    all-cores number beside the 1-core one); GB/s = all processes' data / the longest wall."""
-    import multiprocessing as mp
-    k = max(1, min(64, os.cpu_count() or 1))   # capped: one numpy process per core, ~100 MB each
-    ctx = mp.get_context("spawn")
-    t0 = time.perf_counter()
-    with ctx.Pool(k) as pool:
-        res = pool.map(_oracle_worker, [(wl, i, k, budget_s) for i in range(k)])
-    wall = time.perf_counter() - t0
-    done = sum(r[0] for r in res)
-    longest = max(r[1] for r in res)
-    return {"value": round(done * wl["n"] * wl["B"] / longest / 1e9, 6), "unit": "GB/s",
-            "cores": k, "kind": "oracle",
-            "sample": f"{done} stripe(s) over {k} processes (numpy, one thread each), "
-                      f"{longest:.1f} s per process, {wall:.1f} s with start-up"}
+def oracle_baseline(wl, budget_s=8.0):
+    """The CPU oracle as it stands (oracle/rs_oracle.c) on a bounded sample of the workload,
+    on one host core and on all of them."""
+    from oracle import native as nat
+    smp = OracleSample(wl, 32)
+    out = {}
+    for key, th in (("one_core", 1), ("all_cores", nat.cores())):
+        t0, reps = time.perf_counter(), 0
+        while True:
+            smp.run(th)
+            reps += 1
+            if time.perf_counter() - t0 > budget_s / 2:
+                break
+        dt = time.perf_counter() - t0
+        out[key] = {"value": round(reps * smp.bytes / dt / 1e9, 4), "unit": "GB/s", "cores": th,
+                    "kind": "oracle",
+                    "sample": f"{reps} pass(es) over {smp.k} stripe(s) of the workload "
+                              f"({wl['n']} x {wl['B']} B data each, inputs generated untimed), "
+                              f"oracle/rs_oracle.c on {th} thread(s), {dt:.1f} s"}
+    line = dict(out["all_cores"])
+    line["one_core"] = out["one_core"]
+    return line
 
 
 def run_reference(args, wl, rank, world):
+    """The reference arm: the oracle as it stands on the host cores (rank 0 only); each step is
+    one pass of the C oracle over a bounded sample of the workload's stripes."""
     if rank != 0:
         return
-    import numpy as np  # noqa: F401
-    import synth
-    from oracle import matrices as mx
-    from oracle import rs
-    n, p, B = wl["n"], wl["p"], wl["B"]
-    g = mx.coding_matrix(n, p)
-
-    rows_cache = {}
-
-    def step(s):
-        oracle_stripe(wl, g, s, rows_cache, synth, mx, rs)
-
-    for i in range(args.warmup):
-        step(i)
+    from oracle import native as nat
+    smp = OracleSample(wl, 32)
+    th = nat.cores()
+    for _ in range(args.warmup):
+        smp.run(th)
     t0 = time.perf_counter()
-    for i in range(args.steps):
-        step(args.warmup + i)
+    for _ in range(args.steps):
+        smp.run(th)
     dt = time.perf_counter() - t0
-    v = args.steps * n * B / dt / 1e9
+    v = args.steps * smp.bytes / dt / 1e9
+    sample = (f"each step = {smp.k} stripe(s) of the workload ({wl['n']} x {wl['B']} B data each, "
+              f"inputs generated untimed) through oracle/rs_oracle.c on {th} host thread(s)")
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt / max(1, args.steps) * 1e3, 3), "higher_is_better": True,
             "scaling": "strong" if wl["op"] in SHARDED else "weak", "vs_baseline": None,
             "dtype": "u8", "data": "synthetic",
             "config": config_of(args, wl, None),
-            "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": f"each step = 1 stripe ({n} x {B} B data) of the workload "
-                                       "through oracle/rs.py on one host core"},
+            "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": th, "kind": "oracle",
+                             "sample": sample},
             "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -382,6 +361,14 @@ def config_of(args, wl, stats):
          if wl["op"] == "decode_peer" else f"stripe-sharded x{args.gpus}, no collective"}
     if wl["op"] == "encode_gft":
         c["program"] = "none: GF(2^8) MM with nibble tables (approach (1), P:538-545)"
+    if wl["op"] in SHARDED:
+        per = wl["S"] // max(1, args.gpus)
+        c["chunks_per_gpu"] = -(-per // wl["chunk"])
+        c["chunk_stripes"] = min(per, wl["chunk"])
+        if c["chunks_per_gpu"] > 1:
+            c["chunk_inputs"] = ("every chunk's stripes regenerated on the device (stripe0 = the "
+                                 "chunk's first global stripe) before it runs, untimed; a step's "
+                                 "time = the sum of its chunks' launch intervals")
     if stats:
         c["slp"] = {k: stats[k] for k in ("xor_count", "mem_count", "n_instr", "nvar", "maxlive",
                                           "regs", "spill_bytes", "regs_tma", "spill_bytes_tma",
@@ -390,8 +377,29 @@ def config_of(args, wl, stats):
 
 
 # ------------------------------------------------------------------------------------------
+def launch_ranks(nranks):
+    """`--gpus N` without torchrun: start the N ranks ourselves (one process per GPU, the
+    driver's own launch line) and return their exit code; rank 0 prints the JSON line."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nranks}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        sys.exit(launch_ranks(args.gpus))
+    if env_world is not None and int(env_world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}: launch one rank "
+                         "per GPU (torchrun --nproc-per-node N) or omit torchrun and let --gpus N "
+                         "start the ranks")
     wl = dict(WORKLOADS[args.workload])
     # per-workload tuned launch defaults (profiles/r01_sweep*.md); flags override
     for k, v in wl.get("tuned", {}).items():
@@ -623,11 +631,34 @@ def main():
             X.xslp_decode_batch_grouped(progs, gids, goff, ti, to, B, nstreams=args.streams,
                                         stream=st)
         else:
-            X.xslp_encode_batch(prog, ti, to, S, B, stream=st)
+            X.xslp_encode_batch(prog, ti, to, cur_S[0], B, stream=st)
+
+    cur_S = [S]
 
     def step():
         for _ in range(nchunks):
             launch()
+
+    # Strong-split workloads larger than one GPU's HBM (cfg5/cfg5d at N=1: 8192 stripes x 20 MiB)
+    # run in chunks of wl["chunk"] stripes.  Every chunk's stripes are regenerated on the device
+    # before it runs (xslp_fill_random with stripe0 = the chunk's first global stripe), outside
+    # its timed interval: a step's time is the sum of its chunks' launch intervals
+    # ("process in chunks with on-device regeneration and sum the kernel
+    # times"), so every one of the rank's stripes is computed, none reused.
+    chunked = wl["op"] in SHARDED and nchunks > 1
+    chunk_sizes = [min(S, per - c * S) for c in range(nchunks)] if wl["op"] in SHARDED else [S]
+
+    def regen(c):
+        """Chunk c's inputs on the device; returns the launches it made (not timed work)."""
+        l_ = X.xslp_launch_count()
+        sc = chunk_sizes[c]
+        if wl["op"] == "decode_sharded":   # whole codewords: data from the generator, parity encoded
+            X.xslp_fill_random(din, sc, n + p, B, seed=wl["seed"], stripe0=stripe0 + c * S, stream=stream)
+            X.xslp_encode_batch(enc, tall[:sc, :n].contiguous(), tall[:sc, n:].contiguous(), sc, B,
+                                stream=stream)
+        else:
+            X.xslp_fill_random(din, sc, n_in, B, seed=wl["seed"], stripe0=stripe0 + c * S, stream=stream)
+        return X.xslp_launch_count() - l_
 
     # sanity (torch, not the product): RAID-5 row of the [I; 2^ij] encode
     launch()
@@ -686,29 +717,60 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     l0 = X.xslp_launch_count()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    with ClockSampler(local) as clk:
-        ev[0].record(stream)
-        for i in range(args.steps):
-            step()
-            ev[i + 1].record(stream)
-        torch.cuda.synchronize()
-    launches = X.xslp_launch_count() - l0
+    fills = 0
+    if chunked:
+        # per chunk: regenerate (untimed), then time its launch; a step = the sum over chunks
+        cev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nchunks)]
+               for _ in range(args.steps)]
+        with ClockSampler(local) as clk:
+            for i in range(args.steps):
+                for c in range(nchunks):
+                    fills += regen(c)
+                    cur_S[0] = chunk_sizes[c]
+                    cev[i][2 * c].record(stream)
+                    if graph is not None and chunk_sizes[c] == S:
+                        graph.replay()
+                    else:
+                        launch()
+                    cev[i][2 * c + 1].record(stream)
+            torch.cuda.synchronize()
+        cur_S[0] = S
+        per_step = [sum(cev[i][2 * c].elapsed_time(cev[i][2 * c + 1]) for c in range(nchunks))
+                    for i in range(args.steps)]
+        total_ms = sum(per_step)
+    else:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        with ClockSampler(local) as clk:
+            ev[0].record(stream)
+            for i in range(args.steps):
+                step()
+                ev[i + 1].record(stream)
+            torch.cuda.synchronize()
+        per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+        total_ms = ev[0].elapsed_time(ev[-1])
+    launches = X.xslp_launch_count() - l0 - fills   # the product's coding kernels only
     if graph is not None:                   # kernels replayed from the graph
         launches += graph_launches * nchunks * args.steps
     log('timed region done')
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
-    total_ms = ev[0].elapsed_time(ev[-1])
+    rank_ms = total_ms
     total_ms = max_over_ranks(total_ms, dist, device=red_dev)
-    data_bytes_step = S * nchunks * n * B * world
+    rank_clocks = clk.summary()
+    per_rank = [{"rank": rank, "gbs": round(sum(chunk_sizes) * n * B * args.steps / (rank_ms / 1e3) / 1e9, 3),
+                 "ms_per_step": round(rank_ms / args.steps, 4), "sm_mhz": rank_clocks.get("sm_mhz"),
+                 "reasons": rank_clocks.get("reasons"), "device": torch.cuda.get_device_name(local)}]
+    if dist:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, per_rank[0])
+        per_rank = gathered
+    data_bytes_step = sum(chunk_sizes) * n * B * world
     value = data_bytes_step * args.steps / (total_ms / 1e3) / 1e9
 
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / launch time
     alg_bytes_launch = S * (n_in + m_out) * B        # per step (= per launch unless grouped)
-    launch_ms = sum(per_step) / len(per_step) / nchunks
+    launch_ms = sum(per_step) / len(per_step) / nchunks   # chunks are equal for every N used
     achieved = alg_bytes_launch / (launch_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -808,7 +870,7 @@ def main():
                                   else {}),
                                **({"distinct_diagnostic": args.distinct} if args.distinct else {})),
                 "roofline": roof, "cpu_baseline": cpu,
-                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "per_rank": per_rank,
                 "compile_s": round(compile_s, 3),
                 "paper_context": {"note": "the paper's CPU numbers (not comparable: other hardware, "
                                           "context only; BASELINE.md)",

@@ -134,3 +134,30 @@ def test_product_arm_json_contract_on_gpu():
     assert d["gpu_launches"] >= 3
     c = d["clocks"]
     assert c["sm_mhz"] and c["sm_max_mhz"] and isinstance(c["reasons"], list)
+
+
+def test_gpus_flag_starts_the_ranks_without_torchrun():
+    # `bench.py --gpus N` alone launches N ranks itself (one process per GPU); the line says
+    # n_gpus N because N ranks ran (--gpus must be authoritative)
+    r = _run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1",
+              "--warmup", "1"], timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = _json_lines(r.stdout)
+    assert len(lines) == 1
+    _check_line(lines[0], 1, 1)
+    assert lines[0]["n_gpus"] == 2
+
+
+def test_gpus_flag_disagreeing_with_world_size_fails():
+    r = _run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1",
+              "--warmup", "1"], env={"WORLD_SIZE": "1", "RANK": "0"})
+    assert r.returncode != 0
+    assert not _json_lines(r.stdout)
+    assert "WORLD_SIZE" in r.stderr
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU failure")
+def test_product_arm_multi_rank_fails_loudly_without_gpu():
+    r = _run([sys.executable, "bench.py", "--gpus", "2", "--steps", "1", "--warmup", "0"], timeout=600)
+    assert r.returncode != 0
+    assert not _json_lines(r.stdout)

@@ -19,6 +19,7 @@ pytestmark = pytest.mark.gpu
 import paper_2108_02692_b200 as X  # noqa: E402
 from oracle import matrices as mx  # noqa: E402
 from oracle import rs  # noqa: E402
+from oracle import native as nat  # noqa: E402
 import synth  # noqa: E402
 
 
@@ -356,6 +357,7 @@ def test_syndrome_full_size_bench_config(wname):
         assert (allb[s_].cpu().numpy() == blocks).all(), s_
         surv, rows = mx.decode_rows(og, n, list(pats[s_]))
         assert (out[s_].cpu().numpy() == rs.decode(rows, blocks[surv])).all(), s_
+    verify_all(out, seed, parity_rows=og[n:], n=n, erased=pats)   # every stripe vs the oracle
     del allb, data, out, tin
     torch.cuda.empty_cache()
 
@@ -573,6 +575,26 @@ def test_host_buffer_path():
 
 # ---- BASELINE-size cases in the bench launch configuration ------------------------------
 
+def verify_all(got, seed, rows=None, stripe0=0, parity_rows=None, n=None, erased=None, chunk=128,
+               bytewise=False):
+    """Every byte of every stripe of a device output (S, m, B) against the C oracle
+    (oracle/rs_oracle.c, threads over stripes on the host), copied back in chunks.
+    rows: the outputs are rows . fill(seed, stripe, n_in, B).  erased: the outputs are the
+    codeword blocks erased[s] of [fill(seed, stripe, n, B); parity_rows . data]."""
+    S = got.shape[0]
+    bad = []
+    for a in range(0, S, chunk):
+        h = got[a:a + chunk].cpu().numpy()
+        if erased is None:
+            check = nat.check_bytewise if bytewise else nat.check_apply
+            b = check(np.asarray(rows, dtype=np.uint8), seed, stripe0 + a, h)
+        else:
+            b = nat.check_codeword(np.asarray(parity_rows, dtype=np.uint8), n, seed, stripe0 + a,
+                                   np.asarray(erased[a:a + chunk], dtype=np.int32), h)
+        bad += [a + int(x) for x in b]
+    assert not bad, f"{len(bad)} of {S} stripes differ from the oracle, first {bad[:8]}"
+
+
 def _xor_reduce(t):
     acc = t[:, 0].clone()
     for j in range(1, t.shape[1]):
@@ -582,7 +604,7 @@ def _xor_reduce(t):
 
 @pytest.mark.parametrize("kern,threads,lanes,reuse", [("straight", 128, 1, 0), ("tma", 128, 1, 0),
                                                       ("pipe", 256, 1, 0), ("pipe", 128, 2, "bench")])
-def test_cfg2_full_size_sampled(kern, threads, lanes, reuse):
+def test_cfg2_full_size(kern, threads, lanes, reuse):
     # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); ("pipe", 128, 2 lanes) with bench's
     # stages, input phases and reuse window is the exact launch configuration bench.py times
     n, p, B, S = 10, 4, 1 << 20, 1024
@@ -606,12 +628,13 @@ def test_cfg2_full_size_sampled(kern, threads, lanes, reuse):
         data = synth.stripe_data(2, s, n, B)
         assert (din[s].cpu().numpy() == data).all()
         assert (dout[s].cpu().numpy() == rs.encode(og, n, data)).all(), s
+    verify_all(dout, 2, rows=og[n:])                         # every byte of all 1024 stripes
     del din, dout
     torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("mode", ["grouped", "interp"])
-def test_cfg3_full_size_roundtrip_sampled(mode):
+def test_cfg3_full_size_roundtrip(mode):
     # RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures (configs[2]);
     # "grouped" (per-pattern LDG kernels, T=64, 8 streams) is the bench's launch configuration
     n, p, B, S = 10, 4, 1 << 20, 1024
@@ -661,12 +684,15 @@ def test_cfg3_full_size_roundtrip_sampled(mode):
         assert (allb[s].cpu().numpy() == blocks).all()
         surv, rows = mx.decode_rows(og, n, list(pats[s]))
         assert (out[s].cpu().numpy() == rs.decode(rows, blocks[surv])).all()
+    # every stripe: the parity the encode wrote, and the recovered blocks = the oracle codeword
+    verify_all(allb[:, n:], 3, rows=og[n:])
+    verify_all(out, 3, parity_rows=og[n:], n=n, erased=pats)
     del allb, data, out
     torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("threads,lanes", [(256, 1), (128, 2)])
-def test_pdec_full_size_sampled(threads, lanes):
+def test_pdec_full_size(threads, lanes):
     # the paper's P_dec (erase {2,4,5,6}) on 1024 stripes x 1 MiB in bench's launch configuration
     n, p, B, S = 10, 4, 1 << 20, 1024
     og = mx.coding_matrix(n, p)
@@ -682,6 +708,7 @@ def test_pdec_full_size_sampled(threads, lanes):
     assert list(surv) == osurv
     for s in (0, 777, 1023):
         assert (out[s].cpu().numpy() == rs.decode(rows, din[s].cpu().numpy())).all(), s
+    verify_all(out, 3, rows=rows)                            # every byte of all 1024 stripes
     del din, out
     torch.cuda.empty_cache()
 
@@ -821,7 +848,7 @@ def test_cfg5_rs20_reduced(kern):
     assert (allb[s, n:].cpu().numpy() == rs.encode(og, n, h)).all()
 
 
-def test_cfg5_full_chunk_sampled():
+def test_cfg5_full_chunk():
     # RS(20,4) encode and the seeded 4-erasure decode (configs[4]) over one bench launch: a chunk
     # of 2048 stripes x 24 x 1 MiB, PIPE T=256 S=2 with 2 input phases (bench.py cfg5 / cfg5d
     # launch configuration)
@@ -848,6 +875,9 @@ def test_cfg5_full_chunk_sampled():
         blocks = np.concatenate([d, rs.encode(og, n, d)])
         assert (allb[s].cpu().numpy() == blocks).all(), s
         assert (out[s].cpu().numpy() == rs.decode(rows, blocks[osurv])).all(), s
+    # every stripe of the chunk: the 4 parity blocks, and the recovered blocks vs the codeword
+    verify_all(allb[:, n:], 5, rows=og[n:], chunk=64)
+    verify_all(out, 5, parity_rows=og[n:], n=n, erased=[er] * S, chunk=64)
     del allb, out
     torch.cuda.empty_cache()
 
@@ -954,7 +984,7 @@ def test_gf_table_kernel(n, p, kind, B, S):
     assert (rec.cpu().numpy() == blocks[:, er]).all()
 
 
-def test_gf_table_full_size_sampled():
+def test_gf_table_full_size():
     # approach (1) at bench cfg2t's size: RS(10,4) byte-wise encode of 1024 stripes x 10 x 1 MiB;
     # row 0 of [I; 2^(ij)] is all ones, so parity 0 = XOR of the data on every stripe
     n, p, B, S = 10, 4, 1 << 20, 1024
@@ -969,12 +999,13 @@ def test_gf_table_full_size_sampled():
     for s in (0, 401, 1023):
         want = rs.bytewise_apply(og[n:], synth.stripe_data(2, s, n, B))
         assert (out[s].cpu().numpy() == want).all(), s
+    verify_all(out, 2, rows=og[n:], bytewise=True)           # every byte of all 1024 stripes
     del din, out
     torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("kern,threads", [("straight", 128), ("pipe", 128), ("pipe", 256)])
-def test_byte_layout_full_size_sampled(kern, threads):
+def test_byte_layout_full_size(kern, threads):
     n, p, B, S = 10, 4, 1 << 20, 1024
     og = mx.coding_matrix(n, p)
     _, prog = compile_enc(n, p, layout="byte", block_bytes_hint=B, kernel=kern, threads=threads)
@@ -986,6 +1017,7 @@ def test_byte_layout_full_size_sampled(kern, threads):
     for s in (5, 1000):
         d = synth.stripe_data(2, s, n, B)
         assert (dout[s].cpu().numpy() == rs.bytewise_apply(og[n:], d)).all()
+    verify_all(dout, 2, rows=og[n:], bytewise=True)          # every byte of all 1024 stripes
     del din, dout
     torch.cuda.empty_cache()
 
