@@ -135,7 +135,10 @@ def parse():
     ap.add_argument("--block-bytes", type=int, default=0, help="override block size")
     ap.add_argument("--p", type=int, default=0, help="override parity count (cfg4 sweep)")
     ap.add_argument("--fuse", type=int, default=1)
-    ap.add_argument("--schedule", type=int, default=1, help="1 = DFS, 0 = creation order")
+    ap.add_argument("--schedule", type=int, default=1,
+                    help="1 = DFS (P:1279-1303), 0 = creation order, 2 = capacity-bounded greedy "
+                         "(P:1305-1338, capacity --greedy-capacity)")
+    ap.add_argument("--greedy-capacity", type=int, default=64)
     ap.add_argument("--graph", type=int, default=None,
                     help="1 = capture one step's launches into a CUDA graph and replay it per step")
     ap.add_argument("--no-e2e", action="store_true")
@@ -344,7 +347,8 @@ def config_of(args, wl, stats):
     c = {"workload": f"{args.workload}: {wl['desc']}", "n": wl["n"], "p": wl["p"],
          "block_bytes": wl["B"], "stripes_per_gpu": wl["S"] if wl["op"] not in SHARDED
          else wl["S"] // max(1, args.gpus),
-         "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": args.compress + ("+fuse" if args.fuse else "") + ("+dfs" if args.schedule else ""),
+         "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": args.compress + ("+fuse" if args.fuse else "") +
+         {0: "", 1: "+dfs", 2: f"+greedy(c={args.greedy_capacity})"}.get(args.schedule, ""),
          "kernel": args.kernel, "lane_words": args.lanes, "threads": args.threads,
          "stages": args.stages, "groups": args.groups,
          "phases": args.phases or (-(-(wl["n"] + wl["p"]) // 10) if args.kernel == "syndrome" else
@@ -514,7 +518,8 @@ def main():
         prog = X.xslp_compile(bits, compress=args.compress, kernel=args.kernel,
                               lane_words=args.lanes, threads=args.threads, block_bytes_hint=B,
                               stages=args.stages, groups=args.groups, phases=args.phases,
-                              reuse=args.reuse)
+                              reuse=args.reuse, schedule=args.schedule,
+                              greedy_capacity=args.greedy_capacity)
         m_out = len(erased)
     elif wl["op"] == "encode_gft":    # approach (1): no SLP, the coefficient rows themselves
         prog = None
@@ -524,7 +529,8 @@ def main():
         prog = X.xslp_compile(X.xslp_encode_bitmatrix(G, n, p), compress=args.compress,
                               kernel=args.kernel, lane_words=args.lanes, threads=args.threads,
                               block_bytes_hint=B, stages=args.stages, fuse=args.fuse,
-                              schedule=args.schedule, layout=wl.get("layout", "strip"),
+                              schedule=args.schedule, greedy_capacity=args.greedy_capacity,
+                              layout=wl.get("layout", "strip"),
                               groups=args.groups, phases=args.phases, reuse=args.reuse)
         m_out = p
     compile_s = time.perf_counter() - t0

@@ -139,7 +139,12 @@ std::vector<Slp> phase_programs(const std::vector<Bits> &want, int n_const, int 
     Slp s = o.compress == XSLP_COMPRESS_NONE ? lift(g, n_const, o.fuse != 0)
                                              : compress(g, n_const, o.compress == XSLP_COMPRESS_XORREPAIR);
     if (o.fuse) fuse(s);
-    if (o.schedule != XSLP_SCHED_NONE) schedule_dfs(s, o.goal_order);
+    if (o.schedule == XSLP_SCHED_GREEDY) {
+      std::vector<int> peb;
+      schedule_greedy(s, o.greedy_capacity, peb);
+    } else if (o.schedule != XSLP_SCHED_NONE) {
+      schedule_dfs(s, o.goal_order);
+    }
     auto got = evaluate(s);
     for (size_t r = 0; r < g.size(); ++r)
       if (!(got[r] == g[r])) throw Error(XSLP_EINVAL, "internal: phase program differs from its goals");

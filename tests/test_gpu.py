@@ -427,7 +427,7 @@ def test_copy_and_zero_goals_on_device():
         assert (out.cpu().numpy() == want).all()
 
 
-@pytest.mark.parametrize("case", range(96))
+@pytest.mark.parametrize("case", range(128))
 def test_random_programs_and_launches(case):
     # seeded fuzz over program shape and launch knobs: a random bitmatrix (1-24 input blocks,
     # 1-6 output blocks, random density incl. empty and full rows) through a random launch of
@@ -441,7 +441,7 @@ def test_random_programs_and_launches(case):
     bits[int(rng.integers(0, 8 * m_out))] = 0                      # an all-zero goal
     if case % 3 == 0:
         bits[int(rng.integers(0, 8 * m_out))] = 1                  # a full goal
-    kern = ["straight", "tma", "pipe", "pipe"][case % 4]
+    kern = ["straight", "tma", "pipe", "pipe"][case % 4] if case < 96 else "interp"
     kw = dict(kernel=kern, threads=int(rng.choice([32, 64, 128, 256])),
               reuse=int(rng.choice([-1, 0, 1, 7, 32, 128])))
     if kern != "tma":
@@ -449,11 +449,18 @@ def test_random_programs_and_launches(case):
     if kern == "pipe":
         kw["stages"] = int(rng.integers(1, 5))
         kw["phases"] = int(rng.integers(0, min(4, n_in) + 1))
+    if kern == "interp":                    # the pipelined interpreter: L, stages, no JIT
+        kw.update(lane_words=int(rng.choice([1, 2, 4])), stages=int(rng.integers(1, 5)),
+                  specialise=0)
     B = 128 * int(rng.integers(1, 40))
     S = int(rng.integers(1, 5))
     if rng.random() < 0.5:
         kw["block_bytes_hint"] = B
     one = case % 5 == 0                 # the single-stripe call (block pointers by value)
+    # schedule knob (drawn last: earlier draws keep their cases): creation order, DFS (P:1279-
+    # 1303) or the capacity-bounded greedy schedule at a random capacity
+    kw["schedule"] = int(rng.choice([0, 1, 2]))
+    kw["greedy_capacity"] = int(rng.choice([4, 16, 64, 512]))
     if one:
         S = 1
     try:
@@ -471,6 +478,37 @@ def test_random_programs_and_launches(case):
         pytest.skip(f"launch rejected: {e}")
     for s_ in range(S):
         assert (out[s_].cpu().numpy() == rs.bitmatrix_apply(bits, data[s_])).all(), (case, kw, B, s_)
+
+
+@pytest.mark.parametrize("prog", ["rs10enc", "pdec", "rs20dec"])
+@pytest.mark.parametrize("cap", [16, 64, 512])
+@pytest.mark.parametrize("kern", ["straight", "pipe", "interp"])
+def test_greedy_schedule_on_device(prog, cap, kern):
+    # programs scheduled by the capacity-bounded bottom-up greedy strategy
+    # instead of DFS run through the straight-line, PIPE and interpreter kernels
+    # and give the oracle's bytes (RS(10,4) encode, P_dec, an RS(20,4) decode)
+    n, p, er = {"rs10enc": (10, 4, None), "pdec": (10, 4, [2, 4, 5, 6]),
+                "rs20dec": (20, 4, [0, 5, 21, 23])}[prog]
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    if er is None:
+        bits, rows = X.xslp_encode_bitmatrix(g, n, p), og[n:]
+    else:
+        bits, rows = X.xslp_decode_bitmatrix(g, n, p, er)[0], mx.decode_rows(og, n, er)[1]
+    B, S = 16384 + 128, 3                              # ragged last tile
+    kw = dict(schedule=2, greedy_capacity=cap, kernel=kern, threads=128)
+    if kern == "interp":
+        kw.update(specialise=0, lane_words=2)
+    prog_ = X.xslp_compile(bits, **kw)
+    st = prog_.stats()
+    assert st["xor_count"] > 0
+    data = host_data(321, range(S), n, B)
+    din = torch.from_numpy(data).cuda()
+    out = torch.full((S, len(rows), B), 0x77, dtype=torch.uint8, device="cuda")
+    run_batch(prog_, din, out, B)
+    torch.cuda.synchronize()
+    for s_ in range(S):
+        assert (out[s_].cpu().numpy() == rs.apply_rows(rows, data[s_])).all(), (prog, cap, kern, s_)
 
 
 @pytest.mark.parametrize("case", range(24))
