@@ -46,13 +46,14 @@ WORKLOADS = {
                   n=10, p=4, B=MiB, S=1024, op="encode_gft", seed=2,
                   tuned=dict(kernel="gftable", threads=256, stages=2)),
     "cfg3": dict(desc="RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures, "
-                      "syndrome form: one shared syndrome program over all 14 blocks (erased ones read from a "
-                      "zero block) + a small solve program per pattern, fused with a branch table "
-                      "(16 patterns per kernel); --kernel multi: the patterns' M^-1 programs fused; "
-                      "--kernel grouped: one straight-line kernel per pattern; --kernel interp "
-                      "(BASELINE configs[2])",
+                      "recovered by the inverted-submatrix (M^-1) bitmatrix SLP compiled per erasure "
+                      "pattern (BASELINE configs[2]; P:526-530), the patterns' programs fused into "
+                      "multi-program kernels (20 per kernel, branch table per stripe); --kernel "
+                      "syndrome: shared syndrome program + per-pattern solve programs; --kernel "
+                      "grouped: one straight-line kernel per pattern; --kernel interp",
                  n=10, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=3,
-                 tuned=dict(kernel="syndrome", threads=256, stages=2, per_module=16, reuse=40, graph=1)),
+                 tuned=dict(kernel="multi", threads=256, stages=2, per_module=20, graph=1),
+                 alt=dict(syndrome=dict(threads=256, stages=2, per_module=16, reuse=40, graph=1))),
     "pdec": dict(desc="RS(10,4) decode of the paper's P_dec pattern {2,4,5,6} (P:1670) on every "
                       "stripe, 1024 stripes x 1 MiB",
                  n=10, p=4, B=MiB, S=1024, op="decode_one", erased=(2, 4, 5, 6), seed=3,
@@ -75,7 +76,9 @@ WORKLOADS = {
                        "syndrome program over 24 blocks in 6 input phases + per-pattern solve "
                        "programs, 10 per kernel); --kernel multi: the M^-1 programs fused",
                   n=20, p=4, B=MiB, S=1024, op="decode_multi", e=4, seed=5,
-                  tuned=dict(kernel="syndrome", threads=256, stages=3, phases=6, per_module=10, graph=1)),
+                  tuned=dict(kernel="syndrome", threads=256, stages=3, phases=6, per_module=10, graph=1),
+                  # T=224 keeps the CTA at 8 warps (2 per SMSP): 128 registers, 2 CTAs per SM
+                  alt=dict(multi=dict(threads=224, stages=3, phases=6, per_module=10, graph=1))),
     "xdec": dict(desc="RS(10,4) cross-GPU decode (SURVEY NEXT #4): the 14 blocks of each stripe "
                       "spread over the GPUs (block j of stripe s on rank (s+j) mod N), rank s mod N "
                       "decodes stripe s reading its survivors in place from local and NVLink-peer "
@@ -405,8 +408,12 @@ def main():
                          "per GPU (torchrun --nproc-per-node N) or omit torchrun and let --gpus N "
                          "start the ranks")
     wl = dict(WORKLOADS[args.workload])
-    # per-workload tuned launch defaults (profiles/r01_sweep*.md); flags override
-    for k, v in wl.get("tuned", {}).items():
+    # per-workload tuned launch defaults (profiles/r01_sweep*.md, profiles/r02/); a kernel chosen
+    # with --kernel takes its own tuned set when the workload has one; flags override
+    tuned = dict(wl.get("tuned", {}))
+    if args.kernel and args.kernel in wl.get("alt", {}):
+        tuned = dict(wl["alt"][args.kernel], kernel=args.kernel)
+    for k, v in tuned.items():
         if getattr(args, k) is None:
             setattr(args, k, v)
     args.kernel = args.kernel or "auto"

@@ -78,6 +78,8 @@ def test_workload_table():
         assert wl["B"] % 128 == 0 and wl["S"] >= 1 and 1 <= wl["p"] and wl["n"] + wl["p"] <= 255
         for k in wl.get("tuned", {}):
             assert k in ap_dests, (name, k)   # a tuned default must be a bench flag
+        for kern, t in wl.get("alt", {}).items():
+            assert all(k in ap_dests for k in t), (name, kern)
     # the default line is BASELINE configs[1]: RS(10,4) encode, 1024 stripes x 10 x 1 MiB
     d = bench.WORKLOADS["cfg2"]
     assert (d["n"], d["p"], d["B"], d["S"], d["op"]) == (10, 4, 1 << 20, 1024, "encode")

@@ -313,14 +313,52 @@ def test_syndrome_form_decode(n, p, kind, e, phases):
 
 
 @pytest.mark.parametrize("wname", ["cfg3", "cfg5h"])
+def test_multi_full_size_bench_config(wname):
+    # the configured heterogeneous decode -- the M^-1 bitmatrix SLP of each erasure pattern
+    # (BASELINE configs[2]) fused into multi-program kernels -- at full size in the
+    # launch configuration bench.py times (cfg3's default line; cfg5h's --kernel multi):
+    # every byte of every stripe against the C oracle's codeword
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    wl = bench.WORKLOADS[wname]
+    t = wl["tuned"] if wl["tuned"]["kernel"] == "multi" else wl["alt"]["multi"]
+    n, p, B, S, e, seed = wl["n"], wl["p"], wl["B"], wl["S"], wl["e"], wl["seed"]
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    pats = [tuple(synth.erasure_pattern(seed, s, n + p, e)) for s in range(S)]
+    uniq = sorted(set(pats))
+    dec = [X.xslp_decode_bitmatrix(g, n, p, er) for er in uniq]
+    progs = X.compile_many([d[0] for d in dec], specialise=0)
+    multi = X.Multi(progs, per_module=t["per_module"], threads=t["threads"], stages=t["stages"],
+                    block_bytes_hint=B, phases=t.get("phases", 0), reuse=t.get("reuse", 0))
+    _, enc = compile_enc(n, p, block_bytes_hint=B)
+    allb = dev_buf(S, n + p, B)
+    X.xslp_fill_random(allb, S, n + p, B, seed=seed)          # data words do not depend on nblocks
+    ti = X.block_table(allb, S, n + p, B).view(S, n + p)
+    X.xslp_encode_batch(enc, ti[:, :n].contiguous(), ti[:, n:].contiguous(), S, B)
+    pos = [uniq.index(er) for er in pats]
+    tin = torch.stack([ti[s_, torch.as_tensor(dec[pos[s_]][1], dtype=torch.long)] for s_ in range(S)])
+    out = dev_buf(S, e, B)
+    ids, off = X.group_stripes(pos, len(uniq))
+    X.xslp_multi_decode(multi, torch.tensor(pos, dtype=torch.int32, device="cuda"),
+                        torch.from_numpy(ids).cuda(), off, tin.contiguous(),
+                        X.block_table(out, S, e, B), B)
+    torch.cuda.synchronize()
+    verify_all(allb[:, n:], seed, rows=og[n:])                 # the untimed encode
+    verify_all(out, seed, parity_rows=og[n:], n=n, erased=pats)
+    del allb, out, tin
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("wname", ["cfg3", "cfg5h"])
 def test_syndrome_full_size_bench_config(wname):
     # the heterogeneous decode workloads at full size (1024 stripes x 1 MiB, per-stripe seeded
     # 4-erasures) in exactly the launch configuration bench.py times (read from its table):
     # roundtrip on every stripe, the oracle's decode on sampled stripes
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import bench
-    wl, t = bench.WORKLOADS[wname], bench.WORKLOADS[wname]["tuned"]
-    assert t["kernel"] == "syndrome"
+    wl = bench.WORKLOADS[wname]
+    t = wl["tuned"] if wl["tuned"]["kernel"] == "syndrome" else dict(wl["alt"]["syndrome"], kernel="syndrome")
     n, p, B, S, e, seed = wl["n"], wl["p"], wl["B"], wl["S"], wl["e"], wl["seed"]
     phases = t.get("phases") or -(-(n + p) // 10)      # bench.py's default for the syndrome form
     og = mx.coding_matrix(n, p)
