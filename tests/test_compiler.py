@@ -238,14 +238,28 @@ FIG1 = {(8, 4): (121, 170, 543, 747), (9, 4): (132, 182, 611, 829), (10, 4): (14
 
 @pytest.mark.parametrize("np_", list(FIG1))
 def test_figure1_grid(np_):
-    # Figure 1: instructions and #M of the optimised programs
+    # Figure 1: instructions ("#xor" row, reading R7) and #M of the optimised
+    # programs.  Encode: both within 5% (or 2 instructions for the 26-30-instruction p=2 codes).
+    # Decode: the paper names its pattern only for RS(10,4) (P_dec = {2,4,5,6}), held
+    # to 5% on both; for the other codes (reading R18) #M of {2,4,5,6}[:p] is held to 5% and
+    # the printed instruction count must lie inside the range our compiler gives over ALL
+    # C(n+p, p) erasure patterns (it varies 2-3x with the pattern: RS(8,2) 26-82)
     n, p = np_
     ie, id_, me, md = FIG1[np_]
     er = [2, 4, 5, 6][:p]
     se = X.xslp_compile(_bits("enc", n, p, None), specialise=0).stats()
     sd = X.xslp_compile(_bits("dec", n, p, er), specialise=0).stats()
     assert _within(se["mem_count"], me, 0.05) and _within(sd["mem_count"], md, 0.05)
-    assert _within(se["n_instr"], ie, 0.10) and _within(sd["n_instr"], id_, 0.10)
+    assert _within(se["n_instr"], ie, 0.05) or abs(se["n_instr"] - ie) <= 2
+    if (n, p) == (10, 4):
+        assert _within(sd["n_instr"], id_, 0.05)
+    else:
+        g = X.xslp_coding_matrix(n, p)
+        pats = list(itertools.combinations(range(n + p), p))
+        progs = X.compile_many([X.xslp_decode_bitmatrix(g, n, p, list(pt))[0] for pt in pats],
+                               specialise=0)
+        ins = [q.stats()["n_instr"] for q in progs]
+        assert min(ins) <= id_ <= max(ins), (min(ins), id_, max(ins))
 
 
 def test_copy_and_zero_goals():
