@@ -142,6 +142,9 @@ def parse():
                     help="1 = DFS (P:1279-1303), 0 = creation order, 2 = capacity-bounded greedy "
                          "(P:1305-1338, capacity --greedy-capacity)")
     ap.add_argument("--greedy-capacity", type=int, default=64)
+    ap.add_argument("--peer-tma", type=int, default=0,
+                    help="xdec/xdec1 at N>1: 1 = TMA-staged kernels (PIPE / fused multi-program) "
+                         "bulk-copy peer strips (opt-in; default: LDG straight-line kernels)")
     ap.add_argument("--graph", type=int, default=None,
                     help="1 = capture one step's launches into a CUDA graph and replay it per step")
     ap.add_argument("--no-e2e", action="store_true")
@@ -569,18 +572,22 @@ def main():
         if dist:
             dist.barrier()                # every rank's storage written before any peer read
         pmulti = None
-        if world == 1 and len(progs) == 1:  # all blocks local: the TMA pipeline (peer tables keep
-            # the LDG kernel: TMA bulk copies from peer memory are not validated on this pool)
+        # TMA-staged kernels (PIPE, fused multi-program) when every block is local, or with
+        # --peer-tma 1 (opt-in) also over peer tables; otherwise peer tables keep the LDG
+        # straight-line kernel (the path validated over real NVLink P2P)
+        use_tma = world == 1 or args.peer_tma
+        if use_tma and len(progs) == 1:
             progs = peer.compile_plan(X, G, plan, compress=args.compress, threads=128, lane_words=2,
                                       block_bytes_hint=B, stages=2, kernel="pipe")
             args.kernel, args.threads, args.lanes = "pipe", 128, 2
-        if world == 1 and len(progs) > 1:   # all blocks local: the fused multi-program kernels
+        if use_tma and len(progs) > 1:      # the fused multi-program kernels
             pmulti = X.Multi(X.compile_many([X.xslp_decode_bitmatrix_from(G, n, p, er, sv)
                                              for er, sv in plan.keys], specialise=0),
                              per_module=args.per_module, threads=256, stages=2, block_bytes_hint=B,
                              reuse=args.reuse)
             args.kernel, args.threads = "multi", 256
-        pdec = peer.PeerDecoder(X, pl, din, dout, plan, progs, dist=dist, multi=pmulti)
+        pdec = peer.PeerDecoder(X, pl, din, dout, plan, progs, dist=dist, multi=pmulti,
+                                tma=bool(args.peer_tma))
         remote_blocks, all_blocks = plan.remote_reads()
         if args.xmode == "staged":        # baseline: gather the survivors, then a local decode
             staging = torch.empty((len(plan.stripes), n, B), dtype=torch.uint8, device="cuda")

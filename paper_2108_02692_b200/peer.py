@@ -198,14 +198,18 @@ class PeerDecoder:
     stripes straight from local + peer memory (one grouped launch, or a single batch launch
     when all home stripes share one program)."""
 
-    def __init__(self, X, placement, storage, out, plan, progs, dist=None, group=None, multi=None):
-        """multi: optional X.Multi over `progs` (fused multi-program kernels); used for local
-        data only -- peer blocks are read by the LDG straight-line kernels, whose plain loads
-        are what P2P mappings are exercised with here (TMA bulk copies from peer memory are not)."""
+    def __init__(self, X, placement, storage, out, plan, progs, dist=None, group=None, multi=None,
+                 tma=False):
+        """multi: optional X.Multi over `progs` (fused multi-program kernels).  By default peer
+        blocks are read by the LDG straight-line kernels (plain loads over P2P mappings, the
+        path validated on real NVLink); tma=True (opt-in) lets TMA-staged kernels -- PIPE
+        programs (compile_plan(..., kernel="pipe")) and the fused multi-program kernels --
+        bulk-copy peer strips (cp.async.bulk from the mapped addresses)."""
         import torch
         self.X, self.pl, self.plan, self.progs = X, placement, plan, progs
-        if multi is not None and placement.world > 1:
-            raise ValueError("the fused multi-program kernels are used for local blocks only")
+        if multi is not None and placement.world > 1 and not tma:
+            raise ValueError("the fused multi-program kernels read peer blocks only with tma=True")
+        self.tma = tma
         self.multi = multi
         B = storage.shape[-1]
         self.B = B

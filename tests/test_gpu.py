@@ -1336,14 +1336,14 @@ def test_peer_decode_emulated_ranks(world, e):
             assert (out[i].cpu().numpy() == blocks[list(erased)]).all(), (r, s)
 
 
-def _ipc_worker(rank, world, port, q):
+def _ipc_worker(rank, world, port, q, kernel="straight", devices=1, erased_const=None):
     import os
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     ok = False
     try:
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank % devices)
         from paper_2108_02692_b200 import peer
         n, p, B, S, seed = 10, 4, 65536, 16, 52
         g = X.xslp_coding_matrix(n, p)
@@ -1351,13 +1351,25 @@ def _ipc_worker(rank, world, port, q):
         pl = peer.Placement(n, p, world, S)
         st = torch.zeros(pl.storage_shape(B), dtype=torch.uint8, device="cuda")
         peer.fill_storage(X, pl, rank, st, seed, enc, chunk=8)
-        er = lambda s: synth.erasure_pattern(seed, s, n + p, 3)   # noqa: E731
+        if erased_const is not None:
+            er = lambda s: erased_const                          # noqa: E731
+        else:
+            er = lambda s: synth.erasure_pattern(seed, s, n + p, 3)   # noqa: E731
         plan = peer.Plan(pl, rank, er)
-        progs = peer.compile_plan(X, g, plan, kernel="straight", threads=64, block_bytes_hint=B)
+        multi = None
+        if kernel == "straight":
+            progs = peer.compile_plan(X, g, plan, kernel="straight", threads=64, block_bytes_hint=B)
+        elif kernel == "pipe":       # TMA bulk copies of the peer strips (opt-in path)
+            progs = peer.compile_plan(X, g, plan, kernel="pipe", threads=128, lane_words=2, stages=2,
+                                      block_bytes_hint=B)
+        else:                        # the fused multi-program kernels over peer tables
+            progs = peer.compile_plan(X, g, plan, specialise=0)
+            multi = X.Multi(progs, per_module=4, threads=128, stages=2, block_bytes_hint=B)
         out = torch.zeros((len(plan.stripes), plan.e, B), dtype=torch.uint8, device="cuda")
         torch.cuda.synchronize()
         dist.barrier()                                  # every storage written
-        dec = peer.PeerDecoder(X, pl, st, out, plan, progs, dist=dist)
+        dec = peer.PeerDecoder(X, pl, st, out, plan, progs, dist=dist, multi=multi,
+                               tma=kernel != "straight")
         assert len(dec.mapped) == world - 1
         dec.launch()
         torch.cuda.synchronize()
@@ -1379,16 +1391,35 @@ def _ipc_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_peer_decode_ipc_two_processes():
+def _run_ipc(kernel, devices, erased_const=None, world=2):
     import os
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29900 + os.getpid() % 97
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    port = 29900 + (os.getpid() + 7 * len(kernel) + devices) % 97
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q, kernel, devices, erased_const))
+             for r in range(world)]
     for pr in procs:
         pr.start()
-    res = sorted(q.get(timeout=300) for _ in range(2))
+    res = sorted(q.get(timeout=300) for _ in range(world))
     for pr in procs:
         pr.join(timeout=60)
-    assert res == [(0, True), (1, True)]
+    assert res == [(r, True) for r in range(world)]
+
+
+@pytest.mark.parametrize("kernel", ["straight", "pipe", "multi"])
+def test_peer_decode_ipc_two_processes(kernel):
+    # two processes on cuda:0, each decoding its home stripes from its own and the other's
+    # IPC-mapped storage; "pipe" / "multi" bulk-copy the mapped strips with TMA (opt-in path)
+    if kernel == "pipe":     # one pattern for every stripe: a single PIPE program per rank
+        _run_ipc(kernel, 1, erased_const=[2, 4, 5])
+    else:
+        _run_ipc(kernel, 1)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs (real NVLink P2P)")
+@pytest.mark.parametrize("kernel", ["straight", "pipe", "multi"])
+def test_peer_decode_two_devices(kernel):
+    # the cross-GPU decode over REAL peer memory: rank r on cuda:r, survivors read in place over
+    # NVLink 5 / NVSwitch by the LDG kernel, and by the TMA-staged kernels (opt-in)
+    _run_ipc(kernel, 2, erased_const=[2, 4, 5] if kernel == "pipe" else None)
