@@ -401,7 +401,8 @@ int xslp_codec_reconstruct(const xslp_codec *codec, uint8_t *d_shards, const int
  * place in d_shards. */
 int xslp_codec_decode(const xslp_codec *codec, uint8_t *d_shards, const int32_t *erased, int ne,
                       int64_t len, uint8_t *d_data_out, void *stream);
-/* The memoised program for an erasure pattern (ne == 0: the encode program); owned by the codec. */
+/* The memoised program for an erasure pattern (ne == 0: the encode program); owned by the codec
+ * and valid until xslp_codec_free (a program handed out here is never freed by LRU eviction). */
 int xslp_codec_program(const xslp_codec *codec, const int32_t *erased, int ne,
                        const xslp_program **out);
 int xslp_codec_cached(const xslp_codec *codec);   /* erasure patterns with a memoised decode program */

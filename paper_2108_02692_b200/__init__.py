@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBPATH = os.path.join(_HERE, "libxslp.so")
+# XSLP_LIBRARY: a diagnostic build of the same sources (scripts/sanitize_host.sh: ASan/UBSan, TSan)
+_LIBPATH = os.environ.get("XSLP_LIBRARY") or os.path.join(_HERE, "libxslp.so")
 
 if not os.path.exists(_LIBPATH):
     raise ImportError(

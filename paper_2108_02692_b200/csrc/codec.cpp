@@ -31,6 +31,9 @@ struct Codec {
   // decode-through programs, by (erasure pattern, f): goals = data blocks 0..f-1 (copies of
   // the surviving ones, M^-1 rows for the erased ones) written straight to the caller's buffer
   std::map<std::pair<std::vector<int>, int>, std::shared_ptr<Program>> dthru;
+  // programs handed out by xslp_codec_program: kept alive until xslp_codec_free, so an LRU
+  // eviction by another thread cannot free a program a caller still holds
+  std::set<std::shared_ptr<Program>> handed_out;
 };
 
 std::shared_ptr<Program> compile_bits(const std::vector<uint8_t> &bits, int rows, int cols,
@@ -312,7 +315,12 @@ extern "C" int xslp_codec_program(const xslp_codec *cc, const int32_t *erased, i
     *out = reinterpret_cast<const xslp_program *>(c.enc.get());
     return XSLP_OK;
   }
-  *out = reinterpret_cast<const xslp_program *>(decode_program(c, std::vector<int>(erased, erased + ne)).get());
+  auto prog = decode_program(c, std::vector<int>(erased, erased + ne));
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    c.handed_out.insert(prog);
+  }
+  *out = reinterpret_cast<const xslp_program *>(prog.get());
   API_END
 }
 

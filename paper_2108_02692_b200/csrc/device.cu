@@ -239,6 +239,25 @@ static void drop_pools_of(const Program *p);  // below: pools that contain p's b
 void drop_code32_of(const Program *p);  // interp.cu
 
 Program::~Program() {
+  {
+    // kernels of this program (its JIT library, its code pools) may still be in flight on any
+    // device (e.g. an LRU eviction in a codec while another thread's decode runs): wait for
+    // them before unloading / freeing anything (destruction is rare; launches are async)
+    bool used;
+    {
+      std::lock_guard<std::mutex> g(g_mu);
+      used = g_libs.count(this) != 0;
+    }
+    used = used || !dev.empty();
+    int ndev = 0, cur = -1;
+    if (used && cudaGetDeviceCount(&ndev) == cudaSuccess && cudaGetDevice(&cur) == cudaSuccess) {
+      for (int d = 0; d < ndev; ++d) {
+        cudaSetDevice(d);
+        cudaDeviceSynchronize();
+      }
+      cudaSetDevice(cur);
+    }
+  }
   drop_pools_of(this);  // a later program at the same address must not find this one's pool
   drop_code32_of(this);
   {
