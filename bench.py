@@ -142,6 +142,8 @@ def parse():
                     help="1 = DFS (P:1279-1303), 0 = creation order, 2 = capacity-bounded greedy "
                          "(P:1305-1338, capacity --greedy-capacity)")
     ap.add_argument("--greedy-capacity", type=int, default=64)
+    ap.add_argument("--interp", default="lanes", choices=["lanes", "pairs"],
+                    help="--kernel interp: the lane-parallel (default) or the pair-pipelined interpreter")
     ap.add_argument("--peer-tma", type=int, default=0,
                     help="xdec/xdec1 at N>1: 1 = TMA-staged kernels (PIPE / fused multi-program) "
                          "bulk-copy peer strips (opt-in; default: LDG straight-line kernels)")
@@ -337,7 +339,7 @@ def run_reference(args, wl, rank, world):
 def kernel_name(args, wl, stats):
     k = args.kernel
     if k == "interp":
-        return "xslp_interp_pipe"
+        return "xslp_interp_lanes" if args.interp == "lanes" else "xslp_interp_pipe"
     if k in ("tma", "grouped_tma"):
         return "xslp_sl_tma"
     if k in ("pipe", "grouped_pipe"):
@@ -355,7 +357,8 @@ def config_of(args, wl, stats):
          else wl["S"] // max(1, args.gpus),
          "matrix": "[I; 2^(ij)] over GF(2^8)/0x11D", "program": args.compress + ("+fuse" if args.fuse else "") +
          {0: "", 1: "+dfs", 2: f"+greedy(c={args.greedy_capacity})"}.get(args.schedule, ""),
-         "kernel": args.kernel, "lane_words": args.lanes, "threads": args.threads,
+         "kernel": args.kernel if args.kernel != "interp" else f"interp ({args.interp})",
+         "lane_words": args.lanes, "threads": args.threads,
          "stages": args.stages, "groups": args.groups,
          "phases": args.phases or (-(-(wl["n"] + wl["p"]) // 10) if args.kernel == "syndrome" else
                                    (-(-wl["n"] // 10) if wl["n"] > 10 else 1)),
@@ -497,7 +500,7 @@ def main():
         elif mode == "interp":
             progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=0,
                                    threads=args.threads, lane_words=args.lanes,
-                                   stages=args.stages)
+                                   stages=args.stages, interp=args.interp)
         else:   # one JIT straight-line (or TMA) kernel per distinct erasure pattern
             progs = X.compile_many([d[0] for d in dec], compress=args.compress, specialise=1,
                                    threads=args.threads, lane_words=args.lanes,
@@ -529,7 +532,7 @@ def main():
                               lane_words=args.lanes, threads=args.threads, block_bytes_hint=B,
                               stages=args.stages, groups=args.groups, phases=args.phases,
                               reuse=args.reuse, schedule=args.schedule,
-                              greedy_capacity=args.greedy_capacity)
+                              greedy_capacity=args.greedy_capacity, interp=args.interp)
         m_out = len(erased)
     elif wl["op"] == "encode_gft":    # approach (1): no SLP, the coefficient rows themselves
         prog = None
@@ -540,7 +543,7 @@ def main():
                               kernel=args.kernel, lane_words=args.lanes, threads=args.threads,
                               block_bytes_hint=B, stages=args.stages, fuse=args.fuse,
                               schedule=args.schedule, greedy_capacity=args.greedy_capacity,
-                              layout=wl.get("layout", "strip"),
+                              interp=args.interp, layout=wl.get("layout", "strip"),
                               groups=args.groups, phases=args.phases, reuse=args.reuse)
         m_out = p
     compile_s = time.perf_counter() - t0

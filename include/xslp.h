@@ -81,6 +81,13 @@ extern "C" {
                                   full/empty ring) while `threads` consumer threads compute;
                                   needs block_bytes % 128 == 0 */
 
+/* xslp_opts.interp: organisation of the batched interpreter (XSLP_KERNEL_INTERP) */
+#define XSLP_INTERP_LANES 0 /* default: the 32 lanes of a warp run 32 independent SLP instructions
+                               (a round) over the same 16 bytes of every strip, 128-bit shared
+                               loads; max(16, threads / 32) consumer warps per CTA */
+#define XSLP_INTERP_PAIRS 1 /* every thread owns lane_words words; micro-ops of four operands run
+                               warp-uniformly in software-pipelined pairs; threads consumers */
+
 typedef struct xslp_opts {
   int32_t compress;        /* XSLP_COMPRESS_*; default XORREPAIR */
   int32_t fuse;            /* 1 = XOR fusion; default 1 */
@@ -114,6 +121,7 @@ typedef struct xslp_opts {
                               and the fused M^-1 multi-program kernels, which run one CTA per
                               SM, 16 for the syndrome-form kernels, which keep two CTAs per SM),
                               -1 = a fresh shared-memory read at every use, or 1..4096 */
+  int32_t interp;          /* XSLP_INTERP_*: batched interpreter organisation; default LANES */
 } xslp_opts;
 
 typedef struct xslp_stats {

@@ -51,7 +51,7 @@ class xslp_opts(ctypes.Structure):
                 ("stages", ctypes.c_int32), ("greedy_capacity", ctypes.c_int32),
                 ("layout", ctypes.c_int32), ("groups", ctypes.c_int32),
                 ("phases", ctypes.c_int32),
-                ("reuse", ctypes.c_int32)]
+                ("reuse", ctypes.c_int32), ("interp", ctypes.c_int32)]
 
 
 class xslp_stats(ctypes.Structure):
@@ -193,6 +193,8 @@ def default_opts(**kw):
             v = KERNELS[v]
         if k == "layout" and isinstance(v, str):
             v = LAYOUTS[v]
+        if k == "interp" and isinstance(v, str):
+            v = {"lanes": 0, "pairs": 1}[v]
         if not hasattr(o, k):
             raise TypeError(f"unknown option {k}")
         setattr(o, k, int(v))

@@ -32,6 +32,7 @@ extern "C" void xslp_default_opts(xslp_opts *o) {
   o->groups = 1;
   o->phases = 0;
   o->reuse = 0;
+  o->interp = XSLP_INTERP_LANES;
 }
 
 extern "C" int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out) {
@@ -303,6 +304,8 @@ void check_opts(xslp_opts &o) {
   if (o.phases < 0 || o.phases > 8) throw Error(XSLP_EINVAL, "phases must be 0 (auto) or 1..8");
   if (o.phases > 1 && o.groups > 1) throw Error(XSLP_EINVAL, "phases and groups cannot be combined");
   if (o.reuse < -1 || o.reuse > 4096) throw Error(XSLP_EINVAL, "reuse must be -1, 0 (auto) or 1..4096");
+  if (o.interp != XSLP_INTERP_LANES && o.interp != XSLP_INTERP_PAIRS)
+    throw Error(XSLP_EINVAL, "interp must be XSLP_INTERP_LANES or XSLP_INTERP_PAIRS");
   if (o.threads * o.groups > 992) throw Error(XSLP_EINVAL, "pipe kernel: threads * groups <= 992");
 }
 
@@ -404,6 +407,10 @@ extern "C" int64_t xslp_program_dump(const xslp_program *prog, int form, char *b
       // the pipelined interpreter's micro-op code (stage-0 variant) for this program's opts
       const int L = P.opts.lane_words == 2 || P.opts.lane_words == 4 ? P.opts.lane_words : 1;
       auto w = interp_code_dump(P.slp, P.opts.threads, L, P.opts.stages);
+      for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");
+    } else if (form == 4) {
+      // the lane-parallel interpreter's code (stage-0 variant) for S = opts.stages
+      auto w = interp_lanes_dump(P.slp, P.opts.stages);
       for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");
     } else {
       throw Error(XSLP_EINVAL, "bad dump form");

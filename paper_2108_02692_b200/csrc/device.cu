@@ -237,6 +237,7 @@ static std::shared_ptr<Program::Dev> dev_of(const Program *p) {
 static void drop_pools_of(const Program *p);  // below: pools that contain p's bytecode
 
 void drop_code32_of(const Program *p);  // interp.cu
+void drop_lanes_of(const Program *p);   // interp_lanes.cu
 
 Program::~Program() {
   {
@@ -260,6 +261,7 @@ Program::~Program() {
   }
   drop_pools_of(this);  // a later program at the same address must not find this one's pool
   drop_code32_of(this);
+  drop_lanes_of(this);
   {
     std::lock_guard<std::mutex> g(g_mu);
     auto it = g_libs.find(this);

@@ -537,3 +537,76 @@ def test_syndrome_of_a_codeword_is_zero():
     cw = np.concatenate([data, rs.encode(og, n, data)])
     syn, _ = X.xslp_syndrome_bitmatrices(g, n, p, [0])
     assert not rs.bitmatrix_apply(syn, cw).any()
+
+
+def _emulate_lanes(words, strips, n_goals, loads_first=True):
+    """Host emulation of the lane-parallel interpreter's code (interp_lanes.cu emit_variant, dump
+    form 4): rounds of 32 lane-ops over the same words; lane-op = XOR of its 1-4 operand rows
+    (unused slots 1 / 3 name the zero row, slots 2-3 only when it has more than two operands),
+    stored to a variable row and/or a goal.  loads_first=False runs each lane to completion in
+    lane order instead -- the schedule must be right for any interleaving within a round."""
+    w = np.array(words, dtype=np.int64)
+    nl, nr, total, nvrows, rb, var0, const0, start = (int(x) for x in w[:8])
+    assert total == len(w) and start == 8
+    width = strips.shape[1]
+    rng = np.random.default_rng(1)
+    smem = {var0 + r * rb: rng.integers(0, 2**32, width, dtype=np.uint32) for r in range(1, nvrows)}
+    smem[var0] = np.zeros(width, dtype=np.uint32)
+    loads = w[start + 256 * (nr + 1):start + 256 * (nr + 1) + 2 * nl]
+    for i in range(nl):
+        smem[int(loads[2 * i + 1])] = strips[loads[2 * i]].copy()
+    out = np.full((n_goals, width), 0xDEADBEEF, dtype=np.uint32)
+    for r in range(nr):
+        ops = [w[start + 256 * r + 8 * l:start + 256 * r + 8 * l + 8] for l in range(32)]
+
+        def value(o):
+            cnt = int(o[6]) & 0xFF
+            acc = np.zeros(width, dtype=np.uint32)
+            if cnt > 0:
+                acc = acc ^ smem[int(o[0])] ^ smem[int(o[1])]
+            if cnt > 2:
+                acc = acc ^ smem[int(o[2])] ^ smem[int(o[3])]
+            return acc
+
+        def store(o, acc):
+            fl = int(o[6]) >> 8
+            if fl & 1:
+                assert var0 < o[4] < var0 + nvrows * rb
+                smem[int(o[4])] = acc.copy()
+            if fl & 2:
+                out[((int(o[5]) & 0xFFFF) - 16) // 8 * 8 + (int(o[5]) >> 16)] = acc
+
+        if loads_first:
+            vals = [value(o) for o in ops]
+            for o, v in zip(ops, vals):
+                store(o, v)
+        else:
+            for o in ops:
+                store(o, value(o))
+    assert not smem[var0].any()
+    return out
+
+
+@pytest.mark.parametrize("n,p,comp,er,sched", [
+    (10, 4, "xorrepair", None, 1), (10, 4, "xorrepair", (2, 4, 5, 6), 1), (4, 2, "none", None, 1),
+    (20, 4, "xorrepair", (0, 5, 21, 23), 1), (10, 3, "repair", None, 2), (10, 4, "none", (0, 1, 12, 13), 0)])
+def test_lane_interpreter_code_computes_the_oracle_result(n, p, comp, er, sched):
+    # the lane-parallel interpreter's rounds (dump form 4), emulated with every lane of a round
+    # loading first and with lanes run one after another, reproduce the oracle's RS bytes
+    import synth
+    from oracle import rs
+    kind = "cauchy" if (n, p) == (4, 2) else "isal"
+    og = mx.coding_matrix(n, p, kind)
+    g = X.xslp_coding_matrix(n, p, kind)
+    if er is None:
+        bits, rows = X.xslp_encode_bitmatrix(g, n, p), og[n:]
+    else:
+        bits, rows = X.xslp_decode_bitmatrix(g, n, p, er)[0], mx.decode_rows(og, n, list(er))[1]
+    prog = X.xslp_compile(bits, compress=comp, specialise=0, schedule=sched, greedy_capacity=32)
+    words = [int(x) for x in prog.dump(4).split()]
+    B = 128
+    data = synth.stripe_data(9, 2, n, B)
+    strips = data.reshape(8 * n, B // 8).view(np.uint32)
+    want = rs.apply_rows(rows, data).reshape(bits.shape[0], B // 8).view(np.uint32)
+    for lf in (True, False):
+        assert (_emulate_lanes(words, strips, bits.shape[0], loads_first=lf) == want).all()

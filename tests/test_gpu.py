@@ -46,9 +46,17 @@ def run_batch(prog, din, dout, B, nstripes=None):
     torch.cuda.synchronize()
 
 
+def _kernel_kw(kw):
+    """kernel="interp_pairs": the pair-pipelined interpreter (XSLP_INTERP_PAIRS); "interp" is
+    the lane-parallel one (the default)."""
+    if kw.get("kernel") == "interp_pairs":
+        kw = dict(kw, kernel="interp", interp="pairs")
+    return kw
+
+
 def compile_enc(n, p, kind="isal", **kw):
     g = X.xslp_coding_matrix(n, p, kind)
-    return g, X.xslp_compile(X.xslp_encode_bitmatrix(g, n, p), **kw)
+    return g, X.xslp_compile(X.xslp_encode_bitmatrix(g, n, p), **_kernel_kw(kw))
 
 
 # ---- generator ---------------------------------------------------------------------------
@@ -92,8 +100,8 @@ def test_cfg1_encode_decode(kernel):
 
 @pytest.mark.parametrize("comp", ["none", "repair", "xorrepair"])
 @pytest.mark.parametrize("kern,lanes", [("straight", 1), ("straight", 2), ("straight", 4),
-                                        ("interp", 1), ("tma", 1), ("tma", 2), ("pipe", 1),
-                                        ("pipe", 2)])
+                                        ("interp", 1), ("interp_pairs", 1), ("interp_pairs", 2),
+                                        ("tma", 1), ("tma", 2), ("pipe", 1), ("pipe", 2)])
 @pytest.mark.parametrize("p", [2, 3, 4])
 def test_rs10_encode_small_full_compare(comp, kern, lanes, p):
     n, B, S = 10, 9600, 5          # strip 1200 B = 300 words: two 256-thread tiles, ragged tail
@@ -136,7 +144,8 @@ def _decode_inputs(seed, S, n, p, B, e):
     return pats, blocks
 
 
-@pytest.mark.parametrize("kern", ["interp", "straight", "grouped", "grouped_tma", "grouped_pipe"])
+@pytest.mark.parametrize("kern", ["interp", "interp_pairs", "straight", "grouped", "grouped_tma",
+                                  "grouped_pipe"])
 def test_heterogeneous_decode(kern):
     n, p, B, S = 10, 4, 4096, 24
     pats, blocks = _decode_inputs(3, S, n, p, B, 4)
@@ -145,8 +154,8 @@ def test_heterogeneous_decode(kern):
     progs, survs = [], {}
     for er in uniq:
         bits, surv = X.xslp_decode_bitmatrix(g, n, p, er)
-        progs.append(X.xslp_compile(bits, kernel={"grouped": "straight", "grouped_tma": "tma",
-                                                  "grouped_pipe": "pipe"}.get(kern, kern)))
+        progs.append(X.xslp_compile(bits, **_kernel_kw(dict(kernel={"grouped": "straight", "grouped_tma": "tma",
+                                                                   "grouped_pipe": "pipe"}.get(kern, kern)))))
         survs[er] = surv
     idx = torch.tensor([uniq.index(er) for er in pats], dtype=torch.int32, device="cuda")
     surv_blocks = np.stack([blocks[s][survs[pats[s]]] for s in range(S)])
@@ -154,7 +163,7 @@ def test_heterogeneous_decode(kern):
     dout = dev_buf(S, 4, B)
     ti = X.block_table(din, S, n, B)
     to = X.block_table(dout, S, 4, B)
-    if kern == "interp":
+    if kern.startswith("interp"):
         X.xslp_decode_batch_multi(progs, idx, ti, to, S, B)
     elif kern.startswith("grouped"):
         ids, off = X.group_stripes(idx.cpu().numpy(), len(progs))
@@ -487,9 +496,9 @@ def test_random_programs_and_launches(case):
     if kern == "pipe":
         kw["stages"] = int(rng.integers(1, 5))
         kw["phases"] = int(rng.integers(0, min(4, n_in) + 1))
-    if kern == "interp":                    # the pipelined interpreter: L, stages, no JIT
+    if kern == "interp":                    # the batched interpreters: lanes / pairs, no JIT
         kw.update(lane_words=int(rng.choice([1, 2, 4])), stages=int(rng.integers(1, 5)),
-                  specialise=0)
+                  specialise=0, interp=case % 2)
     B = 128 * int(rng.integers(1, 40))
     S = int(rng.integers(1, 5))
     if rng.random() < 0.5:
@@ -709,7 +718,7 @@ def test_cfg2_full_size(kern, threads, lanes, reuse):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("mode", ["grouped", "interp"])
+@pytest.mark.parametrize("mode", ["grouped", "interp", "interp_pairs"])
 def test_cfg3_full_size_roundtrip(mode):
     # RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures (configs[2]);
     # "grouped" (per-pattern LDG kernels, T=64, 8 streams) is the bench's launch configuration
@@ -734,8 +743,8 @@ def test_cfg3_full_size_roundtrip(mode):
         survs[er] = surv
     if mode == "grouped":
         progs = X.compile_many(bitsl, kernel="straight", threads=64, block_bytes_hint=B)
-    else:
-        progs = X.compile_many(bitsl, specialise=0)
+    else:                     # the lane-parallel (default) or the pair-pipelined interpreter
+        progs = X.compile_many(bitsl, specialise=0, interp="pairs" if mode == "interp_pairs" else "lanes")
     pos = [uniq.index(er) for er in pats]
     idx = torch.tensor(pos, dtype=torch.int32, device="cuda")
     tin = torch.stack([ti[s, torch.as_tensor(survs[pats[s]], dtype=torch.long)] for s in range(S)])
@@ -1100,14 +1109,15 @@ def test_byte_layout_full_size(kern, threads):
 
 # ---- CUDA graphs: launches are capturable after xslp_prepare -----------------------------
 
-@pytest.mark.parametrize("kern", ["pipe", "straight", "interp", "pipe_phases", "pipe_byte"])
+@pytest.mark.parametrize("kern", ["pipe", "straight", "interp", "interp_pairs", "pipe_phases", "pipe_byte"])
 def test_cuda_graph_capture(kern):
     n, p, B, S = (20, 4, 65536, 32) if kern == "pipe_phases" else (10, 4, 65536, 64)
     og = mx.coding_matrix(n, p)
     if kern == "pipe_byte":
         _, prog = compile_enc(n, p, kernel="pipe", threads=128, layout="byte", block_bytes_hint=B)
     else:
-        _, prog = compile_enc(n, p, kernel=kern.split("_")[0], threads=256 if kern.startswith("pipe") else 128,
+        _, prog = compile_enc(n, p, kernel=kern if kern == "interp_pairs" else kern.split("_")[0],
+                              threads=256 if kern.startswith("pipe") else 128,
                               block_bytes_hint=B, phases=2 if kern == "pipe_phases" else 1)
     X.xslp_prepare(prog, B)
     din = dev_buf(S, n, B)
