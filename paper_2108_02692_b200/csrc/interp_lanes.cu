@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cmath>
 #include <map>
 #include <set>
 
@@ -39,7 +40,7 @@ void count_launch();  // device.cu
 namespace lanes {
 
 constexpr int kK = 4;                      // operands per lane-op
-constexpr int kOpWords = 8;                // o0..o3, dst, gsel, ctl, 0
+constexpr int kOpWords = 8;                // 4 operand offsets; dst, goal select, ctl, 0
 constexpr int kRoundWords = 32 * kOpWords; // one round of 32 lane-ops (1 KB)
 constexpr int kHead = 8;
 constexpr int kHdr = 16 + 8 * 32;          // per-stage tile header: stripe, prog, pad, 32 out ptrs
@@ -157,7 +158,21 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
     rng ^= rng << 17;
     return (int)(rng % (uint64_t)m);
   };
-  for (int iter = 0; iter < 64 * n && n > 1; ++iter) {
+  // simulated annealing: a worse move is kept with probability exp(-delta / temp), temp
+  // falling linearly to zero; the best arrangement seen is the result
+  int cur_cost = 0;
+  for (int q = 0; q < 4; ++q) cur_cost += qcost(q);
+  int best_cost = cur_cost;
+  std::vector<int> best_q = qof, best_c = cof;
+  const int iters = 400 * n;
+  auto accept = [&](int delta, int iter) {
+    if (delta <= 0) return true;
+    const double temp = 1.5 * (1.0 - (double)iter / iters);
+    if (temp <= 0.0) return false;
+    const double u = (double)(rnd(1 << 20) + 1) / (1 << 20);
+    return u < std::exp(-delta / temp);
+  };
+  for (int iter = 0; iter < iters && n > 1; ++iter) {
     const int i = rnd(n);
     if (rnd(2) == 0) {  // another slot layout for op i
       const int c = rnd((int)cand[i].size()), q = qof[i], old = cof[i];
@@ -165,7 +180,8 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
       const int before = qcost(q);
       apply(i, q, old, -1);
       apply(i, q, c, +1);
-      if (qcost(q) <= before) cof[i] = c;
+      const int delta = qcost(q) - before;
+      if (accept(delta, iter)) { cof[i] = c; cur_cost += delta; }
       else { apply(i, q, c, -1); apply(i, q, old, +1); }
     } else {            // swap op i with op j of another quarter
       const int j = rnd(n), qi = qof[i], qj = qof[j];
@@ -175,7 +191,8 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
       apply(j, qj, cof[j], -1);
       apply(i, qj, cof[i], +1);
       apply(j, qi, cof[j], +1);
-      if (qcost(qi) + qcost(qj) <= before) { qof[i] = qj; qof[j] = qi; }
+      const int delta = qcost(qi) + qcost(qj) - before;
+      if (accept(delta, iter)) { qof[i] = qj; qof[j] = qi; cur_cost += delta; }
       else {
         apply(i, qj, cof[i], -1);
         apply(j, qi, cof[j], -1);
@@ -183,7 +200,10 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
         apply(j, qj, cof[j], +1);
       }
     }
+    if (cur_cost < best_cost) { best_cost = cur_cost; best_q = qof; best_c = cof; }
   }
+  qof = best_q;
+  cof = best_c;
   std::vector<LOp> rd(32);
   std::vector<int> lane = {0, 8, 16, 24};
   for (int i = 0; i < n; ++i) {
@@ -255,7 +275,7 @@ LSched build_lanes(const Slp &s) {
     for (int t : s.ins[k].ops) terms.push_back(term(t));
     emit(terms, used[v] ? v : -1, goals_of_var[v]);
   }
-  // dependences and critical-path heights
+  // dependences
   const int n = (int)ops.size();
   std::vector<int> prod(nv, -1);
   for (int i = 0; i < n; ++i)
@@ -270,19 +290,16 @@ LSched build_lanes(const Slp &s) {
         succ[p].push_back(i);
         ++indeg[i];
       }
-  std::vector<int> height(n, 1);
-  for (int i = n; i-- > 0;)  // ops are in a topological order (producers first)
-    for (int j : succ[i]) height[i] = std::max(height[i], height[j] + 1);
-  // rounds: up to 32 ready ops, highest first (ties: creation order)
+  // rounds: up to 32 ready ops in creation order
   LSched out;
   std::vector<int> ready;
   for (int i = 0; i < n; ++i)
     if (indeg[i] == 0) ready.push_back(i);
   int done = 0;
   while (done < n) {
-    std::sort(ready.begin(), ready.end(), [&](int a, int b) {
-      return height[a] != height[b] ? height[a] > height[b] : a < b;
-    });
+    // the compiler's (DFS) order: fewer live variables -> more positions per tile
+    // (critical path first gave the same number of rounds with ~15% more variable rows)
+    std::sort(ready.begin(), ready.end());
     const size_t take = std::min<size_t>(32, ready.size());
     if (take == 0) throw Error(XSLP_EINVAL, "lane interpreter: cyclic program");
     std::vector<int> now(ready.begin(), ready.begin() + take);
@@ -301,7 +318,7 @@ LSched build_lanes(const Slp &s) {
   // uses it).  Constant rows in order of first use; variable rows by liveness at round
   // granularity: a row whose last read is in round r is reused from round r+1 on (the lanes of a
   // warp may diverge inside a round, so a store of round r must not race another lane's load of
-  // round r).  (Choosing rows by group as well was measured: more rows, no fewer conflicts.)
+  // round r).
   const int R = (int)out.rounds.size();
   out.crow.assign(nc, -1);
   for (auto &rd : out.rounds)
@@ -317,19 +334,36 @@ LSched build_lanes(const Slp &s) {
       for (int q = 0; q < o.cnt; ++q)
         if (o.op[q] < -1) last[-o.op[q] - 2] = r;
   out.vrow.assign(nv, -1);
-  std::set<int> free_rows;
+  // round by round: deal the ops to lanes (their operands' rows are known), then give each
+  // stored variable a row whose bank group no other store of its quarter uses -- a free row of
+  // that group, else a fresh one -- so the 128-bit stores of a quarter-warp do not conflict
+  std::array<std::vector<int>, 8> free_rows;
+  std::array<int, 8> fresh;  // next unused row of each group (row 0 = the zero row)
+  for (int g = 0; g < 8; ++g) fresh[g] = g == 0 ? 8 : g;
   std::vector<int> freed_now;
-  int next = 1;
+  auto grp = [&](int t) { return t == -1 ? -1 : t >= 0 ? out.crow[t] % 8 : out.vrow[-t - 2] % 8; };
   for (int r = 0; r < R; ++r) {
-    for (auto &o : out.rounds[r]) {
-      if (o.dst < 0) continue;
-      int rr;
-      if (!free_rows.empty()) { rr = *free_rows.begin(); free_rows.erase(free_rows.begin()); }
-      else rr = next++;
-      out.vrow[o.dst] = rr;
+    auto &rd = out.rounds[r];
+    rd = deal_round(rd, grp, [](const LOp &) { return -1; });
+    for (int q = 0; q < 4; ++q) {
+      bool used_g[8] = {};
+      for (int l = 8 * q; l < 8 * q + 8; ++l) {
+        const LOp &o = rd[l];
+        if (o.dst < 0) continue;
+        int bg = -1;
+        for (int g = 0; g < 8 && bg < 0; ++g)  // an unused group with a free row
+          if (!used_g[g] && !free_rows[g].empty()) bg = g;
+        for (int g = 0; g < 8 && bg < 0; ++g)  // an unused group, fresh row
+          if (!used_g[g]) bg = g;
+        int rr;
+        if (!free_rows[bg].empty()) { rr = free_rows[bg].back(); free_rows[bg].pop_back(); }
+        else { rr = fresh[bg]; fresh[bg] += 8; }
+        used_g[bg] = true;
+        out.vrow[o.dst] = rr;
+      }
     }
-    for (auto &o : out.rounds[r])
-      for (int q = 0; q < o.cnt; ++q)
+    for (auto &o : rd)
+      for (int q = 0; q < kK; ++q)
         if (o.op[q] < -1) {
           const int v = -o.op[q] - 2;
           if (out.vrow[v] < 0) throw Error(XSLP_EINVAL, "lane interpreter: read before store");
@@ -337,14 +371,12 @@ LSched build_lanes(const Slp &s) {
         }
     std::sort(freed_now.begin(), freed_now.end());
     freed_now.erase(std::unique(freed_now.begin(), freed_now.end()), freed_now.end());
-    free_rows.insert(freed_now.begin(), freed_now.end());
+    for (int x : freed_now) free_rows[x % 8].push_back(x);
     freed_now.clear();
   }
-  out.nvrows = (next + 7) / 8 * 8;
-  // lanes: deal each round (operand slots become positional; the dst store counts too)
-  for (auto &rd : out.rounds)
-    rd = deal_round(rd, [&](int t) { return t == -1 ? -1 : t >= 0 ? out.crow[t] % 8 : out.vrow[-t - 2] % 8; },
-                    [&](const LOp &o) { return o.dst >= 0 ? out.vrow[o.dst] % 8 : -1; });
+  int maxrow = 0;
+  for (int g = 0; g < 8; ++g) maxrow = std::max(maxrow, fresh[g] - 8);
+  out.nvrows = (maxrow / 8 + 1) * 8;
   return out;
 }
 
@@ -368,9 +400,9 @@ size_t layout_smem(Layout &y) {
 // One code variant (stage st):
 //   [0] nloads [1] nrounds [2] words of this variant [3] variable rows (incl. the zero row 0)
 //   [4] row bytes [5] variable rows offset [6] this stage's constant rows offset [7] 8
-//   rounds: nrounds x 32 lane-ops x 8 words: 4 operand byte offsets (unused slots: the zero
-//           row), dst byte offset, goal select (header offset | (goal & 7) << 16), ctl
-//           (count | flags << 8; flags 1 = store dst, 2 = store goal), 0
+//   rounds: nrounds x 256 words: 32 lanes x 4 operand byte offsets (unused slots: the zero
+//           row), then 32 lanes x (dst byte offset, goal select (header offset | (goal & 7) <<
+//           16), ctl (count | flags << 8; flags 1 = store dst, 2 = store goal), 0)
 //   one empty slack round (the consumer prefetches the next round's code)
 //   loads: nloads x (constant index, byte offset of its row)
 std::vector<uint32_t> emit_variant(const LSched &sc, const Layout &y, int st) {
@@ -389,6 +421,10 @@ std::vector<uint32_t> emit_variant(const LSched &sc, const Layout &y, int st) {
     return y.var0 + (uint32_t)sc.vrow[-t - 2] * y.RB;
   };
   for (const auto &rd : sc.rounds) {
+    // [32 lanes x (4 operand offsets)] then [32 lanes x (dst, goal select, ctl, 0)]: each of
+    // the two 128-bit code loads of a round is one contiguous 512-byte warp access
+    for (int l = 0; l < 32; ++l)
+      w.insert(w.end(), {off_of(rd[l].op[0]), off_of(rd[l].op[1]), off_of(rd[l].op[2]), off_of(rd[l].op[3])});
     for (int l = 0; l < 32; ++l) {
       const LOp &o = rd[l];
       uint32_t flags = 0, dst = 0, gsel = 0;
@@ -400,11 +436,11 @@ std::vector<uint32_t> emit_variant(const LSched &sc, const Layout &y, int st) {
         gsel = (uint32_t)(16 + 8 * (o.goal >> 3)) | ((uint32_t)(o.goal & 7) << 16);
         flags |= 2;
       }
-      w.insert(w.end(), {off_of(o.op[0]), off_of(o.op[1]), off_of(o.op[2]), off_of(o.op[3]), dst, gsel,
-                         (uint32_t)o.cnt | flags << 8, 0u});
+      w.insert(w.end(), {dst, gsel, (uint32_t)o.cnt | flags << 8, 0u});
     }
   }
-  for (int l = 0; l < 32; ++l) w.insert(w.end(), {y.var0, y.var0, y.var0, y.var0, 0u, 0u, 0u, 0u});
+  for (int l = 0; l < 32; ++l) w.insert(w.end(), {y.var0, y.var0, y.var0, y.var0});
+  for (int l = 0; l < 32; ++l) w.insert(w.end(), {0u, 0u, 0u, 0u});
   for (size_t r = 0; r < sc.consts.size(); ++r) {
     if (sc.consts[r] < 0) continue;  // a padding row of the group layout: nothing to load
     w.push_back((uint32_t)sc.consts[r]);
@@ -537,15 +573,15 @@ __global__ void __launch_bounds__(1024, 1) xslp_interp_lanes(Args a) {
     const uint32_t hdr = hdr0 + st * kHdr;
     const uint32_t cp = base + a.code0 + st * a.capw * 4;
     const uint32_t nr = lds128(cp).y;
-    const uint32_t lc = cp + kHead * 4 + lane * kOpWords * 4;  // this lane's op of round 0
+    const uint32_t lc = cp + kHead * 4 + lane * 16;  // this lane's operands in round 0 (+512: ctl)
     for (uint32_t q0 = warp * kJ; q0 < nq; q0 += W * kJ) {
       const uint32_t nj = min((uint32_t)kJ, nq - q0);   // quads of this group (ragged tile end)
       const uint32_t col0 = base + q0 * 16;
       const uint64_t off0 = ((uint64_t)tw * a.tpos + (uint64_t)q0 * 4) * 4;
-      uint4 o = lds128(lc), c = lds128(lc + 16);
+      uint4 o = lds128(lc), c = lds128(lc + 512);
       for (uint32_t r = 0; r < nr; ++r) {
         const uint32_t nx = lc + (r + 1) * kRoundWords * 4;
-        const uint4 on = lds128(nx), cn = lds128(nx + 16);  // prefetch (the slack round at the end)
+        const uint4 on = lds128(nx), cn = lds128(nx + 512);  // prefetch (the slack round at the end)
         const uint32_t cnt = c.z & 0xffu, fl = c.z >> 8;
         if (fl) {  // idle lanes (a partly filled round) issue no loads
           uint64_t gp = 0;
@@ -707,7 +743,10 @@ bool interp_lanes_launch(const Program *const *progs, int np, const int32_t *d_p
   Pool pool;
   if (!lanes_plan(progs, np, B, pool)) return false;
   const uint64_t strip = B / 8;
-  const int W = std::max(16, std::min(31, progs[0]->opts.threads / 32));
+  constexpr int J = 4;  // quads per warp per round (measured: 2 slower, 8 slower)
+  // consumer warps: max(16, threads / 32), but no more than a full tile has 4-quad groups
+  const int groups = (int)((pool.y.Tpos / 4 + J - 1) / J);
+  const int W = std::max(1, std::min(groups, std::max(16, std::min(31, progs[0]->opts.threads / 32))));
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));
   const Layout &y = pool.y;
@@ -736,7 +775,7 @@ bool interp_lanes_launch(const Program *const *progs, int np, const int32_t *d_p
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<uint64_t>(a.ntiles, (uint64_t)sms);
   void *args[] = {&a};
-  const void *fn = (const void *)xslp_interp_lanes<4>;  // J = 4 quads per round (measured: 1/2/8 slower)
+  const void *fn = (const void *)xslp_interp_lanes<J>;
   CUDA_OK(cudaLaunchKernel(fn, dim3(grid), dim3(32 * (W + 1)), args, y.smem, st));
   count_launch();
   return true;

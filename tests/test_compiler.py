@@ -541,10 +541,11 @@ def test_syndrome_of_a_codeword_is_zero():
 
 def _emulate_lanes(words, strips, n_goals, loads_first=True):
     """Host emulation of the lane-parallel interpreter's code (interp_lanes.cu emit_variant, dump
-    form 4): rounds of 32 lane-ops over the same words; lane-op = XOR of its 1-4 operand rows
-    (unused slots 1 / 3 name the zero row, slots 2-3 only when it has more than two operands),
-    stored to a variable row and/or a goal.  loads_first=False runs each lane to completion in
-    lane order instead -- the schedule must be right for any interleaving within a round."""
+    form 4): rounds of 32 lane-ops over the same words; a lane-op XORs its operand rows (slots
+    0-1 loaded when it has operands, 2-3 when it has more than two; unused slots name the zero
+    row) and stores to a variable row and/or a goal.  loads_first=False runs each lane to
+    completion in lane order instead -- the schedule must be right for any interleaving within a
+    round."""
     w = np.array(words, dtype=np.int64)
     nl, nr, total, nvrows, rb, var0, const0, start = (int(x) for x in w[:8])
     assert total == len(w) and start == 8
@@ -557,7 +558,9 @@ def _emulate_lanes(words, strips, n_goals, loads_first=True):
         smem[int(loads[2 * i + 1])] = strips[loads[2 * i]].copy()
     out = np.full((n_goals, width), 0xDEADBEEF, dtype=np.uint32)
     for r in range(nr):
-        ops = [w[start + 256 * r + 8 * l:start + 256 * r + 8 * l + 8] for l in range(32)]
+        ops = [np.concatenate([w[start + 256 * r + 4 * l:start + 256 * r + 4 * l + 4],
+                               w[start + 256 * r + 128 + 4 * l:start + 256 * r + 128 + 4 * l + 4]])
+               for l in range(32)]
 
         def value(o):
             cnt = int(o[6]) & 0xFF
@@ -571,7 +574,7 @@ def _emulate_lanes(words, strips, n_goals, loads_first=True):
         def store(o, acc):
             fl = int(o[6]) >> 8
             if fl & 1:
-                assert var0 < o[4] < var0 + nvrows * rb
+                assert var0 < o[4] < var0 + nvrows * rb       # a variable row, never 0 or a constant
                 smem[int(o[4])] = acc.copy()
             if fl & 2:
                 out[((int(o[5]) & 0xFFFF) - 16) // 8 * 8 + (int(o[5]) >> 16)] = acc
