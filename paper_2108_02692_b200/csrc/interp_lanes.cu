@@ -48,6 +48,7 @@ constexpr int kHdr = 16 + 8 * 32;          // per-stage tile header: stripe, pro
 // operand term: constant c (>= 0), variable v (-(v + 2))
 struct LOp {
   int op[kK] = {-1, -1, -1, -1};
+  int zg[kK] = {0, 0, 0, 0};  // a loaded slot with op -1 reads zero row zg (one per bank group)
   int cnt = 0;
   int dst = -1;   // variable stored to a row (-1: none)
   int goal = -1;  // goal stored to HBM (-1: none)
@@ -58,15 +59,16 @@ struct LSched {
   std::vector<int> consts, crow;  // constant row r holds constant consts[r] (-1: padding)
   int nvars = 0;                  // variables incl. split temporaries
   std::vector<int> vrow;          // variable -> its row (SSA: one row for its lifetime)
-  int nvrows = 8;                 // variable rows incl. the zero row 0, a multiple of 8
+  int nvrows = 16;                // variable rows incl. the zero rows 0-7, a multiple of 8
 };
 
 // Lane order of one round.  A 128-bit shared load is served a quarter-warp (8 lanes) at a
 // time, and a row's 16-byte bank group is (offset / 16) mod 8 (row bytes = 16 mod 128), so for
 // every operand slot the 8 lanes of a quarter should read rows of 8 different groups.  The ops
 // are dealt to the 4 quarters and each op's operands permuted over its loaded slots (XOR is
-// commutative; a 3-operand op may put its zero-row read in any slot), greedily by the number of
-// reads already sharing the group, then improved by re-dealing each op once more.
+// commutative; a 3-operand op may put its zero-row read in any slot, and a zero read may use
+// any of the 8 zero rows, one per bank group), greedily by the number of reads already sharing
+// the group, then improved by annealing on the exact wavefront count.
 template <class Grp, class DGrp>
 std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
   const int n = (int)in.size();
@@ -94,10 +96,21 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
   std::vector<int> qof(n, -1), cof(n, 0), fill(4, 0);
   std::vector<int> dg(n);
   for (int i = 0; i < n; ++i) dg[i] = dgrp(in[i]);
+  std::vector<std::array<int, kK>> zsel(n);  // zero row group of each applied zero read
+  const int kZeroKey = -1000000;             // row key of zero row g: kZeroKey + g
+  auto slots_of = [&](int i) { return in[i].cnt == 0 ? 0 : in[i].cnt <= 2 ? 2 : 4; };
   auto term_cost = [&](int q, int k, int t, int gr) {
     if (gr < 0) return 0;
     auto it = rows[q][k].find(t);
     return it != rows[q][k].end() && it->second > 0 ? 0 : distinct[q][k][gr];
+  };
+  auto zero_pick = [&](int q, int k) {  // the zero row adding fewest wavefronts to this cell
+    int bg = 0, bv = 1 << 30;
+    for (int g = 0; g < 8; ++g) {
+      const int v = term_cost(q, k, kZeroKey + g, g);
+      if (v < bv) { bv = v; bg = g; }
+    }
+    return bg;
   };
   auto term_apply = [&](int q, int k, int t, int gr, int d) {
     if (gr < 0) return;
@@ -110,6 +123,10 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
     for (int k = 0; k < kK; ++k) {
       const int t = cand[i][c][k];
       if (t >= 0) v += term_cost(q, k, in[i].op[t], g[i][t]);
+      else if (k < slots_of(i)) {
+        const int z = zero_pick(q, k);
+        v += term_cost(q, k, kZeroKey + z, z);
+      }
     }
     return v;
   };
@@ -118,6 +135,10 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
     for (int k = 0; k < kK; ++k) {
       const int t = cand[i][c][k];
       if (t >= 0) term_apply(q, k, in[i].op[t], g[i][t], d);
+      else if (k < slots_of(i)) {
+        if (d > 0) zsel[i][k] = zero_pick(q, k);
+        term_apply(q, k, kZeroKey + zsel[i][k], zsel[i][k], d);
+      }
     }
     fill[q] += d;
   };
@@ -202,8 +223,16 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
     }
     if (cur_cost < best_cost) { best_cost = cur_cost; best_q = qof; best_c = cof; }
   }
+  // replay the best arrangement, then re-pick every zero row against the final neighbours
+  for (int i = 0; i < n; ++i) apply(i, qof[i], cof[i], -1);
   qof = best_q;
   cof = best_c;
+  for (int i = 0; i < n; ++i) apply(i, qof[i], cof[i], +1);
+  for (int pass = 0; pass < 2; ++pass)
+    for (int i = 0; i < n; ++i) {
+      apply(i, qof[i], cof[i], -1);
+      apply(i, qof[i], cof[i], +1);
+    }
   std::vector<LOp> rd(32);
   std::vector<int> lane = {0, 8, 16, 24};
   for (int i = 0; i < n; ++i) {
@@ -211,11 +240,88 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
     for (int k = 0; k < kK; ++k) {
       const int t = cand[i][cof[i]][k];
       o.op[k] = t >= 0 ? in[i].op[t] : -1;
+      o.zg[k] = t >= 0 ? 0 : zsel[i][k];
     }
     // slots are now positional: cnt keeps its meaning (2 slots loaded if <= 2, else 4)
     rd[lane[qof[i]]++] = o;
   }
   return rd;
+}
+
+// Constant rows are free to permute (the producer's load list names each constant's row):
+// after dealing and variable rows are fixed, swap constant rows while that lowers the load
+// wavefronts -- the sum over (round, quarter, slot) of the largest number of distinct rows read
+// in one bank group (zero row g, rows 0-7, counts as a row of group g).  Deterministic.
+void polish_constant_rows(LSched &sc) {
+  const int R = (int)sc.rounds.size();
+  const int nused = (int)sc.consts.size();
+  if (nused < 2) return;
+  // the (round, quarter, slot) cells each constant is read in
+  std::vector<std::vector<int>> cells_of(nused);
+  auto cell = [&](int r, int q, int k) { return (r * 4 + q) * kK + k; };
+  for (int r = 0; r < R; ++r)
+    for (int l = 0; l < 32; ++l) {
+      const LOp &o = sc.rounds[r][l];
+      for (int k = 0; k < kK; ++k) {
+        const bool loaded = (k < 2 && o.cnt > 0) || (k >= 2 && o.cnt > 2);
+        if (loaded && o.op[k] >= 0) cells_of[sc.crow[o.op[k]]].push_back(cell(r, l / 8, k));
+      }
+    }
+  for (auto &v : cells_of) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  }
+  auto cell_cost = [&](int c) {
+    const int k = c % kK, q = (c / kK) % 4, r = c / kK / 4;
+    int rows[8], n = 0;
+    for (int l = 8 * q; l < 8 * q + 8; ++l) {
+      const LOp &o = sc.rounds[r][l];
+      const bool loaded = (k < 2 && o.cnt > 0) || (k >= 2 && o.cnt > 2);
+      if (!loaded) continue;
+      const int t = o.op[k];
+      const int key = t == -1 ? o.zg[k] : t >= 0 ? 1000000 + sc.crow[t] : sc.vrow[-t - 2];
+      bool seen = false;
+      for (int i = 0; i < n; ++i) seen |= rows[i] == key;
+      if (!seen) rows[n++] = key;
+    }
+    int cnt[8] = {}, m = 0;
+    for (int i = 0; i < n; ++i) {
+      const int g = rows[i] >= 1000000 ? (rows[i] - 1000000) % 8 : rows[i] % 8;  // zero row g: g
+      m = std::max(m, ++cnt[g]);
+    }
+    return m;
+  };
+  // crow index -> constant (the inverse map); swap two constants' rows
+  std::vector<int> cons_of(nused);
+  for (int i = 0; i < nused; ++i) cons_of[i] = sc.consts[i];
+  auto swap_rows = [&](int i, int j) {  // crow indices
+    const int a = cons_of[i], b = cons_of[j];
+    if (a >= 0) sc.crow[a] = j;
+    if (b >= 0) sc.crow[b] = i;
+    std::swap(cons_of[i], cons_of[j]);
+    std::swap(cells_of[i], cells_of[j]);
+  };
+  uint64_t rng = 0x243F6A8885A308D3ull ^ (uint64_t)nused;
+  auto rnd = [&](int m) {
+    rng ^= rng << 13;
+    rng ^= rng >> 7;
+    rng ^= rng << 17;
+    return (int)(rng % (uint64_t)m);
+  };
+  for (int iter = 0; iter < 60 * nused; ++iter) {
+    const int i = rnd(nused), j = rnd(nused);
+    if (i % 8 == j % 8) continue;  // same bank group: no change
+    std::vector<int> cells(cells_of[i]);
+    cells.insert(cells.end(), cells_of[j].begin(), cells_of[j].end());
+    std::sort(cells.begin(), cells.end());
+    cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
+    int before = 0, after = 0;
+    for (int c : cells) before += cell_cost(c);
+    swap_rows(i, j);
+    for (int c : cells) after += cell_cost(c);
+    if (after > before) swap_rows(i, j);  // undo
+  }
+  for (int i = 0; i < nused; ++i) sc.consts[i] = cons_of[i];
 }
 
 LSched build_lanes(const Slp &s) {
@@ -338,8 +444,8 @@ LSched build_lanes(const Slp &s) {
   // stored variable a row whose bank group no other store of its quarter uses -- a free row of
   // that group, else a fresh one -- so the 128-bit stores of a quarter-warp do not conflict
   std::array<std::vector<int>, 8> free_rows;
-  std::array<int, 8> fresh;  // next unused row of each group (row 0 = the zero row)
-  for (int g = 0; g < 8; ++g) fresh[g] = g == 0 ? 8 : g;
+  std::array<int, 8> fresh;  // next unused row of each group (rows 0-7: the zero rows)
+  for (int g = 0; g < 8; ++g) fresh[g] = 8 + g;
   std::vector<int> freed_now;
   auto grp = [&](int t) { return t == -1 ? -1 : t >= 0 ? out.crow[t] % 8 : out.vrow[-t - 2] % 8; };
   for (int r = 0; r < R; ++r) {
@@ -377,6 +483,7 @@ LSched build_lanes(const Slp &s) {
   int maxrow = 0;
   for (int g = 0; g < 8; ++g) maxrow = std::max(maxrow, fresh[g] - 8);
   out.nvrows = (maxrow / 8 + 1) * 8;
+  polish_constant_rows(out);
   return out;
 }
 
@@ -398,9 +505,9 @@ size_t layout_smem(Layout &y) {
 }
 
 // One code variant (stage st):
-//   [0] nloads [1] nrounds [2] words of this variant [3] variable rows (incl. the zero row 0)
+//   [0] nloads [1] nrounds [2] words of this variant [3] variable rows (incl. zero rows 0-7)
 //   [4] row bytes [5] variable rows offset [6] this stage's constant rows offset [7] 8
-//   rounds: nrounds x 256 words: 32 lanes x 4 operand byte offsets (unused slots: the zero
+//   rounds: nrounds x 256 words: 32 lanes x 4 operand byte offsets (unused slots: a zero
 //           row), then 32 lanes x (dst byte offset, goal select (header offset | (goal & 7) <<
 //           16), ctl (count | flags << 8; flags 1 = store dst, 2 = store goal), 0)
 //   one empty slack round (the consumer prefetches the next round's code)
@@ -415,16 +522,17 @@ std::vector<uint32_t> emit_variant(const LSched &sc, const Layout &y, int st) {
   w[5] = y.var0;
   w[6] = cst;
   w[7] = kHead;
-  auto off_of = [&](int t) -> uint32_t {
+  auto off_of = [&](const LOp &o, int k) -> uint32_t {
+    const int t = o.op[k];
     if (t >= 0) return cst + (uint32_t)sc.crow[t] * y.RB;
-    if (t == -1) return y.var0;  // the zero row
+    if (t == -1) return y.var0 + (uint32_t)o.zg[k] * y.RB;  // zero row zg (group zg)
     return y.var0 + (uint32_t)sc.vrow[-t - 2] * y.RB;
   };
   for (const auto &rd : sc.rounds) {
     // [32 lanes x (4 operand offsets)] then [32 lanes x (dst, goal select, ctl, 0)]: each of
     // the two 128-bit code loads of a round is one contiguous 512-byte warp access
     for (int l = 0; l < 32; ++l)
-      w.insert(w.end(), {off_of(rd[l].op[0]), off_of(rd[l].op[1]), off_of(rd[l].op[2]), off_of(rd[l].op[3])});
+      w.insert(w.end(), {off_of(rd[l], 0), off_of(rd[l], 1), off_of(rd[l], 2), off_of(rd[l], 3)});
     for (int l = 0; l < 32; ++l) {
       const LOp &o = rd[l];
       uint32_t flags = 0, dst = 0, gsel = 0;
@@ -512,8 +620,8 @@ __global__ void __launch_bounds__(1024, 1) xslp_interp_lanes(Args a) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // the zero row (unused operand slots read it): every column of variable row 0
-  for (uint32_t i = tid; i < a.RB / 16; i += nthr) sts128(base + a.var0 + 16 * i, make_uint4(0, 0, 0, 0));
+  // the zero rows (unused operand slots read them): every column of variable rows 0-7
+  for (uint32_t i = tid; i < a.RB / 2; i += nthr) sts128(base + a.var0 + 16 * i, make_uint4(0, 0, 0, 0));
   __syncthreads();
   const uint32_t chunk = (a.ntiles + gridDim.x - 1) / gridDim.x;
   const uint32_t t0 = blockIdx.x * chunk, t1 = min(a.ntiles, t0 + chunk);

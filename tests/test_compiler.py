@@ -419,8 +419,9 @@ def _emulate_microops(words, strips, n_goals):
     assert total == len(w) and start == 8 and npairs % 3 == 0
     width = strips.shape[1]
     rng = np.random.default_rng(0)
-    smem = {var0 + r * rb: rng.integers(0, 2**32, width, dtype=np.uint32) for r in range(1, nvrows)}
-    smem[var0] = np.zeros(width, dtype=np.uint32)
+    smem = {var0 + r * rb: rng.integers(0, 2**32, width, dtype=np.uint32) for r in range(8, nvrows)}
+    for r in range(8):                                   # the zero rows, one per bank group
+        smem[var0 + r * rb] = np.zeros(width, dtype=np.uint32)
     loads = w[start + 12 * (npairs + 2):start + 12 * (npairs + 2) + 2 * nl]
     for i in range(nl):
         assert const0 <= loads[2 * i + 1] < const0 + nl * rb
@@ -542,17 +543,18 @@ def test_syndrome_of_a_codeword_is_zero():
 def _emulate_lanes(words, strips, n_goals, loads_first=True):
     """Host emulation of the lane-parallel interpreter's code (interp_lanes.cu emit_variant, dump
     form 4): rounds of 32 lane-ops over the same words; a lane-op XORs its operand rows (slots
-    0-1 loaded when it has operands, 2-3 when it has more than two; unused slots name the zero
-    row) and stores to a variable row and/or a goal.  loads_first=False runs each lane to
-    completion in lane order instead -- the schedule must be right for any interleaving within a
-    round."""
+    0-1 loaded when it has operands, 2-3 when it has more than two; unused slots name one of
+    the zero rows 0-7) and stores to a variable row and/or a goal.  loads_first=False runs each
+    lane to completion in lane order instead -- the schedule must be right for any interleaving
+    within a round."""
     w = np.array(words, dtype=np.int64)
     nl, nr, total, nvrows, rb, var0, const0, start = (int(x) for x in w[:8])
     assert total == len(w) and start == 8
     width = strips.shape[1]
     rng = np.random.default_rng(1)
-    smem = {var0 + r * rb: rng.integers(0, 2**32, width, dtype=np.uint32) for r in range(1, nvrows)}
-    smem[var0] = np.zeros(width, dtype=np.uint32)
+    smem = {var0 + r * rb: rng.integers(0, 2**32, width, dtype=np.uint32) for r in range(8, nvrows)}
+    for r in range(8):                                   # the zero rows, one per bank group
+        smem[var0 + r * rb] = np.zeros(width, dtype=np.uint32)
     loads = w[start + 256 * (nr + 1):start + 256 * (nr + 1) + 2 * nl]
     for i in range(nl):
         smem[int(loads[2 * i + 1])] = strips[loads[2 * i]].copy()
@@ -574,7 +576,7 @@ def _emulate_lanes(words, strips, n_goals, loads_first=True):
         def store(o, acc):
             fl = int(o[6]) >> 8
             if fl & 1:
-                assert var0 < o[4] < var0 + nvrows * rb       # a variable row, never 0 or a constant
+                assert var0 + 8 * rb <= o[4] < var0 + nvrows * rb  # a variable row, never zero/constant
                 smem[int(o[4])] = acc.copy()
             if fl & 2:
                 out[((int(o[5]) & 0xFFFF) - 16) // 8 * 8 + (int(o[5]) >> 16)] = acc
