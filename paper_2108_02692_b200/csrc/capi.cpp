@@ -410,7 +410,7 @@ extern "C" int64_t xslp_program_dump(const xslp_program *prog, int form, char *b
       for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");
     } else if (form == 4) {
       // the lane-parallel interpreter's code (stage-0 variant) for S = opts.stages
-      auto w = interp_lanes_dump(P.slp, P.opts.stages);
+      auto w = interp_lanes_dump(&P, P.opts.stages);
       for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");
     } else {
       throw Error(XSLP_EINVAL, "bad dump form");

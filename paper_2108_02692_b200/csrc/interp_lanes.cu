@@ -27,9 +27,13 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <cmath>
+#include <iterator>
 #include <map>
+#include <memory>
 #include <set>
+#include <thread>
 
 #include "xslp_api.h"
 
@@ -70,8 +74,14 @@ struct LSched {
 // any of the 8 zero rows, one per bank group), greedily by the number of reads already sharing
 // the group, then improved by annealing on the exact wavefront count.
 template <class Grp, class DGrp>
-std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
+std::vector<LOp> deal_round(std::vector<LOp> in, Grp grp, DGrp dgrp) {
   const int n = (int)in.size();
+  for (auto &o : in) {  // terms first (an op dealt before has positional slots with zero reads)
+    int t[kK], m = 0;
+    for (int k = 0; k < kK; ++k)
+      if (o.op[k] != -1) t[m++] = o.op[k];
+    for (int k = 0; k < kK; ++k) o.op[k] = k < m ? t[k] : -1;
+  }
   // candidate slot layouts of an op: term index per slot (-1 = zero row / not loaded)
   std::vector<std::vector<std::array<int, kK>>> cand(n);
   std::vector<std::array<int, kK>> g(n);
@@ -91,7 +101,15 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
   }
   // per quarter and slot (slot kK: the dst store): the rows already read (a row read by several
   // lanes of a quarter is a broadcast) and the distinct rows per bank group
-  std::map<int, int> rows[4][kK + 1];
+  struct Cell {  // <= 8 lanes read a cell: a flat list of (row key, readers)
+    int key[8], cnt[8], n = 0;
+    int *find(int t) {
+      for (int i = 0; i < n; ++i)
+        if (key[i] == t) return &cnt[i];
+      return nullptr;
+    }
+  };
+  Cell rows[4][kK + 1];
   int distinct[4][kK + 1][8] = {};
   std::vector<int> qof(n, -1), cof(n, 0), fill(4, 0);
   std::vector<int> dg(n);
@@ -101,8 +119,8 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
   auto slots_of = [&](int i) { return in[i].cnt == 0 ? 0 : in[i].cnt <= 2 ? 2 : 4; };
   auto term_cost = [&](int q, int k, int t, int gr) {
     if (gr < 0) return 0;
-    auto it = rows[q][k].find(t);
-    return it != rows[q][k].end() && it->second > 0 ? 0 : distinct[q][k][gr];
+    const int *c = rows[q][k].find(t);
+    return c && *c > 0 ? 0 : distinct[q][k][gr];
   };
   auto zero_pick = [&](int q, int k) {  // the zero row adding fewest wavefronts to this cell
     int bg = 0, bv = 1 << 30;
@@ -114,9 +132,22 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
   };
   auto term_apply = [&](int q, int k, int t, int gr, int d) {
     if (gr < 0) return;
-    int &c = rows[q][k][t];
-    if (d > 0 && c++ == 0) ++distinct[q][k][gr];
-    if (d < 0 && --c == 0) --distinct[q][k][gr];
+    Cell &cl = rows[q][k];
+    int *c = cl.find(t);
+    if (!c) {  // a new key (entries are never removed: a count may fall back to 0)
+      if (cl.n == 8) {  // recycle an entry no lane reads any more
+        int i = 0;
+        while (cl.cnt[i] != 0) ++i;
+        cl.key[i] = t;
+        c = &cl.cnt[i];
+      } else {
+        cl.key[cl.n] = t;
+        cl.cnt[cl.n] = 0;
+        c = &cl.cnt[cl.n++];
+      }
+    }
+    if (d > 0 && (*c)++ == 0) ++distinct[q][k][gr];
+    if (d < 0 && --(*c) == 0) --distinct[q][k][gr];
   };
   auto cost = [&](int i, int q, int c) {
     int v = in[i].dst >= 0 ? term_cost(q, kK, -(in[i].dst + 2), dg[i]) : 0;
@@ -248,81 +279,152 @@ std::vector<LOp> deal_round(const std::vector<LOp> &in, Grp grp, DGrp dgrp) {
   return rd;
 }
 
-// Constant rows are free to permute (the producer's load list names each constant's row):
-// after dealing and variable rows are fixed, swap constant rows while that lowers the load
-// wavefronts -- the sum over (round, quarter, slot) of the largest number of distinct rows read
-// in one bank group (zero row g, rows 0-7, counts as a row of group g).  Deterministic.
-void polish_constant_rows(LSched &sc) {
-  const int R = (int)sc.rounds.size();
-  const int nused = (int)sc.consts.size();
-  if (nused < 2) return;
-  // the (round, quarter, slot) cells each constant is read in
-  std::vector<std::vector<int>> cells_of(nused);
-  auto cell = [&](int r, int q, int k) { return (r * 4 + q) * kK + k; };
-  for (int r = 0; r < R; ++r)
-    for (int l = 0; l < 32; ++l) {
-      const LOp &o = sc.rounds[r][l];
-      for (int k = 0; k < kK; ++k) {
-        const bool loaded = (k < 2 && o.cnt > 0) || (k >= 2 && o.cnt > 2);
-        if (loaded && o.op[k] >= 0) cells_of[sc.crow[o.op[k]]].push_back(cell(r, l / 8, k));
+// Row polish.  After dealing, every (round, quarter, slot) cell's wavefronts -- the largest
+// number of distinct rows one bank group serves in it (slot kK: the dst stores) -- depend only
+// on which row each constant and variable got.  Constant rows may be permuted freely (the
+// producer's load list names each constant's row); a variable may move to any variable row free
+// for its whole lifetime [round stored, round last read] (a row is reused only from the round
+// after its last read).  Moves that do not raise the total are kept; deterministic.
+
+int cell_wavefronts(const LSched &sc, int r, int q, int k) {
+  int rows[8], n = 0;
+  for (int l = 8 * q; l < 8 * q + 8; ++l) {
+    const LOp &o = sc.rounds[r][l];
+    int key;  // a row: zero row g -> g, variable row -> its index, constant row -> 1e6 + index
+    if (k == kK) {
+      if (o.dst < 0) continue;
+      key = sc.vrow[o.dst];
+    } else {
+      if (!((k < 2 && o.cnt > 0) || (k >= 2 && o.cnt > 2))) continue;
+      const int t = o.op[k];
+      key = t == -1 ? o.zg[k] : t >= 0 ? 1000000 + sc.crow[t] : sc.vrow[-t - 2];
+    }
+    bool seen = false;
+    for (int i = 0; i < n; ++i) seen |= rows[i] == key;
+    if (!seen) rows[n++] = key;
+  }
+  int cnt[8] = {}, m = 0;
+  for (int i = 0; i < n; ++i) m = std::max(m, ++cnt[(rows[i] % 1000000) % 8]);
+  return m;
+}
+
+int round_wavefronts(const LSched &sc, int r) {
+  int v = 0;
+  for (int q = 0; q < 4; ++q)
+    for (int k = 0; k <= kK; ++k) v += cell_wavefronts(sc, r, q, k);
+  return v;
+}
+
+int total_wavefronts(const LSched &sc) {
+  int v = 0;
+  for (int r = 0; r < (int)sc.rounds.size(); ++r) v += round_wavefronts(sc, r);
+  return v;
+}
+
+struct RowPolish {
+  LSched &sc;
+  int R;
+  std::vector<std::vector<int>> cells_of_c, cells_of_v;  // cells reading / storing each row user
+  std::vector<int> def, last;                             // variable lifetime in rounds
+  std::vector<std::vector<int>> on_row;                   // variables on each variable row
+  explicit RowPolish(LSched &s) : sc(s), R((int)s.rounds.size()) {
+    const int nv = (int)sc.vrow.size();
+    cells_of_c.assign(sc.consts.size(), {});
+    cells_of_v.assign(nv, {});
+    def.assign(nv, -1);
+    last.assign(nv, -1);
+    on_row.assign(sc.nvrows, {});
+    for (int r = 0; r < R; ++r)
+      for (int l = 0; l < 32; ++l) {
+        const LOp &o = sc.rounds[r][l];
+        for (int k = 0; k < kK; ++k) {
+          if (!loaded(o, k) || o.op[k] == -1) continue;
+          const int t = o.op[k];
+          if (t >= 0) cells_of_c[sc.crow[t]].push_back(cell(r, l / 8, k));
+          else {
+            cells_of_v[-t - 2].push_back(cell(r, l / 8, k));
+            last[-t - 2] = std::max(last[-t - 2], r);
+          }
+        }
+        if (o.dst >= 0) {
+          cells_of_v[o.dst].push_back(cell(r, l / 8, kK));
+          def[o.dst] = r;
+        }
+      }
+    for (auto *vv : {&cells_of_c, &cells_of_v})
+      for (auto &v : *vv) {
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+      }
+    for (int v = 0; v < nv; ++v)
+      if (def[v] >= 0) {
+        last[v] = std::max(last[v], def[v]);
+        on_row[sc.vrow[v]].push_back(v);
+      }
+  }
+  static bool loaded(const LOp &o, int k) { return (k < 2 && o.cnt > 0) || (k >= 2 && o.cnt > 2); }
+  static int cell(int r, int q, int k) { return (r * 4 + q) * (kK + 1) + k; }
+  int cell_cost(int c) const {
+    return cell_wavefronts(sc, c / (kK + 1) / 4, (c / (kK + 1)) % 4, c % (kK + 1));
+  }
+  std::vector<int> scratch;
+  int cost_of(const std::vector<int> &a, const std::vector<int> &b) {  // over a u b (both sorted)
+    scratch.clear();
+    std::set_union(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(scratch));
+    int v = 0;
+    for (int c : scratch) v += cell_cost(c);
+    return v;
+  }
+  bool row_free(int row, int v) const {
+    for (int u : on_row[row])
+      if (u != v && !(last[u] < def[v] || last[v] < def[u])) return false;
+    return true;
+  }
+  void move(int v, int row) {
+    auto &from = on_row[sc.vrow[v]];
+    from.erase(std::find(from.begin(), from.end(), v));
+    on_row[row].push_back(v);
+    sc.vrow[v] = row;
+  }
+  void run(uint64_t seed) {
+    const int nused = (int)sc.consts.size(), nv = (int)sc.vrow.size();
+    std::vector<int> vars;
+    for (int v = 0; v < nv; ++v)
+      if (def[v] >= 0) vars.push_back(v);
+    uint64_t rng = seed;
+    auto rnd = [&](int m) {
+      rng ^= rng << 13;
+      rng ^= rng >> 7;
+      rng ^= rng << 17;
+      return (int)(rng % (uint64_t)m);
+    };
+    const int iters = 60 * (nused + (int)vars.size());
+    const std::vector<int> none;
+    for (int iter = 0; iter < iters; ++iter) {
+      if (rnd(2) == 0 && nused >= 2) {  // swap two constants' rows
+        const int i = rnd(nused), j = rnd(nused);
+        if (i % 8 == j % 8) continue;  // same bank group: no change
+        const int before = cost_of(cells_of_c[i], cells_of_c[j]);
+        auto swap_rows = [&]() {
+          const int a = sc.consts[i], b = sc.consts[j];
+          if (a >= 0) sc.crow[a] = j;
+          if (b >= 0) sc.crow[b] = i;
+          std::swap(sc.consts[i], sc.consts[j]);
+          std::swap(cells_of_c[i], cells_of_c[j]);
+        };
+        swap_rows();
+        if (cost_of(cells_of_c[i], cells_of_c[j]) > before) swap_rows();
+      } else if (!vars.empty() && sc.nvrows > 8) {  // a variable to a free row of another group
+        const int v = vars[rnd((int)vars.size())];
+        const int row = 8 + rnd(sc.nvrows - 8), old = sc.vrow[v];
+        if (row % 8 == old % 8 || !row_free(row, v)) continue;
+        const int before = cost_of(cells_of_v[v], none);
+        move(v, row);
+        if (cost_of(cells_of_v[v], none) > before) move(v, old);
       }
     }
-  for (auto &v : cells_of) {
-    std::sort(v.begin(), v.end());
-    v.erase(std::unique(v.begin(), v.end()), v.end());
   }
-  auto cell_cost = [&](int c) {
-    const int k = c % kK, q = (c / kK) % 4, r = c / kK / 4;
-    int rows[8], n = 0;
-    for (int l = 8 * q; l < 8 * q + 8; ++l) {
-      const LOp &o = sc.rounds[r][l];
-      const bool loaded = (k < 2 && o.cnt > 0) || (k >= 2 && o.cnt > 2);
-      if (!loaded) continue;
-      const int t = o.op[k];
-      const int key = t == -1 ? o.zg[k] : t >= 0 ? 1000000 + sc.crow[t] : sc.vrow[-t - 2];
-      bool seen = false;
-      for (int i = 0; i < n; ++i) seen |= rows[i] == key;
-      if (!seen) rows[n++] = key;
-    }
-    int cnt[8] = {}, m = 0;
-    for (int i = 0; i < n; ++i) {
-      const int g = rows[i] >= 1000000 ? (rows[i] - 1000000) % 8 : rows[i] % 8;  // zero row g: g
-      m = std::max(m, ++cnt[g]);
-    }
-    return m;
-  };
-  // crow index -> constant (the inverse map); swap two constants' rows
-  std::vector<int> cons_of(nused);
-  for (int i = 0; i < nused; ++i) cons_of[i] = sc.consts[i];
-  auto swap_rows = [&](int i, int j) {  // crow indices
-    const int a = cons_of[i], b = cons_of[j];
-    if (a >= 0) sc.crow[a] = j;
-    if (b >= 0) sc.crow[b] = i;
-    std::swap(cons_of[i], cons_of[j]);
-    std::swap(cells_of[i], cells_of[j]);
-  };
-  uint64_t rng = 0x243F6A8885A308D3ull ^ (uint64_t)nused;
-  auto rnd = [&](int m) {
-    rng ^= rng << 13;
-    rng ^= rng >> 7;
-    rng ^= rng << 17;
-    return (int)(rng % (uint64_t)m);
-  };
-  for (int iter = 0; iter < 60 * nused; ++iter) {
-    const int i = rnd(nused), j = rnd(nused);
-    if (i % 8 == j % 8) continue;  // same bank group: no change
-    std::vector<int> cells(cells_of[i]);
-    cells.insert(cells.end(), cells_of[j].begin(), cells_of[j].end());
-    std::sort(cells.begin(), cells.end());
-    cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
-    int before = 0, after = 0;
-    for (int c : cells) before += cell_cost(c);
-    swap_rows(i, j);
-    for (int c : cells) after += cell_cost(c);
-    if (after > before) swap_rows(i, j);  // undo
-  }
-  for (int i = 0; i < nused; ++i) sc.consts[i] = cons_of[i];
-}
+};
 
 LSched build_lanes(const Slp &s) {
   const int nc = s.n_const;
@@ -483,8 +585,22 @@ LSched build_lanes(const Slp &s) {
   int maxrow = 0;
   for (int g = 0; g < 8; ++g) maxrow = std::max(maxrow, fresh[g] - 8);
   out.nvrows = (maxrow / 8 + 1) * 8;
-  polish_constant_rows(out);
-  return out;
+  // alternate row polish and re-dealing each round against the polished rows (the deal now also
+  // sees each store's group), a round's new deal kept only if it is cheaper
+  for (int pass = 0; pass < 3; ++pass) {
+    RowPolish(out).run(0x243F6A8885A308D3ull + (uint64_t)pass);
+    auto dgrp = [&](const LOp &o) { return o.dst >= 0 ? out.vrow[o.dst] % 8 : -1; };
+    for (int r = 0; r < R; ++r) {
+      const int before = round_wavefronts(out, r);
+      std::vector<LOp> live, keep = out.rounds[r];
+      for (const auto &o : keep)
+        if (o.cnt > 0 || o.dst >= 0 || o.goal >= 0) live.push_back(o);
+      out.rounds[r] = deal_round(live, grp, dgrp);
+      if (round_wavefronts(out, r) > before) out.rounds[r] = keep;
+    }
+  }
+  LSched &best = out;
+  return best;
 }
 
 struct Layout {
@@ -734,13 +850,53 @@ struct Pool {
 std::mutex g_mu;
 std::map<std::tuple<int, int, int, std::vector<const Program *>>, Pool> g_pools;  // (dev, S, max T_pos, progs)
 
+// Lane schedules are built once per program (untimed host work, ~0.1-0.3 s for an RS(10,4)
+// decode) and cached until the program is freed; a batch of programs is built on all host cores.
+std::mutex g_smu;
+std::map<const Program *, std::shared_ptr<const LSched>> g_scheds;
+
+std::shared_ptr<const LSched> sched_of(const Program *p) {
+  {
+    std::lock_guard<std::mutex> g(g_smu);
+    auto it = g_scheds.find(p);
+    if (it != g_scheds.end()) return it->second;
+  }
+  auto sc = std::make_shared<const LSched>(build_lanes(p->slp));
+  std::lock_guard<std::mutex> g(g_smu);
+  return g_scheds.emplace(p, sc).first->second;  // a racing builder's equal schedule may win
+}
+
+std::vector<std::shared_ptr<const LSched>> scheds_of(const Program *const *progs, int np) {
+  std::vector<std::shared_ptr<const LSched>> out(np);
+  std::atomic<int> next{0};
+  std::exception_ptr err;
+  std::mutex em;
+  auto work = [&]() {
+    for (int i; (i = next++) < np;) {
+      try {
+        out[i] = sched_of(progs[i]);
+      } catch (...) {
+        std::lock_guard<std::mutex> g(em);
+        if (!err) err = std::current_exception();
+      }
+    }
+  };
+  const int nt = std::min<int>(np, std::max(1u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> ts;
+  for (int t = 1; t < nt; ++t) ts.emplace_back(work);
+  work();
+  for (auto &t : ts) t.join();
+  if (err) std::rethrow_exception(err);
+  return out;
+}
+
 }  // namespace lanes
 
 // Dump form 4: the lane interpreter's stage-0 code variant for this program alone (T_pos = the
 // largest multiple of 32 words that fits with S = opts.stages).
-std::vector<uint32_t> interp_lanes_dump(const Slp &s, int S) {
+std::vector<uint32_t> interp_lanes_dump(const Program *p, int S) {
   using namespace lanes;
-  LSched sc = build_lanes(s);
+  const LSched &sc = *sched_of(p);
   Layout y;
   y.S = std::max(1, std::min(4, S));
   y.NC = std::max<int>(8, ((int)sc.consts.size() + 7) / 8 * 8);  // regions start on group 0
@@ -754,6 +910,10 @@ std::vector<uint32_t> interp_lanes_dump(const Slp &s, int S) {
 
 void drop_lanes_of(const Program *p) {
   using namespace lanes;
+  {
+    std::lock_guard<std::mutex> g(g_smu);
+    g_scheds.erase(p);
+  }
   std::lock_guard<std::mutex> g(g_mu);
   for (auto it = g_pools.begin(); it != g_pools.end();) {
     const auto &progs = std::get<3>(it->first);
@@ -769,6 +929,20 @@ void drop_lanes_of(const Program *p) {
       ++it;
     }
   }
+}
+
+// the kernel's shared-memory opt-in, once per device
+static bool finish_plan(int dev) {
+  using namespace lanes;
+  static std::mutex am;
+  static std::map<int, bool> attr;
+  std::lock_guard<std::mutex> g(am);
+  if (!attr[dev]) {
+    for (const void *f : {(const void *)xslp_interp_lanes<4>})
+      CUDA_OK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr[dev] = true;
+  }
+  return true;
 }
 
 // The code pool and layout of a program set for strips of B/8 bytes on the current device, built
@@ -790,16 +964,25 @@ static bool lanes_plan(const Program *const *progs, int np, size_t B, lanes::Poo
     auto it = g_pools.find({dev, S, maxpos, key});
     if (it != g_pools.end()) {
       pool = it->second;
+      return finish_plan(dev);
+    }
+  }
+  // schedules outside the pool lock (parallel, cached per program)
+  const auto sc = scheds_of(progs, np);
+  {
+    std::vector<const Program *> key(progs, progs + np);
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_pools.find({dev, S, maxpos, key});
+    if (it != g_pools.end()) {
+      pool = it->second;
     } else {
-      std::vector<LSched> sc(np);
       Layout y;
       y.S = S;
       int cw = 0;
       for (int i = 0; i < np; ++i) {
-        sc[i] = build_lanes(progs[i]->slp);
-        y.NC = std::max<int>(y.NC, ((int)sc[i].consts.size() + 7) / 8 * 8);  // group-aligned
-        y.V = std::max(y.V, sc[i].nvrows);
-        cw = std::max(cw, consumer_words(sc[i]));
+        y.NC = std::max<int>(y.NC, ((int)sc[i]->consts.size() + 7) / 8 * 8);  // group-aligned
+        y.V = std::max(y.V, sc[i]->nvrows);
+        cw = std::max(cw, consumer_words(*sc[i]));
       }
       y.capw = (cw + 3) / 4 * 4;
       for (y.Tpos = maxpos; y.Tpos >= 32; y.Tpos -= 32)
@@ -810,7 +993,7 @@ static bool lanes_plan(const Program *const *progs, int np, size_t B, lanes::Poo
       for (int i = 0; i < np; ++i) {
         off.push_back((int64_t)all.size());
         for (int s_ = 0; s_ < S; ++s_) {
-          auto w = emit_variant(sc[i], y, s_);
+          auto w = emit_variant(*sc[i], y, s_);
           all.insert(all.end(), w.begin(), w.end());
         }
       }
@@ -824,15 +1007,7 @@ static bool lanes_plan(const Program *const *progs, int np, size_t B, lanes::Poo
       pool = P;
     }
   }
-  static std::mutex am;
-  static std::map<int, bool> attr;
-  std::lock_guard<std::mutex> g(am);
-  if (!attr[dev]) {
-    for (const void *f : {(const void *)xslp_interp_lanes<4>})
-      CUDA_OK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr[dev] = true;
-  }
-  return true;
+  return finish_plan(dev);
 }
 
 bool interp_lanes_prepare(const Program *p, size_t B) {

@@ -34,7 +34,7 @@ static std::atomic<int> g_fail{0};
 static void use_program(const xslp_program *p) {
   xslp_stats st;
   REQUIRE(xslp_program_stats(p, &st) == XSLP_OK);
-  for (int form : {0, 1, 3}) {
+  for (int form : {0, 1, 3, 4}) {
     const int64_t need = xslp_program_dump(p, form, nullptr, 0);
     REQUIRE(need > 0);
     std::string buf((size_t)need + 1, '\0');
