@@ -87,6 +87,10 @@ extern "C" {
                                loads; max(16, threads / 32) consumer warps per CTA */
 #define XSLP_INTERP_PAIRS 1 /* every thread owns lane_words words; micro-ops of four operands run
                                warp-uniformly in software-pipelined pairs; threads consumers */
+#define XSLP_INTERP_TMEM 2  /* every thread owns lane_words words (1, or 2 falling back to 1 when
+                               the TMEM slots or the shared-memory stages do not fit);
+                               SLP variables live in tensor memory (tcgen05.ld/st, one TMEM lane
+                               per thread), constants in shared memory; 128 consumer threads */
 
 typedef struct xslp_opts {
   int32_t compress;        /* XSLP_COMPRESS_*; default XORREPAIR */

@@ -194,7 +194,7 @@ def default_opts(**kw):
         if k == "layout" and isinstance(v, str):
             v = LAYOUTS[v]
         if k == "interp" and isinstance(v, str):
-            v = {"lanes": 0, "pairs": 1}[v]
+            v = {"lanes": 0, "pairs": 1, "tmem": 2}[v]
         if not hasattr(o, k):
             raise TypeError(f"unknown option {k}")
         setattr(o, k, int(v))

@@ -304,8 +304,8 @@ void check_opts(xslp_opts &o) {
   if (o.phases < 0 || o.phases > 8) throw Error(XSLP_EINVAL, "phases must be 0 (auto) or 1..8");
   if (o.phases > 1 && o.groups > 1) throw Error(XSLP_EINVAL, "phases and groups cannot be combined");
   if (o.reuse < -1 || o.reuse > 4096) throw Error(XSLP_EINVAL, "reuse must be -1, 0 (auto) or 1..4096");
-  if (o.interp != XSLP_INTERP_LANES && o.interp != XSLP_INTERP_PAIRS)
-    throw Error(XSLP_EINVAL, "interp must be XSLP_INTERP_LANES or XSLP_INTERP_PAIRS");
+  if (o.interp != XSLP_INTERP_LANES && o.interp != XSLP_INTERP_PAIRS && o.interp != XSLP_INTERP_TMEM)
+    throw Error(XSLP_EINVAL, "interp must be XSLP_INTERP_LANES, XSLP_INTERP_PAIRS or XSLP_INTERP_TMEM");
   if (o.threads * o.groups > 992) throw Error(XSLP_EINVAL, "pipe kernel: threads * groups <= 992");
 }
 
@@ -411,6 +411,10 @@ extern "C" int64_t xslp_program_dump(const xslp_program *prog, int form, char *b
     } else if (form == 4) {
       // the lane-parallel interpreter's code (stage-0 variant) for S = opts.stages
       auto w = interp_lanes_dump(&P, P.opts.stages);
+      for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");
+    } else if (form == 5) {
+      // the TMEM interpreter's code
+      auto w = interp_tmem_dump(&P);
       for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");
     } else {
       throw Error(XSLP_EINVAL, "bad dump form");

@@ -238,6 +238,7 @@ static void drop_pools_of(const Program *p);  // below: pools that contain p's b
 
 void drop_code32_of(const Program *p);  // interp.cu
 void drop_lanes_of(const Program *p);   // interp_lanes.cu
+void drop_tmem_of(const Program *p);    // interp_tmem.cu
 
 Program::~Program() {
   {
@@ -262,6 +263,7 @@ Program::~Program() {
   drop_pools_of(this);  // a later program at the same address must not find this one's pool
   drop_code32_of(this);
   drop_lanes_of(this);
+  drop_tmem_of(this);
   {
     std::lock_guard<std::mutex> g(g_mu);
     auto it = g_libs.find(this);

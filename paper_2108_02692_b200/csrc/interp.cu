@@ -741,8 +741,12 @@ static bool interp_pipe_plan(const Program *const *progs, int np, size_t B, Inte
 
 bool interp_lanes_prepare(const Program *p, size_t B);  // interp_lanes.cu
 
+bool interp_tmem_prepare(const Program *p, size_t B);  // interp_tmem.cu
+
 bool interp_pipe_prepare(const Program *p, size_t B) {
   if (p->opts.interp == XSLP_INTERP_LANES) return interp_lanes_prepare(p, B);
+  if (p->opts.interp == XSLP_INTERP_TMEM)
+    return interp_tmem_prepare(p, B) || interp_lanes_prepare(p, B);
   const Program *ps[1] = {p};
   InterpPlan plan;
   return interp_pipe_plan(ps, 1, B, plan);
@@ -751,6 +755,9 @@ bool interp_pipe_prepare(const Program *p, size_t B) {
 bool interp_lanes_launch(const Program *const *progs, int np, const int32_t *d_pos,
                          const int32_t *d_ids, const uint8_t *const *in, uint8_t *const *out,
                          int nstripes, size_t B, cudaStream_t st);  // interp_lanes.cu
+bool interp_tmem_launch(const Program *const *progs, int np, const int32_t *d_pos,
+                        const int32_t *d_ids, const uint8_t *const *in, uint8_t *const *out,
+                        int nstripes, size_t B, cudaStream_t st);  // interp_tmem.cu
 
 bool interp_pipe_launch(const Program *const *progs, int np, const int32_t *d_pos,
                         const int32_t *d_ids, const uint8_t *const *in, uint8_t *const *out,
@@ -758,6 +765,9 @@ bool interp_pipe_launch(const Program *const *progs, int np, const int32_t *d_po
   if (!in || !out || nstripes <= 0) return false;
   if (progs[0]->opts.interp == XSLP_INTERP_LANES)
     return interp_lanes_launch(progs, np, d_pos, d_ids, in, out, nstripes, B, st);
+  if (progs[0]->opts.interp == XSLP_INTERP_TMEM)  // the lane interpreter when TMEM does not fit
+    return interp_tmem_launch(progs, np, d_pos, d_ids, in, out, nstripes, B, st) ||
+           interp_lanes_launch(progs, np, d_pos, d_ids, in, out, nstripes, B, st);
   InterpPlan plan;
   if (!interp_pipe_plan(progs, np, B, plan)) return false;
   const Layout &y = plan.pool.y;

@@ -1,0 +1,746 @@
+// TMEM interpreter: the paper's "interpreter style" with the SLP's variables held in
+// Blackwell tensor memory.
+//
+// Why: an interpreter cannot keep SLP variables in registers (their names are data, and an
+// indirect branch per instruction costs ~150 cycles on sm_100a: scripts/dispatch_probe.py), so
+// the shared-memory interpreters (interp.cu, interp_lanes.cu) read every operand from shared
+// memory and are bound by its 128 B/clk/SM.  Tensor memory (256 KB per SM, 128 lanes x 512
+// 32-bit columns) is addressed per thread by a warp-uniform column: exactly the "variable
+// index is data" access an interpreter needs, at ~280-390 B/clk/SM of tcgen05.ld bandwidth and
+// ~17 cycles latency (scripts/tmem_probe.cu).  So: constants stay where TMA puts them (shared
+// memory), variables live in TMEM, and every thread runs the same instruction stream on its own
+// words -- code loads are broadcasts and shared accesses are conflict-free by construction.
+//
+// Work layout (persistent, one CTA per SM): 4 consumer warps (128 threads = the 128 TMEM
+// lanes) + 1 producer warp.  A tile is 128*W consecutive 32-bit words of every strip of one
+// stripe (W = 1 or 2 words per thread); thread t owns words t*W..t*W+W-1.  The producer streams
+// each tile's constant strips by TMA (cp.async.bulk + mbarrier full/empty ring of S stages) and,
+// when a stage's program changes, the program's code into that stage's code buffer.
+//
+// Code (host, build_tmem): the scheduled SLP's instructions (P:803-818 MultiSLP, DFS order
+// P:1279-1303) become ops of up to 4 shared (constant) + 4 TMEM (variable) operands; wider
+// instructions become a tree of partial ops into temporaries.  Ops are list-scheduled into
+// batches of kB mutually independent ops; a consumer issues all loads of a batch, waits once
+// (tcgen05.wait::ld), XORs, then stores the results to TMEM (tcgen05.st) and goals to HBM.
+// TMEM slots (W columns each) are assigned by liveness at batch granularity; a batch reading a
+// slot the previous batch stored first waits for the stores (tcgen05.wait::st).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <array>
+#include <atomic>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <tuple>
+
+#include "xslp_api.h"
+
+namespace xslp {
+
+void count_launch();  // device.cu
+
+namespace tmem {
+
+constexpr int kMaxB = 8;           // ops per batch: batch_size() (4 or 8)
+constexpr int kH = 4;              // tile header / code slots (a ring longer than the S stages)
+constexpr int kHead = 8;           // code header words
+constexpr int kHdr = 16 + 8 * 32;  // per-stage tile header: stripe, prog, pad, 32 out ptrs
+constexpr int kCols = 512;         // TMEM columns allocated per CTA
+constexpr int kZero = 0, kJunk = 1, kConst0 = 2;  // TMEM slots: zero, write sink, constants
+constexpr uint32_t kNone = 0xffff;
+
+inline int batch_size() {
+  static const int b = [] {
+    const char *e = getenv("XSLP_TMEM_BATCH");
+    return e && atoi(e) == 4 ? 4 : 8;
+  }();
+  return b;
+}
+
+struct TOp {
+  int t[4] = {-1, -1, -1, -1};  // operand terms: constant c (< n_const) or variable n_const + v
+  int dst = -1;                 // variable defined (-1: none, the result is a goal only)
+  int goal = -1;                // goal stored (-1: none)
+  int arity() const { return (t[0] >= 0) + (t[1] >= 0) + (t[2] >= 0) + (t[3] >= 0); }
+};
+
+struct TSched {
+  int n_const = 0;
+  int B = 8;                                    // ops per batch
+  std::vector<std::array<TOp, kMaxB>> batches;  // unused entries: no operands, dst = goal = -1
+  std::vector<uint8_t> wait_st;              // batch first waits for earlier TMEM stores
+  std::vector<int> consts;                   // constant row r (TMEM slot kConst0 + r) holds consts[r]
+  std::vector<int> vslot;                    // variable -> TMEM slot
+  int nslots = 0;                            // slots used (zero, sink, constants, variables)
+};
+
+// Lower the scheduled SLP into 4-operand ops and batches of kB independent ops.
+TSched build_tmem(const Slp &s) {
+  TSched out;
+  out.n_const = s.n_const;
+  const int kB = out.B = batch_size();
+  int nv = s.n_vars;
+  std::vector<TOp> ops;
+  std::vector<std::vector<int>> goals_of(s.n_vars);  // variable -> goal indices
+  for (size_t g = 0; g < s.goal.size(); ++g) {
+    const int t = s.goal[g];
+    if (t >= s.n_const) goals_of[t - s.n_const].push_back((int)g);
+  }
+  // an instruction of arity a > 4 becomes partial ops of 4 operands into temporaries
+  auto emit = [&](std::vector<int> ts, int dst, int goal) {
+    while (ts.size() > 4) {
+      TOp p;
+      for (int k = 0; k < 4; ++k, ts.pop_back()) p.t[k] = ts.back();
+      p.dst = nv++;
+      ops.push_back(p);
+      ts.insert(ts.begin(), s.n_const + p.dst);
+    }
+    TOp o;
+    for (size_t k = 0; k < ts.size(); ++k) o.t[k] = ts[k];
+    o.dst = dst;
+    o.goal = goal;
+    ops.push_back(o);
+  };
+  std::vector<int> nuses(s.n_vars, 0);
+  for (const auto &in : s.ins)
+    for (int t : in.ops)
+      if (t >= s.n_const) ++nuses[t - s.n_const];
+  for (const auto &in : s.ins) {
+    const auto &gl = goals_of[in.var];
+    const int dst = nuses[in.var] > 0 ? in.var : -1;
+    if (dst < 0 && gl.empty()) continue;  // dead (the compiler keeps none)
+    emit(in.ops, dst, gl.empty() ? -1 : gl[0]);
+    for (size_t k = 1; k < gl.size(); ++k) {  // duplicate goals: copy ops
+      if (dst < 0) throw Error(XSLP_EINVAL, "tmem: duplicate goal of a dead variable");
+      emit({s.n_const + in.var}, -1, gl[k]);
+    }
+  }
+  for (size_t g = 0; g < s.goal.size(); ++g) {  // constant and zero goals
+    const int t = s.goal[g];
+    if (t >= s.n_const) continue;
+    emit(t >= 0 ? std::vector<int>{t} : std::vector<int>{}, -1, (int)g);
+  }
+  // ---- batches: list scheduling in op order (the DFS order keeps lifetimes short); a batch
+  // of ops with at most two operands skips the loads of operands 3-4, so such ops are batched
+  // together when the window allows
+  std::vector<int> batch_of(ops.size(), -1);
+  std::vector<int> vbatch(nv, -1);  // batch that defines the variable
+  auto ready = [&](size_t i, int nb) {
+    for (int t : ops[i].t)
+      if (t >= s.n_const && (vbatch[t - s.n_const] < 0 || vbatch[t - s.n_const] >= nb)) return false;
+    return true;
+  };
+  size_t first = 0;
+  int nb = 0;
+  const size_t kWindow = 48;
+  while (first < ops.size()) {
+    std::array<TOp, kMaxB> b;
+    int n = 0;
+    // the oldest ready op decides the batch class; fill with ready ops of the same class, then any
+    int cls = -1;
+    for (int pass = 0; pass < 2 && n < kB; ++pass)
+      for (size_t i = first; i < ops.size() && i < first + kWindow && n < kB; ++i) {
+        if (batch_of[i] >= 0 || !ready(i, nb)) continue;
+        const int c = ops[i].arity() > 2;
+        if (cls < 0) cls = c;
+        if (pass == 0 && c != cls) continue;
+        batch_of[i] = nb;
+        b[n++] = ops[i];
+      }
+    if (n == 0) throw Error(XSLP_EINVAL, "tmem: no ready op (bad schedule)");
+    for (int k = 0; k < n; ++k)
+      if (b[k].dst >= 0) vbatch[b[k].dst] = nb;
+    out.batches.push_back(b);
+    ++nb;
+    while (first < ops.size() && batch_of[first] >= 0) ++first;
+  }
+  // ---- constant rows in first-use order
+  std::vector<int> row(s.n_const, -1);
+  for (const auto &b : out.batches)
+    for (const auto &o : b)
+      for (int t : o.t)
+        if (t >= 0 && t < s.n_const && row[t] < 0) {
+          row[t] = (int)out.consts.size();
+          out.consts.push_back(t);
+        }
+  // ---- variable slots by liveness at batch granularity, after the constant slots
+  const int v0 = kConst0 + (int)out.consts.size();
+  std::vector<int> last(nv, -1);
+  for (int bi = 0; bi < nb; ++bi)
+    for (const auto &o : out.batches[bi])
+      for (int t : o.t)
+        if (t >= s.n_const) last[t - s.n_const] = std::max(last[t - s.n_const], bi);
+  out.vslot.assign(nv, -1);
+  std::vector<int> free_at;  // variable slot -> first batch that may overwrite it
+  for (int bi = 0; bi < nb; ++bi)
+    for (const auto &o : out.batches[bi]) {
+      if (o.dst < 0) continue;
+      int k = 0;
+      while (k < (int)free_at.size() && free_at[k] > bi) ++k;
+      if (k == (int)free_at.size()) free_at.push_back(0);
+      out.vslot[o.dst] = v0 + k;
+      free_at[k] = std::max(last[o.dst], bi) + 1;  // read through batch last[dst]
+    }
+  out.nslots = v0 + (int)free_at.size();
+  // a wait::st at the start of batch w completes the stores of batches < w; the tile's
+  // constant copies are waited for before batch 0
+  out.wait_st.assign(nb, 0);
+  int covered = 0;
+  for (int bi = 1; bi < nb; ++bi) {
+    bool need = false;
+    for (const auto &o : out.batches[bi])
+      for (int t : o.t)
+        if (t >= s.n_const && vbatch[t - s.n_const] >= covered) need = true;
+    if (need) {
+      out.wait_st[bi] = 1;
+      covered = bi;
+    }
+  }
+  return out;
+}
+
+// Code (u32 words; TMEM columns = slot * W):
+//   [0] nconst rows [1] nbatches [2] total words [3] slots used [4] kB [5] W [6..7] 0
+//   batches: nbatches x kB ops x 4 words, then one padding batch (the consumer prefetches):
+//     w0 = col(t0) | col(t1) << 16   w1 = col(t2) | col(t3) << 16   (absent operand: the zero slot)
+//     w2 = col(dst) (absent: the sink slot) | (goal + 1) << 16
+//     w3 (op 0 of a batch) = 1: wait for earlier TMEM stores first; 2: the batch has ops of
+//        three or four operands (else operands 3-4 are not loaded)
+//   loads: nconst x (constant index)   (row r = TMEM slot kConst0 + r)
+std::vector<uint32_t> emit_code(const TSched &sc, int W) {
+  const int kB = sc.B;
+  std::vector<uint32_t> w(kHead, 0);
+  std::vector<int> row(sc.n_const, -1);
+  for (size_t r = 0; r < sc.consts.size(); ++r) row[sc.consts[r]] = (int)r;
+  auto col = [&](int t) -> uint32_t {
+    if (t < 0) return (uint32_t)(kZero * W);
+    if (t < sc.n_const) return (uint32_t)((kConst0 + row[t]) * W);
+    return (uint32_t)(sc.vslot[t - sc.n_const] * W);
+  };
+  w[0] = (uint32_t)sc.consts.size();
+  w[1] = (uint32_t)sc.batches.size();
+  w[3] = (uint32_t)sc.nslots;
+  w[4] = kB;
+  w[5] = (uint32_t)W;
+  for (size_t bi = 0; bi < sc.batches.size(); ++bi) {
+    bool quad = false;
+    for (int j = 0; j < kB; ++j) quad |= sc.batches[bi][j].arity() > 2;
+    for (int j = 0; j < kB; ++j) {
+      const TOp &o = sc.batches[bi][j];
+      const uint32_t d = o.dst >= 0 ? (uint32_t)(sc.vslot[o.dst] * W) : (uint32_t)(kJunk * W);
+      const uint32_t fl = j == 0 ? (sc.wait_st[bi] ? 1u : 0u) | (quad ? 2u : 0u) : 0u;
+      w.insert(w.end(), {col(o.t[0]) | col(o.t[1]) << 16, col(o.t[2]) | col(o.t[3]) << 16,
+                         d | (uint32_t)(o.goal + 1) << 16, fl});
+    }
+  }
+  for (int j = 0; j < kB; ++j)  // padding batch
+    w.insert(w.end(), {0u, 0u, (uint32_t)(kJunk * W), 0u});
+  for (int c : sc.consts) w.push_back((uint32_t)c);
+  while (w.size() % 4) w.push_back(0);
+  w[2] = (uint32_t)w.size();
+  return w;
+}
+
+inline int consumer_words(const TSched &sc) { return kHead + 4 * sc.B * ((int)sc.batches.size() + 1); }
+
+struct Layout {
+  int W = 2, CW = 4, S = 2, NC = 1, capw = 0, B = 8;
+  uint32_t code0 = 0, const0 = 0, RB = 0;
+  size_t smem = 0;
+};
+
+size_t layout_smem(Layout &y) {
+  y.RB = (uint32_t)(y.CW * 32 * y.W * 4);
+  y.code0 = 128 + kH * kHdr;
+  size_t c0 = y.code0 + (size_t)kH * y.capw * 4;
+  c0 = (c0 + 127) / 128 * 128;
+  y.const0 = (uint32_t)c0;
+  y.smem = c0 + (size_t)y.S * y.NC * y.RB;
+  // at least half the SM's shared memory: one CTA per SM, so one TMEM allocation of 512 columns
+  y.smem = std::max<size_t>(y.smem, 120 * 1024);
+  return y.smem;
+}
+
+struct Args {
+  const uint32_t *code;
+  const int64_t *prog_off;
+  const int32_t *prog_of_stripe;
+  const int32_t *ids;
+  const uint8_t *const *in_tbl;
+  uint8_t *const *out_tbl;
+  uint64_t strip;
+  uint32_t words, tps, ntiles, tpos;  // tpos = consumer threads * W words per strip per tile
+  int32_t n_in, n_out, S, nprogs;
+  uint32_t code0, capw, const0, RB, NC;
+};
+
+__device__ __forceinline__ uint32_t sm_addr(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool try_wait(uint32_t bar, uint32_t ph) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(bar), "r"(ph) : "memory");
+  return ok;
+}
+
+template <int W>
+struct Vec { uint32_t x[W]; };
+
+template <int W>
+__device__ __forceinline__ void lds_w(uint32_t a, Vec<W> &v) {
+  if constexpr (W == 1) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v.x[0]) : "r"(a) : "memory");
+  else asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x[0]), "=r"(v.x[1]) : "r"(a) : "memory");
+}
+template <int W>
+__device__ __forceinline__ void ldtm_w(uint32_t ta, Vec<W> &v) {
+  if constexpr (W == 1)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v.x[0]) : "r"(ta) : "memory");
+  else
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(v.x[0]), "=r"(v.x[1]) : "r"(ta) : "memory");
+}
+template <int W>
+__device__ __forceinline__ void sttm_w(uint32_t ta, const Vec<W> &v) {
+  if constexpr (W == 1)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(ta), "r"(v.x[0]) : "memory");
+  else
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(ta), "r"(v.x[0]), "r"(v.x[1]) : "memory");
+}
+__device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// W words per thread, CW consumer warps (4: each owns a 32-lane TMEM quarter and 512 columns;
+// 8: warps w and w+4 share a quarter, 256 columns each)
+template <int W, int CW, int kB>
+__global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const uint32_t tid = threadIdx.x;
+  const int S = a.S;
+  const uint32_t base = sm_addr(sm);
+  const uint32_t hdr0 = base + 128;
+  const uint32_t warp = tid / 32, lane = tid & 31;
+  // Tile it uses constant-row stage it % S and header/code slot it % kH.  Barriers: full[k]
+  // +8k (TMA bytes of stage k), rows_empty[k] +32+8k (stage k's rows copied to TMEM),
+  // code_empty[h] +64+8h (the tile of slot h is done with its header and code); TMEM base
+  // address at +120
+  if (tid == 0) {
+    for (int k = 0; k < S; ++k) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(base + 8 * k));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(base + 32 + 8 * k), "r"(CW));
+    }
+    for (int k = 0; k < kH; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(base + 64 + 8 * k), "r"(CW));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(base + 120),
+                 "n"(kCols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  uint32_t tbase;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tbase) : "r"(base + 120) : "memory");
+  const uint32_t chunk = (a.ntiles + gridDim.x - 1) / gridDim.x;
+  const uint32_t t0 = blockIdx.x * chunk, t1 = min(a.ntiles, t0 + chunk);
+  if (warp == CW) {  // ---------------- producer warp (all 32 lanes issue copies)
+    int cur[kH];
+#pragma unroll
+    for (int k = 0; k < kH; ++k) cur[k] = -1;
+    for (uint32_t tile = t0, it = 0; tile < t1; ++tile, ++it) {
+      const uint32_t st = it % S, ph = (it / S) & 1, hs = it % kH, hph = (it / kH) & 1;
+      const uint32_t entry = tile / a.tps, tw = tile % a.tps;
+      const uint32_t stripe = a.ids ? (uint32_t)a.ids[entry] : entry;
+      const int prog = a.prog_of_stripe ? a.prog_of_stripe[stripe] : 0;
+      if (prog < 0 || prog >= a.nprogs) asm volatile("trap;");
+      const uint32_t *pc = a.code + a.prog_off[prog];
+      const uint8_t *const *in = a.in_tbl + (size_t)stripe * a.n_in;
+      uint8_t *const *out = a.out_tbl + (size_t)stripe * a.n_out;
+      const uint32_t nl = pc[0], nb = pc[1];
+      const uint32_t *ld = pc + kHead + 4 * kB * (nb + 1);  // pc[4] == kB
+      const size_t toff = (size_t)tw * a.tpos * 4;
+      const uint64_t optr = lane < (uint32_t)a.n_out ? (uint64_t)out[lane] : 0;
+      const bool newcode = cur[hs] != prog;
+      if (it >= (uint32_t)S)
+        while (!try_wait(base + 32 + 8 * st, ph ^ 1)) __nanosleep(32);
+      if (it >= (uint32_t)kH)  // the tile that last used this header / code slot is done
+        while (!try_wait(base + 64 + 8 * hs, hph ^ 1)) __nanosleep(32);
+      const uint32_t h = hdr0 + hs * kHdr;
+      if (lane < (uint32_t)a.n_out) asm volatile("st.shared.u64 [%0], %1;" ::"r"(h + 16 + 8 * lane), "l"(optr) : "memory");
+      const uint32_t nbytes = min(a.tpos, a.words - tw * a.tpos) * 4;
+      const uint32_t cbytes = newcode ? (kHead + 4 * kB * (nb + 1)) * 4 : 0;
+      cur[hs] = prog;
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(h), "r"(stripe) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(h + 4), "r"((uint32_t)prog) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(base + 8 * st),
+                     "r"(nbytes * nl + cbytes) : "memory");
+        if (cbytes)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              ::"r"(base + a.code0 + hs * a.capw * 4), "l"(pc), "r"(cbytes), "r"(base + 8 * st) : "memory");
+      }
+      __syncwarp();
+      const uint32_t rows = a.const0 + st * a.NC * a.RB;
+      for (uint32_t i = lane; i < nl; i += 32) {
+        const uint32_t c = ld[i];
+        const uint8_t *src = in[c >> 3] + (c & 7) * a.strip + toff;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(base + rows + i * a.RB), "l"(src), "r"(nbytes), "r"(base + 8 * st) : "memory");
+      }
+    }
+  } else {
+    // ---------------- consumer warps: every thread runs the op stream on its W words
+    const uint32_t tl = tbase + (((warp & 3) * 32u) << 16) + (CW == 8 ? (warp >> 2) * (kCols / 2) : 0);
+    {
+      Vec<W> z;
+#pragma unroll
+      for (int w = 0; w < W; ++w) z.x[w] = 0;
+      sttm_w<W>(tl + kZero * W, z);
+      wait_st();
+    }
+    for (uint32_t tile = t0, it = 0; tile < t1; ++tile, ++it) {
+      const uint32_t st = it % S, ph = (it / S) & 1, hs = it % kH;
+      while (!try_wait(base + 8 * st, ph)) {
+      }
+      const uint32_t tw = tile % a.tps;
+      const uint32_t npos = min(a.tpos, a.words - tw * a.tpos);
+      const bool live = tid * W < npos;  // ragged tail: no goal stores past the strip
+      const uint32_t hdr = hdr0 + hs * kHdr;
+      const uint32_t cp = base + a.code0 + hs * a.capw * 4;
+      const uint4 head = lds128(cp);
+      const uint32_t nl = head.x, nb = head.y;
+      // the stage's constant rows -> this thread's TMEM constant slots; then the rows are free
+      {
+        const uint32_t rs = base + a.const0 + st * a.NC * a.RB + tid * W * 4;
+        for (uint32_t r = 0; r < nl; ++r) {
+          Vec<W> v;
+          lds_w<W>(rs + r * a.RB, v);
+          sttm_w<W>(tl + (kConst0 + r) * W, v);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(base + 32 + 8 * st) : "memory");
+      wait_st();
+      const uint64_t toff = ((uint64_t)tw * a.tpos + (uint64_t)tid * W) * 4;
+      uint32_t op = cp + kHead * 4;
+      uint4 o[kB];
+#pragma unroll
+      for (int j = 0; j < kB; ++j) o[j] = lds128(op + 16 * j);
+      for (uint32_t b = 0; b < nb; ++b) {
+        op += 16 * kB;
+        const uint32_t fl = o[0].w;
+        if (fl & 1) wait_st();
+        Vec<W> x[kB][4];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          ldtm_w<W>(tl + (o[j].x & 0xffffu), x[j][0]);
+          ldtm_w<W>(tl + (o[j].x >> 16), x[j][1]);
+        }
+        if (fl & 2) {
+#pragma unroll
+          for (int j = 0; j < kB; ++j) {
+            ldtm_w<W>(tl + (o[j].y & 0xffffu), x[j][2]);
+            ldtm_w<W>(tl + (o[j].y >> 16), x[j][3]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < kB; ++j)
+#pragma unroll
+            for (int w = 0; w < W; ++w) x[j][2].x[w] = x[j][3].x[w] = 0;
+        }
+        uint4 on[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) on[j] = lds128(op + 16 * j);
+        wait_ld();
+        Vec<W> acc[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j)
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            uint32_t y;
+            asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(y) : "r"(x[j][0].x[w]), "r"(x[j][1].x[w]), "r"(x[j][2].x[w]));
+            acc[j].x[w] = y ^ x[j][3].x[w];
+          }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) sttm_w<W>(tl + (o[j].z & 0xffffu), acc[j]);
+        // goal stores, branch-free: the header read and the address are computed for every op
+        // (goal 0 = "none" reads block pointer 0) and the store is predicated
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          const uint32_t g = o[j].z >> 16, gi = g - 1;
+          uint64_t gp;
+          asm volatile("ld.shared.u64 %0, [%1];" : "=l"(gp) : "r"(hdr + 16 + 8 * ((gi >> 3) & 31)) : "memory");
+          gp += (uint64_t)(gi & 7) * a.strip + toff;
+          const uint32_t doit = (g != 0) & live;
+          if constexpr (W == 1)
+            asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.global.cs.u32 [%0], %1;\n}"
+                         ::"l"(gp), "r"(acc[j].x[0]), "r"(doit) : "memory");
+          else
+            asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n @p st.global.cs.v2.u32 [%0], {%1, %2};\n}"
+                         ::"l"(gp), "r"(acc[j].x[0]), "r"(acc[j].x[1]), "r"(doit) : "memory");
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) o[j] = on[j];
+      }
+      // the next tile's constant copies overwrite slots this tile's last batches read/stored
+      wait_st();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(base + 64 + 8 * hs) : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kCols) : "memory");
+}
+
+struct Pool {
+  uint32_t *code = nullptr;
+  int64_t *off = nullptr;
+  Layout y;
+};
+std::mutex g_mu;
+std::map<std::tuple<int, int, int, int, std::vector<const Program *>>, Pool> g_pools;  // (dev, S, W, CW, progs)
+
+std::mutex g_smu;
+std::map<const Program *, std::shared_ptr<const TSched>> g_scheds;
+
+std::shared_ptr<const TSched> sched_of(const Program *p) {
+  {
+    std::lock_guard<std::mutex> g(g_smu);
+    auto it = g_scheds.find(p);
+    if (it != g_scheds.end()) return it->second;
+  }
+  auto sc = std::make_shared<const TSched>(build_tmem(p->slp));
+  std::lock_guard<std::mutex> g(g_smu);
+  return g_scheds.emplace(p, sc).first->second;
+}
+
+std::vector<std::shared_ptr<const TSched>> scheds_of(const Program *const *progs, int np) {
+  std::vector<std::shared_ptr<const TSched>> out(np);
+  std::atomic<int> next{0};
+  std::exception_ptr err;
+  std::mutex em;
+  auto work = [&]() {
+    for (int i; (i = next++) < np;) {
+      try {
+        out[i] = sched_of(progs[i]);
+      } catch (...) {
+        std::lock_guard<std::mutex> g(em);
+        if (!err) err = std::current_exception();
+      }
+    }
+  };
+  const int nt = std::min<int>(np, std::max(1u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> ts;
+  for (int t = 1; t < nt; ++t) ts.emplace_back(work);
+  work();
+  for (auto &t : ts) t.join();
+  if (err) std::rethrow_exception(err);
+  return out;
+}
+
+}  // namespace tmem
+
+// Dump form 5: the TMEM interpreter's code for this program (columns in slot units, W = 1).
+std::vector<uint32_t> interp_tmem_dump(const Program *p) {
+  return tmem::emit_code(*tmem::sched_of(p), 1);
+}
+
+void drop_tmem_of(const Program *p) {
+  using namespace tmem;
+  {
+    std::lock_guard<std::mutex> g(g_smu);
+    g_scheds.erase(p);
+  }
+  std::lock_guard<std::mutex> g(g_mu);
+  for (auto it = g_pools.begin(); it != g_pools.end();) {
+    const auto &progs = std::get<4>(it->first);
+    if (std::find(progs.begin(), progs.end(), p) != progs.end()) {
+      int cur = -1;
+      const bool have = cudaGetDevice(&cur) == cudaSuccess;
+      cudaSetDevice(std::get<0>(it->first));
+      cudaFree(it->second.code);
+      cudaFree(it->second.off);
+      if (have) cudaSetDevice(cur);
+      it = g_pools.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+namespace tmem {
+using KFn = void (*)(Args);
+template <int W, int CW, int B>
+const void *kfn() { return (const void *)(KFn)xslp_interp_tmem<W, CW, B>; }
+template <int B>
+const void *kernel_b(int W, int CW) {
+  return W == 2 ? (CW == 8 ? kfn<2, 8, B>() : kfn<2, 4, B>()) : (CW == 8 ? kfn<1, 8, B>() : kfn<1, 4, B>());
+}
+const void *kernel_of(int W, int CW, int B) { return B == 4 ? kernel_b<4>(W, CW) : kernel_b<8>(W, CW); }
+}  // namespace tmem
+
+static bool tmem_finish_plan(int dev) {
+  using namespace tmem;
+  static std::mutex am;
+  static std::map<int, bool> attr;
+  std::lock_guard<std::mutex> g(am);
+  if (!attr[dev]) {
+    for (int W : {1, 2})
+      for (int CW : {4, 8})
+        for (int B : {4, 8})
+          CUDA_OK(cudaFuncSetAttribute(kernel_of(W, CW, B), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
+    attr[dev] = true;
+  }
+  return true;
+}
+
+// Words per thread: the largest of {want, 1} whose TMEM slots (512 columns per thread with 4
+// consumer warps, 256 with 8) and shared-memory stages fit; 0 if neither fits.
+static int tmem_words(int nc, int nslots, int S, int CW, int capw, int want) {
+  using namespace tmem;
+  for (int W : {2, 1}) {
+    if (W > want) continue;
+    if (nslots * W > kCols / (CW / 4)) continue;
+    Layout y;
+    y.W = W;
+    y.CW = CW;
+    y.S = S;
+    y.NC = std::max(1, nc);
+    y.capw = capw;
+    if (layout_smem(y) <= 227 * 1024) return W;
+  }
+  return 0;
+}
+
+// The code pool and layout of a program set for strips of B/8 bytes on the current device;
+// false if the TMEM interpreter does not apply (strip % 16, > 32 output blocks, or the slots /
+// rows do not fit).  Consumer warps: 8 when opts.threads >= 256, else 4.
+static bool tmem_plan(const Program *const *progs, int np, size_t B, tmem::Pool &pool) {
+  using namespace tmem;
+  const xslp_opts &o = progs[0]->opts;
+  const uint64_t strip = B / 8;
+  if (strip % 16 || progs[0]->n_goals / 8 > 32) return false;
+  const int S = std::max(1, std::min(4, o.stages));
+  const int CW = o.threads >= 256 ? 8 : 4;
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  const int want = o.lane_words >= 2 ? 2 : 1;
+  std::vector<const Program *> key(progs, progs + np);
+  const auto k = std::make_tuple(dev, S, want, CW, key);
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_pools.find(k);
+    if (it != g_pools.end()) {
+      pool = it->second;
+      return tmem_finish_plan(dev);
+    }
+  }
+  std::vector<std::shared_ptr<const TSched>> sc;
+  try {
+    sc = scheds_of(progs, np);
+  } catch (const Error &) {
+    return false;
+  }
+  std::lock_guard<std::mutex> g(g_mu);
+  auto it = g_pools.find(k);
+  if (it != g_pools.end()) {
+    pool = it->second;
+    return tmem_finish_plan(dev);
+  }
+  int nc = 1, ns = 0, cw = 0;
+  for (int i = 0; i < np; ++i) {
+    nc = std::max<int>(nc, (int)sc[i]->consts.size());
+    ns = std::max(ns, sc[i]->nslots);
+    cw = std::max(cw, consumer_words(*sc[i]));
+  }
+  Layout y;
+  y.S = S;
+  y.CW = CW;
+  y.NC = nc;
+  y.B = sc[0]->B;
+  y.capw = (cw + 3) / 4 * 4;
+  y.W = tmem_words(nc, ns, S, CW, y.capw, want);
+  if (y.W == 0) return false;
+  layout_smem(y);
+  std::vector<uint32_t> all;
+  std::vector<int64_t> off;
+  for (int i = 0; i < np; ++i) {
+    off.push_back((int64_t)all.size());
+    auto w = emit_code(*sc[i], y.W);
+    all.insert(all.end(), w.begin(), w.end());
+  }
+  Pool P;
+  P.y = y;
+  CUDA_OK(cudaMalloc(&P.code, all.size() * 4));
+  CUDA_OK(cudaMemcpy(P.code, all.data(), all.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_OK(cudaMalloc(&P.off, off.size() * 8));
+  CUDA_OK(cudaMemcpy(P.off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+  g_pools[k] = P;
+  pool = P;
+  return tmem_finish_plan(dev);
+}
+
+bool interp_tmem_prepare(const Program *p, size_t B) {
+  const Program *ps[1] = {p};
+  tmem::Pool pool;
+  return tmem_plan(ps, 1, B, pool);
+}
+
+bool interp_tmem_launch(const Program *const *progs, int np, const int32_t *d_pos,
+                        const int32_t *d_ids, const uint8_t *const *in, uint8_t *const *out,
+                        int nstripes, size_t B, cudaStream_t st) {
+  using namespace tmem;
+  if (!in || !out || nstripes <= 0) return false;
+  Pool pool;
+  if (!tmem_plan(progs, np, B, pool)) return false;
+  const Layout &y = pool.y;
+  Args a{};
+  a.code = pool.code;
+  a.prog_off = pool.off;
+  a.prog_of_stripe = d_pos;
+  a.ids = d_ids;
+  a.in_tbl = in;
+  a.out_tbl = out;
+  a.strip = B / 8;
+  a.words = (uint32_t)(a.strip / 4);
+  a.tpos = (uint32_t)(y.CW * 32 * y.W);
+  a.tps = (a.words + a.tpos - 1) / a.tpos;
+  if ((uint64_t)a.tps * nstripes > 0xffffffffull) throw Error(XSLP_EINVAL, "too many tiles");
+  a.ntiles = a.tps * (uint32_t)nstripes;
+  a.n_in = progs[0]->n_const / 8;
+  a.n_out = progs[0]->n_goals / 8;
+  a.S = y.S;
+  a.nprogs = np;
+  a.code0 = y.code0;
+  a.capw = (uint32_t)y.capw;
+  a.const0 = y.const0;
+  a.RB = y.RB;
+  a.NC = (uint32_t)y.NC;
+  int dev = 0, sms = 148;
+  CUDA_OK(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<uint64_t>(a.ntiles, (uint64_t)sms);
+  void *args[] = {&a};
+  CUDA_OK(cudaLaunchKernel(kernel_of(y.W, y.CW, y.B), dim3(grid), dim3(y.CW * 32 + 32), args, y.smem, st));
+  count_launch();
+  return true;
+}
+
+}  // namespace xslp

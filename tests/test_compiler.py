@@ -592,6 +592,77 @@ def _emulate_lanes(words, strips, n_goals, loads_first=True):
     return out
 
 
+def _emulate_tmem(words, strips, n_goals):
+    """Run the TMEM interpreter's code (dump form 5, interp_tmem.cu emit_code) on every position
+    at once: TMEM slot 0 reads zero, slot 1 is the write sink, constant row r is slot 2 + r; a
+    batch reads all its operands before any of its stores, reads operands 3-4 only when
+    flagged, and never reads a slot stored since the last wait::st flag (the kernel's tcgen05.st
+    may still be in flight)."""
+    nconst, nb, nslots, kb, w_ = words[0], words[1], words[3], words[4], words[5]
+    assert w_ == 1 and kb in (4, 8)
+    ops = words[8:8 + 4 * kb * (nb + 1)]
+    loads = words[8 + 4 * kb * (nb + 1):8 + 4 * kb * (nb + 1) + nconst]
+    zero = np.zeros_like(strips[0])
+    slots = {0: zero}
+    for r, c in enumerate(loads):
+        slots[2 + r] = strips[c]
+    pending = set()
+    out = np.zeros((n_goals, strips.shape[1]), dtype=np.uint32)
+    done = np.zeros(n_goals, dtype=bool)
+    for b in range(nb + 1):
+        batch = [ops[4 * (b * kb + j):4 * (b * kb + j) + 4] for j in range(kb)]
+        fl = batch[0][3]
+        assert all(op[3] == 0 for op in batch[1:])
+        if fl & 1:
+            pending.clear()
+        res = []
+        for w0, w1, w2, _ in batch:
+            cols = [w0 & 0xFFFF, w0 >> 16, w1 & 0xFFFF, w1 >> 16]
+            if not fl & 2:
+                assert cols[2] == cols[3] == 0
+            acc = zero.copy()
+            for t in cols:
+                assert t < nslots and t != 1 and t in slots and t not in pending, (b, t)
+                acc ^= slots[t]
+            res.append((acc, w2))
+        for acc, w2 in res:
+            d, g = w2 & 0xFFFF, w2 >> 16
+            assert d >= 1 and d < nslots and (d == 1 or d >= 2 + nconst)
+            slots[d] = acc
+            pending.add(d)
+            if g:
+                assert b < nb and not done[g - 1]
+                out[g - 1], done[g - 1] = acc, True
+    assert done.all()
+    return out
+
+
+@pytest.mark.parametrize("n,p,comp,er,sched", [
+    (10, 4, "xorrepair", None, 1), (10, 4, "xorrepair", (2, 4, 5, 6), 1), (4, 2, "none", None, 1),
+    (20, 4, "xorrepair", (0, 5, 21, 23), 1), (10, 3, "repair", None, 2), (10, 4, "none", (0, 1, 12, 13), 0),
+    (10, 4, "xorrepair", (2, 4, 5, 6), 2)])
+def test_tmem_interpreter_code_computes_the_oracle_result(n, p, comp, er, sched):
+    # the TMEM interpreter's batches (dump form 5) reproduce the oracle's RS bytes, never read
+    # a slot before its store is waited for, and fit the 512 TMEM columns at 1 word per thread
+    import synth
+    from oracle import rs
+    kind = "cauchy" if (n, p) == (4, 2) else "isal"
+    og = mx.coding_matrix(n, p, kind)
+    g = X.xslp_coding_matrix(n, p, kind)
+    if er is None:
+        bits, rows = X.xslp_encode_bitmatrix(g, n, p), og[n:]
+    else:
+        bits, rows = X.xslp_decode_bitmatrix(g, n, p, er)[0], mx.decode_rows(og, n, list(er))[1]
+    prog = X.xslp_compile(bits, compress=comp, specialise=0, schedule=sched, greedy_capacity=32)
+    words = [int(x) for x in prog.dump(5).split()]
+    assert words[2] == len(words) and words[3] <= 512
+    B = 128
+    data = synth.stripe_data(9, 2, n, B)
+    strips = data.reshape(8 * n, B // 8).view(np.uint32)
+    want = rs.apply_rows(rows, data).reshape(bits.shape[0], B // 8).view(np.uint32)
+    assert (_emulate_tmem(words, strips, bits.shape[0]) == want).all()
+
+
 @pytest.mark.parametrize("n,p,comp,er,sched", [
     (10, 4, "xorrepair", None, 1), (10, 4, "xorrepair", (2, 4, 5, 6), 1), (4, 2, "none", None, 1),
     (20, 4, "xorrepair", (0, 5, 21, 23), 1), (10, 3, "repair", None, 2), (10, 4, "none", (0, 1, 12, 13), 0)])

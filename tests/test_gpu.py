@@ -49,8 +49,8 @@ def run_batch(prog, din, dout, B, nstripes=None):
 def _kernel_kw(kw):
     """kernel="interp_pairs": the pair-pipelined interpreter (XSLP_INTERP_PAIRS); "interp" is
     the lane-parallel one (the default)."""
-    if kw.get("kernel") == "interp_pairs":
-        kw = dict(kw, kernel="interp", interp="pairs")
+    if kw.get("kernel") in ("interp_pairs", "interp_tmem"):
+        kw = dict(kw, kernel="interp", interp=kw["kernel"][7:])
     return kw
 
 
@@ -101,6 +101,7 @@ def test_cfg1_encode_decode(kernel):
 @pytest.mark.parametrize("comp", ["none", "repair", "xorrepair"])
 @pytest.mark.parametrize("kern,lanes", [("straight", 1), ("straight", 2), ("straight", 4),
                                         ("interp", 1), ("interp_pairs", 1), ("interp_pairs", 2),
+                                        ("interp_tmem", 1), ("interp_tmem", 2),
                                         ("tma", 1), ("tma", 2), ("pipe", 1), ("pipe", 2)])
 @pytest.mark.parametrize("p", [2, 3, 4])
 def test_rs10_encode_small_full_compare(comp, kern, lanes, p):
@@ -144,8 +145,8 @@ def _decode_inputs(seed, S, n, p, B, e):
     return pats, blocks
 
 
-@pytest.mark.parametrize("kern", ["interp", "interp_pairs", "straight", "grouped", "grouped_tma",
-                                  "grouped_pipe"])
+@pytest.mark.parametrize("kern", ["interp", "interp_pairs", "interp_tmem", "straight", "grouped",
+                                  "grouped_tma", "grouped_pipe"])
 def test_heterogeneous_decode(kern):
     n, p, B, S = 10, 4, 4096, 24
     pats, blocks = _decode_inputs(3, S, n, p, B, 4)
@@ -178,6 +179,23 @@ def test_heterogeneous_decode(kern):
     got = dout.cpu().numpy()
     for s in range(S):
         assert (got[s] == blocks[s][list(pats[s])]).all(), (s, pats[s])
+
+
+@pytest.mark.parametrize("lanes", [1, 2])
+def test_tmem_interpreter_kernel_runs(lanes):
+    # the TMEM interpreter (tensor-memory variables) is the kernel that runs, not the fallback
+    n, p, B, S = 10, 4, 65536, 8
+    og = mx.coding_matrix(n, p)
+    _, prog = compile_enc(n, p, kernel="interp_tmem", lane_words=lanes, specialise=0)
+    data = host_data(12, range(S), n, B)
+    din = torch.from_numpy(data).cuda()
+    dout = dev_buf(S, p, B)
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        run_batch(prog, din, dout, B)
+    names = [e.name for e in prof.events() if "xslp" in e.name]
+    assert any("xslp_interp_tmem" in nm for nm in names), names
+    for s in range(S):
+        assert (dout[s].cpu().numpy() == rs.encode(og, n, data[s])).all(), s
 
 
 # ---- edge cases ------------------------------------------------------------------------
@@ -496,9 +514,9 @@ def test_random_programs_and_launches(case):
     if kern == "pipe":
         kw["stages"] = int(rng.integers(1, 5))
         kw["phases"] = int(rng.integers(0, min(4, n_in) + 1))
-    if kern == "interp":                    # the batched interpreters: lanes / pairs, no JIT
+    if kern == "interp":                    # the batched interpreters: lanes / pairs / tmem, no JIT
         kw.update(lane_words=int(rng.choice([1, 2, 4])), stages=int(rng.integers(1, 5)),
-                  specialise=0, interp=case % 2)
+                  specialise=0, interp=case % 3)
     B = 128 * int(rng.integers(1, 40))
     S = int(rng.integers(1, 5))
     if rng.random() < 0.5:
@@ -718,7 +736,7 @@ def test_cfg2_full_size(kern, threads, lanes, reuse):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("mode", ["grouped", "interp", "interp_pairs"])
+@pytest.mark.parametrize("mode", ["grouped", "interp", "interp_pairs", "interp_tmem"])
 def test_cfg3_full_size_roundtrip(mode):
     # RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures (configs[2]);
     # "grouped" (per-pattern LDG kernels, T=64, 8 streams) is the bench's launch configuration
@@ -744,7 +762,7 @@ def test_cfg3_full_size_roundtrip(mode):
     if mode == "grouped":
         progs = X.compile_many(bitsl, kernel="straight", threads=64, block_bytes_hint=B)
     else:                     # the lane-parallel (default) or the pair-pipelined interpreter
-        progs = X.compile_many(bitsl, specialise=0, interp="pairs" if mode == "interp_pairs" else "lanes")
+        progs = X.compile_many(bitsl, specialise=0, interp=mode[7:] if "_" in mode else "lanes")
     pos = [uniq.index(er) for er in pats]
     idx = torch.tensor(pos, dtype=torch.int32, device="cuda")
     tin = torch.stack([ti[s, torch.as_tensor(survs[pats[s]], dtype=torch.long)] for s in range(S)])
@@ -1109,14 +1127,15 @@ def test_byte_layout_full_size(kern, threads):
 
 # ---- CUDA graphs: launches are capturable after xslp_prepare -----------------------------
 
-@pytest.mark.parametrize("kern", ["pipe", "straight", "interp", "interp_pairs", "pipe_phases", "pipe_byte"])
+@pytest.mark.parametrize("kern", ["pipe", "straight", "interp", "interp_pairs", "interp_tmem", "pipe_phases",
+                                  "pipe_byte"])
 def test_cuda_graph_capture(kern):
     n, p, B, S = (20, 4, 65536, 32) if kern == "pipe_phases" else (10, 4, 65536, 64)
     og = mx.coding_matrix(n, p)
     if kern == "pipe_byte":
         _, prog = compile_enc(n, p, kernel="pipe", threads=128, layout="byte", block_bytes_hint=B)
     else:
-        _, prog = compile_enc(n, p, kernel=kern if kern == "interp_pairs" else kern.split("_")[0],
+        _, prog = compile_enc(n, p, kernel=kern if kern.startswith("interp_") else kern.split("_")[0],
                               threads=256 if kern.startswith("pipe") else 128,
                               block_bytes_hint=B, phases=2 if kern == "pipe_phases" else 1)
     X.xslp_prepare(prog, B)
