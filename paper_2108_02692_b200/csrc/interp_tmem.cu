@@ -47,7 +47,7 @@ namespace tmem {
 constexpr int kMaxB = 8;           // ops per batch: batch_size() (4 or 8)
 constexpr int kH = 4;              // tile header / code slots (a ring longer than the S stages)
 constexpr int kHead = 8;           // code header words
-constexpr int kHdr = 16 + 8 * 32;  // per-stage tile header: stripe, prog, pad, 32 out ptrs
+constexpr int kHdr = 16 + 8 * 256;  // tile header: stripe, prog, pad, a pointer per goal strip
 constexpr int kCols = 512;         // TMEM columns allocated per CTA
 constexpr int kZero = 0, kJunk = 1, kConst0 = 2;  // TMEM slots: zero, write sink, constants
 constexpr uint32_t kNone = 0xffff;
@@ -208,7 +208,7 @@ TSched build_tmem(const Slp &s) {
 //     w0 = col(t0) | col(t1) << 16   w1 = col(t2) | col(t3) << 16   (absent operand: the zero slot)
 //     w2 = col(dst) (absent: the sink slot) | (goal + 1) << 16
 //     w3 (op 0 of a batch) = 1: wait for earlier TMEM stores first; 2: the batch has ops of
-//        three or four operands (else operands 3-4 are not loaded)
+//        three or four operands (else operands 3-4 are not loaded); 4: the batch stores goals
 //   loads: nconst x (constant index)   (row r = TMEM slot kConst0 + r)
 std::vector<uint32_t> emit_code(const TSched &sc, int W) {
   const int kB = sc.B;
@@ -226,12 +226,15 @@ std::vector<uint32_t> emit_code(const TSched &sc, int W) {
   w[4] = kB;
   w[5] = (uint32_t)W;
   for (size_t bi = 0; bi < sc.batches.size(); ++bi) {
-    bool quad = false;
-    for (int j = 0; j < kB; ++j) quad |= sc.batches[bi][j].arity() > 2;
+    bool quad = false, goals = false;
+    for (int j = 0; j < kB; ++j) {
+      quad |= sc.batches[bi][j].arity() > 2;
+      goals |= sc.batches[bi][j].goal >= 0;
+    }
     for (int j = 0; j < kB; ++j) {
       const TOp &o = sc.batches[bi][j];
       const uint32_t d = o.dst >= 0 ? (uint32_t)(sc.vslot[o.dst] * W) : (uint32_t)(kJunk * W);
-      const uint32_t fl = j == 0 ? (sc.wait_st[bi] ? 1u : 0u) | (quad ? 2u : 0u) : 0u;
+      const uint32_t fl = j == 0 ? (sc.wait_st[bi] ? 1u : 0u) | (quad ? 2u : 0u) | (goals ? 4u : 0u) : 0u;
       w.insert(w.end(), {col(o.t[0]) | col(o.t[1]) << 16, col(o.t[2]) | col(o.t[3]) << 16,
                          d | (uint32_t)(o.goal + 1) << 16, fl});
     }
@@ -316,6 +319,13 @@ __device__ __forceinline__ void sttm_w(uint32_t ta, const Vec<W> &v) {
   else
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(ta), "r"(v.x[0]), "r"(v.x[1]) : "memory");
 }
+// TMEM address of the column in the low / high 16 bits of a code word (tl: this warp's lane
+// quarter; with 4 consumer warps its column bits are zero, so the low half is one LOP3)
+template <int CW>
+__device__ __forceinline__ uint32_t col_lo(uint32_t tl, uint32_t w) {
+  return CW == 4 ? ((w & 0xffffu) | tl) : (w & 0xffffu) + tl;
+}
+__device__ __forceinline__ uint32_t col_hi(uint32_t tl, uint32_t w) { return (w >> 16) + tl; }
 __device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -352,6 +362,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   uint32_t tbase;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tbase) : "r"(base + 120) : "memory");
+  if (tbase & 0xffffu) asm volatile("trap;");  // all 512 columns: the allocation starts at column 0
   const uint32_t chunk = (a.ntiles + gridDim.x - 1) / gridDim.x;
   const uint32_t t0 = blockIdx.x * chunk, t1 = min(a.ntiles, t0 + chunk);
   if (warp == CW) {  // ---------------- producer warp (all 32 lanes issue copies)
@@ -370,14 +381,17 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       const uint32_t nl = pc[0], nb = pc[1];
       const uint32_t *ld = pc + kHead + 4 * kB * (nb + 1);  // pc[4] == kB
       const size_t toff = (size_t)tw * a.tpos * 4;
-      const uint64_t optr = lane < (uint32_t)a.n_out ? (uint64_t)out[lane] : 0;
       const bool newcode = cur[hs] != prog;
       if (it >= (uint32_t)S)
         while (!try_wait(base + 32 + 8 * st, ph ^ 1)) __nanosleep(32);
       if (it >= (uint32_t)kH)  // the tile that last used this header / code slot is done
         while (!try_wait(base + 64 + 8 * hs, hph ^ 1)) __nanosleep(32);
       const uint32_t h = hdr0 + hs * kHdr;
-      if (lane < (uint32_t)a.n_out) asm volatile("st.shared.u64 [%0], %1;" ::"r"(h + 16 + 8 * lane), "l"(optr) : "memory");
+      // goal strip g of this tile starts at out[g / 8] + (g % 8) * strip + toff
+      for (uint32_t g = lane; g < 8u * a.n_out; g += 32) {
+        const uint64_t gp = (uint64_t)out[g >> 3] + (g & 7) * a.strip + toff;
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(h + 16 + 8 * g), "l"(gp) : "memory");
+      }
       const uint32_t nbytes = min(a.tpos, a.words - tw * a.tpos) * 4;
       const uint32_t cbytes = newcode ? (kHead + 4 * kB * (nb + 1)) * 4 : 0;
       cur[hs] = prog;
@@ -426,7 +440,15 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       // the stage's constant rows -> this thread's TMEM constant slots; then the rows are free
       {
         const uint32_t rs = base + a.const0 + st * a.NC * a.RB + tid * W * 4;
-        for (uint32_t r = 0; r < nl; ++r) {
+        uint32_t r = 0;
+        for (; r + 4 <= nl; r += 4) {
+          Vec<W> v[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) lds_w<W>(rs + (r + k) * a.RB, v[k]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) sttm_w<W>(tl + (kConst0 + r + k) * W, v[k]);
+        }
+        for (; r < nl; ++r) {
           Vec<W> v;
           lds_w<W>(rs + r * a.RB, v);
           sttm_w<W>(tl + (kConst0 + r) * W, v);
@@ -435,7 +457,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(base + 32 + 8 * st) : "memory");
       wait_st();
-      const uint64_t toff = ((uint64_t)tw * a.tpos + (uint64_t)tid * W) * 4;
+      const uint32_t tofs = tid * W * 4;  // this thread's bytes within a goal strip of the tile
       uint32_t op = cp + kHead * 4;
       uint4 o[kB];
 #pragma unroll
@@ -444,54 +466,60 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
         op += 16 * kB;
         const uint32_t fl = o[0].w;
         if (fl & 1) wait_st();
-        Vec<W> x[kB][4];
-#pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          ldtm_w<W>(tl + (o[j].x & 0xffffu), x[j][0]);
-          ldtm_w<W>(tl + (o[j].x >> 16), x[j][1]);
-        }
-        if (fl & 2) {
+        Vec<W> acc[kB];
+        uint4 on[kB];
+        if (fl & 2) {  // ops of up to four operands
+          Vec<W> x[kB][4];
 #pragma unroll
           for (int j = 0; j < kB; ++j) {
-            ldtm_w<W>(tl + (o[j].y & 0xffffu), x[j][2]);
-            ldtm_w<W>(tl + (o[j].y >> 16), x[j][3]);
+            ldtm_w<W>(col_lo<CW>(tl, o[j].x), x[j][0]);
+            ldtm_w<W>(col_hi(tl, o[j].x), x[j][1]);
+            ldtm_w<W>(col_lo<CW>(tl, o[j].y), x[j][2]);
+            ldtm_w<W>(col_hi(tl, o[j].y), x[j][3]);
           }
-        } else {
+#pragma unroll
+          for (int j = 0; j < kB; ++j) on[j] = lds128(op + 16 * j);
+          wait_ld();
 #pragma unroll
           for (int j = 0; j < kB; ++j)
 #pragma unroll
-            for (int w = 0; w < W; ++w) x[j][2].x[w] = x[j][3].x[w] = 0;
-        }
-        uint4 on[kB];
+            for (int w = 0; w < W; ++w) {
+              uint32_t y;
+              asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(y) : "r"(x[j][0].x[w]), "r"(x[j][1].x[w]), "r"(x[j][2].x[w]));
+              acc[j].x[w] = y ^ x[j][3].x[w];
+            }
+        } else {  // binary ops: operands 3-4 are not loaded
+          Vec<W> x[kB][2];
 #pragma unroll
-        for (int j = 0; j < kB; ++j) on[j] = lds128(op + 16 * j);
-        wait_ld();
-        Vec<W> acc[kB];
-#pragma unroll
-        for (int j = 0; j < kB; ++j)
-#pragma unroll
-          for (int w = 0; w < W; ++w) {
-            uint32_t y;
-            asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(y) : "r"(x[j][0].x[w]), "r"(x[j][1].x[w]), "r"(x[j][2].x[w]));
-            acc[j].x[w] = y ^ x[j][3].x[w];
+          for (int j = 0; j < kB; ++j) {
+            ldtm_w<W>(col_lo<CW>(tl, o[j].x), x[j][0]);
+            ldtm_w<W>(col_hi(tl, o[j].x), x[j][1]);
           }
 #pragma unroll
-        for (int j = 0; j < kB; ++j) sttm_w<W>(tl + (o[j].z & 0xffffu), acc[j]);
-        // goal stores, branch-free: the header read and the address are computed for every op
-        // (goal 0 = "none" reads block pointer 0) and the store is predicated
+          for (int j = 0; j < kB; ++j) on[j] = lds128(op + 16 * j);
+          wait_ld();
 #pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          const uint32_t g = o[j].z >> 16, gi = g - 1;
-          uint64_t gp;
-          asm volatile("ld.shared.u64 %0, [%1];" : "=l"(gp) : "r"(hdr + 16 + 8 * ((gi >> 3) & 31)) : "memory");
-          gp += (uint64_t)(gi & 7) * a.strip + toff;
-          const uint32_t doit = (g != 0) & live;
-          if constexpr (W == 1)
-            asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.global.cs.u32 [%0], %1;\n}"
-                         ::"l"(gp), "r"(acc[j].x[0]), "r"(doit) : "memory");
-          else
-            asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n @p st.global.cs.v2.u32 [%0], {%1, %2};\n}"
-                         ::"l"(gp), "r"(acc[j].x[0]), "r"(acc[j].x[1]), "r"(doit) : "memory");
+          for (int j = 0; j < kB; ++j)
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[j].x[w] = x[j][0].x[w] ^ x[j][1].x[w];
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) sttm_w<W>(col_lo<CW>(tl, o[j].z), acc[j]);
+        if (fl & 4) {  // goal stores (predicated: ops without a goal and the ragged tail skip)
+#pragma unroll
+          for (int j = 0; j < kB; ++j) {
+            const uint32_t g = o[j].z >> 16;
+            uint64_t gp;
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(gp) : "r"(hdr + 8 + 8 * g) : "memory");
+            gp += tofs;
+            const uint32_t doit = (g != 0) & live;
+            if constexpr (W == 1)
+              asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.global.cs.u32 [%0], %1;\n}"
+                           ::"l"(gp), "r"(acc[j].x[0]), "r"(doit) : "memory");
+            else
+              asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n @p st.global.cs.v2.u32 [%0], {%1, %2};\n}"
+                           ::"l"(gp), "r"(acc[j].x[0]), "r"(acc[j].x[1]), "r"(doit) : "memory");
+          }
         }
 #pragma unroll
         for (int j = 0; j < kB; ++j) o[j] = on[j];
