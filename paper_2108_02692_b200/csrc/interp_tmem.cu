@@ -133,29 +133,58 @@ TSched build_tmem(const Slp &s) {
       if (t >= s.n_const && (vbatch[t - s.n_const] < 0 || vbatch[t - s.n_const] >= nb)) return false;
     return true;
   };
-  size_t first = 0;
+  // Ops that only store a goal (no later reader) are deferred and batched together, kB at a
+  // time, so that only a few batches run the goal-store code.
+  std::vector<size_t> gq;  // deferred goal-only ops, in order
+  std::vector<uint8_t> deferred(ops.size(), 0);
+  for (size_t i = 0; i < ops.size(); ++i)
+    if (ops[i].dst < 0) {
+      deferred[i] = 1;
+      gq.push_back(i);
+    }
+  size_t first = 0, left = ops.size() - gq.size();
   int nb = 0;
   const size_t kWindow = 48;
-  while (first < ops.size()) {
+  auto skip = [&]() {
+    while (first < ops.size() && (batch_of[first] >= 0 || deferred[first])) ++first;
+  };
+  skip();
+  while (left > 0 || !gq.empty()) {
     std::array<TOp, kMaxB> b;
     int n = 0;
-    // the oldest ready op decides the batch class; fill with ready ops of the same class, then any
-    int cls = -1;
-    for (int pass = 0; pass < 2 && n < kB; ++pass)
-      for (size_t i = first; i < ops.size() && i < first + kWindow && n < kB; ++i) {
-        if (batch_of[i] >= 0 || !ready(i, nb)) continue;
-        const int c = ops[i].arity() > 2;
-        if (cls < 0) cls = c;
-        if (pass == 0 && c != cls) continue;
+    std::vector<size_t> gready;
+    for (size_t i : gq)
+      if (ready(i, nb)) gready.push_back(i);
+    if ((int)gready.size() >= kB || left == 0) {  // a batch of goal-only ops
+      for (size_t i : gready) {
+        if (n == kB) break;
         batch_of[i] = nb;
         b[n++] = ops[i];
       }
+      std::vector<size_t> rest;
+      for (size_t i : gq)
+        if (batch_of[i] < 0) rest.push_back(i);
+      gq.swap(rest);
+    } else {
+      // the oldest ready op decides the batch class; fill with ready ops of that class, then any
+      int cls = -1;
+      for (int pass = 0; pass < 2 && n < kB; ++pass)
+        for (size_t i = first; i < ops.size() && i < first + kWindow && n < kB; ++i) {
+          if (batch_of[i] >= 0 || deferred[i] || !ready(i, nb)) continue;
+          const int c = ops[i].arity() > 2;
+          if (cls < 0) cls = c;
+          if (pass == 0 && c != cls) continue;
+          batch_of[i] = nb;
+          b[n++] = ops[i];
+          --left;
+        }
+    }
     if (n == 0) throw Error(XSLP_EINVAL, "tmem: no ready op (bad schedule)");
     for (int k = 0; k < n; ++k)
       if (b[k].dst >= 0) vbatch[b[k].dst] = nb;
     out.batches.push_back(b);
     ++nb;
-    while (first < ops.size() && batch_of[first] >= 0) ++first;
+    skip();
   }
   // ---- constant rows in first-use order
   std::vector<int> row(s.n_const, -1);
@@ -382,10 +411,11 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       const uint32_t *ld = pc + kHead + 4 * kB * (nb + 1);  // pc[4] == kB
       const size_t toff = (size_t)tw * a.tpos * 4;
       const bool newcode = cur[hs] != prog;
+      // (the producer shares an SMSP with consumer warp 0: sleep rather than spin)
       if (it >= (uint32_t)S)
-        while (!try_wait(base + 32 + 8 * st, ph ^ 1)) __nanosleep(32);
+        while (!try_wait(base + 32 + 8 * st, ph ^ 1)) __nanosleep(256);
       if (it >= (uint32_t)kH)  // the tile that last used this header / code slot is done
-        while (!try_wait(base + 64 + 8 * hs, hph ^ 1)) __nanosleep(32);
+        while (!try_wait(base + 64 + 8 * hs, hph ^ 1)) __nanosleep(256);
       const uint32_t h = hdr0 + hs * kHdr;
       // goal strip g of this tile starts at out[g / 8] + (g % 8) * strip + toff
       for (uint32_t g = lane; g < 8u * a.n_out; g += 32) {
@@ -458,16 +488,12 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(base + 32 + 8 * st) : "memory");
       wait_st();
       const uint32_t tofs = tid * W * 4;  // this thread's bytes within a goal strip of the tile
-      uint32_t op = cp + kHead * 4;
-      uint4 o[kB];
-#pragma unroll
-      for (int j = 0; j < kB; ++j) o[j] = lds128(op + 16 * j);
-      for (uint32_t b = 0; b < nb; ++b) {
-        op += 16 * kB;
+      // one batch: operand loads (TMEM), one wait, XORs, result stores (TMEM), goal stores; the
+      // next batch's ops are read into `on` meanwhile (two buffers, the loop is unrolled twice)
+      auto batch = [&](const uint4 (&o)[kB], uint4 (&on)[kB], uint32_t opn) {
         const uint32_t fl = o[0].w;
         if (fl & 1) wait_st();
         Vec<W> acc[kB];
-        uint4 on[kB];
         if (fl & 2) {  // ops of up to four operands
           Vec<W> x[kB][4];
 #pragma unroll
@@ -478,7 +504,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
             ldtm_w<W>(col_hi(tl, o[j].y), x[j][3]);
           }
 #pragma unroll
-          for (int j = 0; j < kB; ++j) on[j] = lds128(op + 16 * j);
+          for (int j = 0; j < kB; ++j) on[j] = lds128(opn + 16 * j);
           wait_ld();
 #pragma unroll
           for (int j = 0; j < kB; ++j)
@@ -496,7 +522,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
             ldtm_w<W>(col_hi(tl, o[j].x), x[j][1]);
           }
 #pragma unroll
-          for (int j = 0; j < kB; ++j) on[j] = lds128(op + 16 * j);
+          for (int j = 0; j < kB; ++j) on[j] = lds128(opn + 16 * j);
           wait_ld();
 #pragma unroll
           for (int j = 0; j < kB; ++j)
@@ -521,9 +547,18 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
                            ::"l"(gp), "r"(acc[j].x[0]), "r"(acc[j].x[1]), "r"(doit) : "memory");
           }
         }
+      };
+      uint32_t op = cp + kHead * 4;
+      uint4 oa[kB], ob[kB];
 #pragma unroll
-        for (int j = 0; j < kB; ++j) o[j] = on[j];
+      for (int j = 0; j < kB; ++j) oa[j] = lds128(op + 16 * j);
+      uint32_t b = 0;
+      for (; b + 2 <= nb; b += 2) {
+        batch(oa, ob, op + 16 * kB);
+        batch(ob, oa, op + 32 * kB);
+        op += 32 * kB;
       }
+      if (b < nb) batch(oa, ob, op + 16 * kB);
       // the next tile's constant copies overwrite slots this tile's last batches read/stored
       wait_st();
       __syncwarp();
