@@ -412,9 +412,9 @@ extern "C" int64_t xslp_program_dump(const xslp_program *prog, int form, char *b
       // the lane-parallel interpreter's code (stage-0 variant) for S = opts.stages
       auto w = interp_lanes_dump(&P, P.opts.stages);
       for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");
-    } else if (form == 5) {
-      // the TMEM interpreter's code
-      auto w = interp_tmem_dump(&P);
+    } else if (form == 5 || form == 6) {
+      // the TMEM interpreter's schedule (5) and the device code its kernel runs (6)
+      auto w = interp_tmem_dump(&P, form);
       for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");
     } else {
       throw Error(XSLP_EINVAL, "bad dump form");

@@ -45,7 +45,7 @@ void count_launch();  // device.cu
 namespace tmem {
 
 constexpr int kMaxB = 8;           // ops per batch: batch_size() (4 or 8)
-constexpr int kH = 4;              // tile header / code slots (a ring longer than the S stages)
+constexpr int kH = 4;              // tile header slots (a ring longer than the S stages)
 constexpr int kHead = 8;           // code header words
 constexpr int kHdr = 16 + 8 * 256;  // tile header: stripe, prog, pad, a pointer per goal strip
 constexpr int kCols = 512;         // TMEM columns allocated per CTA
@@ -278,6 +278,76 @@ std::vector<uint32_t> emit_code(const TSched &sc, int W) {
 
 inline int consumer_words(const TSched &sc) { return kHead + 4 * sc.B * ((int)sc.batches.size() + 1); }
 
+// Device code (what the kernel runs; the form above is its compact, emulated twin): one
+// variant per consumer warp with the warp's TMEM lane quarter in every address, so an operand
+// costs one R2UR and one tcgen05.ld -- no decode.
+//   [0] nconst [1] nbatches [2] total words [3] slots [4] kB [5] W [6] vw = words per variant [7] 0
+//   4 variants of vw words; per batch: {flags (as w3 above), 0, 0, 0}, then kB ops:
+//     flag 2 (up to four operands): {a0, a1, a2, a3, dst, goal + 1, 0, 0}
+//     else (two operands):          {a0, a1, dst, goal + 1}
+//     (a = TMEM address: lane quarter << 16 | column; absent operand: the zero slot; absent
+//      dst: the sink slot; goal + 1 = 0: none)
+//   loads: nconst x (constant index)
+std::vector<uint32_t> emit_device(const TSched &sc, int W, int nvar = 4) {
+  const int kB = sc.B;
+  std::vector<int> row(sc.n_const, -1);
+  for (size_t r = 0; r < sc.consts.size(); ++r) row[sc.consts[r]] = (int)r;
+  auto col = [&](int t) -> uint32_t {
+    if (t < 0) return (uint32_t)(kZero * W);
+    if (t < sc.n_const) return (uint32_t)((kConst0 + row[t]) * W);
+    return (uint32_t)(sc.vslot[t - sc.n_const] * W);
+  };
+  std::vector<uint32_t> v;   // variant of lane quarter 0
+  std::vector<uint8_t> adr;  // word is a TMEM address
+  auto put = [&](uint32_t x, bool a) {
+    v.push_back(x);
+    adr.push_back(a);
+  };
+  for (size_t bi = 0; bi < sc.batches.size(); ++bi) {
+    bool quad = false, goals = false;
+    for (int j = 0; j < kB; ++j) {
+      quad |= sc.batches[bi][j].arity() > 2;
+      goals |= sc.batches[bi][j].goal >= 0;
+    }
+    put((sc.wait_st[bi] ? 1u : 0u) | (quad ? 2u : 0u) | (goals ? 4u : 0u), false);
+    for (int k = 0; k < 3; ++k) put(0, false);
+    for (int j = 0; j < kB; ++j) {
+      const TOp &o = sc.batches[bi][j];
+      for (int k = 0; k < (quad ? 4 : 2); ++k) put(col(o.t[k]), true);
+      put(o.dst >= 0 ? (uint32_t)(sc.vslot[o.dst] * W) : (uint32_t)(kJunk * W), true);
+      put((uint32_t)(o.goal + 1), false);
+      if (quad) {
+        put(0, false);
+        put(0, false);
+      }
+    }
+  }
+  std::vector<uint32_t> w(kHead, 0);
+  w[0] = (uint32_t)sc.consts.size();
+  w[1] = (uint32_t)sc.batches.size();
+  w[3] = (uint32_t)sc.nslots;
+  w[4] = kB;
+  w[5] = (uint32_t)W;
+  w[6] = (uint32_t)v.size();
+  for (int q = 0; q < nvar; ++q)
+    for (size_t i = 0; i < v.size(); ++i) w.push_back(v[i] | (adr[i] ? (uint32_t)(q * 32) << 16 : 0u));
+  for (int c : sc.consts) w.push_back((uint32_t)c);
+  while (w.size() % 4) w.push_back(0);
+  w[2] = (uint32_t)w.size();
+  return w;
+}
+
+// words of the device code a consumer reads (header + 4 variants): the code slot size
+inline int device_words(const TSched &sc) {
+  int per = 0;
+  for (size_t bi = 0; bi < sc.batches.size(); ++bi) {
+    bool quad = false;
+    for (int j = 0; j < sc.B; ++j) quad |= sc.batches[bi][j].arity() > 2;
+    per += 4 + sc.B * (quad ? 8 : 4);
+  }
+  return kHead + 4 * per;
+}
+
 struct Layout {
   int W = 2, CW = 4, S = 2, NC = 1, capw = 0, B = 8;
   uint32_t code0 = 0, const0 = 0, RB = 0;
@@ -287,7 +357,7 @@ struct Layout {
 size_t layout_smem(Layout &y) {
   y.RB = (uint32_t)(y.CW * 32 * y.W * 4);
   y.code0 = 128 + kH * kHdr;
-  size_t c0 = y.code0 + (size_t)kH * y.capw * 4;
+  size_t c0 = y.code0 + (size_t)y.capw * 4;  // one code slot
   c0 = (c0 + 127) / 128 * 128;
   y.const0 = (uint32_t)c0;
   y.smem = c0 + (size_t)y.S * y.NC * y.RB;
@@ -348,13 +418,6 @@ __device__ __forceinline__ void sttm_w(uint32_t ta, const Vec<W> &v) {
   else
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(ta), "r"(v.x[0]), "r"(v.x[1]) : "memory");
 }
-// TMEM address of the column in the low / high 16 bits of a code word (tl: this warp's lane
-// quarter; with 4 consumer warps its column bits are zero, so the low half is one LOP3)
-template <int CW>
-__device__ __forceinline__ uint32_t col_lo(uint32_t tl, uint32_t w) {
-  return CW == 4 ? ((w & 0xffffu) | tl) : (w & 0xffffu) + tl;
-}
-__device__ __forceinline__ uint32_t col_hi(uint32_t tl, uint32_t w) { return (w >> 16) + tl; }
 __device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -368,9 +431,10 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
   const uint32_t base = sm_addr(sm);
   const uint32_t hdr0 = base + 128;
   const uint32_t warp = tid / 32, lane = tid & 31;
-  // Tile it uses constant-row stage it % S and header/code slot it % kH.  Barriers: full[k]
-  // +8k (TMA bytes of stage k), rows_empty[k] +32+8k (stage k's rows copied to TMEM),
-  // code_empty[h] +64+8h (the tile of slot h is done with its header and code); TMEM base
+  // Tile it uses constant-row stage it % S and header slot it % kH; the program's code sits in
+  // one code slot, rewritten when the program changes (after the previous tile is done).
+  // Barriers: full[k] +8k (TMA bytes of stage k), rows_empty[k] +32+8k (stage k's rows
+  // copied to TMEM), tile_done[h] +64+8h (the tile of header slot h is done); TMEM base
   // address at +120
   if (tid == 0) {
     for (int k = 0; k < S; ++k) {
@@ -395,9 +459,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
   const uint32_t chunk = (a.ntiles + gridDim.x - 1) / gridDim.x;
   const uint32_t t0 = blockIdx.x * chunk, t1 = min(a.ntiles, t0 + chunk);
   if (warp == CW) {  // ---------------- producer warp (all 32 lanes issue copies)
-    int cur[kH];
-#pragma unroll
-    for (int k = 0; k < kH; ++k) cur[k] = -1;
+    int cur = -1;  // the program in the code slot
     for (uint32_t tile = t0, it = 0; tile < t1; ++tile, ++it) {
       const uint32_t st = it % S, ph = (it / S) & 1, hs = it % kH, hph = (it / kH) & 1;
       const uint32_t entry = tile / a.tps, tw = tile % a.tps;
@@ -407,15 +469,19 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       const uint32_t *pc = a.code + a.prog_off[prog];
       const uint8_t *const *in = a.in_tbl + (size_t)stripe * a.n_in;
       uint8_t *const *out = a.out_tbl + (size_t)stripe * a.n_out;
-      const uint32_t nl = pc[0], nb = pc[1];
-      const uint32_t *ld = pc + kHead + 4 * kB * (nb + 1);  // pc[4] == kB
+      const uint32_t nl = pc[0], nw = pc[2];
+      const uint32_t *ld = pc + nw - ((nl + 3) & ~3u);  // the constant list ends the code
       const size_t toff = (size_t)tw * a.tpos * 4;
-      const bool newcode = cur[hs] != prog;
+      const bool newcode = cur != prog;
       // (the producer shares an SMSP with consumer warp 0: sleep rather than spin)
       if (it >= (uint32_t)S)
         while (!try_wait(base + 32 + 8 * st, ph ^ 1)) __nanosleep(256);
-      if (it >= (uint32_t)kH)  // the tile that last used this header / code slot is done
+      if (it >= (uint32_t)kH)  // the tile that last used this header slot is done
         while (!try_wait(base + 64 + 8 * hs, hph ^ 1)) __nanosleep(256);
+      if (newcode && it >= 1) {  // every earlier tile is done with the code slot
+        const uint32_t pit = it - 1;
+        while (!try_wait(base + 64 + 8 * (pit % kH), (pit / kH) & 1)) __nanosleep(256);
+      }
       const uint32_t h = hdr0 + hs * kHdr;
       // goal strip g of this tile starts at out[g / 8] + (g % 8) * strip + toff
       for (uint32_t g = lane; g < 8u * a.n_out; g += 32) {
@@ -423,8 +489,8 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
         asm volatile("st.shared.u64 [%0], %1;" ::"r"(h + 16 + 8 * g), "l"(gp) : "memory");
       }
       const uint32_t nbytes = min(a.tpos, a.words - tw * a.tpos) * 4;
-      const uint32_t cbytes = newcode ? (kHead + 4 * kB * (nb + 1)) * 4 : 0;
-      cur[hs] = prog;
+      const uint32_t cbytes = newcode ? (nw - ((nl + 3) & ~3u)) * 4 : 0;  // header + variants
+      cur = prog;
       __syncwarp();
       if (lane == 0) {
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(h), "r"(stripe) : "memory");
@@ -434,7 +500,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
         if (cbytes)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-              ::"r"(base + a.code0 + hs * a.capw * 4), "l"(pc), "r"(cbytes), "r"(base + 8 * st) : "memory");
+              ::"r"(base + a.code0), "l"(pc), "r"(cbytes), "r"(base + 8 * st) : "memory");
       }
       __syncwarp();
       const uint32_t rows = a.const0 + st * a.NC * a.RB;
@@ -448,7 +514,8 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
     }
   } else {
     // ---------------- consumer warps: every thread runs the op stream on its W words
-    const uint32_t tl = tbase + (((warp & 3) * 32u) << 16) + (CW == 8 ? (warp >> 2) * (kCols / 2) : 0);
+    static_assert(CW == 4, "the device code has one variant per TMEM lane quarter");
+    const uint32_t tl = tbase + ((warp * 32u) << 16);
     {
       Vec<W> z;
 #pragma unroll
@@ -464,9 +531,9 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       const uint32_t npos = min(a.tpos, a.words - tw * a.tpos);
       const bool live = tid * W < npos;  // ragged tail: no goal stores past the strip
       const uint32_t hdr = hdr0 + hs * kHdr;
-      const uint32_t cp = base + a.code0 + hs * a.capw * 4;
-      const uint4 head = lds128(cp);
-      const uint32_t nl = head.x, nb = head.y;
+      const uint32_t cp = base + a.code0;
+      const uint4 head = lds128(cp), head2 = lds128(cp + 16);
+      const uint32_t nl = head.x, nb = head.y, vw = head2.z;
       // the stage's constant rows -> this thread's TMEM constant slots; then the rows are free
       {
         const uint32_t rs = base + a.const0 + st * a.NC * a.RB + tid * W * 4;
@@ -488,23 +555,34 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(base + 32 + 8 * st) : "memory");
       wait_st();
       const uint32_t tofs = tid * W * 4;  // this thread's bytes within a goal strip of the tile
-      // one batch: operand loads (TMEM), one wait, XORs, result stores (TMEM), goal stores; the
-      // next batch's ops are read into `on` meanwhile (two buffers, the loop is unrolled twice)
-      auto batch = [&](const uint4 (&o)[kB], uint4 (&on)[kB], uint32_t opn) {
-        const uint32_t fl = o[0].w;
+      // batches: a batch's code words (broadcast shared loads) -> its operand loads (TMEM), one
+      // wait, XORs -> result stores (TMEM) and goal stores
+      uint32_t p = cp + kHead * 4 + warp * vw * 4;  // this warp's code variant
+      for (uint32_t b = 0; b < nb; ++b) {
+        const uint32_t fl = lds128(p).x;
+        p += 16;
         if (fl & 1) wait_st();
         Vec<W> acc[kB];
-        if (fl & 2) {  // ops of up to four operands
+        uint32_t dst[kB], gw[kB];
+        if (fl & 2) {  // ops of up to four operands: 8 words each
+          uint4 u[kB];
+#pragma unroll
+          for (int j = 0; j < kB; ++j) u[j] = lds128(p + 32 * j);
           Vec<W> x[kB][4];
 #pragma unroll
           for (int j = 0; j < kB; ++j) {
-            ldtm_w<W>(col_lo<CW>(tl, o[j].x), x[j][0]);
-            ldtm_w<W>(col_hi(tl, o[j].x), x[j][1]);
-            ldtm_w<W>(col_lo<CW>(tl, o[j].y), x[j][2]);
-            ldtm_w<W>(col_hi(tl, o[j].y), x[j][3]);
+            ldtm_w<W>(u[j].x, x[j][0]);
+            ldtm_w<W>(u[j].y, x[j][1]);
+            ldtm_w<W>(u[j].z, x[j][2]);
+            ldtm_w<W>(u[j].w, x[j][3]);
           }
 #pragma unroll
-          for (int j = 0; j < kB; ++j) on[j] = lds128(opn + 16 * j);
+          for (int j = 0; j < kB; ++j) {
+            const uint4 t = lds128(p + 32 * j + 16);
+            dst[j] = t.x;
+            gw[j] = t.y;
+          }
+          p += 32 * kB;
           wait_ld();
 #pragma unroll
           for (int j = 0; j < kB; ++j)
@@ -514,15 +592,19 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
               asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(y) : "r"(x[j][0].x[w]), "r"(x[j][1].x[w]), "r"(x[j][2].x[w]));
               acc[j].x[w] = y ^ x[j][3].x[w];
             }
-        } else {  // binary ops: operands 3-4 are not loaded
+        } else {  // binary ops: 4 words each
+          uint4 u[kB];
+#pragma unroll
+          for (int j = 0; j < kB; ++j) u[j] = lds128(p + 16 * j);
           Vec<W> x[kB][2];
 #pragma unroll
           for (int j = 0; j < kB; ++j) {
-            ldtm_w<W>(col_lo<CW>(tl, o[j].x), x[j][0]);
-            ldtm_w<W>(col_hi(tl, o[j].x), x[j][1]);
+            ldtm_w<W>(u[j].x, x[j][0]);
+            ldtm_w<W>(u[j].y, x[j][1]);
+            dst[j] = u[j].z;
+            gw[j] = u[j].w;
           }
-#pragma unroll
-          for (int j = 0; j < kB; ++j) on[j] = lds128(opn + 16 * j);
+          p += 16 * kB;
           wait_ld();
 #pragma unroll
           for (int j = 0; j < kB; ++j)
@@ -530,11 +612,11 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
             for (int w = 0; w < W; ++w) acc[j].x[w] = x[j][0].x[w] ^ x[j][1].x[w];
         }
 #pragma unroll
-        for (int j = 0; j < kB; ++j) sttm_w<W>(col_lo<CW>(tl, o[j].z), acc[j]);
+        for (int j = 0; j < kB; ++j) sttm_w<W>(dst[j], acc[j]);
         if (fl & 4) {  // goal stores (predicated: ops without a goal and the ragged tail skip)
 #pragma unroll
           for (int j = 0; j < kB; ++j) {
-            const uint32_t g = o[j].z >> 16;
+            const uint32_t g = gw[j];
             uint64_t gp;
             asm volatile("ld.shared.u64 %0, [%1];" : "=l"(gp) : "r"(hdr + 8 + 8 * g) : "memory");
             gp += tofs;
@@ -547,18 +629,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
                            ::"l"(gp), "r"(acc[j].x[0]), "r"(acc[j].x[1]), "r"(doit) : "memory");
           }
         }
-      };
-      uint32_t op = cp + kHead * 4;
-      uint4 oa[kB], ob[kB];
-#pragma unroll
-      for (int j = 0; j < kB; ++j) oa[j] = lds128(op + 16 * j);
-      uint32_t b = 0;
-      for (; b + 2 <= nb; b += 2) {
-        batch(oa, ob, op + 16 * kB);
-        batch(ob, oa, op + 32 * kB);
-        op += 32 * kB;
       }
-      if (b < nb) batch(oa, ob, op + 16 * kB);
       // the next tile's constant copies overwrite slots this tile's last batches read/stored
       wait_st();
       __syncwarp();
@@ -619,9 +690,10 @@ std::vector<std::shared_ptr<const TSched>> scheds_of(const Program *const *progs
 
 }  // namespace tmem
 
-// Dump form 5: the TMEM interpreter's code for this program (columns in slot units, W = 1).
-std::vector<uint32_t> interp_tmem_dump(const Program *p) {
-  return tmem::emit_code(*tmem::sched_of(p), 1);
+// Dump form 5: the TMEM interpreter's schedule in its compact form; form 6: the device code the
+// kernel runs (both with W = 1: columns = slots).
+std::vector<uint32_t> interp_tmem_dump(const Program *p, int form) {
+  return form == 5 ? tmem::emit_code(*tmem::sched_of(p), 1) : tmem::emit_device(*tmem::sched_of(p), 1);
 }
 
 void drop_tmem_of(const Program *p) {
@@ -653,7 +725,7 @@ template <int W, int CW, int B>
 const void *kfn() { return (const void *)(KFn)xslp_interp_tmem<W, CW, B>; }
 template <int B>
 const void *kernel_b(int W, int CW) {
-  return W == 2 ? (CW == 8 ? kfn<2, 8, B>() : kfn<2, 4, B>()) : (CW == 8 ? kfn<1, 8, B>() : kfn<1, 4, B>());
+  return W == 2 ? kfn<2, 4, B>() : kfn<1, 4, B>();
 }
 const void *kernel_of(int W, int CW, int B) { return B == 4 ? kernel_b<4>(W, CW) : kernel_b<8>(W, CW); }
 }  // namespace tmem
@@ -665,10 +737,9 @@ static bool tmem_finish_plan(int dev) {
   std::lock_guard<std::mutex> g(am);
   if (!attr[dev]) {
     for (int W : {1, 2})
-      for (int CW : {4, 8})
-        for (int B : {4, 8})
-          CUDA_OK(cudaFuncSetAttribute(kernel_of(W, CW, B), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       227 * 1024));
+      for (int B : {4, 8})
+        CUDA_OK(cudaFuncSetAttribute(kernel_of(W, 4, B), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
     attr[dev] = true;
   }
   return true;
@@ -694,14 +765,14 @@ static int tmem_words(int nc, int nslots, int S, int CW, int capw, int want) {
 
 // The code pool and layout of a program set for strips of B/8 bytes on the current device;
 // false if the TMEM interpreter does not apply (strip % 16, > 32 output blocks, or the slots /
-// rows do not fit).  Consumer warps: 8 when opts.threads >= 256, else 4.
+// rows do not fit).  Four consumer warps: one per TMEM lane quarter, each with all 512 columns.
 static bool tmem_plan(const Program *const *progs, int np, size_t B, tmem::Pool &pool) {
   using namespace tmem;
   const xslp_opts &o = progs[0]->opts;
   const uint64_t strip = B / 8;
   if (strip % 16 || progs[0]->n_goals / 8 > 32) return false;
   const int S = std::max(1, std::min(4, o.stages));
-  const int CW = o.threads >= 256 ? 8 : 4;
+  const int CW = 4;
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));
   const int want = o.lane_words >= 2 ? 2 : 1;
@@ -731,7 +802,7 @@ static bool tmem_plan(const Program *const *progs, int np, size_t B, tmem::Pool 
   for (int i = 0; i < np; ++i) {
     nc = std::max<int>(nc, (int)sc[i]->consts.size());
     ns = std::max(ns, sc[i]->nslots);
-    cw = std::max(cw, consumer_words(*sc[i]));
+    cw = std::max(cw, device_words(*sc[i]));
   }
   Layout y;
   y.S = S;
@@ -746,7 +817,7 @@ static bool tmem_plan(const Program *const *progs, int np, size_t B, tmem::Pool 
   std::vector<int64_t> off;
   for (int i = 0; i < np; ++i) {
     off.push_back((int64_t)all.size());
-    auto w = emit_code(*sc[i], y.W);
+    auto w = emit_device(*sc[i], y.W);
     all.insert(all.end(), w.begin(), w.end());
   }
   Pool P;

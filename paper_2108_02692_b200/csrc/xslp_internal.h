@@ -134,7 +134,7 @@ std::vector<uint32_t> interp_code_dump(const Slp &s, int T, int L, int S);
 // The lane-parallel interpreter's code (interp_lanes.cu; xslp_program_dump form 4).
 std::vector<uint32_t> interp_lanes_dump(const Program *p, int S);
 // The TMEM interpreter's code (interp_tmem.cu; xslp_program_dump form 5).
-std::vector<uint32_t> interp_tmem_dump(const Program *p);
+std::vector<uint32_t> interp_tmem_dump(const Program *p, int form);
 // Input-phase programs of a goal set (capi.cpp; PIPE input phases and the phased multi kernel).
 std::vector<Slp> phase_programs(const std::vector<Bits> &want, int n_const, int nphases,
                                 const xslp_opts &o, int64_t *xor_total);

@@ -637,6 +637,49 @@ def _emulate_tmem(words, strips, n_goals):
     return out
 
 
+def _emulate_tmem_device(words, strips, n_goals):
+    """Run the TMEM kernel's device code (dump form 6, interp_tmem.cu emit_device, W = 1) the
+    way each of the four consumer warps reads its own variant: every TMEM address must carry
+    the warp's lane quarter; the result must be the same for every variant."""
+    nconst, nb, kb, vw = words[0], words[1], words[4], words[6]
+    loads = words[8 + 4 * vw:8 + 4 * vw + nconst]
+    results = []
+    for q in range(4):
+        v = words[8 + q * vw:8 + (q + 1) * vw]
+        zero = np.zeros_like(strips[0])
+        tm = {0: zero}
+        for r, c in enumerate(loads):
+            tm[2 + r] = strips[c]
+        out = np.zeros((n_goals, strips.shape[1]), dtype=np.uint32)
+        p = 0
+
+        def col(a):
+            assert a >> 16 == q * 32, (q, hex(a))
+            return a & 0xFFFF
+        for _ in range(nb):
+            fl = v[p]
+            p += 4
+            per = 8 if fl & 2 else 4
+            nops = 4 if fl & 2 else 2
+            res = []
+            for j in range(kb):
+                o = v[p + per * j:p + per * (j + 1)]
+                acc = zero.copy()
+                for a in o[:nops]:
+                    acc ^= tm[col(a)]
+                res.append((acc, col(o[nops]), o[nops + 1]))
+            p += per * kb
+            for acc, d, g in res:
+                tm[d] = acc
+                if g:
+                    assert fl & 4
+                    out[g - 1] = acc
+        assert p == vw
+        results.append(out)
+    assert all((r == results[0]).all() for r in results)
+    return results[0]
+
+
 @pytest.mark.parametrize("n,p,comp,er,sched", [
     (10, 4, "xorrepair", None, 1), (10, 4, "xorrepair", (2, 4, 5, 6), 1), (4, 2, "none", None, 1),
     (20, 4, "xorrepair", (0, 5, 21, 23), 1), (10, 3, "repair", None, 2), (10, 4, "none", (0, 1, 12, 13), 0),
@@ -661,6 +704,9 @@ def test_tmem_interpreter_code_computes_the_oracle_result(n, p, comp, er, sched)
     strips = data.reshape(8 * n, B // 8).view(np.uint32)
     want = rs.apply_rows(rows, data).reshape(bits.shape[0], B // 8).view(np.uint32)
     assert (_emulate_tmem(words, strips, bits.shape[0]) == want).all()
+    dev = [int(x) for x in prog.dump(6).split()]
+    assert dev[2] == len(dev)
+    assert (_emulate_tmem_device(dev, strips, bits.shape[0]) == want).all()
 
 
 @pytest.mark.parametrize("n,p,comp,er,sched", [
