@@ -418,6 +418,21 @@ __device__ __forceinline__ void sttm_w(uint32_t ta, const Vec<W> &v) {
   else
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(ta), "r"(v.x[0]), "r"(v.x[1]) : "memory");
 }
+// 8 consecutive slots (8W columns) in one store
+template <int W>
+__device__ __forceinline__ void sttm_rows8(uint32_t ta, const Vec<W> (&v)[8]) {
+  if constexpr (W == 1)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+                 ::"r"(ta), "r"(v[0].x[0]), "r"(v[1].x[0]), "r"(v[2].x[0]), "r"(v[3].x[0]), "r"(v[4].x[0]),
+                 "r"(v[5].x[0]), "r"(v[6].x[0]), "r"(v[7].x[0]) : "memory");
+  else
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+                 "%11, %12, %13, %14, %15, %16};"
+                 ::"r"(ta), "r"(v[0].x[0]), "r"(v[0].x[1]), "r"(v[1].x[0]), "r"(v[1].x[1]), "r"(v[2].x[0]),
+                 "r"(v[2].x[1]), "r"(v[3].x[0]), "r"(v[3].x[1]), "r"(v[4].x[0]), "r"(v[4].x[1]),
+                 "r"(v[5].x[0]), "r"(v[5].x[1]), "r"(v[6].x[0]), "r"(v[6].x[1]), "r"(v[7].x[0]),
+                 "r"(v[7].x[1]) : "memory");
+}
 __device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -538,12 +553,11 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       {
         const uint32_t rs = base + a.const0 + st * a.NC * a.RB + tid * W * 4;
         uint32_t r = 0;
-        for (; r + 4 <= nl; r += 4) {
-          Vec<W> v[4];
+        for (; r + 8 <= nl; r += 8) {  // 8 consecutive slots: one tcgen05.st of 8W columns
+          Vec<W> v[8];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) lds_w<W>(rs + (r + k) * a.RB, v[k]);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) sttm_w<W>(tl + (kConst0 + r + k) * W, v[k]);
+          for (int k = 0; k < 8; ++k) lds_w<W>(rs + (r + k) * a.RB, v[k]);
+          sttm_rows8<W>(tl + (kConst0 + r) * W, v);
         }
         for (; r < nl; ++r) {
           Vec<W> v;
