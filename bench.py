@@ -142,9 +142,9 @@ def parse():
                     help="1 = DFS (P:1279-1303), 0 = creation order, 2 = capacity-bounded greedy "
                          "(P:1305-1338, capacity --greedy-capacity)")
     ap.add_argument("--greedy-capacity", type=int, default=64)
-    ap.add_argument("--interp", default="lanes", choices=["lanes", "pairs", "tmem"],
-                    help="--kernel interp: the lane-parallel (default), the pair-pipelined or the "
-                         "TMEM-variable interpreter")
+    ap.add_argument("--interp", default="tmem", choices=["lanes", "pairs", "tmem"],
+                    help="--kernel interp: the TMEM-variable (default), the lane-parallel or the "
+                         "pair-pipelined interpreter")
     ap.add_argument("--peer-tma", type=int, default=0,
                     help="xdec/xdec1 at N>1: 1 = TMA-staged kernels (PIPE / fused multi-program) "
                          "bulk-copy peer strips (opt-in; default: LDG straight-line kernels)")
@@ -428,8 +428,7 @@ def main():
     args.threads = args.threads or 128
     args.stages = args.stages or 2
     args.groups = args.groups or 1
-    # the TMEM interpreter runs 2 words per thread when they fit (else it falls back to 1)
-    args.lanes = args.lanes or (2 if args.kernel == "interp" and args.interp == "tmem" else 1)
+    args.lanes = args.lanes or 1
     args.per_module_raw = args.per_module
     args.reuse = args.reuse or 0
     args.per_module = args.per_module or 20

@@ -82,13 +82,13 @@ extern "C" {
                                   needs block_bytes % 128 == 0 */
 
 /* xslp_opts.interp: organisation of the batched interpreter (XSLP_KERNEL_INTERP) */
-#define XSLP_INTERP_LANES 0 /* default: the 32 lanes of a warp run 32 independent SLP instructions
+#define XSLP_INTERP_LANES 0 /* the 32 lanes of a warp run 32 independent SLP instructions
                                (a round) over the same 16 bytes of every strip, 128-bit shared
                                loads; max(16, threads / 32) consumer warps per CTA */
 #define XSLP_INTERP_PAIRS 1 /* every thread owns lane_words words; micro-ops of four operands run
                                warp-uniformly in software-pipelined pairs; threads consumers */
-#define XSLP_INTERP_TMEM 2  /* every thread owns lane_words words (1, or 2 falling back to 1 when
-                               the TMEM slots or the shared-memory stages do not fit);
+#define XSLP_INTERP_TMEM 2  /* default: every thread owns 2 words (1 when the TMEM slots or the
+                               shared-memory stages do not fit; the lane interpreter when neither);
                                SLP variables live in tensor memory (tcgen05.ld/st, one TMEM lane
                                per thread), constants in shared memory; 128 consumer threads */
 
@@ -125,7 +125,7 @@ typedef struct xslp_opts {
                               and the fused M^-1 multi-program kernels, which run one CTA per
                               SM, 16 for the syndrome-form kernels, which keep two CTAs per SM),
                               -1 = a fresh shared-memory read at every use, or 1..4096 */
-  int32_t interp;          /* XSLP_INTERP_*: batched interpreter organisation; default LANES */
+  int32_t interp;          /* XSLP_INTERP_*: batched interpreter organisation; default TMEM */
 } xslp_opts;
 
 typedef struct xslp_stats {

@@ -32,7 +32,7 @@ extern "C" void xslp_default_opts(xslp_opts *o) {
   o->groups = 1;
   o->phases = 0;
   o->reuse = 0;
-  o->interp = XSLP_INTERP_LANES;
+  o->interp = XSLP_INTERP_TMEM;
 }
 
 extern "C" int xslp_coding_matrix(int n, int p, int kind, uint8_t *gf_out) {

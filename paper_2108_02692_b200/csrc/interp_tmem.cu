@@ -789,7 +789,7 @@ static bool tmem_plan(const Program *const *progs, int np, size_t B, tmem::Pool 
   const int CW = 4;
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));
-  const int want = o.lane_words >= 2 ? 2 : 1;
+  const int want = 2;  // 2 words per thread when they fit (tmem_words), else 1
   std::vector<const Program *> key(progs, progs + np);
   const auto k = std::make_tuple(dev, S, want, CW, key);
   {

@@ -47,9 +47,9 @@ def run_batch(prog, din, dout, B, nstripes=None):
 
 
 def _kernel_kw(kw):
-    """kernel="interp_pairs": the pair-pipelined interpreter (XSLP_INTERP_PAIRS); "interp" is
-    the lane-parallel one (the default)."""
-    if kw.get("kernel") in ("interp_pairs", "interp_tmem"):
+    """kernel="interp_pairs" / "interp_lanes": the pair-pipelined / lane-parallel interpreters
+    (XSLP_INTERP_PAIRS / LANES); "interp" is the TMEM one (the default)."""
+    if kw.get("kernel") in ("interp_pairs", "interp_tmem", "interp_lanes"):
         kw = dict(kw, kernel="interp", interp=kw["kernel"][7:])
     return kw
 
@@ -101,7 +101,7 @@ def test_cfg1_encode_decode(kernel):
 @pytest.mark.parametrize("comp", ["none", "repair", "xorrepair"])
 @pytest.mark.parametrize("kern,lanes", [("straight", 1), ("straight", 2), ("straight", 4),
                                         ("interp", 1), ("interp_pairs", 1), ("interp_pairs", 2),
-                                        ("interp_tmem", 1), ("interp_tmem", 2),
+                                        ("interp_lanes", 1),
                                         ("tma", 1), ("tma", 2), ("pipe", 1), ("pipe", 2)])
 @pytest.mark.parametrize("p", [2, 3, 4])
 def test_rs10_encode_small_full_compare(comp, kern, lanes, p):
@@ -145,7 +145,7 @@ def _decode_inputs(seed, S, n, p, B, e):
     return pats, blocks
 
 
-@pytest.mark.parametrize("kern", ["interp", "interp_pairs", "interp_tmem", "straight", "grouped",
+@pytest.mark.parametrize("kern", ["interp", "interp_pairs", "interp_lanes", "straight", "grouped",
                                   "grouped_tma", "grouped_pipe"])
 def test_heterogeneous_decode(kern):
     n, p, B, S = 10, 4, 4096, 24
@@ -181,12 +181,13 @@ def test_heterogeneous_decode(kern):
         assert (got[s] == blocks[s][list(pats[s])]).all(), (s, pats[s])
 
 
-@pytest.mark.parametrize("lanes", [1, 2])
-def test_tmem_interpreter_kernel_runs(lanes):
-    # the TMEM interpreter (tensor-memory variables) is the kernel that runs, not the fallback
-    n, p, B, S = 10, 4, 65536, 8
+@pytest.mark.parametrize("n,p", [(10, 4), (20, 4)])
+def test_tmem_interpreter_kernel_runs(n, p):
+    # the TMEM interpreter (tensor-memory variables, the default interpreter) is the kernel that
+    # runs, not the fallback: 2 words per thread for RS(10,4), 1 for RS(20,4) (160 constant rows)
+    B, S = 65536, 8
     og = mx.coding_matrix(n, p)
-    _, prog = compile_enc(n, p, kernel="interp_tmem", lane_words=lanes, specialise=0)
+    _, prog = compile_enc(n, p, kernel="interp", specialise=0)
     data = host_data(12, range(S), n, B)
     din = torch.from_numpy(data).cuda()
     dout = dev_buf(S, p, B)
@@ -706,7 +707,8 @@ def _xor_reduce(t):
 
 
 @pytest.mark.parametrize("kern,threads,lanes,reuse", [("straight", 128, 1, 0), ("tma", 128, 1, 0),
-                                                      ("pipe", 256, 1, 0), ("pipe", 128, 2, "bench")])
+                                                      ("pipe", 256, 1, 0), ("pipe", 128, 2, "bench"),
+                                                      ("interp", 128, 1, 0)])
 def test_cfg2_full_size(kern, threads, lanes, reuse):
     # RS(10,4), 1024 stripes x 10 x 1 MiB (configs[1]); ("pipe", 128, 2 lanes) with bench's
     # stages, input phases and reuse window is the exact launch configuration bench.py times
@@ -736,7 +738,7 @@ def test_cfg2_full_size(kern, threads, lanes, reuse):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("mode", ["grouped", "interp", "interp_pairs", "interp_tmem"])
+@pytest.mark.parametrize("mode", ["grouped", "interp", "interp_pairs", "interp_lanes"])
 def test_cfg3_full_size_roundtrip(mode):
     # RS(10,4) decode, 1024 stripes x 1 MiB, per-stripe seeded 4-of-14 erasures (configs[2]);
     # "grouped" (per-pattern LDG kernels, T=64, 8 streams) is the bench's launch configuration
@@ -762,7 +764,7 @@ def test_cfg3_full_size_roundtrip(mode):
     if mode == "grouped":
         progs = X.compile_many(bitsl, kernel="straight", threads=64, block_bytes_hint=B)
     else:                     # the lane-parallel (default) or the pair-pipelined interpreter
-        progs = X.compile_many(bitsl, specialise=0, interp=mode[7:] if "_" in mode else "lanes")
+        progs = X.compile_many(bitsl, specialise=0, interp=mode[7:] if "_" in mode else "tmem")
     pos = [uniq.index(er) for er in pats]
     idx = torch.tensor(pos, dtype=torch.int32, device="cuda")
     tin = torch.stack([ti[s, torch.as_tensor(survs[pats[s]], dtype=torch.long)] for s in range(S)])
@@ -1127,7 +1129,7 @@ def test_byte_layout_full_size(kern, threads):
 
 # ---- CUDA graphs: launches are capturable after xslp_prepare -----------------------------
 
-@pytest.mark.parametrize("kern", ["pipe", "straight", "interp", "interp_pairs", "interp_tmem", "pipe_phases",
+@pytest.mark.parametrize("kern", ["pipe", "straight", "interp", "interp_pairs", "interp_lanes", "pipe_phases",
                                   "pipe_byte"])
 def test_cuda_graph_capture(kern):
     n, p, B, S = (20, 4, 65536, 32) if kern == "pipe_phases" else (10, 4, 65536, 64)
