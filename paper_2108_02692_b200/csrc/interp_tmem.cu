@@ -1,5 +1,5 @@
-// TMEM interpreter: the paper's "interpreter style" with the SLP's variables held in
-// Blackwell tensor memory.
+// TMEM interpreter: the paper's "interpreter style" with the SLP's constants and
+// variables held in Blackwell tensor memory.  The default batched interpreter.
 //
 // Why: an interpreter cannot keep SLP variables in registers (their names are data, and an
 // indirect branch per instruction costs ~150 cycles on sm_100a: scripts/dispatch_probe.py), so
@@ -7,23 +7,28 @@
 // memory and are bound by its 128 B/clk/SM.  Tensor memory (256 KB per SM, 128 lanes x 512
 // 32-bit columns) is addressed per thread by a warp-uniform column: exactly the "variable
 // index is data" access an interpreter needs, at ~280-390 B/clk/SM of tcgen05.ld bandwidth and
-// ~17 cycles latency (scripts/tmem_probe.cu).  So: constants stay where TMA puts them (shared
-// memory), variables live in TMEM, and every thread runs the same instruction stream on its own
-// words -- code loads are broadcasts and shared accesses are conflict-free by construction.
+// ~17 cycles latency (scripts/tmem_probe.cu).  Every thread runs the same instruction stream on
+// its own words, so code reads are broadcasts and the data never crosses lanes.
 //
 // Work layout (persistent, one CTA per SM): 4 consumer warps (128 threads = the 128 TMEM
-// lanes) + 1 producer warp.  A tile is 128*W consecutive 32-bit words of every strip of one
-// stripe (W = 1 or 2 words per thread); thread t owns words t*W..t*W+W-1.  The producer streams
-// each tile's constant strips by TMA (cp.async.bulk + mbarrier full/empty ring of S stages) and,
-// when a stage's program changes, the program's code into that stage's code buffer.
+// lanes, warp w owns lane quarter w and all 512 columns) + 1 producer warp.  A tile is 128*W
+// consecutive 32-bit words of every strip of one stripe (W = 2 words per thread, 1 when the
+// TMEM slots or shared-memory rows do not fit); thread t owns words t*W..t*W+W-1.  The producer
+// streams each tile's constant strips by TMA (cp.async.bulk + mbarrier full/empty ring of S
+// stages) and, when the program changes, the program's code into the code slot.  A consumer
+// copies the tile's constant rows into its TMEM constant slots (8 slots per tcgen05.st) and
+// releases the stage at once, then runs the batches out of TMEM.
 //
 // Code (host, build_tmem): the scheduled SLP's instructions (P:803-818 MultiSLP, DFS order
-// P:1279-1303) become ops of up to 4 shared (constant) + 4 TMEM (variable) operands; wider
-// instructions become a tree of partial ops into temporaries.  Ops are list-scheduled into
-// batches of kB mutually independent ops; a consumer issues all loads of a batch, waits once
-// (tcgen05.wait::ld), XORs, then stores the results to TMEM (tcgen05.st) and goals to HBM.
-// TMEM slots (W columns each) are assigned by liveness at batch granularity; a batch reading a
-// slot the previous batch stored first waits for the stores (tcgen05.wait::st).
+// P:1279-1303) become ops of at most four operands (wider instructions: a tree of partial ops
+// into temporaries), list-scheduled in op order into batches of kB (12) mutually independent
+// ops: two-operand ops together where the window allows, ops that only store a goal deferred
+// into a few goal batches.  A consumer issues all TMEM loads of a batch, waits once
+// (tcgen05.wait::ld), XORs, stores the results to TMEM (tcgen05.st) and goals to HBM.  TMEM
+// slots (W columns each) are assigned by liveness at batch granularity; a batch reading a slot
+// stored since the last wait first waits for the stores (tcgen05.wait::st).  The device code
+// has one variant per lane quarter with the quarter in every TMEM address, so an operand costs
+// one R2UR and one tcgen05.ld.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -44,7 +49,7 @@ void count_launch();  // device.cu
 
 namespace tmem {
 
-constexpr int kMaxB = 8;           // ops per batch: batch_size() (4 or 8)
+constexpr int kMaxB = 12;          // ops per batch: batch_size() (12; 4 or 8 for experiments)
 constexpr int kH = 4;              // tile header slots (a ring longer than the S stages)
 constexpr int kHead = 8;           // code header words
 constexpr int kHdr = 16 + 8 * 256;  // tile header: stripe, prog, pad, a pointer per goal strip
@@ -55,7 +60,7 @@ constexpr uint32_t kNone = 0xffff;
 inline int batch_size() {
   static const int b = [] {
     const char *e = getenv("XSLP_TMEM_BATCH");
-    return e && atoi(e) == 4 ? 4 : 8;
+    return e && (atoi(e) == 4 || atoi(e) == 8) ? atoi(e) : 12;  // measured: 12 > 8 > 16 > 4
   }();
   return b;
 }
@@ -69,7 +74,7 @@ struct TOp {
 
 struct TSched {
   int n_const = 0;
-  int B = 8;                                    // ops per batch
+  int B = 12;                                   // ops per batch
   std::vector<std::array<TOp, kMaxB>> batches;  // unused entries: no operands, dst = goal = -1
   std::vector<uint8_t> wait_st;              // batch first waits for earlier TMEM stores
   std::vector<int> consts;                   // constant row r (TMEM slot kConst0 + r) holds consts[r]
@@ -349,7 +354,7 @@ inline int device_words(const TSched &sc) {
 }
 
 struct Layout {
-  int W = 2, CW = 4, S = 2, NC = 1, capw = 0, B = 8;
+  int W = 2, CW = 4, S = 2, NC = 1, capw = 0, B = 12;
   uint32_t code0 = 0, const0 = 0, RB = 0;
   size_t smem = 0;
 };
@@ -741,7 +746,9 @@ template <int B>
 const void *kernel_b(int W, int CW) {
   return W == 2 ? kfn<2, 4, B>() : kfn<1, 4, B>();
 }
-const void *kernel_of(int W, int CW, int B) { return B == 4 ? kernel_b<4>(W, CW) : kernel_b<8>(W, CW); }
+const void *kernel_of(int W, int CW, int B) {
+  return B == 4 ? kernel_b<4>(W, CW) : B == 8 ? kernel_b<8>(W, CW) : kernel_b<12>(W, CW);
+}
 }  // namespace tmem
 
 static bool tmem_finish_plan(int dev) {
@@ -751,7 +758,7 @@ static bool tmem_finish_plan(int dev) {
   std::lock_guard<std::mutex> g(am);
   if (!attr[dev]) {
     for (int W : {1, 2})
-      for (int B : {4, 8})
+      for (int B : {4, 8, 12})
         CUDA_OK(cudaFuncSetAttribute(kernel_of(W, 4, B), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      227 * 1024));
     attr[dev] = true;

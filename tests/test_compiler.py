@@ -599,7 +599,7 @@ def _emulate_tmem(words, strips, n_goals):
     flagged, and never reads a slot stored since the last wait::st flag (the kernel's tcgen05.st
     may still be in flight)."""
     nconst, nb, nslots, kb, w_ = words[0], words[1], words[3], words[4], words[5]
-    assert w_ == 1 and kb in (4, 8)
+    assert w_ == 1 and kb in (4, 8, 12)
     ops = words[8:8 + 4 * kb * (nb + 1)]
     loads = words[8 + 4 * kb * (nb + 1):8 + 4 * kb * (nb + 1) + nconst]
     zero = np.zeros_like(strips[0])
