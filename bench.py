@@ -421,6 +421,8 @@ def main():
     tuned = dict(wl.get("tuned", {}))
     if args.kernel and args.kernel in wl.get("alt", {}):
         tuned = dict(wl["alt"][args.kernel], kernel=args.kernel)
+    elif args.kernel and args.kernel != tuned.get("kernel"):
+        tuned = {}  # the workload's tuned set is another kernel's
     for k, v in tuned.items():
         if getattr(args, k) is None:
             setattr(args, k, v)

@@ -680,6 +680,27 @@ def _emulate_tmem_device(words, strips, n_goals):
     return results[0]
 
 
+def test_tmem_interpreter_copy_and_zero_goals():
+    # degenerate goals through the TMEM interpreter's schedule and device code: identity rows
+    # (copies of a strip), zero rows, a full row, random rows
+    import synth
+    from oracle import rs
+    rng = np.random.default_rng(1)
+    bits = np.zeros((16, 24), dtype=np.uint8)
+    bits[0, 3] = 1
+    bits[1, 17] = 1
+    bits[2, [1, 2, 5]] = 1
+    bits[5, :] = 1
+    bits[9:, :] = rng.integers(0, 2, size=(7, 24))
+    B = 128
+    data = synth.stripe_data(9, 0, 3, B)
+    strips = data.reshape(24, B // 8).view(np.uint32)
+    want = rs.bitmatrix_apply(bits, data).reshape(16, B // 8).view(np.uint32)
+    prog = X.xslp_compile(bits, kernel="interp", specialise=0)
+    assert (_emulate_tmem([int(x) for x in prog.dump(5).split()], strips, 16) == want).all()
+    assert (_emulate_tmem_device([int(x) for x in prog.dump(6).split()], strips, 16) == want).all()
+
+
 @pytest.mark.parametrize("n,p,comp,er,sched", [
     (10, 4, "xorrepair", None, 1), (10, 4, "xorrepair", (2, 4, 5, 6), 1), (4, 2, "none", None, 1),
     (20, 4, "xorrepair", (0, 5, 21, 23), 1), (10, 3, "repair", None, 2), (10, 4, "none", (0, 1, 12, 13), 0),
