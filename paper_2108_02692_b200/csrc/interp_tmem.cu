@@ -21,11 +21,13 @@
 //
 // Code (host, build_tmem): the scheduled SLP's instructions (P:803-818 MultiSLP, DFS order
 // P:1279-1303) become ops of at most four operands (wider instructions: a tree of partial ops
-// into temporaries), list-scheduled in op order into batches of kB (12) mutually independent
-// ops: two-operand ops together where the window allows, ops that only store a goal deferred
-// into a few goal batches.  A consumer issues all TMEM loads of a batch, waits once
+// into temporaries), list-scheduled into batches of kB (16) mutually independent ops: among
+// the ready ops of a window of 400 in op order, the longest remaining chain first (critical-path
+// priority; the batch count is the kernel's latency count), two-operand ops together where the
+// window allows, ops that only store a goal deferred into a few goal batches.  A consumer issues all TMEM loads of a batch, waits once
 // (tcgen05.wait::ld), XORs, stores the results to TMEM (tcgen05.st) and goals to HBM.  TMEM
-// slots (W columns each) are assigned by liveness at batch granularity; a batch reading a slot
+// slots (W columns each) are assigned by liveness at batch granularity (a constant's slot is
+// reused after the constant's last reader); a batch reading a slot
 // stored since the last wait first waits for the stores (tcgen05.wait::st).  The device code
 // has one variant per lane quarter with the quarter in every TMEM address, so an operand costs
 // one R2UR and one tcgen05.ld.
@@ -49,7 +51,7 @@ void count_launch();  // device.cu
 
 namespace tmem {
 
-constexpr int kMaxB = 12;          // ops per batch: batch_size() (12; 4 or 8 for experiments)
+constexpr int kMaxB = 16;          // ops per batch: batch_size() (16; 4, 8, 12 for experiments)
 constexpr int kH = 4;              // tile header slots (a ring longer than the S stages)
 constexpr int kHead = 8;           // code header words
 constexpr int kHdr = 16 + 8 * 256;  // tile header: stripe, prog, pad, a pointer per goal strip
@@ -60,9 +62,39 @@ constexpr uint32_t kNone = 0xffff;
 inline int batch_size() {
   static const int b = [] {
     const char *e = getenv("XSLP_TMEM_BATCH");
-    return e && (atoi(e) == 4 || atoi(e) == 8) ? atoi(e) : 12;  // measured: 12 > 8 > 16 > 4
+    // measured with the critical-path scheduler: 16 > 20 > 24 > 12 > 8 (profiles/r02/tmem)
+    return e && (atoi(e) == 4 || atoi(e) == 8 || atoi(e) == 12) ? atoi(e) : 16;
   }();
   return b;
+}
+
+inline size_t sched_window() {
+  static const size_t w = [] {
+    const char *e = getenv("XSLP_TMEM_WINDOW");
+    return e && atoi(e) > 0 ? (size_t)atoi(e) : (size_t)400;
+  }();
+  return w;
+}
+inline bool sched_recycle() {
+  static const bool h = [] {
+    const char *e = getenv("XSLP_TMEM_RECYCLE");
+    return !e || atoi(e) > 0;
+  }();
+  return h;
+}
+inline bool sched_height() {
+  static const bool h = [] {
+    const char *e = getenv("XSLP_TMEM_HEIGHT");
+    return !e || atoi(e) > 0;
+  }();
+  return h;
+}
+inline bool sched_mixed() {  // experiment: fill batches by priority only, ignoring the op class
+  static const bool h = [] {
+    const char *e = getenv("XSLP_TMEM_MIXED");
+    return e && atoi(e) > 0;
+  }();
+  return h;
 }
 
 struct TOp {
@@ -74,7 +106,7 @@ struct TOp {
 
 struct TSched {
   int n_const = 0;
-  int B = 12;                                   // ops per batch
+  int B = 16;                                   // ops per batch
   std::vector<std::array<TOp, kMaxB>> batches;  // unused entries: no operands, dst = goal = -1
   std::vector<uint8_t> wait_st;              // batch first waits for earlier TMEM stores
   std::vector<int> consts;                   // constant row r (TMEM slot kConst0 + r) holds consts[r]
@@ -149,7 +181,20 @@ TSched build_tmem(const Slp &s) {
     }
   size_t first = 0, left = ops.size() - gq.size();
   int nb = 0;
-  const size_t kWindow = 48;
+  const size_t kWindow = sched_window();
+  // height of an op: the longest chain of ops that read its result (critical-path priority)
+  std::vector<int> height(ops.size(), 0);
+  {
+    std::vector<int> hv(nv, 0);  // variable -> height of its defining op
+    for (size_t i = ops.size(); i-- > 0;) {
+      int h = 0;
+      if (ops[i].dst >= 0) h = hv[ops[i].dst];
+      height[i] = h + 1;
+      for (int t : ops[i].t)
+        if (t >= s.n_const) hv[t - s.n_const] = std::max(hv[t - s.n_const], height[i]);
+    }
+  }
+  const bool by_height = sched_height();
   auto skip = [&]() {
     while (first < ops.size() && (batch_of[first] >= 0 || deferred[first])) ++first;
   };
@@ -173,12 +218,18 @@ TSched build_tmem(const Slp &s) {
     } else {
       // the oldest ready op decides the batch class; fill with ready ops of that class, then any
       int cls = -1;
+      std::vector<size_t> cand;  // ready ops of the window, in priority order
+      for (size_t i = first; i < ops.size() && i < first + kWindow; ++i)
+        if (batch_of[i] < 0 && !deferred[i] && ready(i, nb)) cand.push_back(i);
+      if (by_height)
+        std::stable_sort(cand.begin(), cand.end(), [&](size_t x, size_t y) { return height[x] > height[y]; });
       for (int pass = 0; pass < 2 && n < kB; ++pass)
-        for (size_t i = first; i < ops.size() && i < first + kWindow && n < kB; ++i) {
-          if (batch_of[i] >= 0 || deferred[i] || !ready(i, nb)) continue;
+        for (size_t i : cand) {
+          if (n == kB) break;
+          if (batch_of[i] >= 0) continue;
           const int c = ops[i].arity() > 2;
           if (cls < 0) cls = c;
-          if (pass == 0 && c != cls) continue;
+          if (pass == 0 && c != cls && !sched_mixed()) continue;
           batch_of[i] = nb;
           b[n++] = ops[i];
           --left;
@@ -208,17 +259,25 @@ TSched build_tmem(const Slp &s) {
       for (int t : o.t)
         if (t >= s.n_const) last[t - s.n_const] = std::max(last[t - s.n_const], bi);
   out.vslot.assign(nv, -1);
-  std::vector<int> free_at;  // variable slot -> first batch that may overwrite it
+  // slot kConst0 + k -> first batch that may overwrite it: a constant's slot is free after the
+  // constant's last reader (the tile's constant copies come before batch 0 and after the
+  // previous tile's last batch), a variable's after its last reader
+  std::vector<int> free_at(out.consts.size(), 0);
+  for (int bi = 0; bi < nb; ++bi)
+    for (const auto &o : out.batches[bi])
+      for (int t : o.t)
+        if (t >= 0 && t < s.n_const) free_at[row[t]] = std::max(free_at[row[t]], bi + 1);
+  if (!sched_recycle()) std::fill(free_at.begin(), free_at.end(), nb + 1);
   for (int bi = 0; bi < nb; ++bi)
     for (const auto &o : out.batches[bi]) {
       if (o.dst < 0) continue;
       int k = 0;
       while (k < (int)free_at.size() && free_at[k] > bi) ++k;
       if (k == (int)free_at.size()) free_at.push_back(0);
-      out.vslot[o.dst] = v0 + k;
+      out.vslot[o.dst] = kConst0 + k;
       free_at[k] = std::max(last[o.dst], bi) + 1;  // read through batch last[dst]
     }
-  out.nslots = v0 + (int)free_at.size();
+  out.nslots = std::max(v0, kConst0 + (int)free_at.size());
   // a wait::st at the start of batch w completes the stores of batches < w; the tile's
   // constant copies are waited for before batch 0
   out.wait_st.assign(nb, 0);
@@ -354,7 +413,7 @@ inline int device_words(const TSched &sc) {
 }
 
 struct Layout {
-  int W = 2, CW = 4, S = 2, NC = 1, capw = 0, B = 12;
+  int W = 2, CW = 4, S = 2, NC = 1, capw = 0, B = 16;
   uint32_t code0 = 0, const0 = 0, RB = 0;
   size_t smem = 0;
 };
@@ -747,7 +806,7 @@ const void *kernel_b(int W, int CW) {
   return W == 2 ? kfn<2, 4, B>() : kfn<1, 4, B>();
 }
 const void *kernel_of(int W, int CW, int B) {
-  return B == 4 ? kernel_b<4>(W, CW) : B == 8 ? kernel_b<8>(W, CW) : kernel_b<12>(W, CW);
+  return B == 4 ? kernel_b<4>(W, CW) : B == 8 ? kernel_b<8>(W, CW) : B == 12 ? kernel_b<12>(W, CW) : kernel_b<16>(W, CW);
 }
 }  // namespace tmem
 
@@ -758,7 +817,7 @@ static bool tmem_finish_plan(int dev) {
   std::lock_guard<std::mutex> g(am);
   if (!attr[dev]) {
     for (int W : {1, 2})
-      for (int B : {4, 8, 12})
+      for (int B : {4, 8, 12, 16})
         CUDA_OK(cudaFuncSetAttribute(kernel_of(W, 4, B), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      227 * 1024));
     attr[dev] = true;

@@ -599,7 +599,7 @@ def _emulate_tmem(words, strips, n_goals):
     flagged, and never reads a slot stored since the last wait::st flag (the kernel's tcgen05.st
     may still be in flight)."""
     nconst, nb, nslots, kb, w_ = words[0], words[1], words[3], words[4], words[5]
-    assert w_ == 1 and kb in (4, 8, 12)
+    assert w_ == 1 and kb in (4, 8, 12, 16)
     ops = words[8:8 + 4 * kb * (nb + 1)]
     loads = words[8 + 4 * kb * (nb + 1):8 + 4 * kb * (nb + 1) + nconst]
     zero = np.zeros_like(strips[0])
@@ -627,7 +627,9 @@ def _emulate_tmem(words, strips, n_goals):
             res.append((acc, w2))
         for acc, w2 in res:
             d, g = w2 & 0xFFFF, w2 >> 16
-            assert d >= 1 and d < nslots and (d == 1 or d >= 2 + nconst)
+            # a constant's slot may take a variable after the constant's last reader (a wrong
+            # reuse shows up as a wrong goal below)
+            assert d >= 1 and d < nslots
             slots[d] = acc
             pending.add(d)
             if g:
