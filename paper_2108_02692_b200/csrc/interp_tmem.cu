@@ -11,7 +11,7 @@
 // its own words, so code reads are broadcasts and the data never crosses lanes.
 //
 // Work layout (persistent, one CTA per SM): 4 consumer warps (128 threads = the 128 TMEM
-// lanes, warp w owns lane quarter w and all 512 columns) + 1 producer warp.  A tile is 128*W
+// lanes, warp w owns lane quarter w and all 512 columns) + 4 producer warps (one per SMSP).  A tile is 128*W
 // consecutive 32-bit words of every strip of one stripe (W = 2 words per thread, 1 when the
 // TMEM slots or shared-memory rows do not fit); thread t owns words t*W..t*W+W-1.  The producer
 // streams each tile's constant strips by TMA (cp.async.bulk + mbarrier full/empty ring of S
@@ -56,6 +56,7 @@ constexpr int kH = 4;              // tile header slots (a ring longer than the 
 constexpr int kHead = 8;           // code header words
 constexpr int kHdr = 16 + 8 * 256;  // tile header: stripe, prog, pad, a pointer per goal strip
 constexpr int kCols = 512;         // TMEM columns allocated per CTA
+constexpr int kNP = 4;             // producer warps
 constexpr int kZero = 0, kJunk = 1, kConst0 = 2;  // TMEM slots: zero, write sink, constants
 constexpr uint32_t kNone = 0xffff;
 
@@ -503,7 +504,7 @@ __device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.
 // W words per thread, CW consumer warps (4: each owns a 32-lane TMEM quarter and 512 columns;
 // 8: warps w and w+4 share a quarter, 256 columns each)
 template <int W, int CW, int kB>
-__global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
+__global__ void __launch_bounds__(CW * 32 + kNP * 32, 1) xslp_interp_tmem(Args a) {
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t tid = threadIdx.x;
   const int S = a.S;
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
   // address at +120
   if (tid == 0) {
     for (int k = 0; k < S; ++k) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(base + 8 * k));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(base + 8 * k), "n"(kNP));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(base + 32 + 8 * k), "r"(CW));
     }
     for (int k = 0; k < kH; ++k)
@@ -537,7 +538,11 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
   if (tbase & 0xffffu) asm volatile("trap;");  // all 512 columns: the allocation starts at column 0
   const uint32_t chunk = (a.ntiles + gridDim.x - 1) / gridDim.x;
   const uint32_t t0 = blockIdx.x * chunk, t1 = min(a.ntiles, t0 + chunk);
-  if (warp == CW) {  // ---------------- producer warp (all 32 lanes issue copies)
+  if (warp >= CW) {  // ---------------- producer warps (all lanes issue copies)
+    // kNP producer warps, one per SMSP, so that the copy-issue work (the compiler serialises
+    // the lanes' bulk copies) lands evenly on the four consumer warps' schedulers: producer pw
+    // issues constant rows pw, pw + kNP, ... and arrives on the full barrier with its own bytes
+    const uint32_t pw = warp - CW;
     int cur = -1;  // the program in the code slot
     for (uint32_t tile = t0, it = 0; tile < t1; ++tile, ++it) {
       const uint32_t st = it % S, ph = (it / S) & 1, hs = it % kH, hph = (it / kH) & 1;
@@ -552,7 +557,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       const uint32_t *ld = pc + nw - ((nl + 3) & ~3u);  // the constant list ends the code
       const size_t toff = (size_t)tw * a.tpos * 4;
       const bool newcode = cur != prog;
-      // (the producer shares an SMSP with consumer warp 0: sleep rather than spin)
+      // (each producer shares an SMSP with a consumer warp: sleep rather than spin)
       if (it >= (uint32_t)S)
         while (!try_wait(base + 32 + 8 * st, ph ^ 1)) __nanosleep(256);
       if (it >= (uint32_t)kH)  // the tile that last used this header slot is done
@@ -563,19 +568,22 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       }
       const uint32_t h = hdr0 + hs * kHdr;
       // goal strip g of this tile starts at out[g / 8] + (g % 8) * strip + toff
-      for (uint32_t g = lane; g < 8u * a.n_out; g += 32) {
+      for (uint32_t g = pw * 32 + lane; g < 8u * a.n_out; g += 32 * kNP) {
         const uint64_t gp = (uint64_t)out[g >> 3] + (g & 7) * a.strip + toff;
         asm volatile("st.shared.u64 [%0], %1;" ::"r"(h + 16 + 8 * g), "l"(gp) : "memory");
       }
       const uint32_t nbytes = min(a.tpos, a.words - tw * a.tpos) * 4;
-      const uint32_t cbytes = newcode ? (nw - ((nl + 3) & ~3u)) * 4 : 0;  // header + variants
+      const uint32_t cbytes = newcode && pw == 0 ? (nw - ((nl + 3) & ~3u)) * 4 : 0;  // header + variants
+      const uint32_t nmine = nl > pw ? (nl - pw + kNP - 1) / kNP : 0;  // rows this warp copies
       cur = prog;
       __syncwarp();
       if (lane == 0) {
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(h), "r"(stripe) : "memory");
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(h + 4), "r"((uint32_t)prog) : "memory");
+        if (pw == 0) {
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(h), "r"(stripe) : "memory");
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(h + 4), "r"((uint32_t)prog) : "memory");
+        }
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(base + 8 * st),
-                     "r"(nbytes * nl + cbytes) : "memory");
+                     "r"(nbytes * nmine + cbytes) : "memory");
         if (cbytes)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -583,7 +591,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       }
       __syncwarp();
       const uint32_t rows = a.const0 + st * a.NC * a.RB;
-      for (uint32_t i = lane; i < nl; i += 32) {
+      for (uint32_t i = pw + kNP * lane; i < nl; i += kNP * 32) {
         const uint32_t c = ld[i];
         const uint8_t *src = in[c >> 3] + (c & 7) * a.strip + toff;
         asm volatile(
@@ -617,6 +625,15 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) xslp_interp_tmem(Args a) {
       {
         const uint32_t rs = base + a.const0 + st * a.NC * a.RB + tid * W * 4;
         uint32_t r = 0;
+        for (; r + 16 <= nl; r += 16) {  // 16 rows' loads in flight, then two stores
+          Vec<W> v[8], u[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) lds_w<W>(rs + (r + k) * a.RB, v[k]);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) lds_w<W>(rs + (r + 8 + k) * a.RB, u[k]);
+          sttm_rows8<W>(tl + (kConst0 + r) * W, v);
+          sttm_rows8<W>(tl + (kConst0 + r + 8) * W, u);
+        }
         for (; r + 8 <= nl; r += 8) {  // 8 consecutive slots: one tcgen05.st of 8W columns
           Vec<W> v[8];
 #pragma unroll
@@ -952,7 +969,7 @@ bool interp_tmem_launch(const Program *const *progs, int np, const int32_t *d_po
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<uint64_t>(a.ntiles, (uint64_t)sms);
   void *args[] = {&a};
-  CUDA_OK(cudaLaunchKernel(kernel_of(y.W, y.CW, y.B), dim3(grid), dim3(y.CW * 32 + 32), args, y.smem, st));
+  CUDA_OK(cudaLaunchKernel(kernel_of(y.W, y.CW, y.B), dim3(grid), dim3(y.CW * 32 + kNP * 32), args, y.smem, st));
   count_launch();
   return true;
 }
