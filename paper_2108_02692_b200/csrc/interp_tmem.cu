@@ -346,8 +346,10 @@ inline int consumer_words(const TSched &sc) { return kHead + 4 * sc.B * ((int)sc
 // Device code (what the kernel runs; the form above is its compact, emulated twin): one
 // variant per consumer warp with the warp's TMEM lane quarter in every address, so an operand
 // costs one R2UR and one tcgen05.ld -- no decode.
-//   [0] nconst [1] nbatches [2] total words [3] slots [4] kB [5] W [6] vw = words per variant [7] 0
-//   4 variants of vw words; per batch: {flags (as w3 above), 0, 0, 0}, then kB ops:
+//   [0] nconst [1] nbatches [2] total words [3] slots [4] kB [5] W [6] vw = words per variant
+//   [7] batch 0's flags
+//   4 variants of vw words; per batch: {flags (as w3 above), the next batch's flags (0 after the
+//   last), 0, 0}, then kB ops:
 //     flag 2 (up to four operands): {a0, a1, a2, a3, dst, goal + 1, 0, 0}
 //     else (two operands):          {a0, a1, dst, goal + 1}
 //     (a = TMEM address: lane quarter << 16 | column; absent operand: the zero slot; absent
@@ -362,6 +364,14 @@ std::vector<uint32_t> emit_device(const TSched &sc, int W, int nvar = 4) {
     if (t < sc.n_const) return (uint32_t)((kConst0 + row[t]) * W);
     return (uint32_t)(sc.vslot[t - sc.n_const] * W);
   };
+  auto bflags = [&](size_t bi) {
+    bool quad = false, goals = false;
+    for (int j = 0; j < kB; ++j) {
+      quad |= sc.batches[bi][j].arity() > 2;
+      goals |= sc.batches[bi][j].goal >= 0;
+    }
+    return (sc.wait_st[bi] ? 1u : 0u) | (quad ? 2u : 0u) | (goals ? 4u : 0u);
+  };
   std::vector<uint32_t> v;   // variant of lane quarter 0
   std::vector<uint8_t> adr;  // word is a TMEM address
   auto put = [&](uint32_t x, bool a) {
@@ -374,8 +384,9 @@ std::vector<uint32_t> emit_device(const TSched &sc, int W, int nvar = 4) {
       quad |= sc.batches[bi][j].arity() > 2;
       goals |= sc.batches[bi][j].goal >= 0;
     }
-    put((sc.wait_st[bi] ? 1u : 0u) | (quad ? 2u : 0u) | (goals ? 4u : 0u), false);
-    for (int k = 0; k < 3; ++k) put(0, false);
+    put(bflags(bi), false);
+    put(bi + 1 < sc.batches.size() ? bflags(bi + 1) : 0u, false);  // read ahead by the kernel
+    for (int k = 0; k < 2; ++k) put(0, false);
     for (int j = 0; j < kB; ++j) {
       const TOp &o = sc.batches[bi][j];
       for (int k = 0; k < (quad ? 4 : 2); ++k) put(col(o.t[k]), true);
@@ -394,6 +405,7 @@ std::vector<uint32_t> emit_device(const TSched &sc, int W, int nvar = 4) {
   w[4] = kB;
   w[5] = (uint32_t)W;
   w[6] = (uint32_t)v.size();
+  w[7] = sc.batches.empty() ? 0u : bflags(0);
   for (int q = 0; q < nvar; ++q)
     for (size_t i = 0; i < v.size(); ++i) w.push_back(v[i] | (adr[i] ? (uint32_t)(q * 32) << 16 : 0u));
   for (int c : sc.consts) w.push_back((uint32_t)c);
@@ -653,8 +665,11 @@ __global__ void __launch_bounds__(CW * 32 + kNP * 32, 1) xslp_interp_tmem(Args a
       // batches: a batch's code words (broadcast shared loads) -> its operand loads (TMEM), one
       // wait, XORs -> result stores (TMEM) and goal stores
       uint32_t p = cp + kHead * 4 + warp * vw * 4;  // this warp's code variant
+      uint32_t fln = head2.w;                        // batch 0's flags
       for (uint32_t b = 0; b < nb; ++b) {
-        const uint32_t fl = lds128(p).x;
+        // this batch's flags were read with the previous batch's header (off the critical path)
+        const uint32_t fl = fln;
+        fln = lds128(p).y;
         p += 16;
         if (fl & 1) wait_st();
         Vec<W> acc[kB];

@@ -654,12 +654,15 @@ def _emulate_tmem_device(words, strips, n_goals):
             tm[2 + r] = strips[c]
         out = np.zeros((n_goals, strips.shape[1]), dtype=np.uint32)
         p = 0
+        fl_next = words[7]  # the kernel reads each batch's flags with the previous batch's header
 
         def col(a):
             assert a >> 16 == q * 32, (q, hex(a))
             return a & 0xFFFF
         for _ in range(nb):
             fl = v[p]
+            assert fl == fl_next
+            fl_next = v[p + 1]
             p += 4
             per = 8 if fl & 2 else 4
             nops = 4 if fl & 2 else 2
@@ -676,7 +679,7 @@ def _emulate_tmem_device(words, strips, n_goals):
                 if g:
                     assert fl & 4
                     out[g - 1] = acc
-        assert p == vw
+        assert p == vw and fl_next == 0
         results.append(out)
     assert all((r == results[0]).all() for r in results)
     return results[0]
