@@ -349,9 +349,8 @@ inline int consumer_words(const TSched &sc) { return kHead + 4 * sc.B * ((int)sc
 //   [0] nconst [1] nbatches [2] total words [3] slots [4] kB [5] W [6] vw = words per variant
 //   [7] batch 0's flags
 //   4 variants of vw words; per batch: {flags (as w3 above), the next batch's flags (0 after the
-//   last), 0, 0}, then kB ops:
-//     flag 2 (up to four operands): {a0, a1, a2, a3, dst, goal + 1, 0, 0}
-//     else (two operands):          {a0, a1, dst, goal + 1}
+//   last), 0, 0}, then the kB ops' operand addresses (flag 2, up to four operands: {a0, a1, a2,
+//   a3} per op; else {a0, a1}), then kB dst addresses, then kB goal words (goal + 1)
 //     (a = TMEM address: lane quarter << 16 | column; absent operand: the zero slot; absent
 //      dst: the sink slot; goal + 1 = 0: none)
 //   loads: nconst x (constant index)
@@ -387,16 +386,13 @@ std::vector<uint32_t> emit_device(const TSched &sc, int W, int nvar = 4) {
     put(bflags(bi), false);
     put(bi + 1 < sc.batches.size() ? bflags(bi + 1) : 0u, false);  // read ahead by the kernel
     for (int k = 0; k < 2; ++k) put(0, false);
+    for (int j = 0; j < kB; ++j)
+      for (int k = 0; k < (quad ? 4 : 2); ++k) put(col(sc.batches[bi][j].t[k]), true);
     for (int j = 0; j < kB; ++j) {
       const TOp &o = sc.batches[bi][j];
-      for (int k = 0; k < (quad ? 4 : 2); ++k) put(col(o.t[k]), true);
       put(o.dst >= 0 ? (uint32_t)(sc.vslot[o.dst] * W) : (uint32_t)(kJunk * W), true);
-      put((uint32_t)(o.goal + 1), false);
-      if (quad) {
-        put(0, false);
-        put(0, false);
-      }
     }
+    for (int j = 0; j < kB; ++j) put((uint32_t)(sc.batches[bi][j].goal + 1), false);
   }
   std::vector<uint32_t> w(kHead, 0);
   w[0] = (uint32_t)sc.consts.size();
@@ -420,7 +416,7 @@ inline int device_words(const TSched &sc) {
   for (size_t bi = 0; bi < sc.batches.size(); ++bi) {
     bool quad = false;
     for (int j = 0; j < sc.B; ++j) quad |= sc.batches[bi][j].arity() > 2;
-    per += 4 + sc.B * (quad ? 8 : 4);
+    per += 4 + sc.B * (quad ? 6 : 4);
   }
   return kHead + 4 * per;
 }
@@ -673,11 +669,12 @@ __global__ void __launch_bounds__(CW * 32 + kNP * 32, 1) xslp_interp_tmem(Args a
         p += 16;
         if (fl & 1) wait_st();
         Vec<W> acc[kB];
-        uint32_t dst[kB], gw[kB];
-        if (fl & 2) {  // ops of up to four operands: 8 words each
+        uint32_t dst[kB];
+        uint32_t pg;  // the batch's goal words
+        if (fl & 2) {  // ops of up to four operands: 4 address words each, then dst and goal words
           uint4 u[kB];
 #pragma unroll
-          for (int j = 0; j < kB; ++j) u[j] = lds128(p + 32 * j);
+          for (int j = 0; j < kB; ++j) u[j] = lds128(p + 16 * j);
           Vec<W> x[kB][4];
 #pragma unroll
           for (int j = 0; j < kB; ++j) {
@@ -687,12 +684,15 @@ __global__ void __launch_bounds__(CW * 32 + kNP * 32, 1) xslp_interp_tmem(Args a
             ldtm_w<W>(u[j].w, x[j][3]);
           }
 #pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            const uint4 t = lds128(p + 32 * j + 16);
-            dst[j] = t.x;
-            gw[j] = t.y;
+          for (int k = 0; k < kB / 4; ++k) {
+            const uint4 t = lds128(p + 16 * kB + 16 * k);
+            dst[4 * k] = t.x;
+            dst[4 * k + 1] = t.y;
+            dst[4 * k + 2] = t.z;
+            dst[4 * k + 3] = t.w;
           }
-          p += 32 * kB;
+          pg = p + 20 * kB;
+          p += 24 * kB;
           wait_ld();
 #pragma unroll
           for (int j = 0; j < kB; ++j)
@@ -702,18 +702,27 @@ __global__ void __launch_bounds__(CW * 32 + kNP * 32, 1) xslp_interp_tmem(Args a
               asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(y) : "r"(x[j][0].x[w]), "r"(x[j][1].x[w]), "r"(x[j][2].x[w]));
               acc[j].x[w] = y ^ x[j][3].x[w];
             }
-        } else {  // binary ops: 4 words each
-          uint4 u[kB];
+        } else {  // binary ops: 2 address words each, then dst and goal words
+          uint4 u[kB / 2];
 #pragma unroll
-          for (int j = 0; j < kB; ++j) u[j] = lds128(p + 16 * j);
+          for (int k = 0; k < kB / 2; ++k) u[k] = lds128(p + 16 * k);
           Vec<W> x[kB][2];
 #pragma unroll
-          for (int j = 0; j < kB; ++j) {
-            ldtm_w<W>(u[j].x, x[j][0]);
-            ldtm_w<W>(u[j].y, x[j][1]);
-            dst[j] = u[j].z;
-            gw[j] = u[j].w;
+          for (int k = 0; k < kB / 2; ++k) {
+            ldtm_w<W>(u[k].x, x[2 * k][0]);
+            ldtm_w<W>(u[k].y, x[2 * k][1]);
+            ldtm_w<W>(u[k].z, x[2 * k + 1][0]);
+            ldtm_w<W>(u[k].w, x[2 * k + 1][1]);
           }
+#pragma unroll
+          for (int k = 0; k < kB / 4; ++k) {
+            const uint4 t = lds128(p + 8 * kB + 16 * k);
+            dst[4 * k] = t.x;
+            dst[4 * k + 1] = t.y;
+            dst[4 * k + 2] = t.z;
+            dst[4 * k + 3] = t.w;
+          }
+          pg = p + 12 * kB;
           p += 16 * kB;
           wait_ld();
 #pragma unroll
@@ -724,6 +733,15 @@ __global__ void __launch_bounds__(CW * 32 + kNP * 32, 1) xslp_interp_tmem(Args a
 #pragma unroll
         for (int j = 0; j < kB; ++j) sttm_w<W>(dst[j], acc[j]);
         if (fl & 4) {  // goal stores (predicated: ops without a goal and the ragged tail skip)
+          uint32_t gw[kB];
+#pragma unroll
+          for (int k = 0; k < kB / 4; ++k) {
+            const uint4 t = lds128(pg + 16 * k);
+            gw[4 * k] = t.x;
+            gw[4 * k + 1] = t.y;
+            gw[4 * k + 2] = t.z;
+            gw[4 * k + 3] = t.w;
+          }
 #pragma unroll
           for (int j = 0; j < kB; ++j) {
             const uint32_t g = gw[j];

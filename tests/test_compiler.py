@@ -664,16 +664,14 @@ def _emulate_tmem_device(words, strips, n_goals):
             assert fl == fl_next
             fl_next = v[p + 1]
             p += 4
-            per = 8 if fl & 2 else 4
             nops = 4 if fl & 2 else 2
             res = []
-            for j in range(kb):
-                o = v[p + per * j:p + per * (j + 1)]
+            for j in range(kb):  # kb operand groups, then kb dst addresses, then kb goal words
                 acc = zero.copy()
-                for a in o[:nops]:
+                for a in v[p + nops * j:p + nops * (j + 1)]:
                     acc ^= tm[col(a)]
-                res.append((acc, col(o[nops]), o[nops + 1]))
-            p += per * kb
+                res.append((acc, col(v[p + nops * kb + j]), v[p + (nops + 1) * kb + j]))
+            p += (nops + 2) * kb
             for acc, d, g in res:
                 tm[d] = acc
                 if g:
