@@ -733,6 +733,22 @@ def test_tmem_interpreter_code_computes_the_oracle_result(n, p, comp, er, sched)
     assert (_emulate_tmem_device(dev, strips, bits.shape[0]) == want).all()
 
 
+def test_tmem_schedule_fits_two_words_for_every_rs_10_4_program():
+    # the TMEM interpreter runs 2 words per thread only when a launch's programs all fit 256 slots
+    # (512 columns); the critical-path batch scheduler (window 400, 16 ops per batch) must keep
+    # every RS(10,4) program there -- the encode and all 1001 four-erasure decode programs -- and
+    # keep the encode at 14 batches (216 ops: ceil(216/16) = 14, the packing bound)
+    g = X.xslp_coding_matrix(10, 4)
+    enc = X.xslp_compile(X.xslp_encode_bitmatrix(g, 10, 4), kernel="interp", specialise=0)
+    w = [int(x) for x in enc.dump(6).split()]
+    assert w[4] == 16 and w[1] == 14 and w[3] <= 256
+    pats = list(itertools.combinations(range(14), 4))
+    progs = X.compile_many([X.xslp_decode_bitmatrix(g, 10, 4, list(p))[0] for p in pats],
+                           kernel="interp", specialise=0)
+    slots = [int(pr.dump(6).split()[3]) for pr in progs]
+    assert max(slots) <= 256, (max(slots), pats[slots.index(max(slots))])
+
+
 @pytest.mark.parametrize("n,p,comp,er,sched", [
     (10, 4, "xorrepair", None, 1), (10, 4, "xorrepair", (2, 4, 5, 6), 1), (4, 2, "none", None, 1),
     (20, 4, "xorrepair", (0, 5, 21, 23), 1), (10, 3, "repair", None, 2), (10, 4, "none", (0, 1, 12, 13), 0)])
