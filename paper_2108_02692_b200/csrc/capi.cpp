@@ -159,6 +159,33 @@ std::vector<Slp> phase_programs(const std::vector<Bits> &want, int n_const, int 
 }
 }  // namespace xslp
 
+namespace xslp {
+// TMEM interpreter streams: the goal rows [0, R/2) and [R/2, R) each compressed, fused and
+// scheduled as a program of its own (the same passes as the whole program), checked by
+// evaluation.  Two consumer warps per TMEM lane quarter run one each, independently.
+std::vector<Slp> stream_programs(const std::vector<Bits> &want, int n_const, const xslp_opts &o) {
+  std::vector<Slp> out;
+  const size_t half = want.size() / 2;
+  for (int k = 0; k < 2; ++k) {
+    std::vector<Bits> g(want.begin() + (k ? half : 0), k ? want.end() : want.begin() + half);
+    Slp s = o.compress == XSLP_COMPRESS_NONE ? lift(g, n_const, o.fuse != 0)
+                                             : compress(g, n_const, o.compress == XSLP_COMPRESS_XORREPAIR);
+    if (o.fuse) fuse(s);
+    if (o.schedule == XSLP_SCHED_GREEDY) {
+      std::vector<int> peb;
+      schedule_greedy(s, o.greedy_capacity, peb);
+    } else if (o.schedule != XSLP_SCHED_NONE) {
+      schedule_dfs(s, o.goal_order);
+    }
+    auto got = evaluate(s);
+    for (size_t r = 0; r < g.size(); ++r)
+      if (!(got[r] == g[r])) throw Error(XSLP_EINVAL, "internal: stream program differs from its goals");
+    out.push_back(std::move(s));
+  }
+  return out;
+}
+}  // namespace xslp
+
 namespace {
 
 void build_phases(Program &P, const std::vector<Bits> &want) {
@@ -201,6 +228,9 @@ void finish(Program &P, const std::vector<Bits> *want, bool lifted) {
     P.pebble.clear();
     P.nvar = P.slp.n_vars;
   }
+  if (want && o.interp == XSLP_INTERP_TMEM && (!o.specialise || o.kernel == XSLP_KERNEL_INTERP) &&
+      want->size() >= 16)
+    P.streams = stream_programs(*want, P.n_const, o);
   int maxlive = 0;
   build_bytecode(P.slp, P.code, P.nslots, maxlive);
   auto &st = P.stats;
@@ -412,7 +442,7 @@ extern "C" int64_t xslp_program_dump(const xslp_program *prog, int form, char *b
       // the lane-parallel interpreter's code (stage-0 variant) for S = opts.stages
       auto w = interp_lanes_dump(&P, P.opts.stages);
       for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");
-    } else if (form == 5 || form == 6) {
+    } else if (form == 5 || form == 6 || form == 7) {
       // the TMEM interpreter's schedule (5) and the device code its kernel runs (6)
       auto w = interp_tmem_dump(&P, form);
       for (size_t i = 0; i < w.size(); ++i) s += std::to_string(w[i]) + (i + 1 < w.size() ? " " : "\n");

@@ -69,6 +69,15 @@ inline int batch_size() {
   return b;
 }
 
+// two-stream code (Program::streams, 8 consumer warps) when available: XSLP_TMEM_STREAMS=1
+// keeps one stream
+inline bool streams_wanted() {
+  static const bool v = [] {
+    const char *e = getenv("XSLP_TMEM_STREAMS");
+    return !(e && atoi(e) == 1);
+  }();
+  return v;
+}
 inline size_t sched_window() {
   static const size_t w = [] {
     const char *e = getenv("XSLP_TMEM_WINDOW");
@@ -116,7 +125,7 @@ struct TSched {
 };
 
 // Lower the scheduled SLP into 4-operand ops and batches of kB independent ops.
-TSched build_tmem(const Slp &s) {
+TSched build_tmem(const Slp &s, bool recycle = true) {
   TSched out;
   out.n_const = s.n_const;
   const int kB = out.B = batch_size();
@@ -268,7 +277,7 @@ TSched build_tmem(const Slp &s) {
     for (const auto &o : out.batches[bi])
       for (int t : o.t)
         if (t >= 0 && t < s.n_const) free_at[row[t]] = std::max(free_at[row[t]], bi + 1);
-  if (!sched_recycle()) std::fill(free_at.begin(), free_at.end(), nb + 1);
+  if (!recycle || !sched_recycle()) std::fill(free_at.begin(), free_at.end(), nb + 1);
   for (int bi = 0; bi < nb; ++bi)
     for (const auto &o : out.batches[bi]) {
       if (o.dst < 0) continue;
@@ -354,14 +363,16 @@ inline int consumer_words(const TSched &sc) { return kHead + 4 * sc.B * ((int)sc
 //     (a = TMEM address: lane quarter << 16 | column; absent operand: the zero slot; absent
 //      dst: the sink slot; goal + 1 = 0: none)
 //   loads: nconst x (constant index)
-std::vector<uint32_t> emit_device(const TSched &sc, int W, int nvar = 4) {
+// One stream's batches (the variant of lane quarter 0): col(t) = the TMEM column of operand
+// term t, vcol(v) = the column of variable v, goals stored as goal + goal0 + 1.  adr marks the
+// words that are TMEM addresses (the other variants add their lane quarter to them).
+void emit_batches(const TSched &sc, int W, const std::vector<uint32_t> &ccol,
+                  const std::vector<uint32_t> &vcol, int goal0, std::vector<uint32_t> &v,
+                  std::vector<uint8_t> &adr, uint32_t &flags0) {
   const int kB = sc.B;
-  std::vector<int> row(sc.n_const, -1);
-  for (size_t r = 0; r < sc.consts.size(); ++r) row[sc.consts[r]] = (int)r;
   auto col = [&](int t) -> uint32_t {
     if (t < 0) return (uint32_t)(kZero * W);
-    if (t < sc.n_const) return (uint32_t)((kConst0 + row[t]) * W);
-    return (uint32_t)(sc.vslot[t - sc.n_const] * W);
+    return t < sc.n_const ? ccol[t] : vcol[t - sc.n_const];
   };
   auto bflags = [&](size_t bi) {
     bool quad = false, goals = false;
@@ -371,18 +382,12 @@ std::vector<uint32_t> emit_device(const TSched &sc, int W, int nvar = 4) {
     }
     return (sc.wait_st[bi] ? 1u : 0u) | (quad ? 2u : 0u) | (goals ? 4u : 0u);
   };
-  std::vector<uint32_t> v;   // variant of lane quarter 0
-  std::vector<uint8_t> adr;  // word is a TMEM address
   auto put = [&](uint32_t x, bool a) {
     v.push_back(x);
     adr.push_back(a);
   };
   for (size_t bi = 0; bi < sc.batches.size(); ++bi) {
-    bool quad = false, goals = false;
-    for (int j = 0; j < kB; ++j) {
-      quad |= sc.batches[bi][j].arity() > 2;
-      goals |= sc.batches[bi][j].goal >= 0;
-    }
+    const bool quad = bflags(bi) & 2;
     put(bflags(bi), false);
     put(bi + 1 < sc.batches.size() ? bflags(bi + 1) : 0u, false);  // read ahead by the kernel
     for (int k = 0; k < 2; ++k) put(0, false);
@@ -390,35 +395,133 @@ std::vector<uint32_t> emit_device(const TSched &sc, int W, int nvar = 4) {
       for (int k = 0; k < (quad ? 4 : 2); ++k) put(col(sc.batches[bi][j].t[k]), true);
     for (int j = 0; j < kB; ++j) {
       const TOp &o = sc.batches[bi][j];
-      put(o.dst >= 0 ? (uint32_t)(sc.vslot[o.dst] * W) : (uint32_t)(kJunk * W), true);
+      put(o.dst >= 0 ? vcol[o.dst] : (uint32_t)(kJunk * W), true);
     }
-    for (int j = 0; j < kB; ++j) put((uint32_t)(sc.batches[bi][j].goal + 1), false);
+    for (int j = 0; j < kB; ++j) {
+      const int g = sc.batches[bi][j].goal;
+      put(g >= 0 ? (uint32_t)(g + goal0 + 1) : 0u, false);
+    }
   }
+  flags0 = sc.batches.empty() ? 0u : bflags(0);
+}
+
+// lane quarter variants of a stream: the quarter in every TMEM address
+inline void put_variants(std::vector<uint32_t> &w, const std::vector<uint32_t> &v,
+                         const std::vector<uint8_t> &adr, int nvar) {
+  for (int q = 0; q < nvar; ++q)
+    for (size_t i = 0; i < v.size(); ++i) w.push_back(v[i] | (adr[i] ? (uint32_t)(q * 32) << 16 : 0u));
+}
+
+std::vector<uint32_t> emit_device(const TSched &sc, int W, int nvar = 4) {
+  std::vector<uint32_t> ccol(sc.n_const, 0), vcol(sc.vslot.size(), 0);
+  for (size_t r = 0; r < sc.consts.size(); ++r) ccol[sc.consts[r]] = (uint32_t)((kConst0 + r) * W);
+  for (size_t x = 0; x < sc.vslot.size(); ++x) vcol[x] = (uint32_t)(sc.vslot[x] * W);
+  std::vector<uint32_t> v;
+  std::vector<uint8_t> adr;
+  uint32_t f0 = 0;
+  emit_batches(sc, W, ccol, vcol, 0, v, adr, f0);
   std::vector<uint32_t> w(kHead, 0);
   w[0] = (uint32_t)sc.consts.size();
   w[1] = (uint32_t)sc.batches.size();
   w[3] = (uint32_t)sc.nslots;
-  w[4] = kB;
+  w[4] = sc.B;
   w[5] = (uint32_t)W;
   w[6] = (uint32_t)v.size();
-  w[7] = sc.batches.empty() ? 0u : bflags(0);
-  for (int q = 0; q < nvar; ++q)
-    for (size_t i = 0; i < v.size(); ++i) w.push_back(v[i] | (adr[i] ? (uint32_t)(q * 32) << 16 : 0u));
+  w[7] = f0;
+  put_variants(w, v, adr, nvar);
   for (int c : sc.consts) w.push_back((uint32_t)c);
   while (w.size() % 4) w.push_back(0);
   w[2] = (uint32_t)w.size();
   return w;
 }
 
+// Two streams (the program's goal halves compiled apart, Program::streams) sharing the
+// constant rows: stream h's variables get slots of their own after the constants (no constant
+// slot is reused: the streams run unsynchronised within a tile).
+struct TStreams {
+  std::shared_ptr<const TSched> sc[2];
+  std::vector<int> consts;  // constant rows: the union, stream 0's first-use order first
+  int base[2] = {0, 0};     // first variable slot of each stream
+  int nslots = 0;
+  int goal0[2] = {0, 0};    // goal offset of each stream
+};
+
+TStreams build_streams(const Program &p) {
+  TStreams t;
+  for (int h = 0; h < 2; ++h) t.sc[h] = std::make_shared<const TSched>(build_tmem(p.streams[h], false));
+  std::vector<char> in(p.n_const, 0);
+  for (int h = 0; h < 2; ++h)
+    for (int c : t.sc[h]->consts)
+      if (!in[c]) {
+        in[c] = 1;
+        t.consts.push_back(c);
+      }
+  int next = kConst0 + (int)t.consts.size();
+  for (int h = 0; h < 2; ++h) {
+    t.base[h] = next;
+    next += t.sc[h]->nslots - (kConst0 + (int)t.sc[h]->consts.size());
+  }
+  t.nslots = next;
+  t.goal0[1] = (int)p.streams[0].goal.size();
+  return t;
+}
+
+// Two-stream device code: header (kHead2 words)
+//   [0] constant rows [1] stream 0 batches [2] total words [3] slots [4] kB [5] W
+//   [6] stream 0 words per variant [7] stream 0 batch 0 flags [8] stream 1 batches
+//   [9] stream 1 words per variant [10] stream 1 batch 0 flags [11] stream 1 offset (words
+//   after the header) [12..15] 0
+// then stream 0's 4 variants, stream 1's 4 variants (as emit_device), the constant list.
+constexpr int kHead2 = 16;
+std::vector<uint32_t> emit_streams(const TStreams &t, int W, int nvar = 4) {
+  std::vector<uint32_t> v[2];
+  std::vector<uint8_t> adr[2];
+  uint32_t f0[2] = {0, 0};
+  for (int h = 0; h < 2; ++h) {
+    const TSched &sc = *t.sc[h];
+    std::vector<uint32_t> ccol(sc.n_const, 0), vcol(sc.vslot.size(), 0);
+    for (size_t r = 0; r < t.consts.size(); ++r) ccol[t.consts[r]] = (uint32_t)((kConst0 + r) * W);
+    const int v0 = kConst0 + (int)sc.consts.size();
+    for (size_t x = 0; x < sc.vslot.size(); ++x)
+      if (sc.vslot[x] >= 0) {
+        if (sc.vslot[x] < v0) throw Error(XSLP_EINVAL, "tmem: stream variable in a constant slot");
+        vcol[x] = (uint32_t)((t.base[h] + sc.vslot[x] - v0) * W);
+      }
+    emit_batches(sc, W, ccol, vcol, t.goal0[h], v[h], adr[h], f0[h]);
+  }
+  std::vector<uint32_t> w(kHead2, 0);
+  w[0] = (uint32_t)t.consts.size();
+  w[1] = (uint32_t)t.sc[0]->batches.size();
+  w[3] = (uint32_t)t.nslots;
+  w[4] = t.sc[0]->B;
+  w[5] = (uint32_t)W;
+  w[6] = (uint32_t)v[0].size();
+  w[7] = f0[0];
+  w[8] = (uint32_t)t.sc[1]->batches.size();
+  w[9] = (uint32_t)v[1].size();
+  w[10] = f0[1];
+  w[11] = (uint32_t)(nvar * v[0].size());
+  put_variants(w, v[0], adr[0], nvar);
+  put_variants(w, v[1], adr[1], nvar);
+  for (int c : t.consts) w.push_back((uint32_t)c);
+  while (w.size() % 4) w.push_back(0);
+  w[2] = (uint32_t)w.size();
+  return w;
+}
+
 // words of the device code a consumer reads (header + 4 variants): the code slot size
-inline int device_words(const TSched &sc) {
+inline int stream_words(const TSched &sc) {
   int per = 0;
   for (size_t bi = 0; bi < sc.batches.size(); ++bi) {
     bool quad = false;
     for (int j = 0; j < sc.B; ++j) quad |= sc.batches[bi][j].arity() > 2;
     per += 4 + sc.B * (quad ? 6 : 4);
   }
-  return kHead + 4 * per;
+  return per;
+}
+inline int device_words(const TSched &sc) { return kHead + 4 * stream_words(sc); }
+inline int device_words(const TStreams &t) {
+  return kHead2 + 4 * (stream_words(*t.sc[0]) + stream_words(*t.sc[1]));
 }
 
 struct Layout {
@@ -428,7 +531,7 @@ struct Layout {
 };
 
 size_t layout_smem(Layout &y) {
-  y.RB = (uint32_t)(y.CW * 32 * y.W * 4);
+  y.RB = (uint32_t)(128 * y.W * 4);  // a row: 128 TMEM lanes x W words
   y.code0 = 128 + kH * kHdr;
   size_t c0 = y.code0 + (size_t)y.capw * 4;  // one code slot
   c0 = (c0 + 127) / 128 * 128;
@@ -609,9 +712,23 @@ __global__ void __launch_bounds__(CW * 32 + kNP * 32, 1) xslp_interp_tmem(Args a
     }
   } else {
     // ---------------- consumer warps: every thread runs the op stream on its W words
-    static_assert(CW == 4, "the device code has one variant per TMEM lane quarter");
-    const uint32_t tl = tbase + ((warp * 32u) << 16);
-    {
+    // CW = 4: warp q owns TMEM lane quarter q.  CW = 8 (two-stream code): warps q and q + 4 share
+    // lane quarter q and its constant slots; warp q + 4h runs stream h (the program's goal half
+    // h, variables in slots of its own) independently of the other; the pair meets after the
+    // tile's constant copies and at the tile's end.
+    static_assert(CW == 4 || CW == 8, "4 consumer warps, or 8 running two streams");
+    constexpr int NH = CW / 4;
+    const uint32_t q = warp & 3, h = warp >> 2;
+    const uint32_t lt = tid & 127;  // TMEM lane = the thread's word position in the tile
+    const uint32_t tl = tbase + ((q * 32u) << 16);
+    auto pair_sync = [&]() {
+      if constexpr (NH > 1) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+    };
+    if (h == 0) {
       Vec<W> z;
 #pragma unroll
       for (int w = 0; w < W; ++w) z.x[w] = 0;
@@ -624,16 +741,27 @@ __global__ void __launch_bounds__(CW * 32 + kNP * 32, 1) xslp_interp_tmem(Args a
       }
       const uint32_t tw = tile % a.tps;
       const uint32_t npos = min(a.tpos, a.words - tw * a.tpos);
-      const bool live = tid * W < npos;  // ragged tail: no goal stores past the strip
+      const bool live = lt * W < npos;  // ragged tail: no goal stores past the strip
       const uint32_t hdr = hdr0 + hs * kHdr;
       const uint32_t cp = base + a.code0;
       const uint4 head = lds128(cp), head2 = lds128(cp + 16);
-      const uint32_t nl = head.x, nb = head.y, vw = head2.z;
-      // the stage's constant rows -> this thread's TMEM constant slots; then the rows are free
+      uint32_t nb = head.y, vw = head2.z, fln = head2.w, voff = 0;  // this warp's stream
+      if constexpr (NH > 1) {
+        const uint4 head3 = lds128(cp + 32);
+        if (h) {
+          nb = head3.x;
+          vw = head3.y;
+          fln = head3.z;
+          voff = head3.w;
+        }
+      }
+      const uint32_t nl = head.x;
+      // the stage's constant rows -> this thread's TMEM constant slots (16-row chunks alternate
+      // between the two warps of a lane quarter); then the rows are free
       {
-        const uint32_t rs = base + a.const0 + st * a.NC * a.RB + tid * W * 4;
-        uint32_t r = 0;
-        for (; r + 16 <= nl; r += 16) {  // 16 rows' loads in flight, then two stores
+        const uint32_t rs = base + a.const0 + st * a.NC * a.RB + lt * W * 4;
+        uint32_t r = 16 * h;
+        for (; r + 16 <= nl; r += 16 * NH) {  // 16 rows' loads in flight, then two stores
           Vec<W> v[8], u[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) lds_w<W>(rs + (r + k) * a.RB, v[k]);
@@ -642,26 +770,30 @@ __global__ void __launch_bounds__(CW * 32 + kNP * 32, 1) xslp_interp_tmem(Args a
           sttm_rows8<W>(tl + (kConst0 + r) * W, v);
           sttm_rows8<W>(tl + (kConst0 + r + 8) * W, u);
         }
-        for (; r + 8 <= nl; r += 8) {  // 8 consecutive slots: one tcgen05.st of 8W columns
-          Vec<W> v[8];
+        if (h == 0) {
+          r = nl / 16 * 16;
+          for (; r + 8 <= nl; r += 8) {  // 8 consecutive slots: one tcgen05.st of 8W columns
+            Vec<W> v[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) lds_w<W>(rs + (r + k) * a.RB, v[k]);
-          sttm_rows8<W>(tl + (kConst0 + r) * W, v);
-        }
-        for (; r < nl; ++r) {
-          Vec<W> v;
-          lds_w<W>(rs + r * a.RB, v);
-          sttm_w<W>(tl + (kConst0 + r) * W, v);
+            for (int k = 0; k < 8; ++k) lds_w<W>(rs + (r + k) * a.RB, v[k]);
+            sttm_rows8<W>(tl + (kConst0 + r) * W, v);
+          }
+          for (; r < nl; ++r) {
+            Vec<W> v;
+            lds_w<W>(rs + r * a.RB, v);
+            sttm_w<W>(tl + (kConst0 + r) * W, v);
+          }
         }
       }
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(base + 32 + 8 * st) : "memory");
       wait_st();
-      const uint32_t tofs = tid * W * 4;  // this thread's bytes within a goal strip of the tile
+      pair_sync();  // both warps' constant copies are done
+      const uint32_t tofs = lt * W * 4;  // this thread's bytes within a goal strip of the tile
       // batches: a batch's code words (broadcast shared loads) -> its operand loads (TMEM), one
       // wait, XORs -> result stores (TMEM) and goal stores
-      uint32_t p = cp + kHead * 4 + warp * vw * 4;  // this warp's code variant
-      uint32_t fln = head2.w;                        // batch 0's flags
+      // this warp's code variant (its stream, its lane quarter)
+      uint32_t p = cp + (NH > 1 ? kHead2 : kHead) * 4 + voff * 4 + q * vw * 4;
       for (uint32_t b = 0; b < nb; ++b) {
         // this batch's flags were read with the previous batch's header (off the critical path)
         const uint32_t fl = fln;
@@ -759,7 +891,9 @@ __global__ void __launch_bounds__(CW * 32 + kNP * 32, 1) xslp_interp_tmem(Args a
         }
       }
       // the next tile's constant copies overwrite slots this tile's last batches read/stored
+      // (in either stream)
       wait_st();
+      pair_sync();
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(base + 64 + 8 * hs) : "memory");
     }
@@ -771,6 +905,7 @@ __global__ void __launch_bounds__(CW * 32 + kNP * 32, 1) xslp_interp_tmem(Args a
 }
 
 struct Pool {
+  bool two = false;  // two-stream code (8 consumer warps)
   uint32_t *code = nullptr;
   int64_t *off = nullptr;
   Layout y;
@@ -792,8 +927,26 @@ std::shared_ptr<const TSched> sched_of(const Program *p) {
   return g_scheds.emplace(p, sc).first->second;
 }
 
-std::vector<std::shared_ptr<const TSched>> scheds_of(const Program *const *progs, int np) {
-  std::vector<std::shared_ptr<const TSched>> out(np);
+std::map<const Program *, std::shared_ptr<const TStreams>> g_streams;
+
+// the two-stream schedule of a program (nullptr: the program has no stream programs)
+std::shared_ptr<const TStreams> streams_of(const Program *p) {
+  if (p->streams.size() != 2) return nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_smu);
+    auto it = g_streams.find(p);
+    if (it != g_streams.end()) return it->second;
+  }
+  auto t = std::make_shared<const TStreams>(build_streams(*p));
+  std::lock_guard<std::mutex> g(g_smu);
+  return g_streams.emplace(p, t).first->second;
+}
+
+// schedules of a program set, built on all host cores: single-stream, and two-stream if `two`
+void scheds_of(const Program *const *progs, int np, bool two, std::vector<std::shared_ptr<const TSched>> &out,
+               std::vector<std::shared_ptr<const TStreams>> &out2) {
+  out.assign(np, nullptr);
+  out2.assign(np, nullptr);
   std::atomic<int> next{0};
   std::exception_ptr err;
   std::mutex em;
@@ -801,6 +954,7 @@ std::vector<std::shared_ptr<const TSched>> scheds_of(const Program *const *progs
     for (int i; (i = next++) < np;) {
       try {
         out[i] = sched_of(progs[i]);
+        if (two) out2[i] = streams_of(progs[i]);
       } catch (...) {
         std::lock_guard<std::mutex> g(em);
         if (!err) err = std::current_exception();
@@ -813,7 +967,6 @@ std::vector<std::shared_ptr<const TSched>> scheds_of(const Program *const *progs
   work();
   for (auto &t : ts) t.join();
   if (err) std::rethrow_exception(err);
-  return out;
 }
 
 }  // namespace tmem
@@ -821,6 +974,11 @@ std::vector<std::shared_ptr<const TSched>> scheds_of(const Program *const *progs
 // Dump form 5: the TMEM interpreter's schedule in its compact form; form 6: the device code the
 // kernel runs (both with W = 1: columns = slots).
 std::vector<uint32_t> interp_tmem_dump(const Program *p, int form) {
+  if (form == 7) {  // the two-stream device code
+    auto t = tmem::streams_of(p);
+    if (!t) throw Error(XSLP_EINVAL, "the program has no TMEM interpreter streams");
+    return tmem::emit_streams(*t, 1);
+  }
   return form == 5 ? tmem::emit_code(*tmem::sched_of(p), 1) : tmem::emit_device(*tmem::sched_of(p), 1);
 }
 
@@ -829,6 +987,7 @@ void drop_tmem_of(const Program *p) {
   {
     std::lock_guard<std::mutex> g(g_smu);
     g_scheds.erase(p);
+    g_streams.erase(p);
   }
   std::lock_guard<std::mutex> g(g_mu);
   for (auto it = g_pools.begin(); it != g_pools.end();) {
@@ -853,6 +1012,8 @@ template <int W, int CW, int B>
 const void *kfn() { return (const void *)(KFn)xslp_interp_tmem<W, CW, B>; }
 template <int B>
 const void *kernel_b(int W, int CW) {
+  if constexpr (B == 16)
+    if (CW == 8) return W == 2 ? kfn<2, 8, 16>() : kfn<1, 8, 16>();
   return W == 2 ? kfn<2, 4, B>() : kfn<1, 4, B>();
 }
 const void *kernel_of(int W, int CW, int B) {
@@ -868,20 +1029,21 @@ static bool tmem_finish_plan(int dev) {
   if (!attr[dev]) {
     for (int W : {1, 2})
       for (int B : {4, 8, 12, 16})
-        CUDA_OK(cudaFuncSetAttribute(kernel_of(W, 4, B), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024));
+        for (int CW : {4, 8})
+          CUDA_OK(cudaFuncSetAttribute(kernel_of(W, CW, B), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
     attr[dev] = true;
   }
   return true;
 }
 
-// Words per thread: the largest of {want, 1} whose TMEM slots (512 columns per thread with 4
-// consumer warps, 256 with 8) and shared-memory stages fit; 0 if neither fits.
+// Words per thread: the largest of {want, 1} whose TMEM slots (512 columns per lane) and
+// shared-memory stages fit; 0 if neither fits.
 static int tmem_words(int nc, int nslots, int S, int CW, int capw, int want) {
   using namespace tmem;
   for (int W : {2, 1}) {
     if (W > want) continue;
-    if (nslots * W > kCols / (CW / 4)) continue;
+    if (nslots * W > kCols) continue;
     Layout y;
     y.W = W;
     y.CW = CW;
@@ -895,19 +1057,23 @@ static int tmem_words(int nc, int nslots, int S, int CW, int capw, int want) {
 
 // The code pool and layout of a program set for strips of B/8 bytes on the current device;
 // false if the TMEM interpreter does not apply (strip % 16, > 32 output blocks, or the slots /
-// rows do not fit).  Four consumer warps: one per TMEM lane quarter, each with all 512 columns.
+// rows do not fit).  Four consumer warps (one per TMEM lane quarter, each with all 512 columns),
+// or eight running the program's two goal-half streams.
 static bool tmem_plan(const Program *const *progs, int np, size_t B, tmem::Pool &pool) {
   using namespace tmem;
   const xslp_opts &o = progs[0]->opts;
   const uint64_t strip = B / 8;
   if (strip % 16 || progs[0]->n_goals / 8 > 32) return false;
   const int S = std::max(1, std::min(4, o.stages));
-  const int CW = 4;
+  // two streams (8 consumer warps) when every program has stream programs and they fit at
+  // least as many words per thread as the single stream
+  bool try2 = streams_wanted() && batch_size() == 16;
+  for (int i = 0; i < np && try2; ++i) try2 = progs[i]->streams.size() == 2;
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));
   const int want = 2;  // 2 words per thread when they fit (tmem_words), else 1
   std::vector<const Program *> key(progs, progs + np);
-  const auto k = std::make_tuple(dev, S, want, CW, key);
+  const auto k = std::make_tuple(dev, S, want, try2 ? 8 : 4, key);
   {
     std::lock_guard<std::mutex> g(g_mu);
     auto it = g_pools.find(k);
@@ -917,8 +1083,9 @@ static bool tmem_plan(const Program *const *progs, int np, size_t B, tmem::Pool 
     }
   }
   std::vector<std::shared_ptr<const TSched>> sc;
+  std::vector<std::shared_ptr<const TStreams>> sc2;
   try {
-    sc = scheds_of(progs, np);
+    scheds_of(progs, np, try2, sc, sc2);
   } catch (const Error &) {
     return false;
   }
@@ -936,22 +1103,41 @@ static bool tmem_plan(const Program *const *progs, int np, size_t B, tmem::Pool 
   }
   Layout y;
   y.S = S;
-  y.CW = CW;
+  y.CW = 4;
   y.NC = nc;
   y.B = sc[0]->B;
   y.capw = (cw + 3) / 4 * 4;
-  y.W = tmem_words(nc, ns, S, CW, y.capw, want);
+  y.W = tmem_words(nc, ns, S, 4, y.capw, want);
+  bool two = false;
+  if (try2) {
+    int nc2 = 1, ns2 = 0, cw2 = 0;
+    for (int i = 0; i < np; ++i) {
+      nc2 = std::max<int>(nc2, (int)sc2[i]->consts.size());
+      ns2 = std::max(ns2, sc2[i]->nslots);
+      cw2 = std::max(cw2, device_words(*sc2[i]));
+    }
+    const int capw2 = (cw2 + 3) / 4 * 4;
+    const int W2 = tmem_words(nc2, ns2, S, 8, capw2, want);
+    if (W2 > 0 && W2 >= y.W) {
+      two = true;
+      y.CW = 8;
+      y.NC = nc2;
+      y.capw = capw2;
+      y.W = W2;
+    }
+  }
   if (y.W == 0) return false;
   layout_smem(y);
   std::vector<uint32_t> all;
   std::vector<int64_t> off;
   for (int i = 0; i < np; ++i) {
     off.push_back((int64_t)all.size());
-    auto w = emit_device(*sc[i], y.W);
+    auto w = two ? emit_streams(*sc2[i], y.W) : emit_device(*sc[i], y.W);
     all.insert(all.end(), w.begin(), w.end());
   }
   Pool P;
   P.y = y;
+  P.two = two;
   CUDA_OK(cudaMalloc(&P.code, all.size() * 4));
   CUDA_OK(cudaMemcpy(P.code, all.data(), all.size() * 4, cudaMemcpyHostToDevice));
   CUDA_OK(cudaMalloc(&P.off, off.size() * 8));
@@ -984,7 +1170,7 @@ bool interp_tmem_launch(const Program *const *progs, int np, const int32_t *d_po
   a.out_tbl = out;
   a.strip = B / 8;
   a.words = (uint32_t)(a.strip / 4);
-  a.tpos = (uint32_t)(y.CW * 32 * y.W);
+  a.tpos = (uint32_t)(128 * y.W);
   a.tps = (a.words + a.tpos - 1) / a.tpos;
   if ((uint64_t)a.tps * nstripes > 0xffffffffull) throw Error(XSLP_EINVAL, "too many tiles");
   a.ntiles = a.tps * (uint32_t)nstripes;

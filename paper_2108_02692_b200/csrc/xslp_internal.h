@@ -89,6 +89,7 @@ struct Program {
   // interpreter bytecode (uint16 words) and slot count
   std::vector<Slp> groups;         // PIPE consumer groups: goal-restricted sub-programs (opts.groups > 1)
   std::vector<Slp> phases;         // PIPE input phases: programs over contiguous input-block ranges
+  std::vector<Slp> streams;        // TMEM interpreter: goals [0, R/2) and [R/2, R) compiled apart
   int stage_used_const = 0;        // constants per PIPE stage fill (max over phases, or n_used_const)
   std::vector<uint16_t> code;
   int nslots = 0;
@@ -136,6 +137,7 @@ std::vector<uint32_t> interp_lanes_dump(const Program *p, int S);
 // The TMEM interpreter's code (interp_tmem.cu; xslp_program_dump form 5).
 std::vector<uint32_t> interp_tmem_dump(const Program *p, int form);
 // Input-phase programs of a goal set (capi.cpp; PIPE input phases and the phased multi kernel).
+std::vector<Slp> stream_programs(const std::vector<Bits> &want, int n_const, const xslp_opts &o);
 std::vector<Slp> phase_programs(const std::vector<Bits> &want, int n_const, int nphases,
                                 const xslp_opts &o, int64_t *xor_total);
 // One persistent pipeline kernel (entry xslp_sl_multi) over several programs with the same

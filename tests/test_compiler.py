@@ -733,6 +733,71 @@ def test_tmem_interpreter_code_computes_the_oracle_result(n, p, comp, er, sched)
     assert (_emulate_tmem_device(dev, strips, bits.shape[0]) == want).all()
 
 
+def _emulate_tmem_streams(words, strips, n_goals, first):
+    """Run the two-stream TMEM code (dump form 7, interp_tmem.cu emit_streams, W = 1, lane
+    quarter 0): the two streams (goal halves, one consumer warp each) meet only after the
+    constant copies and at the tile's end, so one runs to completion before the other (both
+    orders).  Checks that no stream writes a constant slot or a slot the other stream uses."""
+    nconst, nslots, kb = words[0], words[3], words[4]
+    nbs, vws, offs = (words[1], words[8]), (words[6], words[9]), (0, words[11])
+    loads = words[16 + 4 * (vws[0] + vws[1]):16 + 4 * (vws[0] + vws[1]) + nconst]
+    tm = {0: np.zeros_like(strips[0])}
+    for r, c in enumerate(loads):
+        tm[2 + r] = strips[c]
+    out = np.zeros((n_goals, strips.shape[1]), dtype=np.uint32)
+    used = [set(), set()]
+    for h in (first, 1 - first):
+        v = words[16 + offs[h]:16 + offs[h] + vws[h]]
+        p = 0
+        for _ in range(nbs[h]):
+            fl = v[p]
+            p += 4
+            na = 4 if fl & 2 else 2
+            res = []
+            for j in range(kb):
+                acc = np.zeros_like(strips[0])
+                for a in v[p + na * j:p + na * (j + 1)]:
+                    acc ^= tm[a & 0xFFFF]
+                    if a & 0xFFFF >= 2 + nconst:
+                        used[h].add(a & 0xFFFF)
+                res.append((acc, v[p + na * kb + j] & 0xFFFF, v[p + (na + 1) * kb + j]))
+            p += (na + 2) * kb
+            for acc, d, g in res:
+                assert d == 1 or 2 + nconst <= d < nslots
+                if d != 1:
+                    used[h].add(d)
+                    tm[d] = acc
+                if g:
+                    assert fl & 4
+                    out[g - 1] = acc
+        assert p == vws[h]
+    assert not used[0] & used[1]
+    return out
+
+
+@pytest.mark.parametrize("n,p,er", [(10, 4, None), (10, 4, (2, 4, 5, 6)), (10, 4, (0, 1, 9, 12)),
+                                    (20, 4, (3, 10, 19, 20)), (4, 2, None), (10, 3, (0, 11, 12))])
+def test_tmem_two_streams_compute_the_oracle_result(n, p, er):
+    # the program's goal halves, compiled apart and run by two unsynchronised warps per lane
+    # quarter, reproduce the oracle's bytes in either completion order
+    import synth
+    from oracle import rs
+    og = mx.coding_matrix(n, p)
+    g = X.xslp_coding_matrix(n, p)
+    if er is None:
+        bits, rows = X.xslp_encode_bitmatrix(g, n, p), og[n:]
+    else:
+        bits, rows = X.xslp_decode_bitmatrix(g, n, p, er)[0], mx.decode_rows(og, n, list(er))[1]
+    prog = X.xslp_compile(bits, kernel="interp", specialise=0)
+    words = [int(x) for x in prog.dump(7).split()]
+    assert words[2] == len(words)
+    data = synth.stripe_data(9, 5, n, 128)
+    strips = data.reshape(8 * n, 16).view(np.uint32)
+    want = rs.apply_rows(rows, data).reshape(bits.shape[0], 16).view(np.uint32)
+    for first in (0, 1):
+        assert (_emulate_tmem_streams(words, strips, bits.shape[0], first) == want).all()
+
+
 def test_tmem_schedule_fits_two_words_for_every_rs_10_4_program():
     # the TMEM interpreter runs 2 words per thread only when a launch's programs all fit 256 slots
     # (512 columns); the critical-path batch scheduler (window 400, 16 ops per batch) must keep
