@@ -19,6 +19,12 @@
 // copies the tile's constant rows into its TMEM constant slots (8 slots per tcgen05.st) and
 // releases the stage at once, then runs the batches out of TMEM.
 //
+// Two streams (when every program of the launch has Program::streams and their slots fit as
+// many words per thread): the program's goal halves, compiled apart, run on 8 consumer warps,
+// warps q and q + 4 sharing lane quarter q and its constant slots, each with variable slots of
+// its own; the pair meets only after the tile's constant copies and at the tile's end, so two
+// independent op streams hide each other's latencies on each SMSP.
+//
 // Code (host, build_tmem): the scheduled SLP's instructions (P:803-818 MultiSLP, DFS order
 // P:1279-1303) become ops of at most four operands (wider instructions: a tree of partial ops
 // into temporaries), list-scheduled into batches of kB (16) mutually independent ops: among
