@@ -217,7 +217,11 @@ int xslp_program_stats(const xslp_program *prog, xslp_stats *stats);
  * (initial "s<k> = c<j>" loads, slot instructions, "out <g> = ..." stores);
  * form 2: the straight-line kernel's PTX; form 3: the pipelined interpreter's paired micro-op
  * code (stage-0 variant) for T = opts.threads, L = opts.lane_words, S = opts.stages, as decimal
- * 32-bit words (layout in csrc/interp.cu emit_variant).  Forms 0/1 format: one statement per line,
+ * 32-bit words (layout in csrc/interp.cu emit_variant); form 4: the lane-parallel interpreter's
+ * code (csrc/interp_lanes.cu); forms 5 / 6 / 7: the TMEM interpreter's batch schedule, its device
+ * code, and its two-stream device code (XSLP_EINVAL if the program has no goal-half streams),
+ * as decimal words with one word per thread (layouts in csrc/interp_tmem.cu emit_code,
+ * emit_device, emit_streams).  Forms 0/1 format: one statement per line,
  * "<var> = <term> ^ <term> ...", "out <g> = <term>", "return <term> ...", terms
  * c<j> (constant), 0 (empty set) or a variable name; statements are sequential.
  * Writes at most cap bytes including the NUL; returns the full length needed
